@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""MSP-GMRES SOLVE-phase benchmark (BASELINE.json metric: "MSP-GMRES solve s/system at
+SPE10 1.1M cells; GS & SpMV HBM GB/s vs peak").
+
+One step = one full MSP-GMRES solve (x0 = 0 -> ||b-Ax||/||b|| <= 1e-6, GMRES(30)) of the
+C3 workload (SPE10-shaped 60x220x85 grid, 3 components, 4x4 blocks, synthetic
+channelized permeability), i.e. one pass of every §8(a) hot-path row.
+Setup (S1-S4) runs once before timing and is reported separately.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C3]
+
+Prints ONE JSON line (rank 0).  N>1 (torchrun, NCCL): every rank solves its own replica
+(DESIGN.md §7 "replicas" until the z-slab path lands); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MSP-GMRES solve s/system at SPE10 1.1M cells; GS & SpMV HBM GB/s vs peak"
+UNIT = "s/system"
+TOL = 1e-6
+RESTART = 30
+
+
+def workload_desc(name, p):
+    return (f"{name}: {p['nx']}x{p['ny']}x{p['nz']} grid ({p['n']} cells), nc={p['nc']} "
+            f"({p['b']}x{p['b']} blocks), 7-point FIM Jacobian, seeded synthetic "
+            f"(SURVEY §8(d)), tol {TOL:g}, GMRES({RESTART})")
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def oracle_sample(p, iters_full):
+    """The CPU oracle as it stands (1 thread) on a bounded sample of the same workload:
+    oracle SETUP once (not counted), then MSP-GMRES with maxit=2 from x0=0 (2 Arnoldi steps
+    + the cycle-end update: 3 MSP applications and 4 SpMVs).  Per-iteration cost = t/3;
+    s/system = that x (iterations + restart cycles) of a full solve."""
+    import oracle
+    t0 = time.perf_counter()
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"])
+    t1 = time.perf_counter()
+    r = M.solve(p["rhs"], tol=TOL, restart=RESTART, maxit=2)
+    t2 = time.perf_counter()
+    per_it = (t2 - t1) / 3.0
+    units = iters_full + math.ceil(iters_full / RESTART)
+    return dict(value=per_it * units, per_iteration_s=per_it, setup_s=t1 - t0, sample_s=t2 - t1,
+                sample_iters=r["iters"])
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle (plain sequential C++), as it stands, on this arm's
+    config/metric.  Each step = the bounded sample of oracle_sample()."""
+    if rank != 0:
+        return
+    import gen
+    p = gen.make_config(args.config)
+    gold = os.path.join(ROOT, "tests", "golden", f"oracle_{args.config.lower()}.json")
+    iters_full = json.load(open(gold))["iters"] if os.path.exists(gold) else 30
+    import oracle
+    t0 = time.perf_counter()
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"])
+    setup_s = time.perf_counter() - t0
+    vals = []
+    for s in range(args.warmup + args.steps):
+        t1 = time.perf_counter()
+        M.solve(p["rhs"], tol=TOL, restart=RESTART, maxit=2)
+        dt = time.perf_counter() - t1
+        if s >= args.warmup:
+            vals.append(dt / 3.0 * (iters_full + math.ceil(iters_full / RESTART)))
+    v = statistics.mean(vals)
+    sample = (f"per step: oracle MSP-GMRES maxit=2 on {args.config} (3 MSP applications), scaled to "
+              f"{iters_full} iterations (oracle's own full-solve count, tests/golden); oracle setup "
+              f"{setup_s:.1f}s excluded")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": workload_desc(args.config, p)},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    import gen
+    from paper_2208_08594_b200 import MspSolver
+
+    torch.cuda.set_device(local)
+    p = gen.make_config(args.config)
+    N = p["n"] * p["b"]
+    s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"])
+    st0 = s.stats()
+    b_dev = torch.from_numpy(p["rhs"]).cuda()
+    x_dev = torch.zeros_like(b_dev)
+
+    def one_solve():
+        x_dev.zero_()
+        t_before = s.stats()["solve_seconds"]
+        r = s.solve(b_dev, x_dev, tol=TOL, restart=RESTART)
+        return r, s.stats()["solve_seconds"] - t_before
+
+    for _ in range(args.warmup):
+        r, _ = one_solve()
+    iters = r["iters"]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    l0 = s.kernel_launches()
+    times, its, rels = [], [], []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, dt = one_solve()
+        times.append(dt)
+        its.append(r["iters"])
+        rels.append(r["final_rel"])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = s.kernel_launches() - l0
+    clocks = clk.stop()
+    total = sum(times)
+    if ws > 1:
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total = float(t.item())
+        torch.distributed.barrier()
+    ms_per_step = total / args.steps * 1e3
+    value = total / (args.steps * ws)            # seconds per system over the whole job
+
+    # ---- e2e: same solve through the C-ABI with pinned HOST buffers (H2D of b, x0 and
+    # D2H of x inside the library's timed region)
+    b_host = torch.from_numpy(p["rhs"]).pin_memory()
+    x_host = torch.zeros(N, dtype=torch.float64).pin_memory()
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        x_host.zero_()
+        t_before = s.stats()["solve_seconds"]
+        s.solve(b_host, x_host, tol=TOL, restart=RESTART)
+        if k >= args.warmup:
+            e2e.append(s.stats()["solve_seconds"] - t_before)
+    e2e_v = statistics.mean(e2e) / 1.0
+    if ws > 1:
+        t = torch.tensor([e2e_v], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_v = float(t.item()) / ws
+
+    # ---- per-kernel achieved bandwidth (CUDA events on the solver stream, L2 flushed)
+    peak, peak_src = measured_peak()
+    kernels = {}
+    for kind in ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
+                 "a10_multidot16", "a6_coarse_gemv", "msp_apply"):
+        try:
+            ms, by = s.time_kernel(kind, reps=args.kernel_reps)
+        except Exception as e:            # e.g. no AMG level 0 on small configs
+            kernels[kind] = {"error": str(e)}
+            continue
+        kernels[kind] = {"ms": ms, "alg_bytes": by,
+                         "GBps": (by / (ms * 1e-3) / 1e9) if by else None,
+                         "frac": (by / (ms * 1e-3) / 1e9 / peak) if by else None}
+    # per-solve share estimate: launches of each kernel per solve x its time
+    cyc = math.ceil(iters / RESTART)
+    share = {
+        "a2_bsr_spmv": kernels["a2_bsr_spmv"].get("ms", 0) * (iters + 2 * cyc + 1),
+        "a9_bilu_apply": kernels["a9_bilu_apply"].get("ms", 0) * (iters + cyc),
+        "a8_pcol_residual": kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
+        "a4_pgs_sweep_l0": kernels.get("a4_pgs_sweep_l0", {}).get("ms", 0) * 2 * (iters + cyc),
+        "a10_multidot16": kernels["a10_multidot16"].get("ms", 0) * 2 * iters,
+    }
+    dom = max(share, key=share.get)
+    kd = kernels[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": kd["frac"], "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": kd["alg_bytes"], "ms_per_launch": kd["ms"]}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        o = oracle_sample(p, iters)
+        cpu = {"value": o["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": (f"oracle (1 thread) MSP-GMRES maxit=2 on {args.config} after its setup "
+                          f"({o['setup_s']:.1f}s, excluded): {o['sample_s']:.2f}s for 3 MSP "
+                          f"applications -> {o['per_iteration_s']:.2f}s/iteration x "
+                          f"({iters} iterations + {cyc} cycle ends)")}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded generator, SURVEY §8(d)); no datasets",
+               "config": {"workload": workload_desc(args.config, p), "iterations": iters,
+                          "iterations_per_step": its, "final_rel_res": max(rels),
+                          "setup_s": st0["last_setup_seconds"], "levels": st0["level_n"],
+                          "level_colors": st0["level_colors"], "bilu_colors": st0["bilu_colors"],
+                          "l2": "inputs larger than L2 (A alone 1.0 GB); kernel timings flush L2",
+                          "parallelism": "replicas" if ws > 1 else "single GPU",
+                          "wall_s_timed_region": wall},
+               "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
+               "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * N * 8,
+                       "d2h_bytes_per_step": N * 8},
+               "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

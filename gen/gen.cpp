@@ -233,7 +233,7 @@ int gen_jacobian(const gen_params* p, int32_t* row_ptr, int32_t* col, double* va
         if (j + 1 < ny) tsum += 2.0 * trans(c, c + nx, 1);
         if (k + 1 < nz) tsum += 2.0 * trans(c, c + (int64_t)nx * ny, 2);
       }
-  const double dt = 1.0 / (p->acc * (tsum / (double)n));
+  const double dt = (tsum > 0.0) ? 1.0 / (p->acc * (tsum / (double)n)) : 1.0;  // no faces: dt = 1
   if (dt_out) *dt_out = dt;
 
   // assemble

@@ -1,0 +1,198 @@
+/*
+ * msp.h — C-ABI of the B200-native MSP-GMRES SOLVE phase (libmsp.so).
+ *
+ * Method: Zhao, Zhang, Feng, Shu, "An Improved Multi-Stage Preconditioner on GPUs
+ * for Compositional Reservoir Simulation", arXiv 2208.08594 (= PAPER.md; "P:n" is
+ * PAPER.md line n).  Restarted GMRES(m) right-preconditioned by the
+ * multi-stage preconditioner of Eq. 21 / Alg. 1: a pressure stage
+ * Π_P B_P W^T (B_P = UA-AMG V-cycle with NPAIR aggregation, PGS-MC smoothing over the
+ * adjacency-graph coloring of Alg. 2-4, direct coarsest solve)
+ * followed by the block smoother R = BILU(0) on the full block system.
+ * Hierarchy setup is host C++ (timed separately); every SOLVE-phase step runs in
+ * hand-written sm_100a CUDA kernels.  Readings of paper gaps: DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *  - Return value is an msp_status.  On any status other than MSP_OK / MSP_ENOCONV
+ *    the outputs are unspecified and msp_last_error(handle) (or msp_last_error(NULL)
+ *    when no handle exists yet) gives the stage name and the offending row/cell.
+ *  - The caller owns every array it passes.  msp_setup deep-copies A; no caller
+ *    pointer is retained after a call returns.
+ *  - A handle is single-owner and not re-entrant; distinct handles are independent.
+ *  - All GPU work is ordered after prior work on `cuda_stream` (0 = legacy default
+ *    stream) and the call returns after it has completed.
+ *  - Sizes are element counts unless stated.  FP64 everywhere (R9).
+ */
+#ifndef MSP_H_
+#define MSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MSP_OK = 0,
+  MSP_EINVAL = 1,      /* bad shape / unsorted or duplicate column / block != nc+1 / bad pointer */
+  MSP_ESINGULAR = 2,   /* zero A_PP diagonal, singular N-N block (decoupling), singular BILU pivot
+                          block or singular coarsest matrix; index in msp_last_error */
+  MSP_ENOCONV = 3,     /* maxit reached: x, history and final residual are still valid */
+  MSP_EBREAKDOWN = 4,  /* GMRES breakdown with the true residual above tol */
+  MSP_ESTALL = 5,      /* AMG coarsening stalled above coarsest_max_dof on a non-diagonal level */
+  MSP_ECUDA = 6,       /* CUDA runtime / cuSOLVER error (message in msp_last_error) */
+  MSP_ENCCL = 7,       /* NCCL error (distributed entry points) */
+  MSP_ENOMEM = 8       /* device allocation failed */
+} msp_status;
+
+/* Block-sparse Jacobian A_RR of Eq. 20 in BSR form.
+ *  n_cells rows/columns of b x b blocks, b = block = nc + 1 (unknown 0 is the
+ *  pressure P, unknowns 1..nc are N_1..N_nc).
+ *  row_ptr[n_cells+1] (row_ptr[0] = 0), col_idx[nnzb] strictly ascending per row,
+ *  values[nnzb*b*b]: each block ROW-major.  Every row must store its diagonal block.
+ *  device = -1: host pointers; >= 0: pointers live on that CUDA device. */
+typedef struct {
+  int64_t n_cells;
+  int32_t block;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const double* values;
+  int32_t device;
+} msp_bsr;
+
+/* Device allocation callback (e.g. the PyTorch caching allocator).  NULL = cudaMalloc. */
+typedef void* (*msp_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*msp_free_fn)(void* ptr, void* ctx);
+
+/* Solver configuration.  msp_config_default() fills the paper's / DESIGN.md's values. */
+typedef struct {
+  int32_t coarsest_max_dof;  /* 10000: "degree of freedom of the coarsest space" */
+  int32_t max_levels;        /* 20, including the coarsest */
+  int32_t pre_sweeps;        /* 1 PGS-MC pre-sweep, colors 1..g (R6) */
+  int32_t post_sweeps;       /* 1 PGS-MC post-sweep, colors g..1 (R6) */
+  int32_t pair_passes;       /* 2 NPAIR passes per level (R3) */
+  int32_t decoupling;        /* 0 NONE (W = Π_P), 1 QI, 2 TI (default, R4) */
+  int32_t bilu_order;        /* 0 RB (Alg. 2/3 cell colors), 1 ABMC1 (default, R5) */
+  int32_t stages;            /* 2 = P,R (north_star, default); 3 = N,P,R (full Eq. 21) */
+  int32_t orth;              /* 0 CGS2 (default, R8); 1 MGS */
+  int32_t use_graphs;        /* 1: replay each Arnoldi step as a CUDA graph (default) */
+  msp_alloc_fn alloc;        /* optional device allocator */
+  msp_free_fn free_fn;
+  void* alloc_ctx;
+} msp_config;
+
+typedef struct msp_handle msp_handle;
+
+typedef struct {
+  int32_t setup_calls;       /* SETUP executions (ASMSP SetupCalls) */
+  int32_t reuse_calls;       /* msp_update calls that reused the preconditioner */
+  double setup_seconds;      /* host setup + upload, cumulative (wall clock) */
+  double last_setup_seconds;
+  double solve_seconds;      /* cumulative device time of msp_solve (CUDA events) */
+  int32_t levels;            /* AMG smoothing levels L (coarsest is level L) */
+  int32_t n_coarsest;
+  int32_t bilu_colors;       /* block colors g_B of the BILU ordering */
+  int32_t level_n[24];       /* rows per level 0..L */
+  int64_t level_nnz[24];
+  int32_t level_colors[24];  /* PGS-MC colors per smoothing level */
+  int64_t device_bytes;      /* device memory held by the handle */
+  int32_t kernels_per_iter;  /* kernel launches of one Arnoldi step */
+} msp_stats;
+
+void msp_config_default(msp_config* cfg);
+
+/* SETUP (Alg. 1 preamble; §8(a) S1-S4): decoupling weights W and A_PP = W^T A Π_P,
+ * PGS-MC coloring per AMG level (Alg. 2/3 on Eq. 23's graph), NPAIR aggregation and
+ * Galerkin A_{l+1} = P^T A_l P, coarsest dense inverse, ABMC ordering, BILU(0)
+ * factorization; upload.  nc = number of components (block must equal nc+1).
+ * cfg NULL = defaults.  On success *out owns all device memory of the solver. */
+msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda_stream,
+                     msp_handle** out);
+
+/* ASMSP: for Newton step iota with matrix A_new, rebuild the
+ * preconditioner iff iota == 1, last_iterations > mu, or the size changed
+ * (Remark 2); otherwise keep all stage operators and only replace A's values
+ * used by SpMV and the Alg. 1 residuals.  *did_setup = 1 if rebuilt. */
+msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_iterations, int mu,
+                      int* did_setup);
+
+/* SOLVE: restarted right-preconditioned GMRES(restart) to ||b-Ax||/||b|| <= tol.
+ * b[n*block], x[n*block] in the caller's natural cell order, cell-interleaved
+ * (unknown 0 = pressure).  Host or device pointers (detected); x is read as x0 and
+ * overwritten with the solution.  *iterations = Arnoldi steps.  resid_hist
+ * (caller-owned HOST buffer, may be NULL) receives |gamma_{j+1}|/||b|| per Arnoldi
+ * step and the true relative residual at each cycle end, truncated at hist_cap. */
+msp_status msp_solve(msp_handle* h, const double* b, double* x, double tol, int restart, int maxit,
+                     int* iterations, double* final_rel_res, double* resid_hist, int hist_cap,
+                     int* hist_len);
+
+/* One MSP application w = B g (Alg. 1 with w = 0 on entry), natural order; host or
+ * device pointers.  For parity tests. */
+msp_status msp_apply(msp_handle* h, const double* g, double* w);
+
+msp_status msp_get_stats(const msp_handle* h, msp_stats* out);
+const char* msp_last_error(const msp_handle* h);
+void msp_destroy(msp_handle* h);
+
+/* ---- Kernel-level entry points (parity tests and bench; device pointers, internal
+ * order of the handle) ---- */
+
+/* y = A x with the handle's BSR (a2, K1); vectors in the handle's internal (ABMC) cell
+ * order, length n*block, device pointers. */
+msp_status msp_spmv(msp_handle* h, const double* x, double* y);
+/* One PGS-MC sweep (Alg. 4) on AMG level l: b, x of length level_n[l] in natural level
+ * order (device); ascending != 0 -> colors 1..g, else g..1. */
+msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, int ascending);
+/* One V-cycle B_P r (natural level-0 = cell order, device). */
+msp_status msp_vcycle(msp_handle* h, const double* r, double* x);
+/* R r: BILU(0) forward/backward substitution (natural order, device). */
+msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x);
+/* Times `reps` launches of one hot-path kernel on the handle's stream with CUDA events,
+ * flushing L2 (a 256 MB device write) before each launch.  Returns the mean device
+ * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory
+ * traffic, each vector counted once).  kind: 0 a2 BSR SpMV; 1 a4 level-0 PGS-MC sweep
+ * (all colors, descending = full work per color); 2 a8 pressure-column residual;
+ * 3 a9 BILU(0) apply (all colors); 4 a10 CGS2 multidot over 16 basis vectors;
+ * 5 a6 coarsest dense-inverse GEMV; 6 one whole MSP application (bytes = 0).
+ * Scratch contents of the handle are overwritten. */
+msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,
+                           double* bytes_per_launch);
+/* Number of CUDA kernels launched by the handle so far (graph replays counted per kernel). */
+int64_t msp_kernel_launches(const msp_handle* h);
+/* Internal cell order: order[p] = natural cell at position p (host buffer n_cells). */
+msp_status msp_get_order(const msp_handle* h, int32_t* order);
+
+/* ---- Host-setup introspection (no GPU needed): runs setup steps S1-S4 on the host
+ * only and exposes the integer structures and Galerkin values for bit-exact parity
+ * against the oracle. ---- */
+typedef struct msp_host_setup msp_host_setup;
+msp_status msp_host_setup_run(const msp_bsr* A, int nc, const msp_config* cfg,
+                              msp_host_setup** out);
+/* sizes: out[0]=levels L, out[1]=n_coarsest, out[2]=coarse_diag, out[3]=bilu colors */
+msp_status msp_host_setup_info(const msp_host_setup* s, int32_t* out4);
+/* level l (0..L; l == L is the coarsest): n, nnz, colors */
+msp_status msp_host_setup_level_dims(const msp_host_setup* s, int level, int32_t* n, int64_t* nnz,
+                                     int32_t* ncolors);
+/* level CSR in NATURAL level numbering (ptr[n+1], col[nnz], val[nnz]) */
+msp_status msp_host_setup_level_csr(const msp_host_setup* s, int level, int32_t* ptr, int32_t* col,
+                                    double* val);
+/* color of each row (natural numbering), smoothing levels only */
+msp_status msp_host_setup_level_colors(const msp_host_setup* s, int level, int32_t* color);
+/* composite aggregate of each row of level l (l < L) */
+msp_status msp_host_setup_level_agg(const msp_host_setup* s, int level, int32_t* agg);
+/* decoupling weights W[n*block] and BILU cell order[n] */
+msp_status msp_host_setup_weights(const msp_host_setup* s, double* W);
+msp_status msp_host_setup_order(const msp_host_setup* s, int32_t* order);
+void msp_host_setup_free(msp_host_setup* s);
+
+/* ---- Multi-GPU: z-slab row partition, NCCL halo + allreduce ---- */
+/* Host-side partition plan (no GPU): owner rank of each cell for `nranks` z-slabs of
+ * an nx*ny*nz grid (cell c = i + nx*(j + ny*k)), aggregate-owner rule (cells follow
+ * the owner of the lowest-index cell of their level-1 aggregate). */
+msp_status msp_partition_owner(const msp_host_setup* s, int nx, int ny, int nz, int nranks,
+                               int32_t* owner);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSP_H_ */

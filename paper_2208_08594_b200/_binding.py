@@ -1,0 +1,315 @@
+"""ctypes marshalling for libmsp.so.  Names follow include/msp.h."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libmsp.so")
+
+if not os.path.exists(lib_path):
+    raise ImportError(f"{lib_path} is missing: run `python __graft_entry__.py build` "
+                      "(the MSP solve path has no CPU fallback)")
+_lib = ctypes.CDLL(lib_path)
+
+STATUS = {0: "MSP_OK", 1: "MSP_EINVAL", 2: "MSP_ESINGULAR", 3: "MSP_ENOCONV", 4: "MSP_EBREAKDOWN",
+          5: "MSP_ESTALL", 6: "MSP_ECUDA", 7: "MSP_ENCCL", 8: "MSP_ENOMEM"}
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class Bsr(ctypes.Structure):
+    _fields_ = [("n_cells", ctypes.c_int64), ("block", ctypes.c_int32),
+                ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p),
+                ("values", ctypes.c_void_p), ("device", ctypes.c_int32)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("coarsest_max_dof", ctypes.c_int32), ("max_levels", ctypes.c_int32),
+                ("pre_sweeps", ctypes.c_int32), ("post_sweeps", ctypes.c_int32),
+                ("pair_passes", ctypes.c_int32), ("decoupling", ctypes.c_int32),
+                ("bilu_order", ctypes.c_int32), ("stages", ctypes.c_int32),
+                ("orth", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+                ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
+
+    @classmethod
+    def make(cls, **kw):
+        c = cls()
+        _lib.msp_config_default(ctypes.byref(c))
+        for k, v in kw.items():
+            if not hasattr(c, k):
+                raise TypeError(f"unknown msp_config field {k}")
+            setattr(c, k, v)
+        return c
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("setup_calls", ctypes.c_int32), ("reuse_calls", ctypes.c_int32),
+                ("setup_seconds", ctypes.c_double), ("last_setup_seconds", ctypes.c_double),
+                ("solve_seconds", ctypes.c_double), ("levels", ctypes.c_int32),
+                ("n_coarsest", ctypes.c_int32), ("bilu_colors", ctypes.c_int32),
+                ("level_n", ctypes.c_int32 * 24), ("level_nnz", ctypes.c_int64 * 24),
+                ("level_colors", ctypes.c_int32 * 24), ("device_bytes", ctypes.c_int64),
+                ("kernels_per_iter", ctypes.c_int32)]
+
+
+_lib.msp_last_error.restype = ctypes.c_char_p
+_lib.msp_last_error.argtypes = [ctypes.c_void_p]
+for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats", "msp_spmv",
+           "msp_pgs_sweep", "msp_vcycle", "msp_bilu_apply", "msp_get_order", "msp_host_setup_run",
+           "msp_host_setup_info", "msp_host_setup_level_dims", "msp_host_setup_level_csr",
+           "msp_host_setup_level_colors", "msp_host_setup_level_agg", "msp_host_setup_weights",
+           "msp_host_setup_order", "msp_partition_owner"):
+    getattr(_lib, _n).restype = ctypes.c_int
+_lib.msp_destroy.argtypes = [ctypes.c_void_p]
+_lib.msp_time_kernel.restype = ctypes.c_int
+_lib.msp_kernel_launches.restype = ctypes.c_int64
+_lib.msp_kernel_launches.argtypes = [ctypes.c_void_p]
+
+KERNEL_KINDS = {"a2_bsr_spmv": 0, "a4_pgs_sweep_l0": 1, "a8_pcol_residual": 2, "a9_bilu_apply": 3,
+                "a10_multidot16": 4, "a6_coarse_gemv": 5, "msp_apply": 6}
+_lib.msp_host_setup_free.argtypes = [ctypes.c_void_p]
+
+
+class MspError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (contiguous, no copy)."""
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return ctypes.c_void_p(a.ctypes.data)
+    assert a.is_contiguous()
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def _bsr(row_ptr, col, val, device=-1):
+    n = len(row_ptr) - 1
+    b = int(val.shape[-1])
+    keep = (row_ptr, col, val)
+    return Bsr(n, b, _ptr(row_ptr).value, _ptr(col).value, _ptr(val).value, device), keep
+
+
+def _np(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class _TorchAllocator:
+    """Routes the library's device allocations through PyTorch's caching allocator."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.alloc = ALLOC_FN(self._alloc)
+        self.free = FREE_FN(self._free)
+
+    def _alloc(self, size, stream, ctx):
+        try:
+            return self.torch.cuda.caching_allocator_alloc(int(size), stream=int(stream or 0))
+        except Exception:
+            return None
+
+    def _free(self, ptr, ctx):
+        self.torch.cuda.caching_allocator_delete(int(ptr))
+
+
+class MspSolver:
+    """msp_setup / msp_solve handle.  A given as BSR arrays (natural cell order, row-major
+    b x b blocks, unknown 0 = pressure).  Vectors may be numpy arrays (host) or torch
+    tensors (host or CUDA)."""
+
+    def __init__(self, row_ptr, col, val, nc, stream=None, torch_allocator=True, **cfg):
+        self.n = len(row_ptr) - 1
+        self.b = int(val.shape[-1])
+        self.nc = nc
+        self.N = self.n * self.b
+        self._keep_alloc = None
+        c = Config.make(**cfg)
+        if torch_allocator:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    self._keep_alloc = _TorchAllocator()
+                    c.alloc = self._keep_alloc.alloc
+                    c.free_fn = self._keep_alloc.free
+            except ImportError:
+                pass
+        self.cfg = c
+        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
+        A, keep = _bsr(rp, ci, v)
+        h = ctypes.c_void_p()
+        st = _lib.msp_setup(ctypes.byref(A), nc, ctypes.byref(c), ctypes.c_void_p(stream or 0),
+                            ctypes.byref(h))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        self._h = h
+
+    def _check(self, st, ok=(0,)):
+        if st not in ok:
+            raise MspError(st, _lib.msp_last_error(self._h).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.msp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def update(self, row_ptr, col, val, iota, last_iterations, mu):
+        """ASMSP: returns True when SETUP was executed."""
+        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
+        A, keep = _bsr(rp, ci, v)
+        did = ctypes.c_int(0)
+        self._check(_lib.msp_update(self._h, ctypes.byref(A), iota, last_iterations, mu,
+                                    ctypes.byref(did)))
+        return bool(did.value)
+
+    def solve(self, b, x=None, tol=1e-6, restart=30, maxit=1000, hist_cap=None):
+        """Restarted GMRES; b, x natural order.  Returns dict(x, iters, final_rel, hist, status)."""
+        import torch
+        if isinstance(b, np.ndarray):
+            b = _np(b, np.float64)
+            if x is None:
+                x = np.zeros_like(b)
+        else:
+            b = b.contiguous()
+            if x is None:
+                x = torch.zeros_like(b)
+        it = ctypes.c_int(0)
+        fr = ctypes.c_double(0)
+        cap = hist_cap or (maxit + maxit // restart + 8)
+        hist = np.zeros(cap)
+        hl = ctypes.c_int(0)
+        st = _lib.msp_solve(self._h, _ptr(b), _ptr(x), ctypes.c_double(tol), restart, maxit,
+                            ctypes.byref(it), ctypes.byref(fr), _ptr(hist), cap, ctypes.byref(hl))
+        self._check(st, ok=(0, 3))
+        return dict(x=x, iters=it.value, final_rel=fr.value, hist=hist[:hl.value].copy(), status=st)
+
+    def apply(self, g, w):
+        self._check(_lib.msp_apply(self._h, _ptr(g), _ptr(w)))
+        return w
+
+    def spmv_internal(self, x, y):
+        self._check(_lib.msp_spmv(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def pgs_sweep(self, level, b, x, ascending=True):
+        self._check(_lib.msp_pgs_sweep(self._h, level, _ptr(b), _ptr(x), 1 if ascending else 0))
+        return x
+
+    def vcycle(self, r, x):
+        self._check(_lib.msp_vcycle(self._h, _ptr(r), _ptr(x)))
+        return x
+
+    def bilu_apply(self, r, x):
+        self._check(_lib.msp_bilu_apply(self._h, _ptr(r), _ptr(x)))
+        return x
+
+    def order(self):
+        o = np.zeros(self.n, dtype=np.int32)
+        self._check(_lib.msp_get_order(self._h, _ptr(o)))
+        return o
+
+    def time_kernel(self, kind, reps=10):
+        """(ms per launch, algorithmic bytes per launch) of one hot-path kernel, L2 flushed
+        before each launch (CUDA events on the solver's stream)."""
+        k = KERNEL_KINDS[kind] if isinstance(kind, str) else int(kind)
+        ms = ctypes.c_double(0)
+        by = ctypes.c_double(0)
+        self._check(_lib.msp_time_kernel(self._h, k, reps, ctypes.byref(ms), ctypes.byref(by)))
+        return ms.value, by.value
+
+    def kernel_launches(self):
+        return int(_lib.msp_kernel_launches(self._h))
+
+    def stats(self):
+        s = Stats()
+        self._check(_lib.msp_get_stats(self._h, ctypes.byref(s)))
+        L = s.levels
+        return dict(setup_calls=s.setup_calls, reuse_calls=s.reuse_calls,
+                    setup_seconds=s.setup_seconds, last_setup_seconds=s.last_setup_seconds,
+                    solve_seconds=s.solve_seconds, levels=L, n_coarsest=s.n_coarsest,
+                    bilu_colors=s.bilu_colors, level_n=list(s.level_n[:L + 1]),
+                    level_nnz=list(s.level_nnz[:L + 1]), level_colors=list(s.level_colors[:L]),
+                    device_bytes=s.device_bytes, kernels_per_iter=s.kernels_per_iter)
+
+
+class HostSetup:
+    """Host-only SETUP (S1-S4) introspection: integer structures and Galerkin values, no GPU."""
+
+    def __init__(self, row_ptr, col, val, nc, **cfg):
+        self.n = len(row_ptr) - 1
+        self.b = int(val.shape[-1])
+        c = Config.make(**cfg)
+        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
+        A, keep = _bsr(rp, ci, v)
+        h = ctypes.c_void_p()
+        st = _lib.msp_host_setup_run(ctypes.byref(A), nc, ctypes.byref(c), ctypes.byref(h))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.msp_host_setup_free(self._h)
+            self._h = None
+
+    def info(self):
+        o = np.zeros(4, dtype=np.int32)
+        _lib.msp_host_setup_info(self._h, _ptr(o))
+        return dict(levels=int(o[0]), n_coarsest=int(o[1]), coarse_diag=bool(o[2]),
+                    bilu_colors=int(o[3]))
+
+    def level_dims(self, l):
+        n, nnz, g = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()
+        st = _lib.msp_host_setup_level_dims(self._h, l, ctypes.byref(n), ctypes.byref(nnz),
+                                            ctypes.byref(g))
+        if st:
+            raise MspError(st, "bad level")
+        return n.value, nnz.value, g.value
+
+    def level_csr(self, l):
+        n, nnz, _ = self.level_dims(l)
+        ptr = np.zeros(n + 1, np.int32); col = np.zeros(nnz, np.int32); val = np.zeros(nnz)
+        _lib.msp_host_setup_level_csr(self._h, l, _ptr(ptr), _ptr(col), _ptr(val))
+        return ptr, col, val
+
+    def level_colors(self, l):
+        n, _, g = self.level_dims(l)
+        c = np.zeros(n, np.int32)
+        _lib.msp_host_setup_level_colors(self._h, l, _ptr(c))
+        return g, c
+
+    def level_agg(self, l):
+        n, _, _ = self.level_dims(l)
+        a = np.zeros(n, np.int32)
+        _lib.msp_host_setup_level_agg(self._h, l, _ptr(a))
+        return a
+
+    def weights(self):
+        W = np.zeros((self.n, self.b))
+        _lib.msp_host_setup_weights(self._h, _ptr(W))
+        return W
+
+    def order(self):
+        o = np.zeros(self.n, np.int32)
+        _lib.msp_host_setup_order(self._h, _ptr(o))
+        return o
+
+    def partition_owner(self, nx, ny, nz, nranks):
+        o = np.zeros(self.n, np.int32)
+        st = _lib.msp_partition_owner(self._h, nx, ny, nz, nranks, _ptr(o))
+        if st:
+            raise MspError(st, "partition")
+        return o

@@ -1,0 +1,427 @@
+// sm_100a kernels of the MSP-GMRES SOLVE phase.
+// Paper: arXiv 2208.08594 (PAPER.md "P:n").  All FP64, HBM-bound (no dense
+// contraction: no tensor cores).  Layouts:
+//  - cell vectors: internal (ABMC) cell order, cell-interleaved, length n*B;
+//  - BSR / BILU factors: row_ptr/col int32 in internal positions, b x b blocks
+//    COLUMN-major (the pressure column of a block is one contiguous 32 B sector);
+//  - AMG level l: rows permuted by PGS-MC color, SELL-32 slices that never straddle
+//    a color: entry (row lane l, k) at slice_off[s] + 32*k + l; padding col = row,
+//    val = 0.  Diagonal separate.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mspk {
+
+constexpr int kSell = 32;
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// a2 (K1): BSR SpMV.  One team of TS lanes per block row (TS = 4 for b=4, 8 for b=7);
+// lane q < B owns output row q of the cell.  Each block column-major: lane q reads
+// val[e*B*B + t*B + q] for t = 0..B-1, so a team reads each 8-byte column slice of a
+// block as one contiguous B*8-byte segment.  x of the neighbour is loaded once per
+// lane (component q) and broadcast with shuffles.
+//   MODE 0: y = A x          MODE 1: y = g - A x (residual, Alg. 1 lines 3/5)
+//   MODE 2: y = g - A[:,P] xp  (a8: pressure column only, xp per cell)
+// ---------------------------------------------------------------------------
+template <int B, int MODE>
+__global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restrict__ rp,
+                                                       const int* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x,
+                                                       const double* __restrict__ g,
+                                                       double* __restrict__ y) {
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  constexpr int BB = B * B;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gtid / TS;
+  const int q = threadIdx.x % TS;
+  const int lane = threadIdx.x & 31;
+  const int base = lane - q;
+  if (row >= n) return;   // whole teams exit together (n*TS threads padded per team)
+  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  double acc = 0.0;
+  const unsigned mask = (TS == 32) ? 0xffffffffu : (((1u << TS) - 1u) << base);
+  if (MODE == 2) {
+    for (int e = e0; e < e1; ++e) {
+      const int c = ldg(ci + e);
+      const double xc = ldg(x + c);
+      if (q < B) acc = fma(ldg(val + (size_t)e * BB + q), xc, acc);
+    }
+  } else {
+#pragma unroll 2
+    for (int e = e0; e < e1; ++e) {
+      const int c = ldg(ci + e);
+      const double xq = (q < B) ? ldg(x + (size_t)c * B + q) : 0.0;
+      const double* blk = val + (size_t)e * BB;
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const double xt = __shfl_sync(mask, xq, base + t);
+        if (q < B) acc = fma(ldg(blk + t * B + q), xt, acc);
+      }
+    }
+  }
+  if (q < B) {
+    const size_t o = (size_t)row * B + q;
+    y[o] = (MODE == 0) ? acc : (g[o] - acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3: pressure restriction with decoupling weights (R4): rp_l0[dst[c]] = sum_k
+// W[c][k] * g[c*B+k]; dst maps internal cell positions to level-0 rows.
+// ---------------------------------------------------------------------------
+template <int B>
+__global__ void restrict_pressure_kernel(int n, const double* __restrict__ W,
+                                         const double* __restrict__ g, const int* __restrict__ dst,
+                                         double* __restrict__ rp) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < B; ++k) s = fma(ldg(W + (size_t)c * B + k), ldg(g + (size_t)c * B + k), s);
+  rp[ldg(dst + c)] = s;
+}
+
+// gather of the level-0 correction into cell order: wp[c] = x0[dst[c]]
+__global__ void gather_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) out[c] = ldg(src + ldg(idx + c));
+}
+
+// ---------------------------------------------------------------------------
+// a4 (K2): PGS-MC color sweep over SELL-32 (Alg. 4 line 5):
+// x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii for rows i of one color (independent,
+// P:434).  One thread per row; slice s_first.. of this color.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) pgs_color_kernel(int s_first, int s_end,
+                                                        const int* __restrict__ slice_row,
+                                                        const int* __restrict__ slice_off,
+                                                        const int* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ diag,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ x) {
+  const int s = s_first + (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
+  const int l = threadIdx.x % kSell;
+  if (s >= s_end) return;
+  const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
+  const int row = r0 + l;
+  if (row >= r1) return;
+  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
+  double acc = 0.0;
+  int o = o0 + l;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k, o += kSell) acc = fma(ldg(val + o), x[ldg(col + o)], acc);
+  x[row] = (ldg(b + row) - acc) / ldg(diag + row);
+}
+
+// First color of a pre-sweep from the zero initial guess: x_i = b_i / a_ii for the
+// rows of color 1 and x_i = 0 elsewhere (one pass over the whole level).
+__global__ void pgs_init_kernel(int n, int c1_end, const double* __restrict__ diag,
+                                const double* __restrict__ b, double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  x[i] = (i < c1_end) ? ldg(b + i) / ldg(diag + i) : 0.0;
+}
+
+// a5 part 1: residual r = b - A x over all rows of the level (SELL-32 + diagonal).
+__global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
+                                                            const int* __restrict__ slice_row,
+                                                            const int* __restrict__ slice_off,
+                                                            const int* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ diag,
+                                                            const double* __restrict__ b,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ r) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
+  const int l = threadIdx.x % kSell;
+  if (s >= nslices) return;
+  const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
+  const int row = r0 + l;
+  if (row >= r1) return;
+  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
+  double acc = ldg(diag + row) * ldg(x + row);
+  int o = o0 + l;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k, o += kSell) acc = fma(ldg(val + o), ldg(x + ldg(col + o)), acc);
+  r[row] = ldg(b + row) - acc;
+}
+
+// a5 part 2: restriction b_{l+1}[I] = sum_{i in I} r_i (P^T, piecewise-constant P).
+__global__ void restrict_kernel(int nc, const int* __restrict__ pp, const int* __restrict__ pi,
+                                const double* __restrict__ r, double* __restrict__ bc) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= nc) return;
+  double s = 0.0;
+  for (int e = ldg(pp + I); e < ldg(pp + I + 1); ++e) s += ldg(r + ldg(pi + e));
+  bc[I] = s;
+}
+
+// a7: prolongation and correction x_i += e[agg(i)].
+__global__ void prolong_kernel(int n, const int* __restrict__ agg, const double* __restrict__ e,
+                               double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] += ldg(e + ldg(agg + i));
+}
+
+// a6 (K7): coarsest solve as a dense-inverse GEMV x = Ainv b (row-major).
+// One warp per row, 16-byte loads, warp-shuffle reduction.
+__global__ void __launch_bounds__(256) gemv_kernel(int n, int ld, const double* __restrict__ Ainv,
+                                                   const double* __restrict__ b,
+                                                   double* __restrict__ x) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* a = Ainv + (size_t)row * ld;   // ld: multiple of 32 (aligned rows)
+  double acc = 0.0;
+  const int n2 = n & ~1;
+  for (int j = 2 * lane; j < n2; j += 64) {
+    const double2 av = __ldg(reinterpret_cast<const double2*>(a + j));
+    acc = fma(av.x, ldg(b + j), acc);
+    acc = fma(av.y, ldg(b + j + 1), acc);
+  }
+  if ((n & 1) && lane == 0) acc = fma(ldg(a + n - 1), ldg(b + n - 1), acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) x[row] = acc;
+}
+
+__global__ void diag_solve_kernel(int n, const double* __restrict__ d, const double* __restrict__ b,
+                                  double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = ldg(b + i) / ldg(d + i);
+}
+
+// ---------------------------------------------------------------------------
+// a9 (K4): BILU(0) substitution in ABMC order (R5).  One team of TS lanes per
+// aggregate block (blocks of one color are independent); the <= 4 cells of a block
+// are processed in order by the team.  Factors: rows in internal positions, L part
+// = entries [rp[i], dg[i]), U part = (dg[i], rp[i+1]), slot dg[i] holds D~_i^-1;
+// blocks column-major.
+//   forward  (FWD):  y_i = r_i - sum_{k<i} L_ik y_k             (in place in v)
+//   backward (BWD):  x_i = D~_i^-1 (y_i - sum_{j>i} U_ij x_j)   (in place in v),
+//                    and z_i = x_i + (pressure slot) wp[i]  (Alg. 1 line 6: w += R r)
+//   FUSED: forward then backward within the block (last color).
+// ---------------------------------------------------------------------------
+template <int B, bool FWD, bool BWD>
+__global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
+                                                         const int* __restrict__ blk_ptr,
+                                                         const int* __restrict__ rp,
+                                                         const int* __restrict__ ci,
+                                                         const int* __restrict__ dg,
+                                                         const double* __restrict__ F,
+                                                         double* v,
+                                                         const double* __restrict__ wp,
+                                                         double* __restrict__ z) {
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  constexpr int BB = B * B;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int blk = b_first + gtid / TS;
+  const int q = threadIdx.x % TS;
+  const int lane = threadIdx.x & 31;
+  const int base = lane - q;
+  const unsigned mask = ((1u << TS) - 1u) << base;
+  if (blk >= b_end) return;
+  const int c0 = ldg(blk_ptr + blk), c1 = ldg(blk_ptr + blk + 1);
+  if (FWD) {
+    for (int i = c0; i < c1; ++i) {
+      double acc = 0.0;
+      const int d = ldg(dg + i);
+      for (int e = ldg(rp + i); e < d; ++e) {
+        const int k = ldg(ci + e);
+        const double yq = (q < B) ? v[(size_t)k * B + q] : 0.0;
+        const double* blkF = F + (size_t)e * BB;
+#pragma unroll
+        for (int t = 0; t < B; ++t) {
+          const double yt = __shfl_sync(mask, yq, base + t);
+          if (q < B) acc = fma(ldg(blkF + t * B + q), yt, acc);
+        }
+      }
+      if (q < B) v[(size_t)i * B + q] -= acc;
+      __syncwarp(mask);
+    }
+  }
+  if (BWD) {
+    for (int i = c1 - 1; i >= c0; --i) {
+      double acc = 0.0;
+      const int d = ldg(dg + i);
+      const int e1 = ldg(rp + i + 1);
+      for (int e = d + 1; e < e1; ++e) {
+        const int j = ldg(ci + e);
+        const double xq = (q < B) ? v[(size_t)j * B + q] : 0.0;
+        const double* blkF = F + (size_t)e * BB;
+#pragma unroll
+        for (int t = 0; t < B; ++t) {
+          const double xt = __shfl_sync(mask, xq, base + t);
+          if (q < B) acc = fma(ldg(blkF + t * B + q), xt, acc);
+        }
+      }
+      const double tq = (q < B) ? (v[(size_t)i * B + q] - acc) : 0.0;
+      const double* Di = F + (size_t)d * BB;
+      double xi = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double tu = __shfl_sync(mask, tq, base + u);
+        if (q < B) xi = fma(ldg(Di + u * B + q), tu, xi);
+      }
+      if (q < B) {
+        v[(size_t)i * B + q] = xi;
+        z[(size_t)i * B + q] = xi + ((q == 0) ? ldg(wp + i) : 0.0);
+      }
+      __syncwarp(mask);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a10 (K8): GMRES vector kernels with deterministic two-stage reductions.
+// multidot: part[blk][i] = sum over this block's elements of V_i . w, i = 0..nv-1.
+// ---------------------------------------------------------------------------
+constexpr int kRedBlocks = 592;     // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+constexpr int kMaxV = 32;
+
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) multidot_kernel(size_t N, int nv,
+                                                               const double* __restrict__ V,
+                                                               size_t ldv,
+                                                               const double* __restrict__ w,
+                                                               double* __restrict__ part) {
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) {
+    const double wt = ldg(w + t);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nv) acc[i] = fma(ldg(V + i * ldv + t), wt, acc[i]);
+  }
+  __shared__ double sh[kRedThreads / 32][NV];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (i >= nv) break;
+    double a = acc[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) sh[wid][i] = a;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double a = 0.0;
+    for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k][i];
+    part[(size_t)blockIdx.x * kMaxV + i] = a;
+  }
+}
+
+// second stage: out[i] = (accumulate ? out[i] : 0) + sum_blk part[blk][i]; if
+// sqrt_last, out[nv-1] = sqrt(sum).  One block, one warp per output.
+__global__ void reduce_parts_kernel(int nblk, int nv, const double* __restrict__ part,
+                                    double* __restrict__ out, const double* __restrict__ addend,
+                                    int sqrt_index) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < nv; i += nw) {
+    double a = 0.0;
+    for (int k = lane; k < nblk; k += 32) a += part[(size_t)k * kMaxV + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      if (i == sqrt_index) a = sqrt(a);
+      out[i] = addend ? addend[i] + a : a;
+    }
+  }
+}
+
+// multi-axpy: w -= sum_i h[i] V_i  (or, with from_zero, w = sum_i h[i] V_i), with
+// optional per-block partial of ||w||^2 into part[blk][slot].
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) multiaxpy_kernel(size_t N, int nv,
+                                                                const double* __restrict__ V,
+                                                                size_t ldv,
+                                                                const double* __restrict__ h,
+                                                                double* __restrict__ w,
+                                                                int from_zero, double* part,
+                                                                int slot) {
+  __shared__ double hs[NV];
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) hs[i] = (i < nv) ? h[i] : 0.0;
+  __syncthreads();
+  double nrm = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) {
+    double a = from_zero ? 0.0 : w[t];
+    if (from_zero) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        if (i < nv) a = fma(hs[i], ldg(V + i * ldv + t), a);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        if (i < nv) a = fma(-hs[i], ldg(V + i * ldv + t), a);
+    }
+    w[t] = a;
+    nrm = fma(a, a, nrm);
+  }
+  if (part) {
+    __shared__ double sh[kRedThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if (lane == 0) sh[wid] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k];
+      part[(size_t)blockIdx.x * kMaxV + slot] = a;
+    }
+  }
+}
+
+// v = w * (1/s[0])   (Arnoldi normalisation; s on device)
+__global__ void scale_kernel(size_t N, const double* __restrict__ w, const double* __restrict__ s,
+                             double* __restrict__ v) {
+  const double inv = 1.0 / s[0];
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) v[t] = w[t] * inv;
+}
+
+// y = x + alpha*z  (x += z with alpha = 1)
+__global__ void axpy_kernel(size_t N, double alpha, const double* __restrict__ z, double* __restrict__ x) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride)
+    x[t] = fma(alpha, z[t], x[t]);
+}
+
+// permutations between the caller's natural cell order and the internal order
+template <int B>
+__global__ void perm_gather_kernel(int n, const int* __restrict__ order, const double* __restrict__ src,
+                                   double* __restrict__ dst) {   // dst[p] = src[order[p]]
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * B) return;
+  const int p = t / B, q = t - p * B;
+  dst[t] = ldg(src + (size_t)ldg(order + p) * B + q);
+}
+template <int B>
+__global__ void perm_scatter_kernel(int n, const int* __restrict__ order, const double* __restrict__ src,
+                                    double* __restrict__ dst) {  // dst[order[p]] = src[p]
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * B) return;
+  const int p = t / B, q = t - p * B;
+  dst[(size_t)ldg(order + p) * B + q] = src[t];
+}
+
+__global__ void scalar_perm_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                                   double* __restrict__ dst, int scatter) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (scatter) dst[ldg(idx + i)] = src[i];
+  else dst[i] = ldg(src + ldg(idx + i));
+}
+
+}  // namespace mspk

@@ -1,0 +1,584 @@
+// Host SETUP of MSP; see setup.h.  Paper: arXiv 2208.08594
+// (PAPER.md, "P:n").  Readings R1-R10: DESIGN.md §3.
+#include "setup.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <queue>
+#include <utility>
+
+namespace msp {
+
+// ---------------------------------------------------------------------------
+// Adjacency graph of Eq. 23, symmetrised, by value (R7/c-3).
+// Built from a pair list with a counting sort on the row and a per-row sort+unique.
+// ---------------------------------------------------------------------------
+static Graph graph_from_pairs(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& pairs) {
+  Graph G;
+  G.xadj.assign(n + 1, 0);
+  for (auto& p : pairs) G.xadj[p.first + 1]++;
+  for (int32_t i = 0; i < n; ++i) G.xadj[i + 1] += G.xadj[i];
+  std::vector<int32_t> tmp(pairs.size()), fill(G.xadj.begin(), G.xadj.end() - 1);
+  for (auto& p : pairs) tmp[fill[p.first]++] = p.second;
+  G.adj.clear();
+  G.adj.reserve(pairs.size());
+  std::vector<int32_t> nx(n + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    auto b = tmp.begin() + G.xadj[i], e = tmp.begin() + G.xadj[i + 1];
+    std::sort(b, e);
+    auto u = std::unique(b, e);
+    for (auto it = b; it != u; ++it) G.adj.push_back(*it);
+    nx[i + 1] = (int32_t)G.adj.size();
+  }
+  G.xadj = nx;
+  return G;
+}
+
+Graph value_graph(const SpMat& A) {
+  std::vector<std::pair<int32_t, int32_t>> pr;
+  pr.reserve(2 * A.ci.size());
+  for (int32_t i = 0; i < A.n; ++i)
+    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e)
+      if (A.ci[e] != i && A.v[e] != 0.0) { pr.push_back({i, A.ci[e]}); pr.push_back({A.ci[e], i}); }
+  return graph_from_pairs(A.n, pr);
+}
+
+Graph block_graph(const BlockMat& A) {
+  const int bb = A.b * A.b;
+  std::vector<std::pair<int32_t, int32_t>> pr;
+  for (int32_t i = 0; i < A.n; ++i)
+    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+      const int32_t j = A.ci[e];
+      if (j == i) continue;
+      const double* B = &A.v[(size_t)e * bb];
+      bool nz = false;
+      for (int t = 0; t < bb && !nz; ++t) nz = (B[t] != 0.0);
+      if (nz) { pr.push_back({i, j}); pr.push_back({j, i}); }
+    }
+  return graph_from_pairs(A.n, pr);
+}
+
+// ---------------------------------------------------------------------------
+// VerticesGrouping (Alg. 3) over VerticesSplitting (Alg. 2).
+// Selection key (max static degree |S_i|, lowest index) realised as: V scanned in a
+// precomputed degree-sorted order with a monotone cursor; the frontier Ŵ as a binary
+// heap with lazy removal of entries that left V (stale entries have no effect in
+// Alg. 2's else-branch, so skipping them yields the same accepted sequence).
+// ---------------------------------------------------------------------------
+int32_t color_groups(const Graph& G, std::vector<int32_t>& color) {
+  const int32_t n = (int32_t)G.xadj.size() - 1;
+  color.assign(n, -1);
+  std::vector<int32_t> bydeg(n);
+  std::iota(bydeg.begin(), bydeg.end(), 0);
+  std::stable_sort(bydeg.begin(), bydeg.end(),
+                   [&](int32_t a, int32_t b) { return G.deg(a) > G.deg(b); });
+  std::vector<uint8_t> inV(n, 0), inFront(n, 0);
+  std::vector<int32_t> stamp(n, -1);
+  using Key = std::pair<int32_t, int32_t>;  // (-deg, idx)
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> front;
+  std::vector<int32_t> cur = bydeg, nxt;
+  int32_t g = 0;
+  while (!cur.empty()) {
+    for (int32_t v : cur) inV[v] = 1;
+    size_t cursor = 0;
+    while (true) {
+      int32_t v = -1;
+      while (!front.empty()) {
+        int32_t t = front.top().second;
+        if (inV[t]) { v = t; front.pop(); inFront[t] = 0; break; }
+        front.pop();
+        inFront[t] = 0;
+      }
+      if (v < 0) {
+        while (cursor < cur.size() && !inV[cur[cursor]]) ++cursor;
+        if (cursor == cur.size()) break;
+        v = cur[cursor];
+      }
+      bool blocked = false;
+      for (int32_t e = G.xadj[v]; e < G.xadj[v + 1]; ++e)
+        if (color[G.adj[e]] == g) { blocked = true; break; }
+      inV[v] = 0;
+      if (blocked) continue;                       // -> deferred (W̄)
+      color[v] = g;
+      for (int32_t e = G.xadj[v]; e < G.xadj[v + 1]; ++e) {
+        const int32_t u = G.adj[e];
+        inV[u] = 0;                                // undetermined neighbours -> W̄
+        stamp[u] = v;
+      }
+      stamp[v] = v;
+      for (int32_t e = G.xadj[v]; e < G.xadj[v + 1]; ++e) {
+        const int32_t k = G.adj[e];
+        for (int32_t f = G.xadj[k]; f < G.xadj[k + 1]; ++f) {
+          const int32_t u = G.adj[f];
+          if (stamp[u] == v || !inV[u] || inFront[u]) continue;
+          inFront[u] = 1;
+          front.push({-G.deg(u), u});
+        }
+      }
+    }
+    while (!front.empty()) { inFront[front.top().second] = 0; front.pop(); }
+    nxt.clear();
+    for (int32_t v : cur)
+      if (color[v] < 0) nxt.push_back(v);        // keeps degree order for the next call
+    cur.swap(nxt);
+    ++g;
+  }
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// NPAIR pairwise aggregation (reading R3).  Strength via t_ij = a_ij + a_ji,
+// precomputed per symmetric edge from a merged (row, col) triplet list.  The
+// "fewest unaggregated neighbours" selection is a lazy min-heap on (count, index).
+// ---------------------------------------------------------------------------
+int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg) {
+  const int32_t n = A.n;
+  struct Trip { int32_t r, c; double a; bool transposed; };
+  std::vector<Trip> tr;
+  tr.reserve(2 * A.ci.size());
+  for (int32_t i = 0; i < n; ++i)
+    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+      const int32_t j = A.ci[e];
+      if (j == i) continue;
+      tr.push_back({i, j, A.v[e], false});      // a_ij seen from row i
+      tr.push_back({j, i, A.v[e], true});       // a_ij as the transposed entry of row j
+    }
+  std::sort(tr.begin(), tr.end(), [](const Trip& x, const Trip& y) {
+    return x.r != y.r ? x.r < y.r : x.c < y.c;
+  });
+  std::vector<int32_t> xadj(n + 1, 0), adj;
+  std::vector<double> tval;
+  for (size_t s = 0; s < tr.size();) {
+    size_t e = s;
+    double aij = 0.0, aji = 0.0;
+    for (; e < tr.size() && tr[e].r == tr[s].r && tr[e].c == tr[s].c; ++e) {
+      if (tr[e].transposed) aji = tr[e].a;
+      else aij = tr[e].a;
+    }
+    if (aij != 0.0 || aji != 0.0) {
+      adj.push_back(tr[s].c);
+      tval.push_back(aij + aji);
+      xadj[tr[s].r + 1]++;
+    }
+    s = e;
+  }
+  for (int32_t i = 0; i < n; ++i) xadj[i + 1] += xadj[i];
+  std::vector<int32_t> cnt(n);
+  using Key = std::pair<int32_t, int32_t>;
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> q;
+  for (int32_t i = 0; i < n; ++i) { cnt[i] = xadj[i + 1] - xadj[i]; q.push({cnt[i], i}); }
+  std::vector<uint8_t> done(n, 0);
+  agg.assign(n, -1);
+  int32_t na = 0;
+  auto release = [&](int32_t m) {
+    for (int32_t e = xadj[m]; e < xadj[m + 1]; ++e) {
+      const int32_t k = adj[e];
+      if (!done[k]) { --cnt[k]; q.push({cnt[k], k}); }
+    }
+  };
+  while (!q.empty()) {
+    const Key top = q.top();
+    q.pop();
+    const int32_t i = top.second;
+    if (done[i] || top.first != cnt[i]) continue;
+    int32_t best = -1;
+    double bt = 0.0;
+    for (int32_t e = xadj[i]; e < xadj[i + 1]; ++e)
+      if (!done[adj[e]] && tval[e] < bt) { bt = tval[e]; best = adj[e]; }
+    if (best < 0) {
+      double ba = -1.0;
+      for (int32_t e = xadj[i]; e < xadj[i + 1]; ++e)
+        if (!done[adj[e]] && std::fabs(tval[e]) > ba) { ba = std::fabs(tval[e]); best = adj[e]; }
+    }
+    done[i] = 1;
+    agg[i] = na;
+    if (best >= 0) { done[best] = 1; agg[best] = na; }
+    ++na;
+    release(i);
+    if (best >= 0) release(best);
+  }
+  return na;
+}
+
+// Galerkin P^T A P (UA-AMG): per coarse row, members ascending (counting sort),
+// stored entries ascending, accumulated into a marker-indexed slot from +0.0; the
+// row is sorted by coarse column afterwards.  Summation order per slot equals the
+// reading of SURVEY c-5, so values are bit-identical to any implementation of it.
+SpMat galerkin_rap(const SpMat& A, const std::vector<int32_t>& agg, int32_t nagg) {
+  std::vector<int32_t> mp(nagg + 1, 0), mem(A.n);
+  for (int32_t i = 0; i < A.n; ++i) mp[agg[i] + 1]++;
+  for (int32_t I = 0; I < nagg; ++I) mp[I + 1] += mp[I];
+  {
+    std::vector<int32_t> f(mp.begin(), mp.end() - 1);
+    for (int32_t i = 0; i < A.n; ++i) mem[f[agg[i]]++] = i;
+  }
+  SpMat C;
+  C.n = nagg;
+  C.rp.assign(nagg + 1, 0);
+  std::vector<int32_t> mark(nagg, -1), slot(nagg);
+  std::vector<std::pair<int32_t, double>> row;
+  for (int32_t I = 0; I < nagg; ++I) {
+    row.clear();
+    for (int32_t m = mp[I]; m < mp[I + 1]; ++m) {
+      const int32_t i = mem[m];
+      for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+        const int32_t J = agg[A.ci[e]];
+        if (mark[J] != I) { mark[J] = I; slot[J] = (int32_t)row.size(); row.push_back({J, 0.0}); }
+        row[slot[J]].second += A.v[e];
+      }
+    }
+    std::sort(row.begin(), row.end(),
+              [](const std::pair<int32_t, double>& a, const std::pair<int32_t, double>& b) {
+                return a.first < b.first;
+              });
+    for (auto& p : row) { C.ci.push_back(p.first); C.v.push_back(p.second); }
+    C.rp[I + 1] = (int32_t)C.ci.size();
+  }
+  return C;
+}
+
+static bool off_diagonal_zero(const SpMat& A) {
+  for (int32_t i = 0; i < A.n; ++i)
+    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e)
+      if (A.ci[e] != i && A.v[e] != 0.0) return false;
+  return true;
+}
+
+static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t>& comp, SpMat* out) {
+  SpMat cur = A0;
+  comp.resize(A0.n);
+  std::iota(comp.begin(), comp.end(), 0);
+  int32_t na = A0.n;
+  for (int p = 0; p < passes; ++p) {
+    std::vector<int32_t> a;
+    na = pair_aggregate(cur, a);
+    for (auto& c : comp) c = a[c];
+    cur = galerkin_rap(cur, a, na);
+  }
+  if (out) *out = std::move(cur);
+  return na;
+}
+
+// ---------------------------------------------------------------------------
+// Decoupling (R4): column sums via a CSC (counting sort on the block column, rows
+// ascending), then C_NN^T y = -C_0N^T by Gaussian elimination with partial pivoting
+// in the fixed operation order of DESIGN.md R4 (bit-reproducible, no FMA).
+// ---------------------------------------------------------------------------
+static bool weight_solve(int nc, const double* C, int b, double* y) {
+  double M[8][8], r[8];
+  for (int i = 0; i < nc; ++i) {
+    for (int j = 0; j < nc; ++j) M[i][j] = C[(1 + j) * b + 1 + i];
+    r[i] = -C[1 + i];
+  }
+  for (int k = 0; k < nc; ++k) {
+    int p = k;
+    double best = std::fabs(M[k][k]);
+    for (int i = k + 1; i < nc; ++i) {
+      const double a = std::fabs(M[i][k]);
+      if (a > best) { best = a; p = i; }
+    }
+    if (M[p][k] == 0.0) return false;
+    if (p != k) {
+      for (int j = 0; j < nc; ++j) std::swap(M[k][j], M[p][j]);
+      std::swap(r[k], r[p]);
+    }
+    const double piv = M[k][k];
+    for (int i = k + 1; i < nc; ++i) {
+      const double f = M[i][k] / piv;
+      for (int j = k + 1; j < nc; ++j) {
+        const double prod = f * M[k][j];
+        M[i][j] = M[i][j] - prod;
+      }
+      const double pr = f * r[k];
+      r[i] = r[i] - pr;
+    }
+  }
+  for (int i = nc - 1; i >= 0; --i) {
+    double acc = 0.0;
+    for (int j = i + 1; j < nc; ++j) {
+      const double prod = M[i][j] * y[j];
+      acc = acc + prod;
+    }
+    y[i] = (r[i] - acc) / M[i][i];
+  }
+  return true;
+}
+
+static int make_weights(const BlockMat& A, int mode, std::vector<double>& W, std::string& err) {
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b, nc = b - 1;
+  W.assign((size_t)n * b, 0.0);
+  for (int32_t c = 0; c < n; ++c) W[(size_t)c * b] = 1.0;
+  if (mode == 0 || nc == 0) return 0;
+  if (nc > 8) { err = "decoupling: nc > 8 unsupported"; return 1; }
+  std::vector<double> C((size_t)n * bb, 0.0);
+  if (mode == 2) {
+    // CSC of the block pattern (stable in row order) -> sums ascending in p
+    std::vector<int32_t> cp(n + 1, 0), ce(A.ci.size());
+    for (int32_t c : A.ci) cp[c + 1]++;
+    for (int32_t c = 0; c < n; ++c) cp[c + 1] += cp[c];
+    std::vector<int32_t> f(cp.begin(), cp.end() - 1);
+    for (int32_t p = 0; p < n; ++p)
+      for (int32_t e = A.rp[p]; e < A.rp[p + 1]; ++e) ce[f[A.ci[e]]++] = e;
+    for (int32_t c = 0; c < n; ++c) {
+      double* Cc = &C[(size_t)c * bb];
+      for (int32_t q = cp[c]; q < cp[c + 1]; ++q) {
+        const double* B = &A.v[(size_t)ce[q] * bb];
+        for (int t = 0; t < bb; ++t) Cc[t] = Cc[t] + B[t];
+      }
+    }
+  } else {
+    for (int32_t c = 0; c < n; ++c)
+      for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e)
+        if (A.ci[e] == c) std::memcpy(&C[(size_t)c * bb], &A.v[(size_t)e * bb], sizeof(double) * bb);
+  }
+  double y[8];
+  for (int32_t c = 0; c < n; ++c) {
+    if (!weight_solve(nc, &C[(size_t)c * bb], b, y)) {
+      err = "decoupling: singular N-N block at cell " + std::to_string(c);
+      return 2;
+    }
+    for (int i = 0; i < nc; ++i) W[(size_t)c * b + 1 + i] = y[i];
+  }
+  return 0;
+}
+
+static SpMat pressure_matrix(const BlockMat& A, const std::vector<double>& W) {
+  const int b = A.b, bb = b * b;
+  SpMat P;
+  P.n = A.n;
+  P.rp = A.rp;
+  P.ci = A.ci;
+  P.v.resize(A.ci.size());
+  for (int32_t c = 0; c < A.n; ++c) {
+    const double* w = &W[(size_t)c * b];
+    for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) {
+      const double* B = &A.v[(size_t)e * bb];
+      double acc = 0.0;
+      for (int k = 0; k < b; ++k) {
+        const double prod = w[k] * B[k * b];
+        acc = acc + prod;
+      }
+      P.v[e] = acc;
+    }
+  }
+  return P;
+}
+
+// Graph Laplacian of the cell graph (ABMC blocks when A_PP is diagonal, R5).
+static SpMat graph_laplacian(const Graph& G) {
+  SpMat L;
+  L.n = (int32_t)G.xadj.size() - 1;
+  L.rp.assign(L.n + 1, 0);
+  for (int32_t c = 0; c < L.n; ++c) {
+    bool placed = false;
+    for (int32_t e = G.xadj[c]; e < G.xadj[c + 1]; ++e) {
+      const int32_t d = G.adj[e];
+      if (!placed && d > c) { L.ci.push_back(c); L.v.push_back((double)G.deg(c)); placed = true; }
+      L.ci.push_back(d);
+      L.v.push_back(-1.0);
+    }
+    if (!placed) { L.ci.push_back(c); L.v.push_back((double)G.deg(c)); }
+    L.rp[c + 1] = (int32_t)L.ci.size();
+  }
+  return L;
+}
+
+static void make_ordering(HostSetup& S) {
+  const BlockMat& A = S.A;
+  const int32_t n = A.n;
+  Graph G = block_graph(A);
+  std::vector<int32_t> blk(n), bcol;
+  int32_t nb;
+  if (S.prm.bilu_order == 0) {
+    nb = n;
+    std::iota(blk.begin(), blk.end(), 0);
+    S.bilu_ncolor = color_groups(G, bcol);
+  } else {
+    if (off_diagonal_zero(S.App)) nb = aggregate_passes(graph_laplacian(G), S.prm.pair_passes, blk, nullptr);
+    else if (!S.lv.empty()) { blk = S.lv[0].agg; nb = S.lv[0].n_next; }
+    else nb = aggregate_passes(S.App, S.prm.pair_passes, blk, nullptr);
+    std::vector<std::pair<int32_t, int32_t>> pr;
+    for (int32_t c = 0; c < n; ++c)
+      for (int32_t e = G.xadj[c]; e < G.xadj[c + 1]; ++e) {
+        const int32_t d = G.adj[e];
+        if (blk[c] != blk[d]) pr.push_back({blk[c], blk[d]});
+      }
+    Graph Q = graph_from_pairs(nb, pr);
+    S.bilu_ncolor = color_groups(Q, bcol);
+  }
+  S.level1_agg = blk;
+  // counting sort by (color, block, cell): cells ascending within a block, blocks
+  // ascending within a color.
+  std::vector<int32_t> bstart(nb + 1, 0);
+  for (int32_t c = 0; c < n; ++c) bstart[blk[c] + 1]++;
+  std::vector<int32_t> bsize(nb);
+  for (int32_t I = 0; I < nb; ++I) bsize[I] = bstart[I + 1];
+  std::vector<int32_t> cstart(S.bilu_ncolor + 1, 0), ccount(S.bilu_ncolor + 1, 0);
+  for (int32_t I = 0; I < nb; ++I) { cstart[bcol[I] + 1] += bsize[I]; ccount[bcol[I] + 1]++; }
+  for (int32_t g = 0; g < S.bilu_ncolor; ++g) { cstart[g + 1] += cstart[g]; ccount[g + 1] += ccount[g]; }
+  std::vector<int32_t> boff(nb), bpos(nb);
+  {
+    std::vector<int32_t> cf(cstart.begin(), cstart.end() - 1), kf(ccount.begin(), ccount.end() - 1);
+    for (int32_t I = 0; I < nb; ++I) { boff[I] = cf[bcol[I]]; cf[bcol[I]] += bsize[I]; bpos[I] = kf[bcol[I]]++; }
+  }
+  S.order.assign(n, 0);
+  S.pos.assign(n, 0);
+  {
+    std::vector<int32_t> f = boff;
+    for (int32_t c = 0; c < n; ++c) { S.pos[c] = f[blk[c]]++; S.order[S.pos[c]] = c; }
+  }
+  S.blk_ptr.assign(nb + 1, 0);
+  std::vector<int32_t> blk_by_pos(nb);
+  for (int32_t I = 0; I < nb; ++I) blk_by_pos[bpos[I]] = I;
+  for (int32_t k = 0; k < nb; ++k) S.blk_ptr[k + 1] = S.blk_ptr[k] + bsize[blk_by_pos[k]];
+  S.color_blk_ptr = ccount;
+}
+
+int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::string& err) {
+  S.prm = prm;
+  S.A = A;
+  int rc = make_weights(A, prm.decoupling, S.W, err);
+  if (rc) return rc;
+  S.App = pressure_matrix(A, S.W);
+  S.lv.clear();
+  S.coarse_diag = false;
+  SpMat cur = S.App;
+  for (int l = 0;; ++l) {
+    if (cur.n <= prm.coarsest_max_dof) break;
+    if (l + 1 >= prm.max_levels) { err = "AMG: max_levels reached above coarsest_max_dof"; return 5; }
+    HostLevel L;
+    SpMat nxt;
+    const int32_t nn = aggregate_passes(cur, prm.pair_passes, L.agg, &nxt);
+    if ((double)nn > 0.9 * (double)cur.n) {
+      if (off_diagonal_zero(cur)) { S.coarse_diag = true; break; }
+      err = "AMG: coarsening stalled at level " + std::to_string(l);
+      return 5;
+    }
+    L.ncolor = color_groups(value_graph(cur), L.color);
+    L.n_next = nn;
+    L.A = std::move(cur);
+    S.lv.push_back(std::move(L));
+    cur = std::move(nxt);
+  }
+  S.Ac = std::move(cur);
+  for (int32_t i = 0; i < S.Ac.n; ++i) {
+    bool has = false;
+    for (int32_t e = S.Ac.rp[i]; e < S.Ac.rp[i + 1]; ++e)
+      if (S.Ac.ci[e] == i && S.Ac.v[e] != 0.0) has = true;
+    if (!has && S.coarse_diag) { err = "coarsest: zero diagonal at row " + std::to_string(i); return 2; }
+  }
+  for (size_t l = 0; l < S.lv.size(); ++l) {
+    const SpMat& M = S.lv[l].A;
+    for (int32_t i = 0; i < M.n; ++i) {
+      bool has = false;
+      for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e)
+        if (M.ci[e] == i && M.v[e] != 0.0) has = true;
+      if (!has) { err = "PGS-MC: zero diagonal at level " + std::to_string(l) + " row " + std::to_string(i); return 2; }
+    }
+  }
+  make_ordering(S);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Block ILU(0) over A's pattern in the ordering positions (R5).  The matrix is
+// first permuted (rows and columns to positions, columns sorted); then for each row
+// i, for each k < i stored in row i (ascending): L_ik = A_ik D~_k^-1, and every
+// stored (k, j), j > k, that is also stored in row i updates A_ij -= L_ik A_kj
+// (row-marker lookup).  D~_i^-1 by Gauss-Jordan with partial pivoting.
+// ---------------------------------------------------------------------------
+bool invert_block(int b, const double* D, double* Dinv) {
+  double a[8][8], r[8][8];
+  for (int i = 0; i < b; ++i)
+    for (int j = 0; j < b; ++j) { a[i][j] = D[i * b + j]; r[i][j] = (i == j) ? 1.0 : 0.0; }
+  for (int k = 0; k < b; ++k) {
+    int p = k;
+    for (int i = k + 1; i < b; ++i) if (std::fabs(a[i][k]) > std::fabs(a[p][k])) p = i;
+    if (a[p][k] == 0.0) return false;
+    if (p != k) for (int j = 0; j < b; ++j) { std::swap(a[k][j], a[p][j]); std::swap(r[k][j], r[p][j]); }
+    const double inv = 1.0 / a[k][k];
+    for (int j = 0; j < b; ++j) { a[k][j] *= inv; r[k][j] *= inv; }
+    for (int i = 0; i < b; ++i) {
+      if (i == k) continue;
+      const double f = a[i][k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < b; ++j) { a[i][j] -= f * a[k][j]; r[i][j] -= f * r[k][j]; }
+    }
+  }
+  for (int i = 0; i < b; ++i) for (int j = 0; j < b; ++j) Dinv[i * b + j] = r[i][j];
+  return true;
+}
+
+int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp,
+                         std::vector<int32_t>& ci, std::vector<int32_t>& dg,
+                         std::vector<int32_t>& src, std::vector<double>& F, std::string& err) {
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b;
+  rp.assign(n + 1, 0);
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t c = S.order[p];
+    rp[p + 1] = rp[p] + (A.rp[c + 1] - A.rp[c]);
+  }
+  ci.resize(A.ci.size());
+  src.resize(A.ci.size());
+  dg.assign(n, -1);
+  std::vector<std::pair<int32_t, int32_t>> tmp;
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t c = S.order[p];
+    tmp.clear();
+    for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) tmp.push_back({S.pos[A.ci[e]], e});
+    std::sort(tmp.begin(), tmp.end());
+    for (size_t t = 0; t < tmp.size(); ++t) {
+      ci[rp[p] + t] = tmp[t].first;
+      src[rp[p] + t] = tmp[t].second;
+      if (tmp[t].first == p) dg[p] = rp[p] + (int32_t)t;
+    }
+    if (dg[p] < 0) { err = "BILU: missing diagonal block at cell " + std::to_string(c); return 1; }
+  }
+  F.resize(A.v.size());
+  for (size_t e = 0; e < src.size(); ++e)
+    std::memcpy(&F[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
+  std::vector<int32_t> mark(n, -1);
+  double T[64];
+  for (int32_t i = 0; i < n; ++i) {
+    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = e;
+    for (int32_t e = rp[i]; e < dg[i]; ++e) {
+      const int32_t k = ci[e];
+      double* Lik = &F[(size_t)e * bb];
+      const double* Dk = &F[(size_t)dg[k] * bb];      // holds D~_k^-1
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) {
+          double s = 0.0;
+          for (int t = 0; t < b; ++t) s += Lik[r * b + t] * Dk[t * b + c];
+          T[r * b + c] = s;
+        }
+      std::memcpy(Lik, T, sizeof(double) * bb);
+      for (int32_t f = dg[k] + 1; f < rp[k + 1]; ++f) {
+        const int32_t m = mark[ci[f]];
+        if (m < 0) continue;
+        const double* Ukj = &F[(size_t)f * bb];
+        double* Aij = &F[(size_t)m * bb];
+        for (int r = 0; r < b; ++r)
+          for (int c = 0; c < b; ++c) {
+            double s = 0.0;
+            for (int t = 0; t < b; ++t) s += Lik[r * b + t] * Ukj[t * b + c];
+            Aij[r * b + c] -= s;
+          }
+      }
+    }
+    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = -1;
+    double* Dd = &F[(size_t)dg[i] * bb];
+    if (!invert_block(b, Dd, T)) {
+      err = "BILU: singular pivot block at cell " + std::to_string(S.order[i]);
+      return 2;
+    }
+    std::memcpy(Dd, T, sizeof(double) * bb);
+  }
+  return 0;
+}
+
+}  // namespace msp

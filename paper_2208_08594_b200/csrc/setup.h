@@ -1,0 +1,78 @@
+// Host-side SETUP of the MSP preconditioner.  Product code:
+// written independently of oracle/ (different data structures: binary heaps with
+// lazy deletion, degree-sorted scans, counting sorts, marker arrays), reproducing
+// the same deterministic readings so that colorings, aggregates and
+// Galerkin values are bit-identical.  Compiled with -ffp-contract=off.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace msp {
+
+struct SpMat {                       // scalar CSR, ascending columns
+  int32_t n = 0;
+  std::vector<int32_t> rp, ci;
+  std::vector<double> v;
+  int64_t nnz() const { return (int64_t)ci.size(); }
+};
+
+struct BlockMat {                    // BSR, row-major b x b blocks (ABI layout)
+  int32_t n = 0, b = 0;
+  std::vector<int32_t> rp, ci;
+  std::vector<double> v;
+};
+
+struct Graph {                       // symmetric adjacency, ascending neighbours
+  std::vector<int32_t> xadj, adj;
+  int32_t deg(int32_t i) const { return xadj[i + 1] - xadj[i]; }
+};
+
+struct Params {
+  int32_t coarsest_max_dof = 10000, max_levels = 20, pre_sweeps = 1, post_sweeps = 1,
+          pair_passes = 2, decoupling = 2, bilu_order = 1, stages = 2, orth = 0, use_graphs = 1;
+};
+
+struct HostLevel {
+  SpMat A;                           // natural level numbering
+  int32_t ncolor = 0;
+  std::vector<int32_t> color;        // PGS-MC group of each row (Alg. 3)
+  std::vector<int32_t> agg;          // composite aggregate -> row of level l+1
+  int32_t n_next = 0;
+};
+
+struct HostSetup {
+  Params prm;
+  BlockMat A;
+  std::vector<double> W;             // decoupling weights, n*b
+  SpMat App;                         // W^T A Pi_P
+  std::vector<HostLevel> lv;         // smoothing levels
+  SpMat Ac;                          // coarsest
+  bool coarse_diag = false;
+  // BILU ordering (positions -> cells) and its block/color structure
+  std::vector<int32_t> order, pos;
+  int32_t bilu_ncolor = 0;
+  std::vector<int32_t> blk_ptr;        // cell-position ranges of the ordering blocks
+  std::vector<int32_t> color_blk_ptr;  // block ranges per block color
+  std::vector<int32_t> level1_agg;     // ABMC blocks (cell -> block id)
+};
+
+// status codes mirror msp_status
+int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::string& err);
+
+// Block ILU(0) in the ordering of S (positions).  Outputs, in POSITION numbering:
+// rp/ci (ascending positions) of the permuted pattern, diag index per row, and the
+// factor values (row-major blocks; the diagonal slot holds D~^-1).
+int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp,
+                         std::vector<int32_t>& ci, std::vector<int32_t>& dg,
+                         std::vector<int32_t>& src_entry, std::vector<double>& F, std::string& err);
+
+// Building blocks (exposed for the host-setup introspection entry points / tests)
+Graph value_graph(const SpMat& A);
+Graph block_graph(const BlockMat& A);
+int32_t color_groups(const Graph& G, std::vector<int32_t>& color);
+int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg);
+SpMat galerkin_rap(const SpMat& A, const std::vector<int32_t>& agg, int32_t nagg);
+bool invert_block(int b, const double* D, double* Dinv);
+
+}  // namespace msp

@@ -1,0 +1,1183 @@
+// MSP-GMRES SOLVE phase on B200 (sm_100a): device data, upload, orchestration of
+// the hot-path kernels (kernels.cuh), CUDA-graph replay of Arnoldi steps, and the
+// C-ABI of include/msp.h.  Paper: arXiv 2208.08594 (PAPER.md "P:n").
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/msp.h"
+#include "kernels.cuh"
+#include "setup.h"
+
+using namespace mspk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError {
+  cudaError_t e;
+  std::string where;
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) throw CudaError{_e, std::string(#call) + " @" + std::to_string(__LINE__)}; \
+  } while (0)
+
+inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+struct DevLevel {
+  int32_t n = 0, ncolor = 0, nslices = 0;
+  std::vector<int32_t> color_row;    // host: row range per color (permuted)
+  std::vector<int32_t> color_slice;  // host: slice range per color
+  int32_t* slice_row = nullptr;
+  int32_t* slice_off = nullptr;
+  int32_t* col = nullptr;
+  double* val = nullptr;
+  double* diag = nullptr;
+  int32_t* agg = nullptr;            // permuted row -> next-level row
+  int32_t* pt_ptr = nullptr;         // next-level row -> members (permuted rows)
+  int32_t* pt_idx = nullptr;
+  int32_t* perm = nullptr;           // natural -> permuted
+  int32_t* inv = nullptr;            // permuted -> natural
+  double *b = nullptr, *x = nullptr, *r = nullptr;
+  int64_t nnz_alloc = 0;
+};
+
+}  // namespace
+
+struct msp_handle {
+  msp::Params prm;
+  msp_config cfg{};
+  int device = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  std::vector<std::pair<void*, size_t>> allocs;
+  int64_t bytes = 0;
+
+  int32_t n = 0, b = 0, nc = 0;
+  size_t N = 0;
+  int64_t nnzb = 0;
+  std::vector<int32_t> order;        // position -> natural cell
+  std::vector<int32_t> src_entry;    // permuted entry -> natural entry
+  // BSR (internal positions), shared pattern for A and the BILU factors
+  int32_t *rp = nullptr, *ci = nullptr, *dg = nullptr, *d_order = nullptr;
+  double *Aval = nullptr, *Fval = nullptr, *W = nullptr;
+  int32_t* l0_of_cell = nullptr;
+  // ABMC blocks
+  int32_t bilu_ncolor = 0;
+  std::vector<int32_t> color_blk;    // host
+  int32_t* blk_ptr = nullptr;
+  // AMG
+  std::vector<DevLevel> lv;
+  int32_t nL = 0, ldA = 0;
+  bool coarse_diag = false;
+  double *Ainv = nullptr, *cdiag = nullptr, *bL = nullptr, *xL = nullptr;
+  // work vectors
+  double *z = nullptr, *r = nullptr, *wp = nullptr, *xin = nullptr, *bin = nullptr, *u = nullptr;
+  double *V = nullptr;
+  int V_m = -1;
+  double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
+  double* io = nullptr;              // staging for host<->device and natural-order vectors
+  // graphs
+  std::vector<cudaGraphExec_t> graphs;
+  int graphs_m = -1;
+  int kernels_per_step = 0;
+  int64_t nlaunch = 0;
+  std::vector<int64_t> graph_kernels;
+  double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
+  // stats
+  msp_stats st{};
+  std::vector<int32_t> level_n;
+  std::vector<int64_t> level_nnz;
+  std::vector<int32_t> level_colors;
+
+  template <class T>
+  T* dalloc(size_t count) {
+    size_t bytes_ = std::max<size_t>(count, 1) * sizeof(T);
+    void* p = nullptr;
+    if (cfg.alloc) {
+      p = cfg.alloc(bytes_, (void*)s, cfg.alloc_ctx);
+      if (!p) throw CudaError{cudaErrorMemoryAllocation, "alloc callback"};
+    } else {
+      CK(cudaMalloc(&p, bytes_));
+    }
+    allocs.push_back({p, bytes_});
+    bytes += (int64_t)bytes_;
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = dalloc<T>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return p;
+  }
+  void free_all() {
+    if (s) cudaStreamSynchronize(s);
+    for (auto g : graphs) if (g) cudaGraphExecDestroy(g);
+    graphs.clear();
+    graphs_m = -1;
+    for (auto& a : allocs) {
+      if (cfg.free_fn) cfg.free_fn(a.first, cfg.alloc_ctx);
+      else cudaFree(a.first);
+    }
+    allocs.clear();
+    bytes = 0;
+    lv.clear();
+    V = nullptr;
+    V_m = -1;
+    if (hpin) { cudaFreeHost(hpin); hpin = nullptr; }
+  }
+};
+
+namespace {
+
+msp::Params params_of(const msp_config* c) {
+  msp::Params p;
+  if (!c) return p;
+  p.coarsest_max_dof = c->coarsest_max_dof;
+  p.max_levels = c->max_levels;
+  p.pre_sweeps = c->pre_sweeps;
+  p.post_sweeps = c->post_sweeps;
+  p.pair_passes = c->pair_passes;
+  p.decoupling = c->decoupling;
+  p.bilu_order = c->bilu_order;
+  p.stages = c->stages;
+  p.orth = c->orth;
+  p.use_graphs = c->use_graphs;
+  return p;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Copy the ABI's BSR into a host BlockMat (validating it).
+msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err) {
+  if (!A || A->n_cells <= 0 || A->n_cells > INT32_MAX || A->block != nc + 1 || nc < 0 || nc > 7 ||
+      !A->row_ptr || !A->col_idx || !A->values) {
+    err = "msp_bsr: invalid shape/pointers (block must equal nc+1, nc <= 7)";
+    return MSP_EINVAL;
+  }
+  const int32_t n = (int32_t)A->n_cells;
+  const int b = A->block;
+  M.n = n;
+  M.b = b;
+  M.rp.resize(n + 1);
+  if (A->device >= 0) {
+    if (cudaMemcpy(M.rp.data(), A->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      err = "msp_bsr: device copy of row_ptr failed";
+      return MSP_ECUDA;
+    }
+  } else {
+    std::memcpy(M.rp.data(), A->row_ptr, sizeof(int32_t) * (n + 1));
+  }
+  const int64_t nnzb = M.rp[n];
+  if (M.rp[0] != 0 || nnzb <= 0) { err = "msp_bsr: bad row_ptr"; return MSP_EINVAL; }
+  M.ci.resize(nnzb);
+  M.v.resize((size_t)nnzb * b * b);
+  if (A->device >= 0) {
+    if (cudaMemcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(M.v.data(), A->values, sizeof(double) * M.v.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      err = "msp_bsr: device copy failed";
+      return MSP_ECUDA;
+    }
+  } else {
+    std::memcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb);
+    std::memcpy(M.v.data(), A->values, sizeof(double) * M.v.size());
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    if (M.rp[i + 1] < M.rp[i]) { err = "msp_bsr: row_ptr decreasing at row " + std::to_string(i); return MSP_EINVAL; }
+    bool diag = false;
+    for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e) {
+      if (M.ci[e] < 0 || M.ci[e] >= n) { err = "msp_bsr: column out of range in row " + std::to_string(i); return MSP_EINVAL; }
+      if (e > M.rp[i] && M.ci[e] <= M.ci[e - 1]) { err = "msp_bsr: unsorted/duplicate column in row " + std::to_string(i); return MSP_EINVAL; }
+      if (M.ci[e] == i) diag = true;
+    }
+    if (!diag) { err = "msp_bsr: missing diagonal block in row " + std::to_string(i); return MSP_EINVAL; }
+  }
+  return MSP_OK;
+}
+
+// row-major b x b blocks -> column-major
+void transpose_blocks(const double* src, double* dst, size_t nblocks, int b) {
+  const int bb = b * b;
+  for (size_t e = 0; e < nblocks; ++e)
+    for (int r = 0; r < b; ++r)
+      for (int c = 0; c < b; ++c) dst[e * bb + c * b + r] = src[e * bb + r * b + c];
+}
+
+// Build SELL-32 device level from a natural-order CSR + coloring.
+void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolor,
+                  const std::vector<int32_t>& color, std::vector<int32_t>& perm_out) {
+  const int32_t n = A.n;
+  L.n = n;
+  L.ncolor = ncolor;
+  std::vector<int32_t> cnt(ncolor + 1, 0);
+  for (int32_t i = 0; i < n; ++i) cnt[color[i] + 1]++;
+  for (int32_t c = 0; c < ncolor; ++c) cnt[c + 1] += cnt[c];
+  L.color_row = cnt;
+  std::vector<int32_t> perm(n), inv(n);
+  {
+    std::vector<int32_t> f(cnt.begin(), cnt.end() - 1);
+    for (int32_t i = 0; i < n; ++i) { perm[i] = f[color[i]]++; inv[perm[i]] = i; }
+  }
+  // slices per color
+  std::vector<int32_t> slice_row, slice_off;
+  L.color_slice.assign(ncolor + 1, 0);
+  for (int32_t c = 0; c < ncolor; ++c) {
+    for (int32_t r0 = cnt[c]; r0 < cnt[c + 1]; r0 += kSell) slice_row.push_back(r0);
+    L.color_slice[c + 1] = (int32_t)slice_row.size();
+  }
+  L.nslices = (int32_t)slice_row.size();
+  slice_row.push_back(n);
+  slice_off.assign(L.nslices + 1, 0);
+  for (int32_t s = 0; s < L.nslices; ++s) {
+    int32_t r1 = std::min(slice_row[s] + kSell, slice_row[s + 1]);
+    int32_t w = 0;
+    for (int32_t p = slice_row[s]; p < r1; ++p) {
+      const int32_t i = inv[p];
+      w = std::max(w, (int32_t)(A.rp[i + 1] - A.rp[i]) - 1);
+    }
+    slice_off[s + 1] = slice_off[s] + std::max(w, 0) * kSell;
+  }
+  std::vector<int32_t> col(std::max<int32_t>(slice_off[L.nslices], 1));
+  std::vector<double> val(col.size(), 0.0), diag(n, 0.0);
+  for (int32_t s = 0; s < L.nslices; ++s) {
+    const int32_t w = (slice_off[s + 1] - slice_off[s]) / kSell;
+    for (int32_t l = 0; l < kSell; ++l) {
+      const int32_t p = slice_row[s] + l;
+      const bool valid = p < slice_row[s + 1];
+      int k = 0;
+      if (valid) {
+        const int32_t i = inv[p];
+        for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+          if (A.ci[e] == i) { diag[p] = A.v[e]; continue; }
+          col[slice_off[s] + k * kSell + l] = perm[A.ci[e]];
+          val[slice_off[s] + k * kSell + l] = A.v[e];
+          ++k;
+        }
+      }
+      for (; k < w; ++k) {
+        col[slice_off[s] + k * kSell + l] = valid ? p : slice_row[s];
+        val[slice_off[s] + k * kSell + l] = 0.0;
+      }
+    }
+  }
+  L.nnz_alloc = slice_off[L.nslices];
+  L.slice_row = h->upload(slice_row);
+  L.slice_off = h->upload(slice_off);
+  L.col = h->upload(col);
+  L.val = h->upload(val);
+  L.diag = h->upload(diag);
+  L.perm = h->upload(perm);
+  L.inv = h->upload(inv);
+  L.b = h->dalloc<double>(n);
+  L.x = h->dalloc<double>(n);
+  L.r = h->dalloc<double>(n);
+  perm_out = perm;
+}
+
+void do_setup(msp_handle* h, const msp::BlockMat& A) {
+  auto t0 = std::chrono::steady_clock::now();
+  msp::HostSetup S;
+  std::string err;
+  int rc = msp::run_host_setup(A, h->prm, S, err);
+  if (rc) throw std::pair<int, std::string>(rc, err);
+  std::vector<int32_t> rp, ci, dg, src;
+  std::vector<double> F;
+  rc = msp::bilu_factor_permuted(S, A, rp, ci, dg, src, F, err);
+  if (rc) throw std::pair<int, std::string>(rc == 1 ? MSP_EINVAL : MSP_ESINGULAR, err);
+
+  h->free_all();
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b;
+  h->n = n;
+  h->b = b;
+  h->nc = b - 1;
+  h->N = (size_t)n * b;
+  h->nnzb = (int64_t)A.ci.size();
+  h->order = S.order;
+  h->src_entry = src;
+  // BSR pattern + values (column-major blocks)
+  h->rp = h->upload(rp);
+  h->ci = h->upload(ci);
+  h->dg = h->upload(dg);
+  h->d_order = h->upload(S.order);
+  {
+    std::vector<double> tmp(F.size()), Ap(F.size());
+    transpose_blocks(F.data(), tmp.data(), ci.size(), b);
+    h->Fval = h->upload(tmp);
+    for (size_t e = 0; e < src.size(); ++e)
+      std::memcpy(&Ap[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
+    transpose_blocks(Ap.data(), tmp.data(), ci.size(), b);
+    h->Aval = h->upload(tmp);
+    CK(cudaStreamSynchronize(h->s));
+  }
+  {
+    std::vector<double> Wi((size_t)n * b);
+    for (int32_t p = 0; p < n; ++p)
+      std::memcpy(&Wi[(size_t)p * b], &S.W[(size_t)S.order[p] * b], sizeof(double) * b);
+    h->W = h->upload(Wi);
+  }
+  // ABMC blocks
+  h->bilu_ncolor = S.bilu_ncolor;
+  h->color_blk = S.color_blk_ptr;
+  h->blk_ptr = h->upload(S.blk_ptr);
+  // AMG levels
+  h->level_n.clear();
+  h->level_nnz.clear();
+  h->level_colors.clear();
+  const int L = (int)S.lv.size();
+  h->lv.resize(L);
+  std::vector<std::vector<int32_t>> perms(L);
+  for (int l = 0; l < L; ++l) {
+    upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
+    h->level_n.push_back(S.lv[l].A.n);
+    h->level_nnz.push_back(S.lv[l].A.nnz());
+    h->level_colors.push_back(S.lv[l].ncolor);
+  }
+  h->nL = S.Ac.n;
+  h->coarse_diag = S.coarse_diag;
+  h->level_n.push_back(S.Ac.n);
+  h->level_nnz.push_back(S.Ac.nnz());
+  h->level_colors.push_back(0);
+  for (int l = 0; l < L; ++l) {
+    DevLevel& D = h->lv[l];
+    const auto& agg = S.lv[l].agg;
+    const int32_t nn = S.lv[l].n_next;
+    std::vector<int32_t> ap(D.n), inv(D.n);
+    for (int32_t i = 0; i < D.n; ++i) inv[perms[l][i]] = i;
+    for (int32_t p = 0; p < D.n; ++p) {
+      const int32_t I = agg[inv[p]];
+      ap[p] = (l + 1 < L) ? perms[l + 1][I] : I;
+    }
+    std::vector<int32_t> pp(nn + 1, 0), pi(D.n);
+    for (int32_t p = 0; p < D.n; ++p) pp[ap[p] + 1]++;
+    for (int32_t I = 0; I < nn; ++I) pp[I + 1] += pp[I];
+    {
+      std::vector<int32_t> f(pp.begin(), pp.end() - 1);
+      for (int32_t p = 0; p < D.n; ++p) pi[f[ap[p]]++] = p;
+    }
+    D.agg = h->upload(ap);
+    D.pt_ptr = h->upload(pp);
+    D.pt_idx = h->upload(pi);
+  }
+  {
+    std::vector<int32_t> l0(n);
+    for (int32_t p = 0; p < n; ++p) l0[p] = (L > 0) ? perms[0][S.order[p]] : S.order[p];
+    h->l0_of_cell = h->upload(l0);
+  }
+  // coarsest
+  h->bL = h->dalloc<double>(h->nL);
+  h->xL = h->dalloc<double>(h->nL);
+  if (h->coarse_diag) {
+    std::vector<double> d(h->nL, 0.0);
+    for (int32_t i = 0; i < h->nL; ++i)
+      for (int32_t e = S.Ac.rp[i]; e < S.Ac.rp[i + 1]; ++e)
+        if (S.Ac.ci[e] == i) d[i] = S.Ac.v[e];
+    h->cdiag = h->upload(d);
+  } else {
+    const int32_t m = h->nL;
+    std::vector<double> dense((size_t)m * m, 0.0);
+    for (int32_t i = 0; i < m; ++i)
+      for (int32_t e = S.Ac.rp[i]; e < S.Ac.rp[i + 1]; ++e) dense[(size_t)i * m + S.Ac.ci[e]] = S.Ac.v[e];
+    double* dA = h->upload(dense);           // row-major A == column-major A^T
+    h->ldA = (m + 31) / 32 * 32;             // 256-byte aligned rows for the vector loads
+    h->Ainv = h->dalloc<double>((size_t)m * h->ldA);
+    std::vector<double> I((size_t)m * h->ldA, 0.0);
+    for (int32_t i = 0; i < m; ++i) I[(size_t)i * h->ldA + i] = 1.0;
+    CK(cudaMemcpyAsync(h->Ainv, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, h->s));
+    cusolverDnHandle_t cs;
+    if (cusolverDnCreate(&cs) != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnCreate"};
+    cusolverDnSetStream(cs, h->s);
+    int lwork = 0;
+    cusolverDnDgetrf_bufferSize(cs, m, m, dA, m, &lwork);
+    double* work = h->dalloc<double>(lwork);
+    int* ipiv = h->dalloc<int>(m);
+    int* info = h->dalloc<int>(1);
+    cusolverStatus_t s1 = cusolverDnDgetrf(cs, m, m, dA, m, work, ipiv, info);
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    if (s1 != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+      cusolverDnDestroy(cs);
+      throw std::pair<int, std::string>(MSP_ESINGULAR, "coarsest: singular dense matrix (getrf info " + std::to_string(hinfo) + ")");
+    }
+    // (A^T) X = I  =>  X = A^-T column-major  ==  A^-1 row-major
+    cusolverStatus_t s2 = cusolverDnDgetrs(cs, CUBLAS_OP_N, m, m, dA, m, ipiv, h->Ainv, h->ldA, info);
+    CK(cudaStreamSynchronize(h->s));
+    cusolverDnDestroy(cs);
+    if (s2 != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnDgetrs"};
+  }
+  // work vectors
+  h->z = h->dalloc<double>(h->N);
+  h->r = h->dalloc<double>(h->N);
+  h->u = h->dalloc<double>(h->N);
+  h->xin = h->dalloc<double>(h->N);
+  h->bin = h->dalloc<double>(h->N);
+  h->io = h->dalloc<double>(h->N);
+  h->wp = h->dalloc<double>(n);
+  h->part = h->dalloc<double>((size_t)kRedBlocks * kMaxV);
+  h->dh1 = h->dalloc<double>(kMaxV);
+  h->dh2 = h->dalloc<double>(kMaxV);
+  h->hcol = h->dalloc<double>(kMaxV);
+  CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 2));
+  CK(cudaStreamSynchronize(h->s));
+  auto t1 = std::chrono::steady_clock::now();
+  const double secs = std::chrono::duration<double>(t1 - t0).count();
+  h->st.setup_calls++;
+  h->st.setup_seconds += secs;
+  h->st.last_setup_seconds = secs;
+  h->st.levels = L;
+  h->st.n_coarsest = h->nL;
+  h->st.bilu_colors = h->bilu_ncolor;
+}
+
+// ----------------------------------------------------------------- launches
+template <int B>
+void launch_spmv_t(cudaStream_t s, int mode, int n, const int* rp, const int* ci, const double* val,
+                   const double* x, const double* g, double* y) {
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  const unsigned grid = nblk((size_t)n * TS, 256);
+  if (mode == 0) bsr_spmv_kernel<B, 0><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
+  else if (mode == 1) bsr_spmv_kernel<B, 1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
+  else bsr_spmv_kernel<B, 2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
+}
+
+void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
+  ++h->nlaunch;
+  switch (h->b) {
+#define CASE(BV) case BV: launch_spmv_t<BV>(h->s, mode, h->n, h->rp, h->ci, h->Aval, x, g, y); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+}
+
+template <int B>
+void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z) {
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  const int g = h->bilu_ncolor;
+  auto run = [&](int c, int kind) {
+    const int b0 = h->color_blk[c], b1 = h->color_blk[c + 1];
+    if (b1 <= b0) return;
+    const unsigned grid = nblk((size_t)(b1 - b0) * TS, 128);
+    ++h->nlaunch;
+    if (kind == 0)
+      bilu_color_kernel<B, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+    else if (kind == 1)
+      bilu_color_kernel<B, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+    else
+      bilu_color_kernel<B, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+  };
+  for (int c = 0; c < g - 1; ++c) run(c, 0);
+  run(g - 1, 2);
+  for (int c = g - 2; c >= 0; --c) run(c, 1);
+}
+
+void launch_bilu(msp_handle* h, double* v, const double* wp, double* z) {
+  switch (h->b) {
+#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+}
+
+void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0) {
+  const unsigned grid = nblk(h->n, 256);
+  switch (h->b) {
+#define CASE(BV) case BV: restrict_pressure_kernel<BV><<<grid, 256, 0, h->s>>>(h->n, h->W, g, h->l0_of_cell, rp0); ++h->nlaunch; break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+}
+
+void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero) {
+  auto color = [&](int c) {
+    const int s0 = L.color_slice[c], s1 = L.color_slice[c + 1];
+    if (s1 <= s0) return;
+    pgs_color_kernel<<<nblk((size_t)(s1 - s0) * kSell, 128), 128, 0, h->s>>>(
+        s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x); ++h->nlaunch;
+  };
+  if (ascending) {
+    int c = 0;
+    if (from_zero) {
+      pgs_init_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.color_row[1], L.diag, L.b, L.x); ++h->nlaunch;
+      c = 1;
+    }
+    for (; c < L.ncolor; ++c) color(c);
+  } else {
+    for (int c = L.ncolor - 1; c >= 0; --c) color(c);
+  }
+}
+
+// V-cycle on level l; input in lv[l].b (or bL), output in lv[l].x (or xL).
+void vcycle(msp_handle* h, int l) {
+  if (l == (int)h->lv.size()) {
+    ++h->nlaunch;
+    if (h->coarse_diag)
+      diag_solve_kernel<<<nblk(h->nL, 256), 256, 0, h->s>>>(h->nL, h->cdiag, h->bL, h->xL);
+    else
+      gemv_kernel<<<nblk((size_t)h->nL * 32, 256), 256, 0, h->s>>>(h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+    return;
+  }
+  DevLevel& L = h->lv[l];
+  const bool last = (l + 1 == (int)h->lv.size());
+  double* bn = last ? h->bL : h->lv[l + 1].b;
+  double* xn = last ? h->xL : h->lv[l + 1].x;
+  const int nn = last ? h->nL : h->lv[l + 1].n;
+  for (int s = 0; s < h->prm.pre_sweeps; ++s) pgs_sweep(h, L, true, s == 0);
+  if (h->prm.pre_sweeps == 0) CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
+  sell_residual_kernel<<<nblk((size_t)L.nslices * kSell, 128), 128, 0, h->s>>>(
+      L.nslices, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r); ++h->nlaunch;
+  restrict_kernel<<<nblk(nn, 256), 256, 0, h->s>>>(nn, L.pt_ptr, L.pt_idx, L.r, bn); ++h->nlaunch;
+  vcycle(h, l + 1);
+  prolong_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.agg, xn, L.x); ++h->nlaunch;
+  for (int s = 0; s < h->prm.post_sweeps; ++s) pgs_sweep(h, L, false, false);
+}
+
+double* level0_b(msp_handle* h) { return h->lv.empty() ? h->bL : h->lv[0].b; }
+double* level0_x(msp_handle* h) { return h->lv.empty() ? h->xL : h->lv[0].x; }
+
+// z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
+void msp_apply_dev(msp_handle* h, const double* g, double* z) {
+  launch_restrict_pressure(h, g, level0_b(h));                        // a3: r_p = W^T g
+  vcycle(h, 0);                                                        // a4-a7: B_P
+  gather_kernel<<<nblk(h->n, 256), 256, 0, h->s>>>(h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
+  launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
+  launch_bilu(h, h->r, h->wp, h->z == z ? z : z);                      // a9: z = Pi_P x_p + R r
+}
+
+// ----------------------------------------------------------------- GMRES pieces
+template <int NV>
+void multidot_t(msp_handle* h, int nv, const double* V, const double* w) {
+  multidot_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, w, h->part); ++h->nlaunch;
+}
+void multidot(msp_handle* h, int nv, const double* V, const double* w) {
+  if (nv <= 4) multidot_t<4>(h, nv, V, w);
+  else if (nv <= 8) multidot_t<8>(h, nv, V, w);
+  else if (nv <= 16) multidot_t<16>(h, nv, V, w);
+  else multidot_t<32>(h, nv, V, w);
+}
+template <int NV>
+void maxpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
+  multiaxpy_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, coef, w, from_zero, part, 0); ++h->nlaunch;
+}
+void maxpy(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
+  if (nv <= 4) maxpy_t<4>(h, nv, V, coef, w, from_zero, part);
+  else if (nv <= 8) maxpy_t<8>(h, nv, V, coef, w, from_zero, part);
+  else if (nv <= 16) maxpy_t<16>(h, nv, V, coef, w, from_zero, part);
+  else maxpy_t<32>(h, nv, V, coef, w, from_zero, part);
+}
+void reduce(msp_handle* h, int nv, double* out, const double* addend, double* raw, int sqrt_index) {
+  // raw (optional) receives the plain sums, out = addend + sums
+  if (raw) {
+    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, nv, h->part, raw, nullptr, sqrt_index);
+    ++h->nlaunch;
+  }
+  reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, nv, h->part, out, addend, sqrt_index); ++h->nlaunch;
+}
+
+// ||w||^2 -> out[0] = ||w||
+void norm_dev(msp_handle* h, const double* w, double* out) {
+  multidot_t<4>(h, 1, w, w);
+  reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
+}
+
+// One Arnoldi step j: z = B v_j; w = A z (into V[j+1]); orthogonalise (CGS2 or MGS);
+// hcol[0..j+1] = H(:, j); V[j+1] normalised; hcol copied to pinned host memory.
+void arnoldi_step(msp_handle* h, int j) {
+  const size_t N = h->N;
+  double* vj = h->V + (size_t)j * N;
+  double* w = h->V + (size_t)(j + 1) * N;
+  msp_apply_dev(h, vj, h->z);
+  launch_spmv(h, 0, h->z, nullptr, w);
+  const int nv = j + 1;
+  if (h->prm.orth == 0) {
+    multidot(h, nv, h->V, w);
+    reduce(h, nv, h->dh1, nullptr, nullptr, -1);                 // h1
+    maxpy(h, nv, h->V, h->dh1, w, 0, nullptr);                   // w -= V h1
+    multidot(h, nv, h->V, w);
+    reduce(h, nv, h->hcol, h->dh1, h->dh2, -1);                  // h2; hcol = h1 + h2
+    maxpy(h, nv, h->V, h->dh2, w, 0, h->part);                   // w -= V h2, ||w||^2 partials
+    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
+  } else {
+    for (int i = 0; i < nv; ++i) {
+      multidot_t<4>(h, 1, h->V + (size_t)i * N, w);
+      reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + i, nullptr, -1); ++h->nlaunch;
+      maxpy_t<4>(h, 1, h->V + (size_t)i * N, h->hcol + i, w, 0, (i == nv - 1) ? h->part : nullptr);
+    }
+    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
+  }
+  scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + nv, w); ++h->nlaunch;
+  CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
+}
+
+void ensure_basis(msp_handle* h, int m) {
+  if (h->V_m >= m) return;
+  h->V = h->dalloc<double>((size_t)(m + 1) * h->N);
+  h->V_m = m;
+  for (auto g : h->graphs) if (g) cudaGraphExecDestroy(g);
+  h->graphs.clear();
+  h->graphs_m = -1;
+}
+
+void run_step(msp_handle* h, int j, int m) {
+  if (!h->prm.use_graphs) {
+    arnoldi_step(h, j);
+    return;
+  }
+  if (h->graphs_m != m) {
+    for (auto g : h->graphs) if (g) cudaGraphExecDestroy(g);
+    h->graphs.assign(m, nullptr);
+    h->graphs_m = m;
+  }
+  if (!h->graphs[j]) {
+    cudaGraph_t graph;
+    const int64_t before = h->nlaunch;
+    CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    arnoldi_step(h, j);
+    CK(cudaStreamEndCapture(h->s, &graph));
+    if ((int)h->graph_kernels.size() < m) h->graph_kernels.assign(m, 0);
+    h->graph_kernels[j] = h->nlaunch - before;
+    h->nlaunch = before;
+    CK(cudaGraphInstantiate(&h->graphs[j], graph, 0));
+    if (j == 0) {
+      h->kernels_per_step = (int)h->graph_kernels[j];
+    }
+    cudaGraphDestroy(graph);
+  }
+  CK(cudaGraphLaunch(h->graphs[j], h->s));
+  h->nlaunch += h->graph_kernels[j];
+}
+
+// GMRES(m), right preconditioned (R8); vectors internal order; xin holds x0 and
+// the solution; bin holds b.
+msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double* final_rel,
+                 double* hist, int cap, int* hlen) {
+  const size_t N = h->N;
+  ensure_basis(h, m);
+  int it = 0, hl = 0;
+  auto push = [&](double v) { if (hist && hl < cap) hist[hl] = v; ++hl; };
+  norm_dev(h, h->bin, h->hcol);
+  CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  const double bnorm = h->hpin[0];
+  *iters = 0;
+  if (bnorm == 0.0) {
+    CK(cudaMemsetAsync(h->xin, 0, sizeof(double) * N, h->s));
+    *final_rel = 0.0;
+    if (hlen) *hlen = 0;
+    return MSP_OK;
+  }
+  launch_spmv(h, 1, h->xin, h->bin, h->r);                    // r = b - A x0
+  norm_dev(h, h->r, h->hcol);
+  CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  double beta = h->hpin[0];
+  double rel = beta / bnorm;
+  msp_status status = MSP_OK;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gam(m + 1), y(m);
+  if (rel > tol) {
+    while (true) {
+      scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, h->r, h->hcol, h->V); ++h->nlaunch;   // v_0 = r / beta
+      std::fill(gam.begin(), gam.end(), 0.0);
+      gam[0] = beta;
+      int k = 0;
+      for (int j = 0; j < m; ++j) {
+        run_step(h, j, m);
+        CK(cudaStreamSynchronize(h->s));
+        auto Hc = [&](int i) -> double& { return H[(size_t)i * m + j]; };
+        for (int i = 0; i <= j + 1; ++i) Hc(i) = h->hpin[i];
+        const double hn = Hc(j + 1);
+        ++it;
+        for (int i = 0; i < j; ++i) {
+          const double a = Hc(i), c = Hc(i + 1);
+          Hc(i) = cs[i] * a + sn[i] * c;
+          Hc(i + 1) = -sn[i] * a + cs[i] * c;
+        }
+        const double rho = std::hypot(Hc(j), Hc(j + 1));
+        cs[j] = Hc(j) / rho;
+        sn[j] = Hc(j + 1) / rho;
+        Hc(j) = rho;
+        Hc(j + 1) = 0.0;
+        gam[j + 1] = -sn[j] * gam[j];
+        gam[j] = cs[j] * gam[j];
+        const double est = std::fabs(gam[j + 1]) / bnorm;
+        push(est);
+        k = j + 1;
+        if (est <= tol || hn < 1e-14 * bnorm || it >= maxit) break;
+      }
+      for (int i = k - 1; i >= 0; --i) {
+        double s = 0.0;
+        for (int l = i + 1; l < k; ++l) s += H[(size_t)i * m + l] * y[l];
+        y[i] = (gam[i] - s) / H[(size_t)i * m + i];
+      }
+      // u = V_k y ; x += B u ; r = b - A x
+      CK(cudaMemcpyAsync(h->dh1, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, h->s));
+      maxpy(h, k, h->V, h->dh1, h->u, 1, nullptr);
+      msp_apply_dev(h, h->u, h->z);
+      axpy_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, 1.0, h->z, h->xin); ++h->nlaunch;
+      launch_spmv(h, 1, h->xin, h->bin, h->r);
+      norm_dev(h, h->r, h->hcol);
+      CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
+      CK(cudaStreamSynchronize(h->s));
+      beta = h->hpin[0];
+      rel = beta / bnorm;
+      push(rel);
+      if (rel <= tol) break;
+      if (it >= maxit) { status = MSP_ENOCONV; break; }
+    }
+  }
+  *iters = it;
+  *final_rel = rel;
+  if (hlen) *hlen = std::min(hl, cap);
+  return status;
+}
+
+msp_status fail(msp_handle* h, msp_status st, const std::string& msg) {
+  if (h) h->err = msg;
+  g_last_error = msg;
+  return st;
+}
+
+template <class F>
+msp_status guarded(msp_handle* h, F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    return fail(h, e.e == cudaErrorMemoryAllocation ? MSP_ENOMEM : MSP_ECUDA,
+                std::string("CUDA: ") + cudaGetErrorString(e.e) + " in " + e.where);
+  } catch (const std::pair<int, std::string>& e) {
+    return fail(h, (msp_status)e.first, e.second);
+  } catch (const std::bad_alloc&) {
+    return fail(h, MSP_ENOMEM, "host allocation failed");
+  }
+}
+
+// copy a caller vector (host or device, natural order) into internal order (dst)
+void to_internal(msp_handle* h, const double* src, double* dst, size_t count_cells, int b) {
+  const size_t N = count_cells * b;
+  if (is_device_ptr(src)) {
+    CK(cudaMemcpyAsync(h->io, src, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
+  } else {
+    CK(cudaMemcpyAsync(h->io, src, sizeof(double) * N, cudaMemcpyHostToDevice, h->s));
+  }
+  switch (b) {
+#define CASE(BV) case BV: perm_gather_kernel<BV><<<nblk(N, 256), 256, 0, h->s>>>(h->n, h->d_order, h->io, dst); ++h->nlaunch; break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+}
+void from_internal(msp_handle* h, const double* src, double* dst, int b) {
+  const size_t N = (size_t)h->n * b;
+  switch (b) {
+#define CASE(BV) case BV: perm_scatter_kernel<BV><<<nblk(N, 256), 256, 0, h->s>>>(h->n, h->d_order, src, h->io); ++h->nlaunch; break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  if (is_device_ptr(dst)) CK(cudaMemcpyAsync(dst, h->io, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->s));
+  else CK(cudaMemcpyAsync(dst, h->io, sizeof(double) * N, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+extern "C" {
+
+void msp_config_default(msp_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->coarsest_max_dof = 10000;
+  c->max_levels = 20;
+  c->pre_sweeps = 1;
+  c->post_sweeps = 1;
+  c->pair_passes = 2;
+  c->decoupling = 2;
+  c->bilu_order = 1;
+  c->stages = 2;
+  c->orth = 0;
+  c->use_graphs = 1;
+}
+
+const char* msp_last_error(const msp_handle* h) { return h ? h->err.c_str() : g_last_error.c_str(); }
+
+msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda_stream, msp_handle** out) {
+  if (!out) return fail(nullptr, MSP_EINVAL, "msp_setup: out is NULL");
+  *out = nullptr;
+  msp_config c;
+  msp_config_default(&c);
+  if (cfg) c = *cfg;
+  if (c.stages != 2) return fail(nullptr, MSP_EINVAL, "msp_setup: only stages=2 (P,R) is implemented on the GPU path");
+  if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1)
+    return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
+  std::unique_ptr<msp_handle> h(new msp_handle);
+  h->cfg = c;
+  h->prm = params_of(&c);
+  msp::BlockMat M;
+  std::string err;
+  msp_status st = read_bsr(A, nc, M, err);
+  if (st) return fail(nullptr, st, err);
+  st = guarded(h.get(), [&]() -> msp_status {
+    CK(cudaGetDevice(&h->device));
+    if (A->device >= 0) { CK(cudaSetDevice(A->device)); h->device = A->device; }
+    CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    if (cuda_stream) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, (cudaStream_t)cuda_stream));
+      CK(cudaStreamWaitEvent(h->s, e, 0));
+      cudaEventDestroy(e);
+    }
+    do_setup(h.get(), M);
+    return MSP_OK;
+  });
+  if (st) {
+    g_last_error = h->err;
+    h->free_all();
+    return st;
+  }
+  *out = h.release();
+  return MSP_OK;
+}
+
+msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_iterations, int mu,
+                      int* did_setup) {
+  if (!h) return fail(nullptr, MSP_EINVAL, "msp_update: NULL handle");
+  msp::BlockMat M;
+  std::string err;
+  msp_status st = read_bsr(A_new, h->nc, M, err);
+  if (st) return fail(h, st, err);
+  const bool dims_changed = (M.n != h->n) || ((int64_t)M.ci.size() != h->nnzb);
+  // ASMSP rule (Remark 2)
+  const bool rebuild = (iota <= 1) || dims_changed || (last_iterations > mu);
+  if (did_setup) *did_setup = rebuild ? 1 : 0;
+  return guarded(h, [&]() -> msp_status {
+    if (rebuild) {
+      do_setup(h, M);
+      return MSP_OK;
+    }
+    // reuse: keep W, hierarchy and BILU factors; refresh A for SpMV / Alg. 1 residuals
+    const int bb = h->b * h->b;
+    std::vector<double> Ap(M.v.size()), tmp(M.v.size());
+    for (size_t e = 0; e < h->src_entry.size(); ++e)
+      std::memcpy(&Ap[e * bb], &M.v[(size_t)h->src_entry[e] * bb], sizeof(double) * bb);
+    transpose_blocks(Ap.data(), tmp.data(), h->src_entry.size(), h->b);
+    CK(cudaMemcpyAsync(h->Aval, tmp.data(), sizeof(double) * tmp.size(), cudaMemcpyHostToDevice, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    h->st.reuse_calls++;
+    return MSP_OK;
+  });
+}
+
+msp_status msp_solve(msp_handle* h, const double* b, double* x, double tol, int restart, int maxit,
+                     int* iterations, double* final_rel_res, double* resid_hist, int hist_cap,
+                     int* hist_len) {
+  if (!h || !b || !x || restart < 1 || restart > kMaxV - 2 || maxit < 0)
+    return fail(h, MSP_EINVAL, "msp_solve: invalid arguments (1 <= restart <= 30)");
+  int it_dummy = 0;
+  double fr_dummy = 0.0;
+  if (!iterations) iterations = &it_dummy;
+  if (!final_rel_res) final_rel_res = &fr_dummy;
+  return guarded(h, [&]() -> msp_status {
+    CK(cudaEventRecord(h->ev0, h->s));
+    to_internal(h, b, h->bin, h->n, h->b);
+    to_internal(h, x, h->xin, h->n, h->b);
+    msp_status st = gmres(h, tol, restart, maxit, iterations, final_rel_res, resid_hist, hist_cap, hist_len);
+    from_internal(h, h->xin, x, h->b);
+    CK(cudaEventRecord(h->ev1, h->s));
+    CK(cudaEventSynchronize(h->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->st.solve_seconds += ms * 1e-3;
+    return st;
+  });
+}
+
+msp_status msp_apply(msp_handle* h, const double* g, double* w) {
+  if (!h || !g || !w) return fail(h, MSP_EINVAL, "msp_apply: NULL argument");
+  return guarded(h, [&]() -> msp_status {
+    to_internal(h, g, h->bin, h->n, h->b);
+    msp_apply_dev(h, h->bin, h->z);
+    from_internal(h, h->z, w, h->b);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_spmv(msp_handle* h, const double* x, double* y) {
+  if (!h || !x || !y) return fail(h, MSP_EINVAL, "msp_spmv: NULL argument");
+  return guarded(h, [&]() -> msp_status {
+    launch_spmv(h, 0, x, nullptr, y);
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, int ascending) {
+  if (!h || level < 0 || level >= (int)h->lv.size()) return fail(h, MSP_EINVAL, "msp_pgs_sweep: bad level");
+  return guarded(h, [&]() -> msp_status {
+    DevLevel& L = h->lv[level];
+    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, b, L.b, 1); ++h->nlaunch;
+    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, x, L.x, 1); ++h->nlaunch;
+    pgs_sweep(h, L, ascending != 0, false);
+    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, L.x, x, 0); ++h->nlaunch;
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_vcycle(msp_handle* h, const double* r, double* x) {
+  if (!h || !r || !x) return fail(h, MSP_EINVAL, "msp_vcycle: NULL argument");
+  return guarded(h, [&]() -> msp_status {
+    if (h->lv.empty()) {
+      CK(cudaMemcpyAsync(h->bL, r, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
+      vcycle(h, 0);
+      CK(cudaMemcpyAsync(x, h->xL, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
+    } else {
+      DevLevel& L = h->lv[0];
+      scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, r, L.b, 1); ++h->nlaunch;
+      vcycle(h, 0);
+      scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, L.x, x, 0); ++h->nlaunch;
+    }
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x) {
+  if (!h || !r || !x) return fail(h, MSP_EINVAL, "msp_bilu_apply: NULL argument");
+  return guarded(h, [&]() -> msp_status {
+    to_internal(h, r, h->r, h->n, h->b);
+    CK(cudaMemsetAsync(h->wp, 0, sizeof(double) * h->n, h->s));
+    launch_bilu(h, h->r, h->wp, h->z);
+    from_internal(h, h->z, x, h->b);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_get_order(const msp_handle* h, int32_t* order) {
+  if (!h || !order) return MSP_EINVAL;
+  std::memcpy(order, h->order.data(), sizeof(int32_t) * h->n);
+  return MSP_OK;
+}
+
+msp_status msp_get_stats(const msp_handle* h, msp_stats* out) {
+  if (!h || !out) return MSP_EINVAL;
+  *out = h->st;
+  for (size_t l = 0; l < h->level_n.size() && l < 24; ++l) {
+    out->level_n[l] = h->level_n[l];
+    out->level_nnz[l] = h->level_nnz[l];
+    out->level_colors[l] = h->level_colors[l];
+  }
+  out->device_bytes = h->bytes;
+  out->kernels_per_iter = h->kernels_per_step;
+  return MSP_OK;
+}
+
+void msp_destroy(msp_handle* h) {
+  if (!h) return;
+  h->free_all();
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->s) cudaStreamDestroy(h->s);
+  delete h;
+}
+
+int64_t msp_kernel_launches(const msp_handle* h) { return h ? h->nlaunch : 0; }
+
+msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,
+                           double* bytes_per_launch) {
+  if (!h || reps < 1 || !ms_per_launch || !bytes_per_launch) return fail(h, MSP_EINVAL, "msp_time_kernel: bad args");
+  if ((kind == 1) && h->lv.empty()) return fail(h, MSP_EINVAL, "msp_time_kernel: no AMG level 0");
+  return guarded(h, [&]() -> msp_status {
+    const size_t kFlush = (size_t)256 << 20;
+    if (!h->flush) h->flush = h->dalloc<double>(kFlush / sizeof(double));
+    ensure_basis(h, 30);
+    const size_t N = h->N;
+    const double n = h->n, b = h->b, nnzb = (double)h->nnzb;
+    double bytes = 0.0;
+    // deterministic non-trivial inputs
+    CK(cudaMemsetAsync(h->r, 0, sizeof(double) * N, h->s));
+    scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, h->V, h->hcol, h->z); ++h->nlaunch;
+    std::function<void()> fn;
+    switch (kind) {
+      case 0:
+        fn = [&]() { launch_spmv(h, 0, h->xin, nullptr, h->u); };
+        bytes = nnzb * (8 * b * b + 4) + 4 * (n + 1) + 2 * 8 * (double)N;
+        break;
+      case 1: {
+        DevLevel& L = h->lv[0];
+        fn = [&]() { pgs_sweep(h, L, false, false); };
+        const double nnz_off = (double)h->level_nnz[0] - L.n;
+        bytes = 12 * nnz_off + 32.0 * L.n;
+        break;
+      }
+      case 2:
+        fn = [&]() { launch_spmv(h, 2, h->wp, h->bin, h->u); };
+        bytes = nnzb * (8 * b + 4) + 4 * (n + 1) + 8 * n + 2 * 8 * (double)N;
+        break;
+      case 3:
+        fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
+        bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
+        break;
+      case 4:
+        fn = [&]() { multidot(h, 16, h->V, h->u); };
+        bytes = 17.0 * 8 * (double)N;
+        break;
+      case 5:
+        fn = [&]() { vcycle(h, (int)h->lv.size()); };
+        bytes = h->coarse_diag ? 24.0 * h->nL : 8.0 * (double)h->nL * h->nL;
+        break;
+      case 6:
+        fn = [&]() { msp_apply_dev(h, h->bin, h->z); };
+        bytes = 0.0;
+        break;
+      default:
+        throw std::pair<int, std::string>(MSP_EINVAL, "msp_time_kernel: unknown kind");
+    }
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaMemsetAsync(h->flush, r & 0xff, kFlush, h->s));
+      CK(cudaEventRecord(h->ev0, h->s));
+      fn();
+      CK(cudaEventRecord(h->ev1, h->s));
+      CK(cudaEventSynchronize(h->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+      total += ms;
+    }
+    *ms_per_launch = total / reps;
+    *bytes_per_launch = bytes;
+    return MSP_OK;
+  });
+}
+
+// ----------------------------------------------------------- host-setup introspection
+struct msp_host_setup {
+  msp::HostSetup S;
+};
+
+msp_status msp_host_setup_run(const msp_bsr* A, int nc, const msp_config* cfg, msp_host_setup** out) {
+  if (!out) return MSP_EINVAL;
+  *out = nullptr;
+  msp::BlockMat M;
+  std::string err;
+  msp_status st = read_bsr(A, nc, M, err);
+  if (st) return fail(nullptr, st, err);
+  msp_config c;
+  msp_config_default(&c);
+  if (cfg) c = *cfg;
+  std::unique_ptr<msp_host_setup> s(new msp_host_setup);
+  int rc = msp::run_host_setup(M, params_of(&c), s->S, err);
+  if (rc) return fail(nullptr, (msp_status)rc, err);
+  *out = s.release();
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_info(const msp_host_setup* s, int32_t* o) {
+  if (!s || !o) return MSP_EINVAL;
+  o[0] = (int32_t)s->S.lv.size();
+  o[1] = s->S.Ac.n;
+  o[2] = s->S.coarse_diag ? 1 : 0;
+  o[3] = s->S.bilu_ncolor;
+  return MSP_OK;
+}
+
+static const msp::SpMat* level_mat(const msp_host_setup* s, int l) {
+  if (l < 0 || l > (int)s->S.lv.size()) return nullptr;
+  return l < (int)s->S.lv.size() ? &s->S.lv[l].A : &s->S.Ac;
+}
+
+msp_status msp_host_setup_level_dims(const msp_host_setup* s, int l, int32_t* n, int64_t* nnz, int32_t* ncolors) {
+  if (!s) return MSP_EINVAL;
+  const msp::SpMat* A = level_mat(s, l);
+  if (!A) return MSP_EINVAL;
+  *n = A->n;
+  *nnz = A->nnz();
+  *ncolors = l < (int)s->S.lv.size() ? s->S.lv[l].ncolor : 0;
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_level_csr(const msp_host_setup* s, int l, int32_t* ptr, int32_t* col, double* val) {
+  if (!s) return MSP_EINVAL;
+  const msp::SpMat* A = level_mat(s, l);
+  if (!A) return MSP_EINVAL;
+  std::memcpy(ptr, A->rp.data(), sizeof(int32_t) * (A->n + 1));
+  std::memcpy(col, A->ci.data(), sizeof(int32_t) * A->ci.size());
+  std::memcpy(val, A->v.data(), sizeof(double) * A->v.size());
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_level_colors(const msp_host_setup* s, int l, int32_t* color) {
+  if (!s || l < 0 || l >= (int)s->S.lv.size()) return MSP_EINVAL;
+  std::memcpy(color, s->S.lv[l].color.data(), sizeof(int32_t) * s->S.lv[l].color.size());
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_level_agg(const msp_host_setup* s, int l, int32_t* agg) {
+  if (!s || l < 0 || l >= (int)s->S.lv.size()) return MSP_EINVAL;
+  std::memcpy(agg, s->S.lv[l].agg.data(), sizeof(int32_t) * s->S.lv[l].agg.size());
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_weights(const msp_host_setup* s, double* W) {
+  if (!s || !W) return MSP_EINVAL;
+  std::memcpy(W, s->S.W.data(), sizeof(double) * s->S.W.size());
+  return MSP_OK;
+}
+
+msp_status msp_host_setup_order(const msp_host_setup* s, int32_t* order) {
+  if (!s || !order) return MSP_EINVAL;
+  std::memcpy(order, s->S.order.data(), sizeof(int32_t) * s->S.order.size());
+  return MSP_OK;
+}
+
+void msp_host_setup_free(msp_host_setup* s) { delete s; }
+
+msp_status msp_partition_owner(const msp_host_setup* s, int nx, int ny, int nz, int nranks, int32_t* owner) {
+  if (!s || !owner || nranks < 1 || nranks > nz) return MSP_EINVAL;
+  const int64_t plane = (int64_t)nx * ny;
+  const int32_t n = s->S.A.n;
+  if ((int64_t)nx * ny * nz != n) return MSP_EINVAL;
+  std::vector<int32_t> zstart(nranks + 1, 0);
+  const int base = nz / nranks, extra = nz % nranks;
+  for (int r = 0; r < nranks; ++r) zstart[r + 1] = zstart[r] + base + (r < extra ? 1 : 0);
+  auto slab = [&](int32_t c) {
+    const int k = (int)(c / plane);
+    return (int32_t)(std::upper_bound(zstart.begin(), zstart.end(), k) - zstart.begin() - 1);
+  };
+  if (s->S.prm.bilu_order == 0) {
+    for (int32_t c = 0; c < n; ++c) owner[c] = slab(c);
+    return MSP_OK;
+  }
+  const auto& blk = s->S.level1_agg;
+  int32_t nb = 0;
+  for (int32_t v : blk) nb = std::max(nb, v + 1);
+  std::vector<int32_t> lowest(nb, INT32_MAX);
+  for (int32_t c = 0; c < n; ++c) lowest[blk[c]] = std::min(lowest[blk[c]], c);
+  for (int32_t c = 0; c < n; ++c) owner[c] = slab(lowest[blk[c]]);
+  return MSP_OK;
+}
+
+}  // extern "C"
