@@ -76,6 +76,9 @@ typedef struct {
   int32_t stages;            /* 2 = P,R (north_star, default); 3 = N,P,R (full Eq. 21) */
   int32_t orth;              /* 0 CGS2 (default, R8); 1 MGS */
   int32_t use_graphs;        /* 1: replay each Arnoldi step as a CUDA graph (default) */
+  int32_t use_coop;          /* 0 (default): one graph node per PGS-MC color / transfer;
+                                1: whole V-cycle as one cooperative persistent kernel (measured
+                                slower on B200: grid.sync ~1.3 us vs ~1.2 us per graph node) */
   msp_alloc_fn alloc;        /* optional device allocator */
   msp_free_fn free_fn;
   void* alloc_ctx;
@@ -147,13 +150,16 @@ msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, i
 msp_status msp_vcycle(msp_handle* h, const double* r, double* x);
 /* R r: BILU(0) forward/backward substitution (natural order, device). */
 msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x);
-/* Times `reps` launches of one hot-path kernel on the handle's stream with CUDA events,
+/* Times `reps` launches of one hot-path piece on the handle's stream with CUDA events,
  * flushing L2 (a 256 MB device write) before each launch.  Returns the mean device
  * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory
  * traffic, each vector counted once).  kind: 0 a2 BSR SpMV; 1 a4 level-0 PGS-MC sweep
  * (all colors, descending = full work per color); 2 a8 pressure-column residual;
  * 3 a9 BILU(0) apply (all colors); 4 a10 CGS2 multidot over 16 basis vectors;
- * 5 a6 coarsest dense-inverse GEMV; 6 one whole MSP application (bytes = 0).
+ * 5 a6 coarsest dense-inverse GEMV; 6 one whole MSP application; 7 one V-cycle B_P;
+ * 8 BILU apply; 9 one whole Arnoldi step (j = 15); 10 the CGS2 of step 15 (bytes = 0 for
+ * kinds 6-10).  kind | 0x100: no L2 flush (warm caches).  Each piece is captured once
+ * into a CUDA graph and replayed (as in the solve); the first replay is a warm-up.
  * Scratch contents of the handle are overwritten. */
 msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,
                            double* bytes_per_launch);

@@ -33,6 +33,7 @@ class Config(ctypes.Structure):
                 ("pair_passes", ctypes.c_int32), ("decoupling", ctypes.c_int32),
                 ("bilu_order", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("orth", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+                ("use_coop", ctypes.c_int32),
                 ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
 
     @classmethod
@@ -70,7 +71,8 @@ _lib.msp_kernel_launches.restype = ctypes.c_int64
 _lib.msp_kernel_launches.argtypes = [ctypes.c_void_p]
 
 KERNEL_KINDS = {"a2_bsr_spmv": 0, "a4_pgs_sweep_l0": 1, "a8_pcol_residual": 2, "a9_bilu_apply": 3,
-                "a10_multidot16": 4, "a6_coarse_gemv": 5, "msp_apply": 6}
+                "a10_multidot16": 4, "a6_coarse_gemv": 5, "msp_apply": 6, "vcycle": 7,
+                "bilu": 8, "arnoldi_step15": 9, "cgs2_step15": 10}
 _lib.msp_host_setup_free.argtypes = [ctypes.c_void_p]
 
 
@@ -116,7 +118,10 @@ class _TorchAllocator:
             return None
 
     def _free(self, ptr, ctx):
-        self.torch.cuda.caching_allocator_delete(int(ptr))
+        try:
+            self.torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:          # interpreter teardown: torch already unloaded
+            pass
 
 
 class MspSolver:
@@ -221,10 +226,12 @@ class MspSolver:
         self._check(_lib.msp_get_order(self._h, _ptr(o)))
         return o
 
-    def time_kernel(self, kind, reps=10):
+    def time_kernel(self, kind, reps=10, flush=True):
         """(ms per launch, algorithmic bytes per launch) of one hot-path kernel, L2 flushed
         before each launch (CUDA events on the solver's stream)."""
         k = KERNEL_KINDS[kind] if isinstance(kind, str) else int(kind)
+        if not flush:
+            k |= 0x100
         ms = ctypes.c_double(0)
         by = ctypes.c_double(0)
         self._check(_lib.msp_time_kernel(self._h, k, reps, ctypes.byref(ms), ctypes.byref(by)))

@@ -25,7 +25,9 @@ __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
 // block as one contiguous B*8-byte segment.  x of the neighbour is loaded once per
 // lane (component q) and broadcast with shuffles.
 //   MODE 0: y = A x          MODE 1: y = g - A x (residual, Alg. 1 lines 3/5)
-//   MODE 2: y = g - A[:,P] xp  (a8: pressure column only, xp per cell)
+//   MODE 2: y = g - A[:,P] xp  (a8: pressure column only, xp per cell); `val` is then
+//           the contiguous pressure-column array Pcol[e*B + q] = A_e[q][0] (one 32 B
+//           sector per block for b=4, consecutive blocks contiguous).
 // ---------------------------------------------------------------------------
 template <int B, int MODE>
 __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restrict__ rp,
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
     for (int e = e0; e < e1; ++e) {
       const int c = ldg(ci + e);
       const double xc = ldg(x + c);
-      if (q < B) acc = fma(ldg(val + (size_t)e * BB + q), xc, acc);
+      if (q < B) acc = fma(ldg(val + (size_t)e * B + q), xc, acc);
     }
   } else {
 #pragma unroll 2

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -16,7 +17,7 @@
 #include <vector>
 
 #include "../../include/msp.h"
-#include "kernels.cuh"
+#include "coop.cuh"
 #include "setup.h"
 
 using namespace mspk;
@@ -54,6 +55,7 @@ struct DevLevel {
   int32_t* inv = nullptr;            // permuted -> natural
   double *b = nullptr, *x = nullptr, *r = nullptr;
   int64_t nnz_alloc = 0;
+  int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
 };
 
 }  // namespace
@@ -75,7 +77,7 @@ struct msp_handle {
   std::vector<int32_t> src_entry;    // permuted entry -> natural entry
   // BSR (internal positions), shared pattern for A and the BILU factors
   int32_t *rp = nullptr, *ci = nullptr, *dg = nullptr, *d_order = nullptr;
-  double *Aval = nullptr, *Fval = nullptr, *W = nullptr;
+  double *Aval = nullptr, *Fval = nullptr, *W = nullptr, *Pcol = nullptr;
   int32_t* l0_of_cell = nullptr;
   // ABMC blocks
   int32_t bilu_ncolor = 0;
@@ -84,6 +86,8 @@ struct msp_handle {
   // AMG
   std::vector<DevLevel> lv;
   int32_t nL = 0, ldA = 0;
+  VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
+  int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
   bool coarse_diag = false;
   double *Ainv = nullptr, *cdiag = nullptr, *bL = nullptr, *xL = nullptr;
   // work vectors
@@ -158,6 +162,7 @@ msp::Params params_of(const msp_config* c) {
   p.stages = c->stages;
   p.orth = c->orth;
   p.use_graphs = c->use_graphs;
+  p.use_coop = c->use_coop;
   return p;
 }
 
@@ -283,6 +288,18 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
     }
   }
   L.nnz_alloc = slice_off[L.nslices];
+  {
+    std::vector<int32_t> rs(n), rw(n);
+    for (int32_t s = 0; s < L.nslices; ++s)
+      for (int32_t p = slice_row[s]; p < slice_row[s + 1]; ++p) {
+        rs[p] = slice_off[s] + (p - slice_row[s]);
+        rw[p] = (slice_off[s + 1] - slice_off[s]) / kSell;
+      }
+    L.row_start = h->upload(rs);
+    L.row_width = h->upload(rw);
+    L.d_color_row = h->upload(L.color_row);
+    L.d_color_slice = h->upload(L.color_slice);
+  }
   L.slice_row = h->upload(slice_row);
   L.slice_off = h->upload(slice_off);
   L.col = h->upload(col);
@@ -330,6 +347,10 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
       std::memcpy(&Ap[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
     transpose_blocks(Ap.data(), tmp.data(), ci.size(), b);
     h->Aval = h->upload(tmp);
+    std::vector<double> pc(ci.size() * b);
+    for (size_t e = 0; e < ci.size(); ++e)
+      for (int q = 0; q < b; ++q) pc[e * b + q] = Ap[e * bb + q * b];
+    h->Pcol = h->upload(pc);
     CK(cudaStreamSynchronize(h->s));
   }
   {
@@ -450,6 +471,58 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->st.levels = L;
   h->st.n_coarsest = h->nL;
   h->st.bilu_colors = h->bilu_ncolor;
+  // cooperative V-cycle parameters
+  if (h->prm.use_coop && L <= kMaxLevels) {
+    VParams vp;
+    std::memset(&vp, 0, sizeof(vp));
+    vp.L = L;
+    vp.pre = h->prm.pre_sweeps;
+    vp.post = h->prm.post_sweeps;
+    vp.nL = h->nL;
+    vp.ldA = h->ldA;
+    vp.coarse_diag = h->coarse_diag ? 1 : 0;
+    vp.Ainv = h->Ainv;
+    vp.cdiag = h->cdiag;
+    vp.bL = h->bL;
+    vp.xL = h->xL;
+    for (int l = 0; l < L; ++l) {
+      const DevLevel& D = h->lv[l];
+      LevelDev& E = vp.lv[l];
+      E.n = D.n;
+      E.ncolor = D.ncolor;
+      E.nslices = D.nslices;
+      E.fuse_rr = (l > 0) ? 1 : 0;
+      E.n_next = (l + 1 < L) ? h->lv[l + 1].n : h->nL;
+      E.color_row = D.d_color_row;
+      E.color_slice = D.d_color_slice;
+      E.slice_row = D.slice_row;
+      E.slice_off = D.slice_off;
+      E.col = D.col;
+      E.val = D.val;
+      E.diag = D.diag;
+      E.agg = D.agg;
+      E.pt_ptr = D.pt_ptr;
+      E.pt_idx = D.pt_idx;
+      E.row_start = D.row_start;
+      E.row_width = D.row_width;
+      E.b = D.b;
+      E.x = D.x;
+      E.r = D.r;
+    }
+    h->dvp = h->dalloc<VParams>(1);
+    CK(cudaMemcpyAsync(h->dvp, &vp, sizeof(vp), cudaMemcpyHostToDevice, h->s));
+    int nb = 0, nsm = 0;
+    h->coop_tpb = (h->coop_tpb == 256 || h->coop_tpb == 512) ? h->coop_tpb : 1024;
+    if (h->coop_tpb == 1024) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<1024>, 1024, 0));
+    else if (h->coop_tpb == 512) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<512>, 512, 0));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<256>, 256, 0));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    int bps = std::min(nb, h->coop_bps > 0 ? h->coop_bps : 1);
+    h->coop_grid = std::max(1, bps) * nsm;
+    CK(cudaStreamSynchronize(h->s));
+  } else {
+    h->dvp = nullptr;
+  }
 }
 
 // ----------------------------------------------------------------- launches
@@ -465,8 +538,9 @@ void launch_spmv_t(cudaStream_t s, int mode, int n, const int* rp, const int* ci
 
 void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
   ++h->nlaunch;
+  const double* val = (mode == 2) ? h->Pcol : h->Aval;
   switch (h->b) {
-#define CASE(BV) case BV: launch_spmv_t<BV>(h->s, mode, h->n, h->rp, h->ci, h->Aval, x, g, y); break;
+#define CASE(BV) case BV: launch_spmv_t<BV>(h->s, mode, h->n, h->rp, h->ci, val, x, g, y); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -557,10 +631,22 @@ void vcycle(msp_handle* h, int l) {
 double* level0_b(msp_handle* h) { return h->lv.empty() ? h->bL : h->lv[0].b; }
 double* level0_x(msp_handle* h) { return h->lv.empty() ? h->xL : h->lv[0].x; }
 
+void vcycle_any(msp_handle* h) {
+  if (h->dvp) {
+    void* args[] = {(void*)&h->dvp};
+    void* fn = (h->coop_tpb == 1024) ? (void*)vcycle_coop_kernel<1024>
+             : (h->coop_tpb == 512) ? (void*)vcycle_coop_kernel<512> : (void*)vcycle_coop_kernel<256>;
+    CK(cudaLaunchCooperativeKernel(fn, h->coop_grid, h->coop_tpb, args, 0, h->s));
+    ++h->nlaunch;
+  } else {
+    vcycle(h, 0);
+  }
+}
+
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
   launch_restrict_pressure(h, g, level0_b(h));                        // a3: r_p = W^T g
-  vcycle(h, 0);                                                        // a4-a7: B_P
+  vcycle_any(h);                                                       // a4-a7: B_P
   gather_kernel<<<nblk(h->n, 256), 256, 0, h->s>>>(h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
   launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
   launch_bilu(h, h->r, h->wp, h->z == z ? z : z);                      // a9: z = Pi_P x_p + R r
@@ -817,6 +903,7 @@ void msp_config_default(msp_config* c) {
   c->stages = 2;
   c->orth = 0;
   c->use_graphs = 1;
+  c->use_coop = 0;
 }
 
 const char* msp_last_error(const msp_handle* h) { return h ? h->err.c_str() : g_last_error.c_str(); }
@@ -832,6 +919,8 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
   std::unique_ptr<msp_handle> h(new msp_handle);
   h->cfg = c;
+  if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
+  if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
@@ -885,6 +974,10 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
       std::memcpy(&Ap[e * bb], &M.v[(size_t)h->src_entry[e] * bb], sizeof(double) * bb);
     transpose_blocks(Ap.data(), tmp.data(), h->src_entry.size(), h->b);
     CK(cudaMemcpyAsync(h->Aval, tmp.data(), sizeof(double) * tmp.size(), cudaMemcpyHostToDevice, h->s));
+    std::vector<double> pc(h->src_entry.size() * h->b);
+    for (size_t e = 0; e < h->src_entry.size(); ++e)
+      for (int q = 0; q < h->b; ++q) pc[e * h->b + q] = Ap[e * bb + q * h->b];
+    CK(cudaMemcpyAsync(h->Pcol, pc.data(), sizeof(double) * pc.size(), cudaMemcpyHostToDevice, h->s));
     CK(cudaStreamSynchronize(h->s));
     h->st.reuse_calls++;
     return MSP_OK;
@@ -952,12 +1045,12 @@ msp_status msp_vcycle(msp_handle* h, const double* r, double* x) {
   return guarded(h, [&]() -> msp_status {
     if (h->lv.empty()) {
       CK(cudaMemcpyAsync(h->bL, r, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
-      vcycle(h, 0);
+      vcycle_any(h);
       CK(cudaMemcpyAsync(x, h->xL, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
     } else {
       DevLevel& L = h->lv[0];
       scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, r, L.b, 1); ++h->nlaunch;
-      vcycle(h, 0);
+      vcycle_any(h);
       scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, L.x, x, 0); ++h->nlaunch;
     }
     CK(cudaStreamSynchronize(h->s));
@@ -1009,6 +1102,8 @@ int64_t msp_kernel_launches(const msp_handle* h) { return h ? h->nlaunch : 0; }
 msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,
                            double* bytes_per_launch) {
   if (!h || reps < 1 || !ms_per_launch || !bytes_per_launch) return fail(h, MSP_EINVAL, "msp_time_kernel: bad args");
+  const bool flush_l2 = (kind & 0x100) == 0;
+  kind &= 0xff;
   if ((kind == 1) && h->lv.empty()) return fail(h, MSP_EINVAL, "msp_time_kernel: no AMG level 0");
   return guarded(h, [&]() -> msp_status {
     const size_t kFlush = (size_t)256 << 20;
@@ -1053,20 +1148,57 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         fn = [&]() { msp_apply_dev(h, h->bin, h->z); };
         bytes = 0.0;
         break;
+      case 7:
+        fn = [&]() { vcycle_any(h); };
+        bytes = 0.0;
+        break;
+      case 8:
+        fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
+        bytes = 0.0;
+        break;
+      case 9:
+        fn = [&]() { arnoldi_step(h, 15); };
+        bytes = 0.0;
+        break;
+      case 10:                                   // CGS2 of step j=15 alone
+        fn = [&]() {
+          double* w = h->V + (size_t)16 * N;
+          multidot(h, 16, h->V, w);
+          reduce(h, 16, h->dh1, nullptr, nullptr, -1);
+          maxpy(h, 16, h->V, h->dh1, w, 0, nullptr);
+          multidot(h, 16, h->V, w);
+          reduce(h, 16, h->hcol, h->dh1, h->dh2, -1);
+          maxpy(h, 16, h->V, h->dh2, w, 0, h->part);
+          reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + 16, nullptr, 0);
+          scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + 16, w);
+        };
+        bytes = 0.0;
+        break;
       default:
         throw std::pair<int, std::string>(MSP_EINVAL, "msp_time_kernel: unknown kind");
     }
+    // replay the piece as a CUDA graph, exactly as inside the Arnoldi-step graphs
+    cudaGraph_t graph;
+    cudaGraphExec_t gexec;
+    const int64_t before = h->nlaunch;
+    CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    fn();
+    CK(cudaStreamEndCapture(h->s, &graph));
+    h->nlaunch = before;
+    CK(cudaGraphInstantiate(&gexec, graph, 0));
+    cudaGraphDestroy(graph);
     double total = 0.0;
-    for (int r = 0; r < reps; ++r) {
-      CK(cudaMemsetAsync(h->flush, r & 0xff, kFlush, h->s));
+    for (int r = 0; r < reps + 1; ++r) {
+      if (flush_l2) CK(cudaMemsetAsync(h->flush, r & 0xff, kFlush, h->s));
       CK(cudaEventRecord(h->ev0, h->s));
-      fn();
+      CK(cudaGraphLaunch(gexec, h->s));
       CK(cudaEventRecord(h->ev1, h->s));
       CK(cudaEventSynchronize(h->ev1));
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-      total += ms;
+      if (r > 0) total += ms;                  // first replay = warm-up
     }
+    cudaGraphExecDestroy(gexec);
     *ms_per_launch = total / reps;
     *bytes_per_launch = bytes;
     return MSP_OK;

@@ -102,11 +102,12 @@ def test_pgs_sweep_parity_every_level(asc):
 
 # ------------------------------------------------------------------ V-cycle, BILU, MSP
 @pytest.mark.parametrize("kw", [dict(coarsest_max_dof=200), dict(coarsest_max_dof=200, pair_passes=1),
-                                dict()])
+                                dict(), dict(coarsest_max_dof=200, use_coop=0),
+                                dict(coarsest_max_dof=200, pre_sweeps=2, post_sweeps=2)])
 def test_vcycle_parity(kw):
     p = gen.make_config("C2", nx=40, ny=30, nz=6)
     s = solver(p, **kw)
-    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], **kw)
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], **{k: v for k, v in kw.items() if k != "use_coop"})
     r = gen.random_vector(p["n"], 7)
     ref = O.vcycle(r)
     xd = torch.zeros(p["n"], dtype=torch.float64, device="cuda")
@@ -137,7 +138,8 @@ def test_bilu_and_msp_apply_parity(kw):
 # ------------------------------------------------------------------ full solve
 def check_solve(p, tol=1e-6, restart=30, **kw):
     s = solver(p, **kw)
-    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], **{k: v for k, v in kw.items() if k != "use_graphs"})
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"],
+                   **{k: v for k, v in kw.items() if k not in ("use_graphs", "use_coop")})
     o = O.solve(p["rhs"], tol=tol, restart=restart)
     r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=tol, restart=restart)
     x = r["x"].cpu().numpy()
@@ -158,6 +160,8 @@ def check_solve(p, tol=1e-6, restart=30, **kw):
     ("C1", {}, dict(coarsest_max_dof=50)),
     ("C1", {}, dict(coarsest_max_dof=50, bilu_order=0)),
     ("C1", {}, dict(coarsest_max_dof=50, use_graphs=0)),
+    ("C1", {}, dict(coarsest_max_dof=50, use_coop=0)),
+    ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100, use_coop=0)),
     ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100)),
     ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100)),
     ("C3", dict(nx=12, ny=44, nz=17), dict(coarsest_max_dof=300)),
