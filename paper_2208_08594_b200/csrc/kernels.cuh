@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
   double acc = 0.0;
   const unsigned mask = (TS == 32) ? 0xffffffffu : (((1u << TS) - 1u) << base);
   if (MODE == 2) {
+#pragma unroll 4
     for (int e = e0; e < e1; ++e) {
       const int c = ldg(ci + e);
       const double xc = ldg(x + c);
@@ -282,6 +283,128 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
 }
 
 // ---------------------------------------------------------------------------
+// a9 v2: BILU(0) color phase with one lane group (TS lanes) per CELL of an aggregate
+// block (<= MAXC cells): team = MAXC*TS lanes.  Phase 1 gathers, for every cell of
+// the block in parallel, the EXTERNAL part of its L (forward) or U (backward) sum,
+// whose operands are final (earlier / later colors).  Phase 2 resolves the intra-block
+// triangle (<= MAXC-1 coupled predecessors) in order, passing the finished cell
+// vectors through register shuffles.  Same arithmetic as bilu_color_kernel, only
+// the summation order differs (external before intra-block terms).
+// ---------------------------------------------------------------------------
+template <int B, int MAXC, bool FWD, bool BWD>
+__global__ void __launch_bounds__(128) bilu_block_kernel(int b_first, int b_end,
+                                                         const int* __restrict__ blk_ptr,
+                                                         const int* __restrict__ rp,
+                                                         const int* __restrict__ ci,
+                                                         const int* __restrict__ dg,
+                                                         const double* __restrict__ F,
+                                                         double* v,
+                                                         const double* __restrict__ wp,
+                                                         double* __restrict__ z) {
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  constexpr int TM = MAXC * TS;
+  static_assert(TM <= 32, "team must fit in a warp");
+  constexpr int BB = B * B;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int blk = b_first + gtid / TM;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane % TM;                 // lane within team
+  const int cq = tl / TS, q = tl % TS;      // cell slot, row
+  const int tbase = lane - tl;              // first lane of the team
+  const int cbase = lane - q;               // first lane of this cell group
+  const unsigned tmask = (TM == 32) ? 0xffffffffu : (((1u << TM) - 1u) << tbase);
+  const unsigned cmask = ((1u << TS) - 1u) << cbase;
+  if (blk >= b_end) return;
+  const int c0 = ldg(blk_ptr + blk), c1 = ldg(blk_ptr + blk + 1);
+  const int nc = c1 - c0;
+  const bool valid = cq < nc;
+  const int i = c0 + (valid ? cq : 0);
+  const bool act = valid && q < B;
+  double t = 0.0;                           // working value of row q of cell i
+  if (FWD) {
+    int e = valid ? ldg(rp + i) : 0;
+    const int d = valid ? ldg(dg + i) : 0;
+    double acc = 0.0;
+    for (; e < d; ++e) {                    // external L part: columns before the block
+      const int k = ldg(ci + e);
+      if (k >= c0) break;
+      const double yq = (q < B) ? v[(size_t)k * B + q] : 0.0;
+      const double* blkF = F + (size_t)e * BB;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double yu = __shfl_sync(cmask, yq, cbase + u);
+        if (q < B) acc = fma(ldg(blkF + u * B + q), yu, acc);
+      }
+    }
+    t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
+    // intra-block triangle, cells in ascending order
+#pragma unroll
+    for (int sidx = 0; sidx < MAXC - 1; ++sidx) {
+      // cell sidx is final: broadcast its vector, later cells subtract L_{i,sidx} y_sidx
+      double contrib = 0.0;
+      const bool use = valid && cq > sidx && e < d && ldg(ci + e) == c0 + sidx;
+      const double* blkF = F + (size_t)e * BB;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double yu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
+        if (use && q < B) contrib = fma(ldg(blkF + u * B + q), yu, contrib);
+      }
+      if (use) { t -= contrib; ++e; }
+    }
+    if (act) v[(size_t)i * B + q] = t;
+    __syncwarp(tmask);
+  }
+  if (BWD) {
+    if (!FWD) t = act ? v[(size_t)i * B + q] : 0.0;
+    const int d = valid ? ldg(dg + i) : 0;
+    const int e1 = valid ? ldg(rp + i + 1) : 0;
+    int ei = d + 1;                          // intra U entries: columns inside the block
+    while (ei < e1 && ldg(ci + ei) < c1) ++ei;
+    double acc = 0.0;
+    for (int e = ei; e < e1; ++e) {          // external U part: columns after the block
+      const int j = ldg(ci + e);
+      const double xq = (q < B) ? v[(size_t)j * B + q] : 0.0;
+      const double* blkF = F + (size_t)e * BB;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double xu = __shfl_sync(cmask, xq, cbase + u);
+        if (q < B) acc = fma(ldg(blkF + u * B + q), xu, acc);
+      }
+    }
+    t -= acc;
+    int ep = ei - 1;                         // last intra U entry (descending consumption)
+    const double* Dg = F + (size_t)(valid ? d : 0) * BB;
+    double x = 0.0;
+#pragma unroll
+    for (int sidx = MAXC - 1; sidx >= 0; --sidx) {
+      // cell sidx: x = D~^-1 t (its t is complete once all later cells were applied)
+      double xs = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double tu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
+        if (cq == sidx && act) xs = fma(ldg(Dg + u * B + q), tu, xs);
+      }
+      if (cq == sidx) x = xs;
+      if (sidx == 0) break;
+      // earlier cells subtract U_{i,sidx} x_sidx
+      const bool use = valid && cq < sidx && ep > d && ldg(ci + ep) == c0 + sidx;
+      const double* blkF = F + (size_t)(use ? ep : 0) * BB;
+      double contrib = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double xu = __shfl_sync(tmask, xs, tbase + sidx * TS + u);
+        if (use && q < B) contrib = fma(ldg(blkF + u * B + q), xu, contrib);
+      }
+      if (use) { t -= contrib; --ep; }
+    }
+    if (act) {
+      v[(size_t)i * B + q] = x;
+      z[(size_t)i * B + q] = x + ((q == 0) ? ldg(wp + i) : 0.0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // a10 (K8): GMRES vector kernels with deterministic two-stage reductions.
 // multidot: part[blk][i] = sum over this block's elements of V_i . w, i = 0..nv-1.
 // ---------------------------------------------------------------------------
@@ -382,6 +505,126 @@ __global__ void __launch_bounds__(kRedThreads) multiaxpy_kernel(size_t N, int nv
       for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k];
       part[(size_t)blockIdx.x * kMaxV + slot] = a;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a10 v2: fused CGS2 passes with in-kernel deterministic finalisation.
+// Every block writes its partial sums to part[blk][0..nv); the last block to finish
+// (atomic ticket) sums the partials in fixed block order 0..nblk-1 (deterministic
+// for a fixed grid) and writes out[i] = addend[i] + sum (addend may be null),
+// raw[i] = sum (optional), sqrt applied to out[sqrt_index].  ticket is reset for the
+// next graph replay.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, double* part) {
+  __shared__ double sh[kRedThreads / 32][NV];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (i >= nv) break;
+    double a = acc[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) sh[wid][i] = a;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double a = 0.0;
+    for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k][i];
+    part[(size_t)blockIdx.x * kMaxV + i] = a;
+  }
+}
+
+__device__ __forceinline__ void finalize_partials(int nv, const double* part, double* out,
+                                                  const double* addend, double* raw, int sqrt_index,
+                                                  unsigned* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < nv; i += nw) {
+    double a = 0.0;
+    for (int k = lane; k < (int)gridDim.x; k += 32) a += __ldcg(part + (size_t)k * kMaxV + i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      if (raw) raw[i] = a;
+      double v = addend ? addend[i] + a : a;
+      if (i == sqrt_index) v = sqrt(v);
+      out[i] = v;
+    }
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// pass A: h = V^T w (nv vectors), 16-byte loads (N even, vectors 16 B aligned)
+template <int NV>
+__global__ void __launch_bounds__(kRedThreads) cgs_dot_kernel(size_t N2, int nv, const double* __restrict__ V,
+                                                              size_t ldv, const double* __restrict__ w,
+                                                              double* part, double* out, const double* addend,
+                                                              double* raw, int sqrt_index, unsigned* ticket) {
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N2; t += stride) {
+    const double2 wt = __ldg(reinterpret_cast<const double2*>(w) + t);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nv) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(V + i * ldv) + t);
+        acc[i] = fma(v.x, wt.x, acc[i]);
+        acc[i] = fma(v.y, wt.y, acc[i]);
+      }
+  }
+  block_partials<NV>(acc, nv, part);
+  finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
+}
+
+// pass B: w <- w - V h  and  h2 = V^T w (the V values are reused from registers);
+// pass C (DOT=false, NORM=true): w <- w - V h and ||w||^2.
+template <int NV, bool DOT>
+__global__ void __launch_bounds__(kRedThreads) cgs_axpy_kernel(size_t N, int nv, const double* __restrict__ V,
+                                                               size_t ldv, const double* __restrict__ h,
+                                                               double* __restrict__ w, double* part,
+                                                               double* out, const double* addend,
+                                                               double* raw, int sqrt_index, unsigned* ticket) {
+  __shared__ double hs[NV];
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) hs[i] = (i < nv) ? h[i] : 0.0;
+  __syncthreads();
+  double acc[DOT ? NV : 1];
+#pragma unroll
+  for (int i = 0; i < (DOT ? NV : 1); ++i) acc[i] = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) {
+    double v[NV];
+    double a = w[t];
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nv) {
+        v[i] = __ldg(V + i * ldv + t);
+        a = fma(-hs[i], v[i], a);
+      }
+    w[t] = a;
+    if constexpr (DOT) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        if (i < nv) acc[i] = fma(v[i], a, acc[i]);
+    } else {
+      acc[0] = fma(a, a, acc[0]);
+    }
+  }
+  if constexpr (DOT) {
+    block_partials<NV>(acc, nv, part);
+    finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
+  } else {
+    block_partials<1>(acc, 1, part);
+    finalize_partials(1, part, out, addend, raw, sqrt_index, ticket);
   }
 }
 

@@ -80,7 +80,7 @@ struct msp_handle {
   double *Aval = nullptr, *Fval = nullptr, *W = nullptr, *Pcol = nullptr;
   int32_t* l0_of_cell = nullptr;
   // ABMC blocks
-  int32_t bilu_ncolor = 0;
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0;
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   // AMG
@@ -95,6 +95,7 @@ struct msp_handle {
   double *V = nullptr;
   int V_m = -1;
   double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
+  unsigned* ticket = nullptr;
   double* io = nullptr;              // staging for host<->device and natural-order vectors
   // graphs
   std::vector<cudaGraphExec_t> graphs;
@@ -363,6 +364,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->bilu_ncolor = S.bilu_ncolor;
   h->color_blk = S.color_blk_ptr;
   h->blk_ptr = h->upload(S.blk_ptr);
+  h->max_blk = 1;
+  for (size_t k = 0; k + 1 < S.blk_ptr.size(); ++k) h->max_blk = std::max(h->max_blk, S.blk_ptr[k + 1] - S.blk_ptr[k]);
   // AMG levels
   h->level_n.clear();
   h->level_nnz.clear();
@@ -461,6 +464,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->dh1 = h->dalloc<double>(kMaxV);
   h->dh2 = h->dalloc<double>(kMaxV);
   h->hcol = h->dalloc<double>(kMaxV);
+  h->ticket = h->dalloc<unsigned>(4);
+  CK(cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned), h->s));
   CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 2));
   CK(cudaStreamSynchronize(h->s));
   auto t1 = std::chrono::steady_clock::now();
@@ -546,8 +551,35 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
   }
 }
 
+template <int B, int MAXC>
+void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
+  constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
+  const int g = h->bilu_ncolor;
+  auto run = [&](int c, int kind) {
+    const int b0 = h->color_blk[c], b1 = h->color_blk[c + 1];
+    if (b1 <= b0) return;
+    const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
+    ++h->nlaunch;
+    if (kind == 0)
+      bilu_block_kernel<B, MAXC, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+    else if (kind == 1)
+      bilu_block_kernel<B, MAXC, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+    else
+      bilu_block_kernel<B, MAXC, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+  };
+  for (int c = 0; c < g - 1; ++c) run(c, 0);
+  run(g - 1, 2);
+  for (int c = g - 2; c >= 0; --c) run(c, 1);
+}
+
 template <int B>
 void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z) {
+  if (!h->bilu_v1 && h->max_blk <= 4) {
+    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z);
+    else launch_bilu_block<B, 4>(h, v, wp, z);
+    return;
+  }
   constexpr int TS = (B <= 4) ? 4 : 8;
   const int g = h->bilu_ncolor;
   auto run = [&](int c, int kind) {
@@ -688,6 +720,47 @@ void norm_dev(msp_handle* h, const double* w, double* out) {
   reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
 }
 
+template <int NV>
+void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
+               double* raw, int sq) {
+  cgs_dot_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / 2, nv, V, h->N, w, h->part, out, addend, raw, sq,
+                                                          h->ticket);
+  ++h->nlaunch;
+}
+void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
+             double* raw, int sq) {
+  if (nv <= 4) cgs_dot_t<4>(h, nv, V, w, out, addend, raw, sq);
+  else if (nv <= 8) cgs_dot_t<8>(h, nv, V, w, out, addend, raw, sq);
+  else if (nv <= 16) cgs_dot_t<16>(h, nv, V, w, out, addend, raw, sq);
+  else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
+}
+template <int NV, bool DOT>
+void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
+                const double* addend, double* raw, int sq) {
+  cgs_axpy_kernel<NV, DOT><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, coef, w, h->part, out, addend,
+                                                                raw, sq, h->ticket);
+  ++h->nlaunch;
+}
+template <bool DOT>
+void cgs_axpy(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
+              const double* addend, double* raw, int sq) {
+  if (nv <= 4) cgs_axpy_t<4, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
+  else if (nv <= 8) cgs_axpy_t<8, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
+  else if (nv <= 16) cgs_axpy_t<16, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
+  else cgs_axpy_t<32, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
+}
+
+// CGS2 (R8) on w = V[nv] against V[0..nv): hcol[0..nv) = h1 + h2, hcol[nv] = ||w||,
+// V[nv] = w / ||w||.  Three passes over the basis:
+//   A: h1 = V^T w;  B: w -= V h1 and h2 = V^T w (fused);  C: w -= V h2 and ||w||^2.
+void cgs2(msp_handle* h, int nv, double* w) {
+  cgs_dot(h, nv, h->V, w, h->dh1, nullptr, nullptr, -1);
+  cgs_axpy<true>(h, nv, h->V, h->dh1, w, h->hcol, h->dh1, h->dh2, -1);
+  cgs_axpy<false>(h, nv, h->V, h->dh2, w, h->hcol + nv, nullptr, nullptr, 0);
+  scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, w, h->hcol + nv, w);
+  ++h->nlaunch;
+}
+
 // One Arnoldi step j: z = B v_j; w = A z (into V[j+1]); orthogonalise (CGS2 or MGS);
 // hcol[0..j+1] = H(:, j); V[j+1] normalised; hcol copied to pinned host memory.
 void arnoldi_step(msp_handle* h, int j) {
@@ -698,13 +771,7 @@ void arnoldi_step(msp_handle* h, int j) {
   launch_spmv(h, 0, h->z, nullptr, w);
   const int nv = j + 1;
   if (h->prm.orth == 0) {
-    multidot(h, nv, h->V, w);
-    reduce(h, nv, h->dh1, nullptr, nullptr, -1);                 // h1
-    maxpy(h, nv, h->V, h->dh1, w, 0, nullptr);                   // w -= V h1
-    multidot(h, nv, h->V, w);
-    reduce(h, nv, h->hcol, h->dh1, h->dh2, -1);                  // h2; hcol = h1 + h2
-    maxpy(h, nv, h->V, h->dh2, w, 0, h->part);                   // w -= V h2, ||w||^2 partials
-    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
+    cgs2(h, nv, w);
   } else {
     for (int i = 0; i < nv; ++i) {
       multidot_t<4>(h, 1, h->V + (size_t)i * N, w);
@@ -712,8 +779,8 @@ void arnoldi_step(msp_handle* h, int j) {
       maxpy_t<4>(h, 1, h->V + (size_t)i * N, h->hcol + i, w, 0, (i == nv - 1) ? h->part : nullptr);
     }
     reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
+    scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + nv, w); ++h->nlaunch;
   }
-  scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + nv, w); ++h->nlaunch;
   CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
 }
 
@@ -921,6 +988,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   h->cfg = c;
   if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
+  if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
@@ -1161,17 +1229,7 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         bytes = 0.0;
         break;
       case 10:                                   // CGS2 of step j=15 alone
-        fn = [&]() {
-          double* w = h->V + (size_t)16 * N;
-          multidot(h, 16, h->V, w);
-          reduce(h, 16, h->dh1, nullptr, nullptr, -1);
-          maxpy(h, 16, h->V, h->dh1, w, 0, nullptr);
-          multidot(h, 16, h->V, w);
-          reduce(h, 16, h->hcol, h->dh1, h->dh2, -1);
-          maxpy(h, 16, h->V, h->dh2, w, 0, h->part);
-          reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + 16, nullptr, 0);
-          scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + 16, w);
-        };
+        fn = [&]() { cgs2(h, 16, h->V + (size_t)16 * N); };
         bytes = 0.0;
         break;
       default:

@@ -8,9 +8,12 @@ from paper_2208_08594_b200 import MspSolver  # noqa
 
 p = gen.make_config(sys.argv[1] if len(sys.argv) > 1 else "C3")
 variants = [("multi", dict(use_coop=0))]
+if "bilu_v1" in sys.argv:
+    variants.append(("bilu_v1", dict(use_coop=0)))
 if "coop" in sys.argv:
     variants.append(("coop", dict(use_coop=1)))
 for tag, kw in variants:
+    os.environ["MSP_BILU_V1"] = "1" if tag == "bilu_v1" else "0"
     s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], **kw)
     b = torch.from_numpy(p["rhs"]).cuda()
     r = s.solve(b)
