@@ -132,6 +132,82 @@ __global__ void pgs_init_kernel(int n, int c1_end, const double* __restrict__ di
   x[i] = (i < c1_end) ? ldg(b + i) / ldg(diag + i) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// a4/a5 with LPR lanes per row (coarse levels: few rows per color, wide Galerkin
+// rows -> the per-row dependent load chain, not bandwidth, sets the time).  Lane u of
+// a row handles SELL entries k = u, u+LPR, ...; the LPR partial sums are combined by
+// shuffles.  Slices (32 rows) map to 32*LPR consecutive threads (whole warps).
+// WRITE_R: also write the residual of the updated row, r = (b - sum_{j!=i}) - a_ii x_i
+// (rows of the LAST pre-sweep color: their neighbours are final, so this is exactly
+// the a5 residual, fused).  MODE_RES: residual only (rows of the other colors).
+// ---------------------------------------------------------------------------
+template <int LPR, bool WRITE_R, bool MODE_RES>
+__global__ void __launch_bounds__(128) sell_row_kernel(int s_first, int s_end,
+                                                       const int* __restrict__ slice_row,
+                                                       const int* __restrict__ slice_off,
+                                                       const int* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ diag,
+                                                       const double* __restrict__ b,
+                                                       double* __restrict__ x,
+                                                       double* __restrict__ r) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = s_first + t / (kSell * LPR);
+  if (s >= s_end) return;                      // whole warps (32*LPR threads per slice)
+  const int rem = t % (kSell * LPR);
+  const int l = rem / LPR, u = rem % LPR;
+  const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
+  const int row = r0 + l;
+  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
+  double acc = 0.0;
+  for (int k = u; k < w; k += LPR) {
+    const int o = o0 + k * kSell + l;
+    acc = fma(ldg(val + o), x[ldg(col + o)], acc);
+  }
+#pragma unroll
+  for (int m = LPR / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (u != 0 || row >= r1) return;
+  const double d = ldg(diag + row);
+  if (MODE_RES) {
+    r[row] = ldg(b + row) - fma(d, x[row], acc);
+  } else {
+    const double bs = ldg(b + row) - acc;
+    const double xi = bs / d;
+    x[row] = xi;
+    if (WRITE_R) r[row] = fma(-d, xi, bs);
+  }
+}
+
+// coarsest GEMV, 4 independent 16-byte loads in flight per lane
+__global__ void __launch_bounds__(256) gemv4_kernel(int n, int ld, const double* __restrict__ Ainv,
+                                                    const double* __restrict__ b, double* __restrict__ x) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double2* a = reinterpret_cast<const double2*>(Ainv + (size_t)row * ld);
+  const double2* bb = reinterpret_cast<const double2*>(b);
+  const int n2 = n >> 1;                       // pairs
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  int j = lane;
+  for (; j + 96 < n2; j += 128) {
+    const double2 a0 = __ldg(a + j), a1 = __ldg(a + j + 32), a2 = __ldg(a + j + 64), a3 = __ldg(a + j + 96);
+    const double2 b0 = __ldg(bb + j), b1 = __ldg(bb + j + 32), b2 = __ldg(bb + j + 64), b3 = __ldg(bb + j + 96);
+    acc0 = fma(a0.x, b0.x, fma(a0.y, b0.y, acc0));
+    acc1 = fma(a1.x, b1.x, fma(a1.y, b1.y, acc1));
+    acc2 = fma(a2.x, b2.x, fma(a2.y, b2.y, acc2));
+    acc3 = fma(a3.x, b3.x, fma(a3.y, b3.y, acc3));
+  }
+  for (; j < n2; j += 32) {
+    const double2 a0 = __ldg(a + j), b0 = __ldg(bb + j);
+    acc0 = fma(a0.x, b0.x, fma(a0.y, b0.y, acc0));
+  }
+  double acc = (acc0 + acc1) + (acc2 + acc3);
+  if ((n & 1) && lane == 0) acc = fma(ldg(Ainv + (size_t)row * ld + n - 1), ldg(b + n - 1), acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) x[row] = acc;
+}
+
 // a5 part 1: residual r = b - A x over all rows of the level (SELL-32 + diagonal).
 __global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
                                                             const int* __restrict__ slice_row,

@@ -55,6 +55,7 @@ struct DevLevel {
   int32_t* inv = nullptr;            // permuted -> natural
   double *b = nullptr, *x = nullptr, *r = nullptr;
   int64_t nnz_alloc = 0;
+  int lpr = 1;                       // lanes per row (coarse levels)
   int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
 };
 
@@ -289,6 +290,11 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
     }
   }
   L.nnz_alloc = slice_off[L.nslices];
+  {
+    const double avg = (double)A.nnz() / std::max<int32_t>(n, 1);
+    L.lpr = (avg <= 8.0) ? 1 : (avg <= 20.0 ? 4 : 8);
+    if (const char* e = std::getenv("MSP_LPR")) L.lpr = std::atoi(e);
+  }
   {
     std::vector<int32_t> rs(n), rw(n);
     for (int32_t s = 0; s < L.nslices; ++s)
@@ -616,22 +622,45 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0) {
   }
 }
 
-void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero) {
-  auto color = [&](int c) {
-    const int s0 = L.color_slice[c], s1 = L.color_slice[c + 1];
-    if (s1 <= s0) return;
-    pgs_color_kernel<<<nblk((size_t)(s1 - s0) * kSell, 128), 128, 0, h->s>>>(
-        s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x); ++h->nlaunch;
-  };
+template <int LPR, bool WR, bool RES>
+void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
+  if (s1 <= s0) return;
+  sell_row_kernel<LPR, WR, RES><<<nblk((size_t)(s1 - s0) * kSell * LPR, 128), 128, 0, h->s>>>(
+      s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
+  ++h->nlaunch;
+}
+template <bool WR, bool RES>
+void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
+  switch (L.lpr) {
+    case 2: sell_rows<2, WR, RES>(h, L, s0, s1); break;
+    case 4: sell_rows<4, WR, RES>(h, L, s0, s1); break;
+    case 8: sell_rows<8, WR, RES>(h, L, s0, s1); break;
+    default: sell_rows<1, WR, RES>(h, L, s0, s1); break;
+  }
+}
+
+// One PGS-MC sweep of level L (Alg. 4).  write_r: the last color also writes the
+// residual of its rows (caller then computes the residual of the other colors).
+void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool write_r = false) {
   if (ascending) {
     int c = 0;
     if (from_zero) {
       pgs_init_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.color_row[1], L.diag, L.b, L.x); ++h->nlaunch;
       c = 1;
+      if (L.ncolor == 1 && write_r) {              // single color: residual of all rows
+        sell_rows_any<false, true>(h, L, 0, L.nslices);
+        return;
+      }
     }
-    for (; c < L.ncolor; ++c) color(c);
+    for (; c < L.ncolor; ++c) {
+      const bool last = (c == L.ncolor - 1);
+      if (last && write_r) sell_rows_any<true, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
+      else sell_rows_any<false, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
+    }
+    if (write_r && L.ncolor > 1)                   // residual of colors 1..g-1 (not the last)
+      sell_rows_any<false, true>(h, L, 0, L.color_slice[L.ncolor - 1]);
   } else {
-    for (int c = L.ncolor - 1; c >= 0; --c) color(c);
+    for (int c = L.ncolor - 1; c >= 0; --c) sell_rows_any<false, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
   }
 }
 
@@ -642,7 +671,7 @@ void vcycle(msp_handle* h, int l) {
     if (h->coarse_diag)
       diag_solve_kernel<<<nblk(h->nL, 256), 256, 0, h->s>>>(h->nL, h->cdiag, h->bL, h->xL);
     else
-      gemv_kernel<<<nblk((size_t)h->nL * 32, 256), 256, 0, h->s>>>(h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+      gemv4_kernel<<<nblk((size_t)h->nL * 32, 256), 256, 0, h->s>>>(h->nL, h->ldA, h->Ainv, h->bL, h->xL);
     return;
   }
   DevLevel& L = h->lv[l];
@@ -650,10 +679,11 @@ void vcycle(msp_handle* h, int l) {
   double* bn = last ? h->bL : h->lv[l + 1].b;
   double* xn = last ? h->xL : h->lv[l + 1].x;
   const int nn = last ? h->nL : h->lv[l + 1].n;
-  for (int s = 0; s < h->prm.pre_sweeps; ++s) pgs_sweep(h, L, true, s == 0);
-  if (h->prm.pre_sweeps == 0) CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
-  sell_residual_kernel<<<nblk((size_t)L.nslices * kSell, 128), 128, 0, h->s>>>(
-      L.nslices, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r); ++h->nlaunch;
+  for (int s = 0; s < h->prm.pre_sweeps; ++s) pgs_sweep(h, L, true, s == 0, s + 1 == h->prm.pre_sweeps);
+  if (h->prm.pre_sweeps == 0) {
+    CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
+    sell_rows_any<false, true>(h, L, 0, L.nslices);
+  }
   restrict_kernel<<<nblk(nn, 256), 256, 0, h->s>>>(nn, L.pt_ptr, L.pt_idx, L.r, bn); ++h->nlaunch;
   vcycle(h, l + 1);
   prolong_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.agg, xn, L.x); ++h->nlaunch;
