@@ -368,11 +368,12 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
 template <int B, int MAXC, bool FWD, bool BWD>
-__global__ void __launch_bounds__(128) bilu_block_kernel(int b_first, int b_end,
+__global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const int* __restrict__ dg,
+                                                         const int* __restrict__ cnt,
                                                          const double* __restrict__ F,
                                                          double* v,
                                                          const double* __restrict__ wp,
@@ -397,15 +398,19 @@ __global__ void __launch_bounds__(128) bilu_block_kernel(int b_first, int b_end,
   const int i = c0 + (valid ? cq : 0);
   const bool act = valid && q < B;
   double t = 0.0;                           // working value of row q of cell i
+  // cnt[i] = (#external L entries) | (#intra-block U entries << 8), from setup
+  const int cn = valid ? ldg(cnt + i) : 0;
   if (FWD) {
-    int e = valid ? ldg(rp + i) : 0;
+    const int e0 = valid ? ldg(rp + i) : 0;
     const int d = valid ? ldg(dg + i) : 0;
+    const int eext = e0 + (cn & 0xff);       // [e0, eext): external L; [eext, d): intra L
+    int e = eext;
     double acc = 0.0;
-    for (; e < d; ++e) {                    // external L part: columns before the block
-      const int k = ldg(ci + e);
-      if (k >= c0) break;
-      const double yq = (q < B) ? v[(size_t)k * B + q] : 0.0;
-      const double* blkF = F + (size_t)e * BB;
+#pragma unroll 2
+    for (int ee = e0; ee < eext; ++ee) {    // external L part: columns before the block
+      const int k = ldg(ci + ee);
+      const double yq = (q < B) ? ldg(v + (size_t)k * B + q) : 0.0;
+      const double* blkF = F + (size_t)ee * BB;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const double yu = __shfl_sync(cmask, yq, cbase + u);
@@ -434,12 +439,12 @@ __global__ void __launch_bounds__(128) bilu_block_kernel(int b_first, int b_end,
     if (!FWD) t = act ? v[(size_t)i * B + q] : 0.0;
     const int d = valid ? ldg(dg + i) : 0;
     const int e1 = valid ? ldg(rp + i + 1) : 0;
-    int ei = d + 1;                          // intra U entries: columns inside the block
-    while (ei < e1 && ldg(ci + ei) < c1) ++ei;
+    const int ei = d + 1 + (cn >> 8);        // (d, ei): intra U; [ei, e1): external U
     double acc = 0.0;
+#pragma unroll 2
     for (int e = ei; e < e1; ++e) {          // external U part: columns after the block
       const int j = ldg(ci + e);
-      const double xq = (q < B) ? v[(size_t)j * B + q] : 0.0;
+      const double xq = (q < B) ? ldg(v + (size_t)j * B + q) : 0.0;
       const double* blkF = F + (size_t)e * BB;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
@@ -638,66 +643,98 @@ __device__ __forceinline__ void finalize_partials(int nv, const double* part, do
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// pass A: h = V^T w (nv vectors), 16-byte loads (N even, vectors 16 B aligned)
-template <int NV>
-__global__ void __launch_bounds__(kRedThreads) cgs_dot_kernel(size_t N2, int nv, const double* __restrict__ V,
-                                                              size_t ldv, const double* __restrict__ w,
-                                                              double* part, double* out, const double* addend,
-                                                              double* raw, int sqrt_index, unsigned* ticket) {
+// vector of EW doubles (EW = 2: one 16-byte load; EW = 1: 8-byte load)
+template <int EW> struct VecT;
+template <> struct VecT<1> {
+  double x;
+  __device__ static VecT ld(const double* p, size_t t) { return {__ldg(p + t)}; }
+  __device__ static VecT ldcg(const double* p, size_t t) { return {__ldcg(p + t)}; }
+};
+template <> struct VecT<2> {
+  double x, y;
+  __device__ static VecT ld(const double* p, size_t t) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p) + t);
+    return {v.x, v.y};
+  }
+  __device__ static VecT ldcg(const double* p, size_t t) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p) + t);
+    return {v.x, v.y};
+  }
+};
+template <int EW> __device__ __forceinline__ double vdot(const VecT<EW>& a, const VecT<EW>& b, double acc);
+template <> __device__ __forceinline__ double vdot<1>(const VecT<1>& a, const VecT<1>& b, double acc) {
+  return fma(a.x, b.x, acc);
+}
+template <> __device__ __forceinline__ double vdot<2>(const VecT<2>& a, const VecT<2>& b, double acc) {
+  return fma(a.x, b.x, fma(a.y, b.y, acc));
+}
+template <int EW> __device__ __forceinline__ void vaxpy(double c, const VecT<EW>& v, VecT<EW>& a);
+template <> __device__ __forceinline__ void vaxpy<1>(double c, const VecT<1>& v, VecT<1>& a) { a.x = fma(c, v.x, a.x); }
+template <> __device__ __forceinline__ void vaxpy<2>(double c, const VecT<2>& v, VecT<2>& a) {
+  a.x = fma(c, v.x, a.x);
+  a.y = fma(c, v.y, a.y);
+}
+
+// pass A: h = V^T w (nv vectors); NE = N / EW elements of EW doubles
+template <int NV, int EW>
+__global__ void __launch_bounds__(kRedThreads, 2) cgs_dot_kernel(size_t NE, int nv, const double* __restrict__ V,
+                                                                 size_t ldv, const double* __restrict__ w,
+                                                                 double* part, double* out, const double* addend,
+                                                                 double* raw, int sqrt_index, unsigned* ticket) {
+  using T = VecT<EW>;
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N2; t += stride) {
-    const double2 wt = __ldg(reinterpret_cast<const double2*>(w) + t);
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < NE; t += stride) {
+    const T wt = T::ld(w, t);
 #pragma unroll
     for (int i = 0; i < NV; ++i)
-      if (i < nv) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(V + i * ldv) + t);
-        acc[i] = fma(v.x, wt.x, acc[i]);
-        acc[i] = fma(v.y, wt.y, acc[i]);
-      }
+      if (i < nv) acc[i] = vdot<EW>(T::ld(V + i * ldv, t), wt, acc[i]);
   }
   block_partials<NV>(acc, nv, part);
   finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
 }
 
-// pass B: w <- w - V h  and  h2 = V^T w (the V values are reused from registers);
-// pass C (DOT=false, NORM=true): w <- w - V h and ||w||^2.
-template <int NV, bool DOT>
-__global__ void __launch_bounds__(kRedThreads) cgs_axpy_kernel(size_t N, int nv, const double* __restrict__ V,
-                                                               size_t ldv, const double* __restrict__ h,
-                                                               double* __restrict__ w, double* part,
-                                                               double* out, const double* addend,
-                                                               double* raw, int sqrt_index, unsigned* ticket) {
+// pass B (DOT=true): w <- w - V h and h2 = V^T w; pass C (DOT=false): w <- w - V h and
+// ||w||^2.  16-byte loads (two elements per thread and step).  In pass B the basis is
+// read twice per element pair by the same thread (axpy, then dot); the second read is
+// an L1 hit, which keeps registers low (full occupancy) instead of holding NV values.
+// NVD: the dot part covers only the first min(nv, NVD) vectors (the rest by a
+// separate cgs_dot pass), so that NV=32 axpys stay register-light.
+template <int NV, int EW, bool DOT, int NVD = NV>
+__global__ void __launch_bounds__(kRedThreads, 2) cgs_axpy_kernel(size_t NE, int nv, const double* __restrict__ V,
+                                                                  size_t ldv, const double* __restrict__ h,
+                                                                  double* __restrict__ w, double* part,
+                                                                  double* out, const double* addend,
+                                                                  double* raw, int sqrt_index, unsigned* ticket) {
+  using T = VecT<EW>;
   __shared__ double hs[NV];
   for (int i = threadIdx.x; i < NV; i += blockDim.x) hs[i] = (i < nv) ? h[i] : 0.0;
   __syncthreads();
-  double acc[DOT ? NV : 1];
+  double acc[DOT ? NVD : 1];
 #pragma unroll
-  for (int i = 0; i < (DOT ? NV : 1); ++i) acc[i] = 0.0;
+  for (int i = 0; i < (DOT ? NVD : 1); ++i) acc[i] = 0.0;
+  const int nvd = nv < NVD ? nv : NVD;
+  T* wT = reinterpret_cast<T*>(w);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) {
-    double v[NV];
-    double a = w[t];
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < NE; t += stride) {
+    T a = wT[t];
 #pragma unroll
     for (int i = 0; i < NV; ++i)
-      if (i < nv) {
-        v[i] = __ldg(V + i * ldv + t);
-        a = fma(-hs[i], v[i], a);
-      }
-    w[t] = a;
+      if (i < nv) vaxpy<EW>(-hs[i], T::ld(V + i * ldv, t), a);
+    wT[t] = a;
     if constexpr (DOT) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i)
-        if (i < nv) acc[i] = fma(v[i], a, acc[i]);
+      for (int i = 0; i < NVD; ++i)  // re-read through L2 (.cg): not merged with the first read
+        if (i < nvd) acc[i] = vdot<EW>(T::ldcg(V + i * ldv, t), a, acc[i]);
     } else {
-      acc[0] = fma(a, a, acc[0]);
+      acc[0] = vdot<EW>(a, a, acc[0]);
     }
   }
   if constexpr (DOT) {
-    block_partials<NV>(acc, nv, part);
-    finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
+    block_partials<NVD>(acc, nvd, part);
+    finalize_partials(nvd, part, out, addend, raw, sqrt_index, ticket);
   } else {
     block_partials<1>(acc, 1, part);
     finalize_partials(1, part, out, addend, raw, sqrt_index, ticket);

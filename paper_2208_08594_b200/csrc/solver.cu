@@ -84,6 +84,7 @@ struct msp_handle {
   int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0;
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
+  int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
   // AMG
   std::vector<DevLevel> lv;
   int32_t nL = 0, ldA = 0;
@@ -372,6 +373,20 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->blk_ptr = h->upload(S.blk_ptr);
   h->max_blk = 1;
   for (size_t k = 0; k + 1 < S.blk_ptr.size(); ++k) h->max_blk = std::max(h->max_blk, S.blk_ptr[k + 1] - S.blk_ptr[k]);
+  {
+    std::vector<int32_t> cnt(n, 0);
+    for (size_t k = 0; k + 1 < S.blk_ptr.size(); ++k) {
+      const int32_t c0 = S.blk_ptr[k], c1 = S.blk_ptr[k + 1];
+      for (int32_t i = c0; i < c1; ++i) {
+        int32_t next = 0, nint = 0;
+        for (int32_t e = rp[i]; e < dg[i]; ++e) if (ci[e] < c0) ++next;
+        for (int32_t e = dg[i] + 1; e < rp[i + 1]; ++e) if (ci[e] < c1) ++nint;
+        if (next > 255 || nint > 255) throw std::pair<int, std::string>(MSP_EINVAL, "BILU: row too long for the block kernel");
+        cnt[i] = next | (nint << 8);
+      }
+    }
+    h->bcnt = h->upload(cnt);
+  }
   // AMG levels
   h->level_n.clear();
   h->level_nnz.clear();
@@ -567,11 +582,11 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
     if (kind == 0)
-      bilu_block_kernel<B, MAXC, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      bilu_block_kernel<B, MAXC, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else if (kind == 1)
-      bilu_block_kernel<B, MAXC, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      bilu_block_kernel<B, MAXC, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else
-      bilu_block_kernel<B, MAXC, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      bilu_block_kernel<B, MAXC, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
   };
   for (int c = 0; c < g - 1; ++c) run(c, 0);
   run(g - 1, 2);
@@ -753,8 +768,9 @@ void norm_dev(msp_handle* h, const double* w, double* out) {
 template <int NV>
 void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
                double* raw, int sq) {
-  cgs_dot_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / 2, nv, V, h->N, w, h->part, out, addend, raw, sq,
-                                                          h->ticket);
+  constexpr int EW = (NV <= 16) ? 2 : 1;
+  cgs_dot_kernel<NV, EW><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
+                                                              sq, h->ticket);
   ++h->nlaunch;
 }
 void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
@@ -767,8 +783,9 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
 template <int NV, bool DOT>
 void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
                 const double* addend, double* raw, int sq) {
-  cgs_axpy_kernel<NV, DOT><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, coef, w, h->part, out, addend,
-                                                                raw, sq, h->ticket);
+  constexpr int EW = (NV <= 16) ? 2 : 1;
+  cgs_axpy_kernel<NV, EW, DOT><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / EW, nv, V, h->N, coef, w, h->part, out,
+                                                                    addend, raw, sq, h->ticket);
   ++h->nlaunch;
 }
 template <bool DOT>
@@ -1260,6 +1277,14 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         break;
       case 10:                                   // CGS2 of step j=15 alone
         fn = [&]() { cgs2(h, 16, h->V + (size_t)16 * N); };
+        bytes = 0.0;
+        break;
+      case 11:
+        fn = [&]() { arnoldi_step(h, 25); };
+        bytes = 0.0;
+        break;
+      case 12:
+        fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
         bytes = 0.0;
         break;
       default:
