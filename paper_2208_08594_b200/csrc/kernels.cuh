@@ -18,6 +18,16 @@ constexpr int kSell = 32;
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
 
+// Programmatic dependent launch (PDL).  Every kernel is launched with programmatic
+// stream serialisation: it may start while its predecessor still runs, so it must
+// call pdl_wait() before touching anything a predecessor produced (vectors); only
+// immutable data (matrix values/indices) may be read before.  pdl_trigger() right
+// after the wait lets the successor start its own prologue (at most two kernels
+// overlap).  Both are no-ops when the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define PDL_ENTRY() do { pdl_wait(); pdl_trigger(); } while (0)
+
 // ---------------------------------------------------------------------------
 // a2 (K1): BSR SpMV.  One team of TS lanes per block row (TS = 4 for b=4, 8 for b=7);
 // lane q < B owns output row q of the cell.  Each block column-major: lane q reads
@@ -36,6 +46,7 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
                                                        const double* __restrict__ x,
                                                        const double* __restrict__ g,
                                                        double* __restrict__ y) {
+  PDL_ENTRY();
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int BB = B * B;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,21 +88,30 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
 // a3: pressure restriction with decoupling weights (R4): rp_l0[dst[c]] = sum_k
 // W[c][k] * g[c*B+k]; dst maps internal cell positions to level-0 rows.
 // ---------------------------------------------------------------------------
+// One thread per LEVEL-0 row i (coalesced writes); src[i] = the internal cell of row i
+// (its W row and g block are one aligned 32-byte sector each for b = 4).
+// Fused first color of the level-0 pre-sweep (zero guess): when x0 != null, also
+// x0[i] = b_i / a_ii for rows of color 1 (i < c1_end), 0 otherwise.
 template <int B>
 __global__ void restrict_pressure_kernel(int n, const double* __restrict__ W,
-                                         const double* __restrict__ g, const int* __restrict__ dst,
-                                         double* __restrict__ rp) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+                                         const double* __restrict__ g, const int* __restrict__ src,
+                                         double* __restrict__ rp, double* __restrict__ x0,
+                                         const double* __restrict__ diag0, int c1_end) {
+  PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = ldg(src + i);
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < B; ++k) s = fma(ldg(W + (size_t)c * B + k), ldg(g + (size_t)c * B + k), s);
-  rp[ldg(dst + c)] = s;
+  rp[i] = s;
+  if (x0) x0[i] = (i < c1_end) ? s / ldg(diag0 + i) : 0.0;
 }
 
 // gather of the level-0 correction into cell order: wp[c] = x0[dst[c]]
 __global__ void gather_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                               double* __restrict__ out) {
+  PDL_ENTRY();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n) out[c] = ldg(src + ldg(idx + c));
 }
@@ -109,6 +129,7 @@ __global__ void __launch_bounds__(128) pgs_color_kernel(int s_first, int s_end,
                                                         const double* __restrict__ diag,
                                                         const double* __restrict__ b,
                                                         double* __restrict__ x) {
+  PDL_ENTRY();
   const int s = s_first + (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
   const int l = threadIdx.x % kSell;
   if (s >= s_end) return;
@@ -127,6 +148,7 @@ __global__ void __launch_bounds__(128) pgs_color_kernel(int s_first, int s_end,
 // rows of color 1 and x_i = 0 elsewhere (one pass over the whole level).
 __global__ void pgs_init_kernel(int n, int c1_end, const double* __restrict__ diag,
                                 const double* __restrict__ b, double* __restrict__ x) {
+  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   x[i] = (i < c1_end) ? ldg(b + i) / ldg(diag + i) : 0.0;
@@ -159,15 +181,31 @@ __global__ void __launch_bounds__(128) sell_row_kernel(int s_first, int s_end,
   const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
   const int row = r0 + l;
   const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
+  // prologue (overlaps the predecessor kernel): the first PF matrix entries of this
+  // lane and the diagonal are immutable
+  constexpr int PF = 4;
+  int pc[PF];
+  double pv[PF];
+#pragma unroll
+  for (int m = 0; m < PF; ++m) {
+    const int k = u + m * LPR;
+    const int o = o0 + k * kSell + l;
+    pc[m] = (k < w) ? ldg(col + o) : row;
+    pv[m] = (k < w) ? ldg(val + o) : 0.0;
+  }
+  const double d = (row < r1) ? ldg(diag + row) : 1.0;
+  pdl_wait();
+  pdl_trigger();
   double acc = 0.0;
-  for (int k = u; k < w; k += LPR) {
+#pragma unroll
+  for (int m = 0; m < PF; ++m) acc = fma(pv[m], x[pc[m]], acc);
+  for (int k = u + PF * LPR; k < w; k += LPR) {
     const int o = o0 + k * kSell + l;
     acc = fma(ldg(val + o), x[ldg(col + o)], acc);
   }
 #pragma unroll
   for (int m = LPR / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
   if (u != 0 || row >= r1) return;
-  const double d = ldg(diag + row);
   if (MODE_RES) {
     r[row] = ldg(b + row) - fma(d, x[row], acc);
   } else {
@@ -178,9 +216,60 @@ __global__ void __launch_bounds__(128) sell_row_kernel(int s_first, int s_end,
   }
 }
 
+// Trailing colors c_first..c_last of one level in ONE CTA: every row of these colors is
+// owned by this CTA, so consecutive colors are separated by __syncthreads (global
+// writes of the CTA are visible to the CTA after the barrier) instead of kernel
+// boundaries.  Same per-row arithmetic as sell_row_kernel (LPR lanes per row).
+// Ascending (pre-sweep) order if asc, descending otherwise.  WRITE_R on the last color
+// of an ascending sweep writes the residual of its rows (see sell_row_kernel).
+template <int LPR>
+__global__ void __launch_bounds__(1024) sell_tail_kernel(int c_first, int c_last, int asc, int write_r,
+                                                         const int* __restrict__ color_slice,
+                                                         const int* __restrict__ slice_row,
+                                                         const int* __restrict__ slice_off,
+                                                         const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ diag,
+                                                         const double* __restrict__ b, double* x,
+                                                         double* __restrict__ r) {
+  PDL_ENTRY();
+  const int nc = c_last - c_first + 1;
+  for (int step = 0; step < nc; ++step) {
+    const int c = asc ? c_first + step : c_last - step;
+    const bool wr = write_r && asc && step == nc - 1;
+    const int s0 = ldg(color_slice + c), s1 = ldg(color_slice + c + 1);
+    const int items = (s1 - s0) * kSell * LPR;
+    for (int t0 = 0; t0 < items; t0 += blockDim.x) {     // uniform trip count: shuffles safe
+      const int t = t0 + threadIdx.x;
+      const bool in = t < items;
+      const int s = s0 + (in ? t / (kSell * LPR) : 0);
+      const int rem = t % (kSell * LPR);
+      const int l = rem / LPR, u = rem % LPR;
+      const int row = ldg(slice_row + s) + l;
+      const int o0 = ldg(slice_off + s), w = in ? (ldg(slice_off + s + 1) - o0) / kSell : 0;
+      double acc = 0.0;
+      for (int k = u; k < w; k += LPR) {
+        const int o = o0 + k * kSell + l;
+        acc = fma(ldg(val + o), x[ldg(col + o)], acc);
+      }
+#pragma unroll
+      for (int m = LPR / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      if (in && u == 0 && row < ldg(slice_row + s + 1)) {
+        const double d = ldg(diag + row);
+        const double bs = ldg(b + row) - acc;
+        const double xi = bs / d;
+        x[row] = xi;
+        if (wr) r[row] = fma(-d, xi, bs);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // coarsest GEMV, 4 independent 16-byte loads in flight per lane
 __global__ void __launch_bounds__(256) gemv4_kernel(int n, int ld, const double* __restrict__ Ainv,
                                                     const double* __restrict__ b, double* __restrict__ x) {
+  PDL_ENTRY();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -218,6 +307,7 @@ __global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
                                                             const double* __restrict__ b,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ r) {
+  PDL_ENTRY();
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
   const int l = threadIdx.x % kSell;
   if (s >= nslices) return;
@@ -233,18 +323,23 @@ __global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
 }
 
 // a5 part 2: restriction b_{l+1}[I] = sum_{i in I} r_i (P^T, piecewise-constant P).
+// (fused: xc != null -> first color of the next level's pre-sweep from the zero guess)
 __global__ void restrict_kernel(int nc, const int* __restrict__ pp, const int* __restrict__ pi,
-                                const double* __restrict__ r, double* __restrict__ bc) {
+                                const double* __restrict__ r, double* __restrict__ bc,
+                                double* __restrict__ xc, const double* __restrict__ dc, int c1_end) {
+  PDL_ENTRY();
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= nc) return;
   double s = 0.0;
   for (int e = ldg(pp + I); e < ldg(pp + I + 1); ++e) s += ldg(r + ldg(pi + e));
   bc[I] = s;
+  if (xc) xc[I] = (I < c1_end) ? s / ldg(dc + I) : 0.0;
 }
 
 // a7: prolongation and correction x_i += e[agg(i)].
 __global__ void prolong_kernel(int n, const int* __restrict__ agg, const double* __restrict__ e,
                                double* __restrict__ x) {
+  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] += ldg(e + ldg(agg + i));
 }
@@ -254,6 +349,7 @@ __global__ void prolong_kernel(int n, const int* __restrict__ agg, const double*
 __global__ void __launch_bounds__(256) gemv_kernel(int n, int ld, const double* __restrict__ Ainv,
                                                    const double* __restrict__ b,
                                                    double* __restrict__ x) {
+  PDL_ENTRY();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -273,6 +369,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(int n, int ld, const double* 
 
 __global__ void diag_solve_kernel(int n, const double* __restrict__ d, const double* __restrict__ b,
                                   double* __restrict__ x) {
+  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = ldg(b + i) / ldg(d + i);
 }
@@ -298,6 +395,7 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
                                                          double* v,
                                                          const double* __restrict__ wp,
                                                          double* __restrict__ z) {
+  PDL_ENTRY();
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int BB = B * B;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -400,6 +498,8 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
   double t = 0.0;                           // working value of row q of cell i
   // cnt[i] = (#external L entries) | (#intra-block U entries << 8), from setup
   const int cn = valid ? ldg(cnt + i) : 0;
+  pdl_wait();
+  pdl_trigger();
   if (FWD) {
     const int e0 = valid ? ldg(rp + i) : 0;
     const int d = valid ? ldg(dg + i) : 0;
@@ -499,6 +599,7 @@ __global__ void __launch_bounds__(kRedThreads) multidot_kernel(size_t N, int nv,
                                                                size_t ldv,
                                                                const double* __restrict__ w,
                                                                double* __restrict__ part) {
+  PDL_ENTRY();
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
@@ -532,6 +633,7 @@ __global__ void __launch_bounds__(kRedThreads) multidot_kernel(size_t N, int nv,
 __global__ void reduce_parts_kernel(int nblk, int nv, const double* __restrict__ part,
                                     double* __restrict__ out, const double* __restrict__ addend,
                                     int sqrt_index) {
+  PDL_ENTRY();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = wid; i < nv; i += nw) {
     double a = 0.0;
@@ -555,6 +657,7 @@ __global__ void __launch_bounds__(kRedThreads) multiaxpy_kernel(size_t N, int nv
                                                                 double* __restrict__ w,
                                                                 int from_zero, double* part,
                                                                 int slot) {
+  PDL_ENTRY();
   __shared__ double hs[NV];
   for (int i = threadIdx.x; i < NV; i += blockDim.x) hs[i] = (i < nv) ? h[i] : 0.0;
   __syncthreads();
@@ -681,6 +784,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_dot_kernel(size_t NE, int 
                                                                  size_t ldv, const double* __restrict__ w,
                                                                  double* part, double* out, const double* addend,
                                                                  double* raw, int sqrt_index, unsigned* ticket) {
+  PDL_ENTRY();
   using T = VecT<EW>;
   double acc[NV];
 #pragma unroll
@@ -708,6 +812,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_axpy_kernel(size_t NE, int
                                                                   double* __restrict__ w, double* part,
                                                                   double* out, const double* addend,
                                                                   double* raw, int sqrt_index, unsigned* ticket) {
+  PDL_ENTRY();
   using T = VecT<EW>;
   __shared__ double hs[NV];
   for (int i = threadIdx.x; i < NV; i += blockDim.x) hs[i] = (i < nv) ? h[i] : 0.0;
@@ -744,6 +849,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_axpy_kernel(size_t NE, int
 // v = w * (1/s[0])   (Arnoldi normalisation; s on device)
 __global__ void scale_kernel(size_t N, const double* __restrict__ w, const double* __restrict__ s,
                              double* __restrict__ v) {
+  PDL_ENTRY();
   const double inv = 1.0 / s[0];
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride) v[t] = w[t] * inv;
@@ -751,6 +857,7 @@ __global__ void scale_kernel(size_t N, const double* __restrict__ w, const doubl
 
 // y = x + alpha*z  (x += z with alpha = 1)
 __global__ void axpy_kernel(size_t N, double alpha, const double* __restrict__ z, double* __restrict__ x) {
+  PDL_ENTRY();
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += stride)
     x[t] = fma(alpha, z[t], x[t]);
@@ -759,7 +866,8 @@ __global__ void axpy_kernel(size_t N, double alpha, const double* __restrict__ z
 // permutations between the caller's natural cell order and the internal order
 template <int B>
 __global__ void perm_gather_kernel(int n, const int* __restrict__ order, const double* __restrict__ src,
-                                   double* __restrict__ dst) {   // dst[p] = src[order[p]]
+                                   double* __restrict__ dst) {
+  PDL_ENTRY();   // dst[p] = src[order[p]]
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * B) return;
   const int p = t / B, q = t - p * B;
@@ -767,7 +875,8 @@ __global__ void perm_gather_kernel(int n, const int* __restrict__ order, const d
 }
 template <int B>
 __global__ void perm_scatter_kernel(int n, const int* __restrict__ order, const double* __restrict__ src,
-                                    double* __restrict__ dst) {  // dst[order[p]] = src[p]
+                                    double* __restrict__ dst) {
+  PDL_ENTRY();  // dst[order[p]] = src[p]
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * B) return;
   const int p = t / B, q = t - p * B;
@@ -776,6 +885,7 @@ __global__ void perm_scatter_kernel(int n, const int* __restrict__ order, const 
 
 __global__ void scalar_perm_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                                    double* __restrict__ dst, int scatter) {
+  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (scatter) dst[ldg(idx + i)] = src[i];

@@ -39,6 +39,22 @@ struct CudaError {
 
 inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Launch with programmatic stream serialisation (PDL, see kernels.cuh) when enabled.
+template <typename... KArgs, typename... Args>
+void klaunch(cudaStream_t s, bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 struct DevLevel {
   int32_t n = 0, ncolor = 0, nslices = 0;
   std::vector<int32_t> color_row;    // host: row range per color (permuted)
@@ -56,6 +72,7 @@ struct DevLevel {
   double *b = nullptr, *x = nullptr, *r = nullptr;
   int64_t nnz_alloc = 0;
   int lpr = 1;                       // lanes per row (coarse levels)
+  int tail = 1 << 30;                // first color handled by the single-CTA tail kernel
   int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
 };
 
@@ -80,6 +97,7 @@ struct msp_handle {
   int32_t *rp = nullptr, *ci = nullptr, *dg = nullptr, *d_order = nullptr;
   double *Aval = nullptr, *Fval = nullptr, *W = nullptr, *Pcol = nullptr;
   int32_t* l0_of_cell = nullptr;
+  int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
   int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0;
   std::vector<int32_t> color_blk;    // host
@@ -90,6 +108,7 @@ struct msp_handle {
   int32_t nL = 0, ldA = 0;
   VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
   int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
+  bool pdl = true;                   // programmatic dependent launch for every kernel
   bool coarse_diag = false;
   double *Ainv = nullptr, *cdiag = nullptr, *bL = nullptr, *xL = nullptr;
   // work vectors
@@ -295,6 +314,18 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
     const double avg = (double)A.nnz() / std::max<int32_t>(n, 1);
     L.lpr = (avg <= 8.0) ? 1 : (avg <= 20.0 ? 4 : 8);
     if (const char* e = std::getenv("MSP_LPR")) L.lpr = std::atoi(e);
+    // trailing colors whose rows fit one 1024-thread CTA pass each (rows * LPR <= 1024 per
+    // color and <= 2048 in total) run as one single-CTA kernel
+    int tail_rows = 0, t = ncolor;
+    const int lim_env = std::getenv("MSP_TAIL_ROWS") ? std::atoi(std::getenv("MSP_TAIL_ROWS")) : 2048;
+    const int lim_col = std::getenv("MSP_TAIL_COLOR") ? std::atoi(std::getenv("MSP_TAIL_COLOR")) : 1024;
+    while (t > 1) {
+      const int rows = cnt[t] - cnt[t - 1];
+      if (rows * L.lpr > lim_col || tail_rows + rows * L.lpr > lim_env) break;
+      tail_rows += rows * L.lpr;
+      --t;
+    }
+    L.tail = (ncolor - t >= 2) ? t : (1 << 30);
   }
   {
     std::vector<int32_t> rs(n), rw(n);
@@ -430,6 +461,9 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     std::vector<int32_t> l0(n);
     for (int32_t p = 0; p < n; ++p) l0[p] = (L > 0) ? perms[0][S.order[p]] : S.order[p];
     h->l0_of_cell = h->upload(l0);
+    std::vector<int32_t> inv(n);
+    for (int32_t p = 0; p < n; ++p) inv[l0[p]] = p;
+    h->cell_of_l0 = h->upload(inv);
   }
   // coarsest
   h->bL = h->dalloc<double>(h->nL);
@@ -553,20 +587,20 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
 
 // ----------------------------------------------------------------- launches
 template <int B>
-void launch_spmv_t(cudaStream_t s, int mode, int n, const int* rp, const int* ci, const double* val,
+void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, const int* ci, const double* val,
                    const double* x, const double* g, double* y) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   const unsigned grid = nblk((size_t)n * TS, 256);
-  if (mode == 0) bsr_spmv_kernel<B, 0><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
-  else if (mode == 1) bsr_spmv_kernel<B, 1><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
-  else bsr_spmv_kernel<B, 2><<<grid, 256, 0, s>>>(n, rp, ci, val, x, g, y);
+  if (mode == 0) klaunch(s, pdl, bsr_spmv_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
+  else if (mode == 1) klaunch(s, pdl, bsr_spmv_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
+  else klaunch(s, pdl, bsr_spmv_kernel<B, 2>, grid, 256, n, rp, ci, val, x, g, y);
 }
 
 void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
   switch (h->b) {
-#define CASE(BV) case BV: launch_spmv_t<BV>(h->s, mode, h->n, h->rp, h->ci, val, x, g, y); break;
+#define CASE(BV) case BV: launch_spmv_t<BV>(h->s, h->pdl, mode, h->n, h->rp, h->ci, val, x, g, y); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -582,11 +616,11 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
     if (kind == 0)
-      bilu_block_kernel<B, MAXC, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else if (kind == 1)
-      bilu_block_kernel<B, MAXC, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else
-      bilu_block_kernel<B, MAXC, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
   };
   for (int c = 0; c < g - 1; ++c) run(c, 0);
   run(g - 1, 2);
@@ -609,11 +643,11 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z) {
     const unsigned grid = nblk((size_t)(b1 - b0) * TS, 128);
     ++h->nlaunch;
     if (kind == 0)
-      bilu_color_kernel<B, true, false><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_color_kernel<B, true, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
     else if (kind == 1)
-      bilu_color_kernel<B, false, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_color_kernel<B, false, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
     else
-      bilu_color_kernel<B, true, true><<<grid, 128, 0, h->s>>>(b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_color_kernel<B, true, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->Fval, v, wp, z);
   };
   for (int c = 0; c < g - 1; ++c) run(c, 0);
   run(g - 1, 2);
@@ -628,19 +662,29 @@ void launch_bilu(msp_handle* h, double* v, const double* wp, double* z) {
   }
 }
 
-void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0) {
+// a3 (+ the fused zero-guess first color of level 0 when it has a PGS-MC level)
+void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool fuse_init) {
   const unsigned grid = nblk(h->n, 256);
+  double* x0 = nullptr;
+  const double* d0 = nullptr;
+  int c1 = 0;
+  if (fuse_init && !h->lv.empty() && h->prm.pre_sweeps > 0) {
+    x0 = h->lv[0].x;
+    d0 = h->lv[0].diag;
+    c1 = h->lv[0].color_row[1];
+  }
   switch (h->b) {
-#define CASE(BV) case BV: restrict_pressure_kernel<BV><<<grid, 256, 0, h->s>>>(h->n, h->W, g, h->l0_of_cell, rp0); ++h->nlaunch; break;
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, restrict_pressure_kernel<BV>, grid, 256, h->n, h->W, g, h->cell_of_l0, rp0, x0, d0, c1); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
+  ++h->nlaunch;
 }
 
 template <int LPR, bool WR, bool RES>
 void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
   if (s1 <= s0) return;
-  sell_row_kernel<LPR, WR, RES><<<nblk((size_t)(s1 - s0) * kSell * LPR, 128), 128, 0, h->s>>>(
+  klaunch(h->s, h->pdl, sell_row_kernel<LPR, WR, RES>, nblk((size_t)(s1 - s0) * kSell * LPR, 128), 128, 
       s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
   ++h->nlaunch;
 }
@@ -654,39 +698,65 @@ void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
   }
 }
 
+void sell_tail(msp_handle* h, DevLevel& L, int c0, int c1, bool asc, bool write_r) {
+  switch (L.lpr) {
+#define CASE(LP) case LP: klaunch(h->s, h->pdl, sell_tail_kernel<LP>, 1, 1024, c0, c1, asc, write_r, L.d_color_slice, \
+      L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r); break;
+    CASE(2) CASE(4) CASE(8)
+    default: klaunch(h->s, h->pdl, sell_tail_kernel<1>, 1, 1024, c0, c1, asc, write_r, L.d_color_slice, L.slice_row,
+                                                       L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
+#undef CASE
+  }
+  ++h->nlaunch;
+}
+
 // One PGS-MC sweep of level L (Alg. 4).  write_r: the last color also writes the
 // residual of its rows (caller then computes the residual of the other colors).
-void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool write_r = false) {
+// from_zero: the first color starts from the zero guess; init_done: that first color was
+// already computed by the kernel that produced b (fused a3 / restriction).
+void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool write_r = false,
+               bool init_done = false) {
   if (ascending) {
     int c = 0;
     if (from_zero) {
-      pgs_init_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.color_row[1], L.diag, L.b, L.x); ++h->nlaunch;
+      if (!init_done) {
+        klaunch(h->s, h->pdl, pgs_init_kernel, nblk(L.n, 256), 256, L.n, L.color_row[1], L.diag, L.b, L.x);
+        ++h->nlaunch;
+      }
       c = 1;
       if (L.ncolor == 1 && write_r) {              // single color: residual of all rows
         sell_rows_any<false, true>(h, L, 0, L.nslices);
         return;
       }
     }
-    for (; c < L.ncolor; ++c) {
+    const int cend = std::min(L.ncolor, std::max(c, L.tail));
+    for (; c < cend; ++c) {
       const bool last = (c == L.ncolor - 1);
       if (last && write_r) sell_rows_any<true, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
       else sell_rows_any<false, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
     }
+    if (c < L.ncolor) sell_tail(h, L, c, L.ncolor - 1, true, write_r);
     if (write_r && L.ncolor > 1)                   // residual of colors 1..g-1 (not the last)
       sell_rows_any<false, true>(h, L, 0, L.color_slice[L.ncolor - 1]);
   } else {
-    for (int c = L.ncolor - 1; c >= 0; --c) sell_rows_any<false, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
+    int c = L.ncolor - 1;
+    if (L.tail <= c) {
+      sell_tail(h, L, L.tail, c, false, false);
+      c = L.tail - 1;
+    }
+    for (; c >= 0; --c) sell_rows_any<false, false>(h, L, L.color_slice[c], L.color_slice[c + 1]);
   }
 }
 
 // V-cycle on level l; input in lv[l].b (or bL), output in lv[l].x (or xL).
-void vcycle(msp_handle* h, int l) {
+// init_done: the zero-guess first color of level l was fused into b's producer.
+void vcycle(msp_handle* h, int l, bool init_done = false) {
   if (l == (int)h->lv.size()) {
     ++h->nlaunch;
     if (h->coarse_diag)
-      diag_solve_kernel<<<nblk(h->nL, 256), 256, 0, h->s>>>(h->nL, h->cdiag, h->bL, h->xL);
+      klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
     else
-      gemv4_kernel<<<nblk((size_t)h->nL * 32, 256), 256, 0, h->s>>>(h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+      klaunch(h->s, h->pdl, gemv4_kernel, nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
     return;
   }
   DevLevel& L = h->lv[l];
@@ -694,21 +764,27 @@ void vcycle(msp_handle* h, int l) {
   double* bn = last ? h->bL : h->lv[l + 1].b;
   double* xn = last ? h->xL : h->lv[l + 1].x;
   const int nn = last ? h->nL : h->lv[l + 1].n;
-  for (int s = 0; s < h->prm.pre_sweeps; ++s) pgs_sweep(h, L, true, s == 0, s + 1 == h->prm.pre_sweeps);
+  for (int s = 0; s < h->prm.pre_sweeps; ++s)
+    pgs_sweep(h, L, true, s == 0, s + 1 == h->prm.pre_sweeps, s == 0 && init_done);
   if (h->prm.pre_sweeps == 0) {
     CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
     sell_rows_any<false, true>(h, L, 0, L.nslices);
   }
-  restrict_kernel<<<nblk(nn, 256), 256, 0, h->s>>>(nn, L.pt_ptr, L.pt_idx, L.r, bn); ++h->nlaunch;
-  vcycle(h, l + 1);
-  prolong_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.agg, xn, L.x); ++h->nlaunch;
+  const bool fuse_next = !last && h->prm.pre_sweeps > 0;
+  klaunch(h->s, h->pdl, restrict_kernel, nblk(nn, 256), 256, nn, L.pt_ptr, L.pt_idx, L.r, bn,
+                                                   fuse_next ? h->lv[l + 1].x : nullptr,
+                                                   fuse_next ? h->lv[l + 1].diag : nullptr,
+                                                   fuse_next ? h->lv[l + 1].color_row[1] : 0);
+  ++h->nlaunch;
+  vcycle(h, l + 1, fuse_next);
+  klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, xn, L.x); ++h->nlaunch;
   for (int s = 0; s < h->prm.post_sweeps; ++s) pgs_sweep(h, L, false, false);
 }
 
 double* level0_b(msp_handle* h) { return h->lv.empty() ? h->bL : h->lv[0].b; }
 double* level0_x(msp_handle* h) { return h->lv.empty() ? h->xL : h->lv[0].x; }
 
-void vcycle_any(msp_handle* h) {
+void vcycle_any(msp_handle* h, bool init_done = false) {
   if (h->dvp) {
     void* args[] = {(void*)&h->dvp};
     void* fn = (h->coop_tpb == 1024) ? (void*)vcycle_coop_kernel<1024>
@@ -716,15 +792,16 @@ void vcycle_any(msp_handle* h) {
     CK(cudaLaunchCooperativeKernel(fn, h->coop_grid, h->coop_tpb, args, 0, h->s));
     ++h->nlaunch;
   } else {
-    vcycle(h, 0);
+    vcycle(h, 0, init_done);
   }
 }
 
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
-  launch_restrict_pressure(h, g, level0_b(h));                        // a3: r_p = W^T g
-  vcycle_any(h);                                                       // a4-a7: B_P
-  gather_kernel<<<nblk(h->n, 256), 256, 0, h->s>>>(h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
+  const bool fuse = !h->dvp;                                           // coop path inits itself
+  launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
+  vcycle_any(h, fuse);                                                 // a4-a7: B_P
+  klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
   launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
   launch_bilu(h, h->r, h->wp, h->z == z ? z : z);                      // a9: z = Pi_P x_p + R r
 }
@@ -732,7 +809,7 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
 // ----------------------------------------------------------------- GMRES pieces
 template <int NV>
 void multidot_t(msp_handle* h, int nv, const double* V, const double* w) {
-  multidot_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, w, h->part); ++h->nlaunch;
+  klaunch(h->s, h->pdl, multidot_kernel<NV>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, w, h->part); ++h->nlaunch;
 }
 void multidot(msp_handle* h, int nv, const double* V, const double* w) {
   if (nv <= 4) multidot_t<4>(h, nv, V, w);
@@ -742,7 +819,7 @@ void multidot(msp_handle* h, int nv, const double* V, const double* w) {
 }
 template <int NV>
 void maxpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
-  multiaxpy_kernel<NV><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, nv, V, h->N, coef, w, from_zero, part, 0); ++h->nlaunch;
+  klaunch(h->s, h->pdl, multiaxpy_kernel<NV>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, coef, w, from_zero, part, 0); ++h->nlaunch;
 }
 void maxpy(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
   if (nv <= 4) maxpy_t<4>(h, nv, V, coef, w, from_zero, part);
@@ -753,23 +830,23 @@ void maxpy(msp_handle* h, int nv, const double* V, const double* coef, double* w
 void reduce(msp_handle* h, int nv, double* out, const double* addend, double* raw, int sqrt_index) {
   // raw (optional) receives the plain sums, out = addend + sums
   if (raw) {
-    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, nv, h->part, raw, nullptr, sqrt_index);
+    klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, nv, h->part, raw, nullptr, sqrt_index);
     ++h->nlaunch;
   }
-  reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, nv, h->part, out, addend, sqrt_index); ++h->nlaunch;
+  klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, nv, h->part, out, addend, sqrt_index); ++h->nlaunch;
 }
 
 // ||w||^2 -> out[0] = ||w||
 void norm_dev(msp_handle* h, const double* w, double* out) {
   multidot_t<4>(h, 1, w, w);
-  reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
+  klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
 }
 
 template <int NV>
 void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
                double* raw, int sq) {
   constexpr int EW = (NV <= 16) ? 2 : 1;
-  cgs_dot_kernel<NV, EW><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
+  klaunch(h->s, h->pdl, cgs_dot_kernel<NV, EW>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
                                                               sq, h->ticket);
   ++h->nlaunch;
 }
@@ -784,7 +861,7 @@ template <int NV, bool DOT>
 void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
                 const double* addend, double* raw, int sq) {
   constexpr int EW = (NV <= 16) ? 2 : 1;
-  cgs_axpy_kernel<NV, EW, DOT><<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N / EW, nv, V, h->N, coef, w, h->part, out,
+  klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, EW, DOT>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, coef, w, h->part, out,
                                                                     addend, raw, sq, h->ticket);
   ++h->nlaunch;
 }
@@ -804,7 +881,7 @@ void cgs2(msp_handle* h, int nv, double* w) {
   cgs_dot(h, nv, h->V, w, h->dh1, nullptr, nullptr, -1);
   cgs_axpy<true>(h, nv, h->V, h->dh1, w, h->hcol, h->dh1, h->dh2, -1);
   cgs_axpy<false>(h, nv, h->V, h->dh2, w, h->hcol + nv, nullptr, nullptr, 0);
-  scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(h->N, w, h->hcol + nv, w);
+  klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, h->N, w, h->hcol + nv, w);
   ++h->nlaunch;
 }
 
@@ -822,11 +899,11 @@ void arnoldi_step(msp_handle* h, int j) {
   } else {
     for (int i = 0; i < nv; ++i) {
       multidot_t<4>(h, 1, h->V + (size_t)i * N, w);
-      reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + i, nullptr, -1); ++h->nlaunch;
+      klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, h->hcol + i, nullptr, -1); ++h->nlaunch;
       maxpy_t<4>(h, 1, h->V + (size_t)i * N, h->hcol + i, w, 0, (i == nv - 1) ? h->part : nullptr);
     }
-    reduce_parts_kernel<<<1, 1024, 0, h->s>>>(kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
-    scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, w, h->hcol + nv, w); ++h->nlaunch;
+    klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, w, h->hcol + nv, w); ++h->nlaunch;
   }
   CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
 }
@@ -898,7 +975,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gam(m + 1), y(m);
   if (rel > tol) {
     while (true) {
-      scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, h->r, h->hcol, h->V); ++h->nlaunch;   // v_0 = r / beta
+      klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, h->r, h->hcol, h->V); ++h->nlaunch;   // v_0 = r / beta
       std::fill(gam.begin(), gam.end(), 0.0);
       gam[0] = beta;
       int k = 0;
@@ -935,7 +1012,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       CK(cudaMemcpyAsync(h->dh1, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, h->s));
       maxpy(h, k, h->V, h->dh1, h->u, 1, nullptr);
       msp_apply_dev(h, h->u, h->z);
-      axpy_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, 1.0, h->z, h->xin); ++h->nlaunch;
+      klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->z, h->xin); ++h->nlaunch;
       launch_spmv(h, 1, h->xin, h->bin, h->r);
       norm_dev(h, h->r, h->hcol);
       CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
@@ -982,7 +1059,7 @@ void to_internal(msp_handle* h, const double* src, double* dst, size_t count_cel
     CK(cudaMemcpyAsync(h->io, src, sizeof(double) * N, cudaMemcpyHostToDevice, h->s));
   }
   switch (b) {
-#define CASE(BV) case BV: perm_gather_kernel<BV><<<nblk(N, 256), 256, 0, h->s>>>(h->n, h->d_order, h->io, dst); ++h->nlaunch; break;
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, perm_gather_kernel<BV>, nblk(N, 256), 256, h->n, h->d_order, h->io, dst); ++h->nlaunch; break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -990,7 +1067,7 @@ void to_internal(msp_handle* h, const double* src, double* dst, size_t count_cel
 void from_internal(msp_handle* h, const double* src, double* dst, int b) {
   const size_t N = (size_t)h->n * b;
   switch (b) {
-#define CASE(BV) case BV: perm_scatter_kernel<BV><<<nblk(N, 256), 256, 0, h->s>>>(h->n, h->d_order, src, h->io); ++h->nlaunch; break;
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, perm_scatter_kernel<BV>, nblk(N, 256), 256, h->n, h->d_order, src, h->io); ++h->nlaunch; break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -1036,6 +1113,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
@@ -1146,10 +1224,10 @@ msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, i
   if (!h || level < 0 || level >= (int)h->lv.size()) return fail(h, MSP_EINVAL, "msp_pgs_sweep: bad level");
   return guarded(h, [&]() -> msp_status {
     DevLevel& L = h->lv[level];
-    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, b, L.b, 1); ++h->nlaunch;
-    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, x, L.x, 1); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, b, L.b, 1); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, x, L.x, 1); ++h->nlaunch;
     pgs_sweep(h, L, ascending != 0, false);
-    scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, L.x, x, 0); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, L.x, x, 0); ++h->nlaunch;
     CK(cudaStreamSynchronize(h->s));
     return MSP_OK;
   });
@@ -1164,9 +1242,9 @@ msp_status msp_vcycle(msp_handle* h, const double* r, double* x) {
       CK(cudaMemcpyAsync(x, h->xL, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
     } else {
       DevLevel& L = h->lv[0];
-      scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, r, L.b, 1); ++h->nlaunch;
+      klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, r, L.b, 1); ++h->nlaunch;
       vcycle_any(h);
-      scalar_perm_kernel<<<nblk(L.n, 256), 256, 0, h->s>>>(L.n, L.perm, L.x, x, 0); ++h->nlaunch;
+      klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, L.x, x, 0); ++h->nlaunch;
     }
     CK(cudaStreamSynchronize(h->s));
     return MSP_OK;
@@ -1229,7 +1307,7 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
     double bytes = 0.0;
     // deterministic non-trivial inputs
     CK(cudaMemsetAsync(h->r, 0, sizeof(double) * N, h->s));
-    scale_kernel<<<kRedBlocks, kRedThreads, 0, h->s>>>(N, h->V, h->hcol, h->z); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, h->V, h->hcol, h->z); ++h->nlaunch;
     std::function<void()> fn;
     switch (kind) {
       case 0:
