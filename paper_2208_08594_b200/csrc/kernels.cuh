@@ -779,8 +779,8 @@ template <> __device__ __forceinline__ void vaxpy<2>(double c, const VecT<2>& v,
 }
 
 // pass A: h = V^T w (nv vectors); NE = N / EW elements of EW doubles
-template <int NV, int EW>
-__global__ void __launch_bounds__(kRedThreads, 2) cgs_dot_kernel(size_t NE, int nv, const double* __restrict__ V,
+template <int NV, int EW, int MINB = 2>
+__global__ void __launch_bounds__(kRedThreads, MINB) cgs_dot_kernel(size_t NE, int nv, const double* __restrict__ V,
                                                                  size_t ldv, const double* __restrict__ w,
                                                                  double* part, double* out, const double* addend,
                                                                  double* raw, int sqrt_index, unsigned* ticket) {
@@ -793,8 +793,10 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_dot_kernel(size_t NE, int 
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < NE; t += stride) {
     const T wt = T::ld(w, t);
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
+    for (int i = 0; i < NV; ++i) {
       if (i < nv) acc[i] = vdot<EW>(T::ld(V + i * ldv, t), wt, acc[i]);
+      if (i % 16 == 15) asm volatile("" ::: "memory");   // <= 16 loads in flight (registers)
+    }
   }
   block_partials<NV>(acc, nv, part);
   finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
@@ -806,8 +808,8 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_dot_kernel(size_t NE, int 
 // an L1 hit, which keeps registers low (full occupancy) instead of holding NV values.
 // NVD: the dot part covers only the first min(nv, NVD) vectors (the rest by a
 // separate cgs_dot pass), so that NV=32 axpys stay register-light.
-template <int NV, int EW, bool DOT, int NVD = NV>
-__global__ void __launch_bounds__(kRedThreads, 2) cgs_axpy_kernel(size_t NE, int nv, const double* __restrict__ V,
+template <int NV, int EW, bool DOT, int NVD = NV, int MINB = 2>
+__global__ void __launch_bounds__(kRedThreads, MINB) cgs_axpy_kernel(size_t NE, int nv, const double* __restrict__ V,
                                                                   size_t ldv, const double* __restrict__ h,
                                                                   double* __restrict__ w, double* part,
                                                                   double* out, const double* addend,
@@ -826,13 +828,17 @@ __global__ void __launch_bounds__(kRedThreads, 2) cgs_axpy_kernel(size_t NE, int
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < NE; t += stride) {
     T a = wT[t];
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
+    for (int i = 0; i < NV; ++i) {
       if (i < nv) vaxpy<EW>(-hs[i], T::ld(V + i * ldv, t), a);
+      if (i % 16 == 15) asm volatile("" ::: "memory");
+    }
     wT[t] = a;
     if constexpr (DOT) {
 #pragma unroll
-      for (int i = 0; i < NVD; ++i)  // re-read through L2 (.cg): not merged with the first read
+      for (int i = 0; i < NVD; ++i) {  // re-read through L2 (.cg): not merged with the first read
         if (i < nvd) acc[i] = vdot<EW>(T::ldcg(V + i * ldv, t), a, acc[i]);
+        if (i % 16 == 15) asm volatile("" ::: "memory");
+      }
     } else {
       acc[0] = vdot<EW>(a, a, acc[0]);
     }

@@ -109,6 +109,7 @@ struct msp_handle {
   VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
   int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
   bool pdl = true;                   // programmatic dependent launch for every kernel
+  int cgs_split = 0;                 // nv > 16: 16-vector halves (see cgs_dot / cgs_axpy)
   bool coarse_diag = false;
   double *Ainv = nullptr, *cdiag = nullptr, *bL = nullptr, *xL = nullptr;
   // work vectors
@@ -842,11 +843,14 @@ void norm_dev(msp_handle* h, const double* w, double* out) {
   klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
 }
 
+constexpr bool kCgsWide32 = false;         // NV=32 basis kernels use 8-byte loads
+
 template <int NV>
 void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
                double* raw, int sq) {
-  constexpr int EW = (NV <= 16) ? 2 : 1;
-  klaunch(h->s, h->pdl, cgs_dot_kernel<NV, EW>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
+  constexpr int EW = (NV <= 16 || kCgsWide32) ? 2 : 1;
+  constexpr int MINB = 2;
+  klaunch(h->s, h->pdl, cgs_dot_kernel<NV, EW, MINB>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
                                                               sq, h->ticket);
   ++h->nlaunch;
 }
@@ -855,13 +859,18 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
   if (nv <= 4) cgs_dot_t<4>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_dot_t<8>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_dot_t<16>(h, nv, V, w, out, addend, raw, sq);
-  else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
+  else if (h->cgs_split) {                   // 16-vector halves, 16-byte loads
+    cgs_dot_t<16>(h, 16, V, w, out, addend, raw, -1);
+    cgs_dot(h, nv - 16, V + (size_t)16 * h->N, w, out + 16, addend ? addend + 16 : nullptr,
+            raw ? raw + 16 : nullptr, sq >= 16 ? sq - 16 : -1);
+  } else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
 }
 template <int NV, bool DOT>
 void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
                 const double* addend, double* raw, int sq) {
-  constexpr int EW = (NV <= 16) ? 2 : 1;
-  klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, EW, DOT>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, coef, w, h->part, out,
+  constexpr int EW = (NV <= 16 || kCgsWide32) ? 2 : 1;
+  constexpr int MINB = 2;
+  klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, EW, DOT, NV, MINB>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, coef, w, h->part, out,
                                                                     addend, raw, sq, h->ticket);
   ++h->nlaunch;
 }
@@ -871,7 +880,15 @@ void cgs_axpy(msp_handle* h, int nv, const double* V, const double* coef, double
   if (nv <= 4) cgs_axpy_t<4, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_axpy_t<8, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_axpy_t<16, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
-  else cgs_axpy_t<32, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
+  else if (DOT && h->cgs_split) {
+    // axpy over all nv vectors (16-byte loads, 16 in flight) with the dot over the first
+    // 16, then the dot of the remaining vectors as a separate pass
+    klaunch(h->s, h->pdl, cgs_axpy_kernel<32, 2, true, 16, 2>, kRedBlocks, kRedThreads, h->N / 2, nv, V, h->N,
+            coef, w, h->part, out, addend, raw, -1, h->ticket);
+    ++h->nlaunch;
+    cgs_dot(h, nv - 16, V + (size_t)16 * h->N, w, out + 16, addend ? addend + 16 : nullptr,
+            raw ? raw + 16 : nullptr, -1);
+  } else cgs_axpy_t<32, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
 }
 
 // CGS2 (R8) on w = V[nv] against V[0..nv): hcol[0..nv) = h1 + h2, hcol[nv] = ||w||,
@@ -1114,6 +1131,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
