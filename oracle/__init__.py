@@ -39,7 +39,7 @@ def lib():
         for name in ("orc_msp_update_values", "orc_msp_destroy", "orc_msp_info", "orc_msp_level_n",
                      "orc_msp_level_csr", "orc_msp_level_colors", "orc_msp_level_agg",
                      "orc_msp_weights", "orc_msp_order", "orc_msp_bilu_factors", "orc_msp_vcycle",
-                     "orc_msp_bilu_apply", "orc_msp_apply", "orc_msp_solve"):
+                     "orc_msp_bilu_apply", "orc_msp_apply", "orc_msp_solve", "orc_msp_bgs_apply"):
             getattr(_lib, name).argtypes = None
     return _lib
 
@@ -268,6 +268,12 @@ class Msp:
         x = np.zeros(self.n * self.b)
         lib().orc_msp_bilu_apply(self.h, _p(_c(r, F64)), _p(x))
         return x
+
+    def bgs_apply(self, r):
+        wN = np.zeros(self.n * (self.b - 1))
+        if lib().orc_msp_bgs_apply(self.h, _p(_c(r, F64)), _p(wN)):
+            raise OracleError("bgs_apply needs stages=3")
+        return wN
 
     def apply(self, g):
         w = np.zeros(self.n * self.b)

@@ -734,8 +734,9 @@ static void bilu_apply(const Bilu& R, const double* r, double* x) {
 }
 
 // ---------------------------------------------------------------------------
-// NEXT-1: B_N = block GS on Π_N^T A Π_N: one forward sweep in natural
-// cell order, zero initial guess, on the nc x nc N-N blocks.
+// NEXT-1: B_N = block GS on A_NN = Π_N^T A Π_N (R12): one forward
+// block Gauss-Seidel sweep from the zero guess over the nc x nc N-N blocks, in the
+// BILU (ABMC) cell order of c-9: w_i = D_NN,i^-1 (r_N,i - sum_{k before i} A_NN,ik w_k).
 // ---------------------------------------------------------------------------
 struct Bgs {
   std::vector<double> Dinv;   // n * nc*nc inverse of the N-N diagonal block
@@ -791,16 +792,17 @@ static bool pressure_stage(const Msp& M, const std::vector<double>& r, std::vect
 }
 
 static void bgs_stage(const Msp& M, const std::vector<double>& r, std::vector<double>& wN) {
-  // one forward block GS sweep on A_NN in natural order, zero initial guess
+  // one forward block GS sweep on A_NN in the BILU cell order, zero initial guess
   const int n = M.A.n, b = M.A.b, nc = b - 1;
   wN.assign((size_t)n * nc, 0.0);
   std::vector<double> t(nc);
-  for (int c = 0; c < n; ++c) {
+  for (int p = 0; p < n; ++p) {
+    const int c = M.R.order[p];
     for (int i = 0; i < nc; ++i) {
       double s = 0.0;
       for (int e = M.A.ptr[c]; e < M.A.ptr[c + 1]; ++e) {
-        int d = M.A.col[e];
-        if (d == c) continue;
+        const int d = M.A.col[e];
+        if (M.R.pos[d] >= p) continue;        // only cells before c in the order
         for (int k = 0; k < nc; ++k) s += M.A.blk(e)[(1 + i) * b + 1 + k] * wN[(size_t)d * nc + k];
       }
       t[i] = r[(size_t)c * b + 1 + i] - s;
@@ -1192,6 +1194,16 @@ int orc_msp_bilu_apply(void* h, const double* r, double* x) {
   return 0;
 }
 int orc_msp_apply(void* h, const double* g, double* w) { return msp_apply(*(Msp*)h, g, w) ? 0 : 2; }
+
+// B_N r (stages = 3 handles only): N-part of the result, n*nc doubles
+int orc_msp_bgs_apply(void* h, const double* r, double* wN) {
+  Msp* M = (Msp*)h;
+  if (M->cfg.stages != 3) return 1;
+  std::vector<double> rv(r, r + (size_t)M->A.n * M->A.b), w;
+  bgs_stage(*M, rv, w);
+  std::copy(w.begin(), w.end(), wN);
+  return 0;
+}
 
 int orc_msp_solve(void* h, const double* b, double* x, double tol, int restart, int maxit, int* iters,
                   double* final_rel, double* hist, int cap, int* hlen) {

@@ -514,6 +514,50 @@ def test_msp_operator_identity_eq21():
     assert np.allclose(M.apply(2 * g1 - g2), 2 * M.apply(g1) - M.apply(g2), atol=1e-12)
 
 
+def test_msp_operator_identity_eq21_three_stages():
+    """Full Eq. 21 with stages NPR: I - BA == (I - RA)(I - Pi_P B_P W^T A)(I - Pi_N B_N Pi_N^T A)."""
+    p = gen.make_config("C1", nx=2, ny=2, nz=1, nc=2)        # 4 cells, b=3 -> 12 unknowns
+    n, b = p["n"], p["b"]
+    N, nc = n * b, b - 1
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=2, stages=3)
+    A = bsr_dense(p)
+    W = M.weights()
+    Wt = np.zeros((n, N)); Pi = np.zeros((N, n)); PiN = np.zeros((N, n * nc))
+    for c in range(n):
+        Wt[c, c * b:(c + 1) * b] = W[c]; Pi[c * b, c] = 1
+        for i in range(nc):
+            PiN[c * b + 1 + i, c * nc + i] = 1
+    I = np.eye(N)
+    B = np.column_stack([M.apply(e) for e in I])
+    R = np.column_stack([M.bilu_apply(e) for e in I])
+    BP = np.column_stack([M.vcycle(e) for e in np.eye(n)])
+    BN = np.column_stack([M.bgs_apply(PiN @ e) for e in np.eye(n * nc)])   # B_N on Pi_N^T r
+    rhs = (I - R @ A) @ (I - Pi @ BP @ Wt @ A) @ (I - PiN @ BN @ PiN.T @ A)
+    assert np.allclose(I - B @ A, rhs, atol=1e-12 * max(1, np.abs(rhs).max()))
+
+
+def test_bgs_is_block_forward_substitution_in_order():
+    """B_N = one forward block GS sweep on A_NN from zero in the BILU order: equals the
+    exact solve of the block-lower-triangular part (in that order) of A_NN (brute force)."""
+    p = gen.make_config("C2", nx=4, ny=3, nz=2, nc=2)
+    n, b = p["n"], p["b"]
+    nc = b - 1
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], stages=3)
+    order = M.order()
+    pos = np.empty(n, int); pos[order] = np.arange(n)
+    A = bsr_dense(p)
+    idxN = [c * b + 1 + i for c in range(n) for i in range(nc)]
+    ANN = A[np.ix_(idxN, idxN)]
+    Lw = np.zeros_like(ANN)
+    for c in range(n):
+        for d in range(n):
+            if pos[d] <= pos[c]:
+                Lw[c * nc:(c + 1) * nc, d * nc:(d + 1) * nc] = ANN[c * nc:(c + 1) * nc, d * nc:(d + 1) * nc]
+    r = np.random.default_rng(3).normal(size=n * b)
+    ref = np.linalg.solve(Lw, r[idxN])
+    assert np.allclose(M.bgs_apply(r), ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+
+
 def test_msp_exact_on_one_cell():
     rng = np.random.default_rng(11)
     blk = rng.normal(size=(4, 4)) + 5 * np.eye(4)
