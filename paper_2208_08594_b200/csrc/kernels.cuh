@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
 // vectors through register shuffles.  Same arithmetic as bilu_color_kernel, only
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
-template <int B, int MAXC, bool FWD, bool BWD>
+template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false>
 __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
@@ -580,9 +580,100 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     }
     if (act) {
       v[(size_t)i * B + q] = x;
-      z[(size_t)i * B + q] = x + ((q == 0) ? ldg(wp + i) : 0.0);
+      // z = w + R r: WFULL -> w is a full cell vector (stages NPR), else only the
+      // pressure correction wp (stages PR)
+      z[(size_t)i * B + q] = x + (WFULL ? ldg(wp + (size_t)i * B + q) : ((q == 0) ? ldg(wp + i) : 0.0));
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-1: B_N stage (Alg. 1 line 2): one forward block Gauss-Seidel sweep on
+// A_NN = Π_N^T A Π_N in the BILU (ABMC) order, zero initial guess (R12):
+//   w_i = D_NN,i^-1 (r_N,i - sum_{k before i} A_NN,ik w_k).
+// One launch per block color; team per aggregate block as bilu_block_kernel (lane q
+// = row q of the cell; rows 1..B-1 are the N rows).  A's blocks are column-major; the
+// N-N diagonal inverses Dn are (B-1)x(B-1) column-major per cell.  Output w is the full
+// cell-interleaved vector with w_i[0] = 0 (pressure slot).
+// ---------------------------------------------------------------------------
+template <int B, int MAXC>
+__global__ void __launch_bounds__(128) bgs_block_kernel(int b_first, int b_end,
+                                                        const int* __restrict__ blk_ptr,
+                                                        const int* __restrict__ rp,
+                                                        const int* __restrict__ ci,
+                                                        const int* __restrict__ dg,
+                                                        const int* __restrict__ cnt,
+                                                        const double* __restrict__ A,
+                                                        const double* __restrict__ Dn,
+                                                        const double* __restrict__ r,
+                                                        double* __restrict__ w) {
+  PDL_ENTRY();
+  constexpr int TS = (B <= 4) ? 4 : 8;
+  constexpr int TM = MAXC * TS;
+  constexpr int BB = B * B;
+  constexpr int NC = B - 1;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int blk = b_first + gtid / TM;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane % TM;
+  const int cq = tl / TS, q = tl % TS;
+  const int tbase = lane - tl, cbase = lane - q;
+  const unsigned tmask = (TM == 32) ? 0xffffffffu : (((1u << TM) - 1u) << tbase);
+  const unsigned cmask = ((1u << TS) - 1u) << cbase;
+  if (blk >= b_end) return;
+  const int c0 = ldg(blk_ptr + blk), c1 = ldg(blk_ptr + blk + 1);
+  const int nc = c1 - c0;
+  const bool valid = cq < nc;
+  const int i = c0 + (valid ? cq : 0);
+  const bool act = valid && q >= 1 && q < B;       // N rows
+  const int cn = valid ? ldg(cnt + i) : 0;
+  const int e0 = valid ? ldg(rp + i) : 0;
+  const int d = valid ? ldg(dg + i) : 0;
+  const int eext = e0 + (cn & 0xff);
+  double acc = 0.0;
+  for (int e = e0; e < eext; ++e) {                 // external part (earlier colors)
+    const int k = ldg(ci + e);
+    const double wq = (q >= 1 && q < B) ? w[(size_t)k * B + q] : 0.0;
+    const double* blkA = A + (size_t)e * BB;
+#pragma unroll
+    for (int u = 1; u < B; ++u) {
+      const double wu = __shfl_sync(cmask, wq, cbase + u);
+      if (act) acc = fma(ldg(blkA + u * B + q), wu, acc);
+    }
+  }
+  double t = act ? (ldg(r + (size_t)i * B + q) - acc) : 0.0;
+  double wi = 0.0;
+  int e = eext;                                     // intra-block entries (earlier cells)
+  const double* Di = Dn + (size_t)(valid ? i : 0) * NC * NC;
+#pragma unroll
+  for (int sidx = 0; sidx < MAXC; ++sidx) {
+    // cell sidx is complete: w_sidx = Dn^-1 t_sidx
+    double ws = 0.0;
+#pragma unroll
+    for (int u = 1; u < B; ++u) {
+      const double tu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
+      if (cq == sidx && act) ws = fma(ldg(Di + (u - 1) * NC + (q - 1)), tu, ws);
+    }
+    if (cq == sidx) wi = ws;
+    if (sidx == MAXC - 1) break;
+    const bool use = valid && cq > sidx && e < d && ldg(ci + e) == c0 + sidx;
+    const double* blkA = A + (size_t)(use ? e : 0) * BB;
+    double contrib = 0.0;
+#pragma unroll
+    for (int u = 1; u < B; ++u) {
+      const double wu = __shfl_sync(tmask, ws, tbase + sidx * TS + u);
+      if (use && act) contrib = fma(ldg(blkA + u * B + q), wu, contrib);
+    }
+    if (use) { t -= contrib; ++e; }
+  }
+  if (valid && q < B) w[(size_t)i * B + q] = (q == 0) ? 0.0 : wi;
+}
+
+// w_i[0] = wp_i (adds the pressure correction into the pressure slots of a full vector)
+__global__ void set_pressure_kernel(int n, int B, const double* __restrict__ wp, double* __restrict__ w) {
+  PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[(size_t)i * B] = ldg(wp + i);
 }
 
 // ---------------------------------------------------------------------------

@@ -96,6 +96,7 @@ struct msp_handle {
   // BSR (internal positions), shared pattern for A and the BILU factors
   int32_t *rp = nullptr, *ci = nullptr, *dg = nullptr, *d_order = nullptr;
   double *Aval = nullptr, *Fval = nullptr, *W = nullptr, *Pcol = nullptr;
+  double *Dn = nullptr, *wfull = nullptr, *r1 = nullptr;  // B_N stage (stages = 3)
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
@@ -393,6 +394,25 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->Pcol = h->upload(pc);
     CK(cudaStreamSynchronize(h->s));
   }
+  if (h->prm.stages == 3) {
+    const int nc = b - 1;
+    std::vector<double> Dn((size_t)n * nc * nc), D(nc * nc), Di(nc * nc);
+    for (int32_t p = 0; p < n; ++p) {
+      const int32_t c = S.order[p];
+      int32_t ed = -1;
+      for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) if (A.ci[e] == c) ed = e;
+      for (int i = 0; i < nc; ++i)
+        for (int k = 0; k < nc; ++k) D[i * nc + k] = A.v[(size_t)ed * bb + (1 + i) * b + 1 + k];
+      if (!msp::invert_block(nc, D.data(), Di.data()))
+        throw std::pair<int, std::string>(MSP_ESINGULAR, "BGS: singular N-N block at cell " + std::to_string(c));
+      for (int i = 0; i < nc; ++i)
+        for (int k = 0; k < nc; ++k) Dn[(size_t)p * nc * nc + k * nc + i] = Di[i * nc + k];   // column-major
+    }
+    h->Dn = h->upload(Dn);
+    h->wfull = h->dalloc<double>((size_t)n * b);
+    h->r1 = h->dalloc<double>((size_t)n * b);
+    if (h->max_blk > 4) throw std::pair<int, std::string>(MSP_EINVAL, "stages=3 needs aggregate blocks of <= 4 cells");
+  }
   {
     std::vector<double> Wi((size_t)n * b);
     for (int32_t p = 0; p < n; ++p)
@@ -607,7 +627,7 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
   }
 }
 
-template <int B, int MAXC>
+template <int B, int MAXC, bool WF = false>
 void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
   const int g = h->bilu_ncolor;
@@ -617,11 +637,11 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
     if (kind == 0)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else if (kind == 1)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
   };
   for (int c = 0; c < g - 1; ++c) run(c, 0);
   run(g - 1, 2);
@@ -629,7 +649,13 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
 }
 
 template <int B>
-void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z) {
+void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false) {
+  if (wfull) {                                         // z = w (full vector) + R r
+    if (h->max_blk <= 1) launch_bilu_block<B, 1, true>(h, v, wp, z);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2, true>(h, v, wp, z);
+    else launch_bilu_block<B, 4, true>(h, v, wp, z);
+    return;
+  }
   if (!h->bilu_v1 && h->max_blk <= 4) {
     if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z);
     else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z);
@@ -655,9 +681,9 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z) {
   for (int c = g - 2; c >= 0; --c) run(c, 1);
 }
 
-void launch_bilu(msp_handle* h, double* v, const double* wp, double* z) {
+void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false) {
   switch (h->b) {
-#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z); break;
+#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -797,14 +823,60 @@ void vcycle_any(msp_handle* h, bool init_done = false) {
   }
 }
 
+void msp_apply_npr(msp_handle* h, const double* g, double* z);
+
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
+  if (h->prm.stages == 3) {
+    msp_apply_npr(h, g, z);
+    return;
+  }
   const bool fuse = !h->dvp;                                           // coop path inits itself
   launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
   vcycle_any(h, fuse);                                                 // a4-a7: B_P
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
   launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
   launch_bilu(h, h->r, h->wp, h->z == z ? z : z);                      // a9: z = Pi_P x_p + R r
+}
+
+template <int B, int MAXC>
+void launch_bgs_t(msp_handle* h, const double* r, double* w) {
+  constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
+  for (int c = 0; c < h->bilu_ncolor; ++c) {
+    const int b0 = h->color_blk[c], b1 = h->color_blk[c + 1];
+    if (b1 <= b0) continue;
+    klaunch(h->s, h->pdl, bgs_block_kernel<B, MAXC>, nblk((size_t)(b1 - b0) * TM, 128), 128, b0, b1, h->blk_ptr,
+            h->rp, h->ci, h->dg, h->bcnt, h->Aval, h->Dn, r, w);
+    ++h->nlaunch;
+  }
+}
+template <int B>
+void launch_bgs_b(msp_handle* h, const double* r, double* w) {
+  if (h->max_blk <= 1) launch_bgs_t<B, 1>(h, r, w);
+  else if (h->max_blk <= 2) launch_bgs_t<B, 2>(h, r, w);
+  else launch_bgs_t<B, 4>(h, r, w);
+}
+void launch_bgs(msp_handle* h, const double* r, double* w) {
+  switch (h->b) {
+#define CASE(BV) case BV: launch_bgs_b<BV>(h, r, w); break;
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+}
+
+// Alg. 1 with all three stages (N, P, R; Eq. 21): w = Π_N B_N Π_N^T g; r = g - A w;
+// w += Π_P B_P W^T r; r = g - A w; z = w + R r.
+void msp_apply_npr(msp_handle* h, const double* g, double* z) {
+  launch_bgs(h, g, h->wfull);                                          // line 2 (r = g)
+  launch_spmv(h, 1, h->wfull, g, h->r1);                               // line 3: r = g - A w
+  launch_restrict_pressure(h, h->r1, level0_b(h), true);
+  vcycle(h, 0, true);                                                  // line 4
+  klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp);
+  ++h->nlaunch;
+  klaunch(h->s, h->pdl, set_pressure_kernel, nblk(h->n, 256), 256, h->n, h->b, h->wp, h->wfull);
+  ++h->nlaunch;
+  launch_spmv(h, 1, h->wfull, g, h->r);                                // line 5: r = g - A w
+  launch_bilu(h, h->r, h->wfull, z, true);                             // line 6: z = w + R r
 }
 
 // ----------------------------------------------------------------- GMRES pieces
@@ -1122,7 +1194,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   msp_config c;
   msp_config_default(&c);
   if (cfg) c = *cfg;
-  if (c.stages != 2) return fail(nullptr, MSP_EINVAL, "msp_setup: only stages=2 (P,R) is implemented on the GPU path");
+  if (c.stages != 2 && c.stages != 3) return fail(nullptr, MSP_EINVAL, "msp_setup: stages must be 2 (P,R) or 3 (N,P,R)");
   if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
   std::unique_ptr<msp_handle> h(new msp_handle);

@@ -116,7 +116,7 @@ def test_vcycle_parity(kw):
     assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0), dict(decoupling=1)])
+@pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0), dict(decoupling=1), dict(stages=3)])
 def test_bilu_and_msp_apply_parity(kw):
     p = gen.make_config("C2", nx=25, ny=20, nz=5)
     s = solver(p, coarsest_max_dof=100, **kw)
@@ -165,6 +165,9 @@ def check_solve(p, tol=1e-6, restart=30, **kw):
     ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100)),
     ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100)),
     ("C3", dict(nx=12, ny=44, nz=17), dict(coarsest_max_dof=300)),
+    ("C1", {}, dict(coarsest_max_dof=50, stages=3)),
+    ("C2", dict(nx=25, ny=20, nz=5), dict(coarsest_max_dof=100, stages=3)),
+    ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100, stages=3)),
 ])
 def test_solve_parity(name, gkw, kw):
     check_solve(gen.make_config(name, **gkw), **kw)
