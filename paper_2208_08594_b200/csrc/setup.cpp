@@ -3,7 +3,10 @@
 #include "setup.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -38,27 +41,82 @@ static Graph graph_from_pairs(int32_t n, const std::vector<std::pair<int32_t, in
 }
 
 Graph value_graph(const SpMat& A) {
-  std::vector<std::pair<int32_t, int32_t>> pr;
-  pr.reserve(2 * A.ci.size());
-  for (int32_t i = 0; i < A.n; ++i)
-    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e)
-      if (A.ci[e] != i && A.v[e] != 0.0) { pr.push_back({i, A.ci[e]}); pr.push_back({A.ci[e], i}); }
-  return graph_from_pairs(A.n, pr);
+  const int32_t n = A.n;
+  std::vector<int32_t> tp(n + 1, 0), tc(A.ci.size());
+  std::vector<uint8_t> tnz(A.ci.size());
+  for (int32_t j : A.ci) tp[j + 1]++;
+  for (int32_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+  {
+    std::vector<int32_t> f(tp.begin(), tp.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+      for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+        const int32_t q = f[A.ci[e]]++;
+        tc[q] = i;
+        tnz[q] = A.v[e] != 0.0;
+      }
+  }
+  Graph G;
+  G.xadj.assign(n + 1, 0);
+  G.adj.reserve(2 * A.ci.size());
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t e = A.rp[i], f = tp[i];
+    const int32_t ee = A.rp[i + 1], fe = tp[i + 1];
+    while (e < ee || f < fe) {
+      int32_t j;
+      bool on = false;
+      if (f >= fe || (e < ee && A.ci[e] < tc[f])) { j = A.ci[e]; on = A.v[e] != 0.0; ++e; }
+      else if (e >= ee || tc[f] < A.ci[e]) { j = tc[f]; on = tnz[f]; ++f; }
+      else { j = A.ci[e]; on = (A.v[e] != 0.0) || tnz[f]; ++e; ++f; }
+      if (j != i && on) G.adj.push_back(j);
+    }
+    G.xadj[i + 1] = (int32_t)G.adj.size();
+  }
+  return G;
 }
 
 Graph block_graph(const BlockMat& A) {
+  // nonzero flag per stored block, then symmetrise by merging each row with the
+  // transposed row (counting-sort transpose keeps both ascending)
   const int bb = A.b * A.b;
-  std::vector<std::pair<int32_t, int32_t>> pr;
-  for (int32_t i = 0; i < A.n; ++i)
-    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
-      const int32_t j = A.ci[e];
-      if (j == i) continue;
-      const double* B = &A.v[(size_t)e * bb];
-      bool nz = false;
-      for (int t = 0; t < bb && !nz; ++t) nz = (B[t] != 0.0);
-      if (nz) { pr.push_back({i, j}); pr.push_back({j, i}); }
+  const int32_t n = A.n;
+  std::vector<uint8_t> nz(A.ci.size(), 0);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < (int64_t)A.ci.size(); ++e) {
+    const double* B = &A.v[(size_t)e * bb];
+    bool f = false;
+    for (int t = 0; t < bb && !f; ++t) f = (B[t] != 0.0);
+    nz[e] = f;
+  }
+  std::vector<int32_t> tp(n + 1, 0), tc(A.ci.size());
+  std::vector<uint8_t> tnz(A.ci.size());
+  for (int32_t j : A.ci) tp[j + 1]++;
+  for (int32_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+  {
+    std::vector<int32_t> f(tp.begin(), tp.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+      for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+        const int32_t q = f[A.ci[e]]++;
+        tc[q] = i;
+        tnz[q] = nz[e];
+      }
+  }
+  Graph G;
+  G.xadj.assign(n + 1, 0);
+  G.adj.reserve(A.ci.size());
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t e = A.rp[i], f = tp[i];
+    const int32_t ee = A.rp[i + 1], fe = tp[i + 1];
+    while (e < ee || f < fe) {
+      int32_t j;
+      bool on = false;
+      if (f >= fe || (e < ee && A.ci[e] < tc[f])) { j = A.ci[e]; on = nz[e]; ++e; }
+      else if (e >= ee || tc[f] < A.ci[e]) { j = tc[f]; on = tnz[f]; ++f; }
+      else { j = A.ci[e]; on = nz[e] || tnz[f]; ++e; ++f; }
+      if (j != i && on) G.adj.push_back(j);
     }
-  return graph_from_pairs(A.n, pr);
+    G.xadj[i + 1] = (int32_t)G.adj.size();
+  }
+  return G;
 }
 
 // ---------------------------------------------------------------------------
@@ -136,34 +194,41 @@ int32_t color_groups(const Graph& G, std::vector<int32_t>& color) {
 // ---------------------------------------------------------------------------
 int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg) {
   const int32_t n = A.n;
-  struct Trip { int32_t r, c; double a; bool transposed; };
-  std::vector<Trip> tr;
-  tr.reserve(2 * A.ci.size());
-  for (int32_t i = 0; i < n; ++i)
-    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
-      const int32_t j = A.ci[e];
-      if (j == i) continue;
-      tr.push_back({i, j, A.v[e], false});      // a_ij seen from row i
-      tr.push_back({j, i, A.v[e], true});       // a_ij as the transposed entry of row j
-    }
-  std::sort(tr.begin(), tr.end(), [](const Trip& x, const Trip& y) {
-    return x.r != y.r ? x.r < y.r : x.c < y.c;
-  });
+  // transpose (counting sort by column keeps rows ascending), then per-row merge of
+  // the row (j, a_ij) and the transposed row (j, a_ji): t_ij = a_ij + a_ji
+  std::vector<int32_t> tp(n + 1, 0), tc(A.ci.size());
+  std::vector<double> tv(A.ci.size());
+  for (int32_t j : A.ci) tp[j + 1]++;
+  for (int32_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+  {
+    std::vector<int32_t> f(tp.begin(), tp.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+      for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+        const int32_t q = f[A.ci[e]]++;
+        tc[q] = i;
+        tv[q] = A.v[e];
+      }
+  }
   std::vector<int32_t> xadj(n + 1, 0), adj;
   std::vector<double> tval;
-  for (size_t s = 0; s < tr.size();) {
-    size_t e = s;
-    double aij = 0.0, aji = 0.0;
-    for (; e < tr.size() && tr[e].r == tr[s].r && tr[e].c == tr[s].c; ++e) {
-      if (tr[e].transposed) aji = tr[e].a;
-      else aij = tr[e].a;
+  adj.reserve(2 * A.ci.size());
+  tval.reserve(2 * A.ci.size());
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t e = A.rp[i], f = tp[i];
+    const int32_t ee = A.rp[i + 1], fe = tp[i + 1];
+    while (e < ee || f < fe) {
+      int32_t j;
+      double aij = 0.0, aji = 0.0;
+      if (f >= fe || (e < ee && A.ci[e] < tc[f])) { j = A.ci[e]; aij = A.v[e]; ++e; }
+      else if (e >= ee || tc[f] < A.ci[e]) { j = tc[f]; aji = tv[f]; ++f; }
+      else { j = A.ci[e]; aij = A.v[e]; aji = tv[f]; ++e; ++f; }
+      if (j == i) continue;
+      if (aij != 0.0 || aji != 0.0) {
+        adj.push_back(j);
+        tval.push_back(aij + aji);
+        xadj[i + 1]++;
+      }
     }
-    if (aij != 0.0 || aji != 0.0) {
-      adj.push_back(tr[s].c);
-      tval.push_back(aij + aji);
-      xadj[tr[s].r + 1]++;
-    }
-    s = e;
   }
   for (int32_t i = 0; i < n; ++i) xadj[i + 1] += xadj[i];
   std::vector<int32_t> cnt(n);
@@ -218,6 +283,8 @@ SpMat galerkin_rap(const SpMat& A, const std::vector<int32_t>& agg, int32_t nagg
   SpMat C;
   C.n = nagg;
   C.rp.assign(nagg + 1, 0);
+  C.ci.reserve(A.ci.size());
+  C.v.reserve(A.ci.size());
   std::vector<int32_t> mark(nagg, -1), slot(nagg);
   std::vector<std::pair<int32_t, double>> row;
   for (int32_t I = 0; I < nagg; ++I) {
@@ -335,13 +402,19 @@ static int make_weights(const BlockMat& A, int mode, std::vector<double>& W, std
       for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e)
         if (A.ci[e] == c) std::memcpy(&C[(size_t)c * bb], &A.v[(size_t)e * bb], sizeof(double) * bb);
   }
-  double y[8];
+  int32_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
   for (int32_t c = 0; c < n; ++c) {
+    double y[8];
     if (!weight_solve(nc, &C[(size_t)c * bb], b, y)) {
-      err = "decoupling: singular N-N block at cell " + std::to_string(c);
-      return 2;
+      bad = std::max(bad, c);
+      continue;
     }
     for (int i = 0; i < nc; ++i) W[(size_t)c * b + 1 + i] = y[i];
+  }
+  if (bad >= 0) {
+    err = "decoupling: singular N-N block at cell " + std::to_string(bad);
+    return 2;
   }
   return 0;
 }
@@ -353,6 +426,7 @@ static SpMat pressure_matrix(const BlockMat& A, const std::vector<double>& W) {
   P.rp = A.rp;
   P.ci = A.ci;
   P.v.resize(A.ci.size());
+#pragma omp parallel for schedule(static)
   for (int32_t c = 0; c < A.n; ++c) {
     const double* w = &W[(size_t)c * b];
     for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) {
@@ -388,7 +462,7 @@ static SpMat graph_laplacian(const Graph& G) {
 }
 
 static void make_ordering(HostSetup& S) {
-  const BlockMat& A = S.A;
+  const BlockMat& A = *S.A;
   const int32_t n = A.n;
   Graph G = block_graph(A);
   std::vector<int32_t> blk(n), bcol;
@@ -438,12 +512,29 @@ static void make_ordering(HostSetup& S) {
   S.color_blk_ptr = ccount;
 }
 
+namespace {
+struct PhaseTimer {
+  bool on = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[msp setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
 int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::string& err) {
+  PhaseTimer T;
   S.prm = prm;
-  S.A = A;
+  S.A = &A;
+  S.n = A.n;
   int rc = make_weights(A, prm.decoupling, S.W, err);
   if (rc) return rc;
+  T.mark("decoupling weights");
   S.App = pressure_matrix(A, S.W);
+  T.mark("A_PP");
   S.lv.clear();
   S.coarse_diag = false;
   SpMat cur = S.App;
@@ -453,12 +544,14 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
     HostLevel L;
     SpMat nxt;
     const int32_t nn = aggregate_passes(cur, prm.pair_passes, L.agg, &nxt);
+    T.mark("NPAIR + Galerkin level");
     if ((double)nn > 0.9 * (double)cur.n) {
       if (off_diagonal_zero(cur)) { S.coarse_diag = true; break; }
       err = "AMG: coarsening stalled at level " + std::to_string(l);
       return 5;
     }
     L.ncolor = color_groups(value_graph(cur), L.color);
+    T.mark("coloring level");
     L.n_next = nn;
     L.A = std::move(cur);
     S.lv.push_back(std::move(L));
@@ -480,7 +573,9 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
       if (!has) { err = "PGS-MC: zero diagonal at level " + std::to_string(l) + " row " + std::to_string(i); return 2; }
     }
   }
+  T.mark("checks");
   make_ordering(S);
+  T.mark("ABMC ordering");
   return 0;
 }
 
@@ -542,41 +637,57 @@ int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int3
   F.resize(A.v.size());
   for (size_t e = 0; e < src.size(); ++e)
     std::memcpy(&F[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
-  std::vector<int32_t> mark(n, -1);
-  double T[64];
-  for (int32_t i = 0; i < n; ++i) {
-    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = e;
-    for (int32_t e = rp[i]; e < dg[i]; ++e) {
-      const int32_t k = ci[e];
-      double* Lik = &F[(size_t)e * bb];
-      const double* Dk = &F[(size_t)dg[k] * bb];      // holds D~_k^-1
-      for (int r = 0; r < b; ++r)
-        for (int c = 0; c < b; ++c) {
-          double s = 0.0;
-          for (int t = 0; t < b; ++t) s += Lik[r * b + t] * Dk[t * b + c];
-          T[r * b + c] = s;
-        }
-      std::memcpy(Lik, T, sizeof(double) * bb);
-      for (int32_t f = dg[k] + 1; f < rp[k + 1]; ++f) {
-        const int32_t m = mark[ci[f]];
-        if (m < 0) continue;
-        const double* Ukj = &F[(size_t)f * bb];
-        double* Aij = &F[(size_t)m * bb];
-        for (int r = 0; r < b; ++r)
-          for (int c = 0; c < b; ++c) {
-            double s = 0.0;
-            for (int t = 0; t < b; ++t) s += Lik[r * b + t] * Ukj[t * b + c];
-            Aij[r * b + c] -= s;
+  // rows of one block color are independent (ABMC / RB orders); cells inside an
+  // aggregate block are eliminated in order by one thread
+  int32_t bad = -1;
+  const int ncol = (int)S.color_blk_ptr.size() - 1;
+  for (int col = 0; col < ncol; ++col) {
+#pragma omp parallel reduction(max : bad)
+    {
+      std::vector<int32_t> mark(n, -1);
+      double T[64];
+#pragma omp for schedule(dynamic, 256)
+      for (int32_t k = S.color_blk_ptr[col]; k < S.color_blk_ptr[col + 1]; ++k) {
+        for (int32_t i = S.blk_ptr[k]; i < S.blk_ptr[k + 1]; ++i) {
+          for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = e;
+          for (int32_t e = rp[i]; e < dg[i]; ++e) {
+            const int32_t kk = ci[e];
+            double* Lik = &F[(size_t)e * bb];
+            const double* Dk = &F[(size_t)dg[kk] * bb];      // holds D~_k^-1
+            for (int r = 0; r < b; ++r)
+              for (int c = 0; c < b; ++c) {
+                double sum = 0.0;
+                for (int t = 0; t < b; ++t) sum += Lik[r * b + t] * Dk[t * b + c];
+                T[r * b + c] = sum;
+              }
+            std::memcpy(Lik, T, sizeof(double) * bb);
+            for (int32_t f = dg[kk] + 1; f < rp[kk + 1]; ++f) {
+              const int32_t m = mark[ci[f]];
+              if (m < 0) continue;
+              const double* Ukj = &F[(size_t)f * bb];
+              double* Aij = &F[(size_t)m * bb];
+              for (int r = 0; r < b; ++r)
+                for (int c = 0; c < b; ++c) {
+                  double sum = 0.0;
+                  for (int t = 0; t < b; ++t) sum += Lik[r * b + t] * Ukj[t * b + c];
+                  Aij[r * b + c] -= sum;
+                }
+            }
           }
+          for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = -1;
+          double* Dd = &F[(size_t)dg[i] * bb];
+          if (!invert_block(b, Dd, T)) {
+            bad = std::max(bad, i);
+            continue;
+          }
+          std::memcpy(Dd, T, sizeof(double) * bb);
+        }
       }
     }
-    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) mark[ci[e]] = -1;
-    double* Dd = &F[(size_t)dg[i] * bb];
-    if (!invert_block(b, Dd, T)) {
-      err = "BILU: singular pivot block at cell " + std::to_string(S.order[i]);
+    if (bad >= 0) {
+      err = "BILU: singular pivot block at cell " + std::to_string(S.order[bad]);
       return 2;
     }
-    std::memcpy(Dd, T, sizeof(double) * bb);
   }
   return 0;
 }

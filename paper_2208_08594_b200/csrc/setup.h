@@ -44,7 +44,8 @@ struct HostLevel {
 
 struct HostSetup {
   Params prm;
-  BlockMat A;
+  const BlockMat* A = nullptr;       // caller-owned; valid during setup only
+  int32_t n = 0;
   std::vector<double> W;             // decoupling weights, n*b
   SpMat App;                         // W^T A Pi_P
   std::vector<HostLevel> lv;         // smoothing levels

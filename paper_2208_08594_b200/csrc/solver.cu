@@ -1488,21 +1488,21 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
 
 // ----------------------------------------------------------- host-setup introspection
 struct msp_host_setup {
+  msp::BlockMat M;                   // owns the matrix S.A points to
   msp::HostSetup S;
 };
 
 msp_status msp_host_setup_run(const msp_bsr* A, int nc, const msp_config* cfg, msp_host_setup** out) {
   if (!out) return MSP_EINVAL;
   *out = nullptr;
-  msp::BlockMat M;
+  std::unique_ptr<msp_host_setup> s(new msp_host_setup);
   std::string err;
-  msp_status st = read_bsr(A, nc, M, err);
+  msp_status st = read_bsr(A, nc, s->M, err);
   if (st) return fail(nullptr, st, err);
   msp_config c;
   msp_config_default(&c);
   if (cfg) c = *cfg;
-  std::unique_ptr<msp_host_setup> s(new msp_host_setup);
-  int rc = msp::run_host_setup(M, params_of(&c), s->S, err);
+  int rc = msp::run_host_setup(s->M, params_of(&c), s->S, err);
   if (rc) return fail(nullptr, (msp_status)rc, err);
   *out = s.release();
   return MSP_OK;
@@ -1571,7 +1571,7 @@ void msp_host_setup_free(msp_host_setup* s) { delete s; }
 msp_status msp_partition_owner(const msp_host_setup* s, int nx, int ny, int nz, int nranks, int32_t* owner) {
   if (!s || !owner || nranks < 1 || nranks > nz) return MSP_EINVAL;
   const int64_t plane = (int64_t)nx * ny;
-  const int32_t n = s->S.A.n;
+  const int32_t n = s->S.n;
   if ((int64_t)nx * ny * nz != n) return MSP_EINVAL;
   std::vector<int32_t> zstart(nranks + 1, 0);
   const int base = nz / nranks, extra = nz % nranks;
