@@ -676,6 +676,23 @@ __global__ void set_pressure_kernel(int n, int B, const double* __restrict__ wp,
   if (i < n) w[(size_t)i * B] = ldg(wp + i);
 }
 
+// ASMSP reuse: refresh A in the internal layout from the caller's
+// natural-order row-major values: A_cm[e] = transpose(A_nat[src[e]]), Pcol[e] = column 0.
+template <int B>
+__global__ void refresh_values_kernel(int64_t nnzb, const int* __restrict__ src, const double* __restrict__ nat,
+                                      double* __restrict__ Acm, double* __restrict__ Pcol) {
+  PDL_ENTRY();
+  constexpr int BB = B * B;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnzb * BB) return;
+  const int64_t e = t / BB;
+  const int k = (int)(t - e * BB);          // destination index (column-major): k = c*B + r
+  const int c = k / B, r = k - c * B;
+  const double v = ldg(nat + (size_t)ldg(src + e) * BB + r * B + c);
+  Acm[t] = v;
+  if (c == 0) Pcol[e * B + r] = v;
+}
+
 // ---------------------------------------------------------------------------
 // a10 (K8): GMRES vector kernels with deterministic two-stage reductions.
 // multidot: part[blk][i] = sum over this block's elements of V_i . w, i = 0..nv-1.

@@ -390,6 +390,7 @@ static int make_weights(const BlockMat& A, int mode, std::vector<double>& W, std
     std::vector<int32_t> f(cp.begin(), cp.end() - 1);
     for (int32_t p = 0; p < n; ++p)
       for (int32_t e = A.rp[p]; e < A.rp[p + 1]; ++e) ce[f[A.ci[e]]++] = e;
+#pragma omp parallel for schedule(static)
     for (int32_t c = 0; c < n; ++c) {
       double* Cc = &C[(size_t)c * bb];
       for (int32_t q = cp[c]; q < cp[c + 1]; ++q) {

@@ -93,6 +93,9 @@ struct msp_handle {
   int64_t nnzb = 0;
   std::vector<int32_t> order;        // position -> natural cell
   std::vector<int32_t> src_entry;    // permuted entry -> natural entry
+  std::vector<int32_t> nat_rp, nat_ci;  // natural pattern of the setup matrix (reuse check)
+  int32_t* d_src = nullptr;          // device copy of src_entry
+  double* stage = nullptr;           // natural-order values staging (reuse path)
   // BSR (internal positions), shared pattern for A and the BILU factors
   int32_t *rp = nullptr, *ci = nullptr, *dg = nullptr, *d_order = nullptr;
   double *Aval = nullptr, *Fval = nullptr, *W = nullptr, *Pcol = nullptr;
@@ -249,6 +252,7 @@ msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err
 // row-major b x b blocks -> column-major
 void transpose_blocks(const double* src, double* dst, size_t nblocks, int b) {
   const int bb = b * b;
+#pragma omp parallel for schedule(static)
   for (size_t e = 0; e < nblocks; ++e)
     for (int r = 0; r < b; ++r)
       for (int c = 0; c < b; ++c) dst[e * bb + c * b + r] = src[e * bb + r * b + c];
@@ -354,16 +358,30 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
   perm_out = perm;
 }
 
+struct SetupTimer {
+  bool on = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[msp setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
+  SetupTimer T;
   msp::HostSetup S;
   std::string err;
   int rc = msp::run_host_setup(A, h->prm, S, err);
   if (rc) throw std::pair<int, std::string>(rc, err);
   std::vector<int32_t> rp, ci, dg, src;
   std::vector<double> F;
+  T.mark("host setup S1-S4");
   rc = msp::bilu_factor_permuted(S, A, rp, ci, dg, src, F, err);
   if (rc) throw std::pair<int, std::string>(rc == 1 ? MSP_EINVAL : MSP_ESINGULAR, err);
+  T.mark("BILU factorization");
 
   h->free_all();
   const int32_t n = A.n;
@@ -375,15 +393,20 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->nnzb = (int64_t)A.ci.size();
   h->order = S.order;
   h->src_entry = src;
+  h->nat_rp = A.rp;
+  h->nat_ci = A.ci;
   // BSR pattern + values (column-major blocks)
   h->rp = h->upload(rp);
   h->ci = h->upload(ci);
+  h->d_src = h->upload(src);
+  h->stage = nullptr;
   h->dg = h->upload(dg);
   h->d_order = h->upload(S.order);
   {
     std::vector<double> tmp(F.size()), Ap(F.size());
     transpose_blocks(F.data(), tmp.data(), ci.size(), b);
     h->Fval = h->upload(tmp);
+#pragma omp parallel for schedule(static)
     for (size_t e = 0; e < src.size(); ++e)
       std::memcpy(&Ap[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
     transpose_blocks(Ap.data(), tmp.data(), ci.size(), b);
@@ -394,6 +417,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->Pcol = h->upload(pc);
     CK(cudaStreamSynchronize(h->s));
   }
+  T.mark("A/F/Pcol transpose+upload");
   if (h->prm.stages == 3) {
     const int nc = b - 1;
     std::vector<double> Dn((size_t)n * nc * nc), D(nc * nc), Di(nc * nc);
@@ -486,6 +510,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     for (int32_t p = 0; p < n; ++p) inv[l0[p]] = p;
     h->cell_of_l0 = h->upload(inv);
   }
+  T.mark("levels upload");
   // coarsest
   h->bL = h->dalloc<double>(h->nL);
   h->xL = h->dalloc<double>(h->nL);
@@ -528,6 +553,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     cusolverDnDestroy(cs);
     if (s2 != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnDgetrs"};
   }
+  T.mark("coarsest inverse");
   // work vectors
   h->z = h->dalloc<double>(h->N);
   h->r = h->dalloc<double>(h->N);
@@ -1237,30 +1263,60 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
 msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_iterations, int mu,
                       int* did_setup) {
   if (!h) return fail(nullptr, MSP_EINVAL, "msp_update: NULL handle");
-  msp::BlockMat M;
-  std::string err;
-  msp_status st = read_bsr(A_new, h->nc, M, err);
-  if (st) return fail(h, st, err);
-  const bool dims_changed = (M.n != h->n) || ((int64_t)M.ci.size() != h->nnzb);
-  // ASMSP rule (Remark 2)
-  const bool rebuild = (iota <= 1) || dims_changed || (last_iterations > mu);
+  if (!A_new || A_new->block != h->b || !A_new->row_ptr || !A_new->col_idx || !A_new->values)
+    return fail(h, MSP_EINVAL, "msp_update: invalid matrix");
+  // Remark 2: the preconditioner must be regenerated when the size changed
+  bool same = (A_new->n_cells == h->n);
+  if (same) {
+    std::vector<int32_t> rp(h->n + 1);
+    if (A_new->device >= 0) {
+      if (cudaMemcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (h->n + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(h, MSP_ECUDA, "msp_update: row_ptr copy failed");
+    } else {
+      std::memcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (h->n + 1));
+    }
+    same = (rp == h->nat_rp);
+    if (same) {
+      std::vector<int32_t> ci(h->nat_ci.size());
+      if (A_new->device >= 0) {
+        if (cudaMemcpy(ci.data(), A_new->col_idx, sizeof(int32_t) * ci.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+          return fail(h, MSP_ECUDA, "msp_update: col_idx copy failed");
+      } else {
+        std::memcpy(ci.data(), A_new->col_idx, sizeof(int32_t) * ci.size());
+      }
+      same = (ci == h->nat_ci);
+    }
+  }
+  // ASMSP rule: rebuild iff iota == 1, It^(iota-1) > mu, or size changed
+  const bool rebuild = (iota <= 1) || !same || (last_iterations > mu);
   if (did_setup) *did_setup = rebuild ? 1 : 0;
-  return guarded(h, [&]() -> msp_status {
-    if (rebuild) {
+  if (rebuild) {
+    msp::BlockMat M;
+    std::string err;
+    msp_status st = read_bsr(A_new, h->nc, M, err);
+    if (st) return fail(h, st, err);
+    return guarded(h, [&]() -> msp_status {
       do_setup(h, M);
       return MSP_OK;
-    }
-    // reuse: keep W, hierarchy and BILU factors; refresh A for SpMV / Alg. 1 residuals
+    });
+  }
+  // reuse: keep W, hierarchy and BILU factors; refresh A (SpMV, Alg. 1 residuals) on the GPU
+  return guarded(h, [&]() -> msp_status {
     const int bb = h->b * h->b;
-    std::vector<double> Ap(M.v.size()), tmp(M.v.size());
-    for (size_t e = 0; e < h->src_entry.size(); ++e)
-      std::memcpy(&Ap[e * bb], &M.v[(size_t)h->src_entry[e] * bb], sizeof(double) * bb);
-    transpose_blocks(Ap.data(), tmp.data(), h->src_entry.size(), h->b);
-    CK(cudaMemcpyAsync(h->Aval, tmp.data(), sizeof(double) * tmp.size(), cudaMemcpyHostToDevice, h->s));
-    std::vector<double> pc(h->src_entry.size() * h->b);
-    for (size_t e = 0; e < h->src_entry.size(); ++e)
-      for (int q = 0; q < h->b; ++q) pc[e * h->b + q] = Ap[e * bb + q * h->b];
-    CK(cudaMemcpyAsync(h->Pcol, pc.data(), sizeof(double) * pc.size(), cudaMemcpyHostToDevice, h->s));
+    const size_t nv = (size_t)h->nnzb * bb;
+    const double* nat = A_new->values;
+    if (A_new->device < 0) {
+      if (!h->stage) h->stage = h->dalloc<double>(nv);
+      CK(cudaMemcpyAsync(h->stage, A_new->values, sizeof(double) * nv, cudaMemcpyHostToDevice, h->s));
+      nat = h->stage;
+    }
+    switch (h->b) {
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, refresh_values_kernel<BV>, nblk(nv, 256), 256, (int64_t)h->nnzb, \
+                                  h->d_src, nat, h->Aval, h->Pcol); break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    }
+    ++h->nlaunch;
     CK(cudaStreamSynchronize(h->s));
     h->st.reuse_calls++;
     return MSP_OK;
