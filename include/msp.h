@@ -192,6 +192,32 @@ msp_status msp_host_setup_order(const msp_host_setup* s, int32_t* order);
 void msp_host_setup_free(msp_host_setup* s);
 
 /* ---- Multi-GPU: z-slab row partition, NCCL halo + allreduce ---- */
+/* Distributed SETUP on rank `rank` of `nranks` (one process per GPU).  A_global_host:
+ * the whole matrix on every rank (every rank runs the same deterministic host setup, so
+ * the preconditioner equals the single-GPU one); owner[n_cells] = rank of every cell
+ * (e.g. z-slabs from msp_partition_owner), NULL = contiguous index ranges.  Every ABMC
+ * block / level-1 aggregate is assigned whole to the owner of its lowest-index cell.
+ * Each rank keeps its rows plus ghost cells; halos (ncclSend/ncclRecv) follow every
+ * level-0 PGS-MC color and every BILU color phase, dot products use ncclAllReduce and
+ * the replicated coarse levels receive the level-1 right-hand side by ncclAllGather.
+ * nccl_unique_id: 128 bytes from msp_nccl_unique_id() on rank 0, broadcast by the
+ * caller.  Supports stages=2, 1 pre/post sweep, ABMC1 order.  Afterwards msp_solve /
+ * msp_update / msp_apply take this rank's owned cells (ascending natural cell id, see
+ * msp_dist_owned_cells); all ranks must call them collectively. */
+msp_status msp_nccl_unique_id(void* id128);
+msp_status msp_setup_dist(const msp_bsr* A_global_host, int nc, const msp_config* cfg, const int32_t* owner,
+                          const void* nccl_unique_id, int rank, int nranks, void* cuda_stream,
+                          msp_handle** out);
+int32_t msp_dist_n_owned(const msp_handle* h);
+msp_status msp_dist_owned_cells(const msp_handle* h, int32_t* cells);
+/* Test harness of the distributed path on ONE GPU: nranks virtual ranks as host threads,
+ * each with its own handle and stream; halos/collectives are device copies ordered by
+ * CUDA events (no kernel waits on another).  b, x: global natural order (x in: x0, out:
+ * solution).  rank_info (optional, 4*nranks): n_own, n_ghost, level-0 rows, level-0
+ * ghosts per rank. */
+msp_status msp_loopback_solve(const msp_bsr* A, int nc, const msp_config* cfg, const int32_t* owner, int nranks,
+                              const double* b, double* x, double tol, int restart, int maxit,
+                              int* iterations, double* final_rel_res, int32_t* rank_info);
 /* Host-side partition plan (no GPU): owner rank of each cell for `nranks` z-slabs of
  * an nx*ny*nz grid (cell c = i + nx*(j + ny*k)), aggregate-owner rule (cells follow
  * the owner of the lowest-index cell of their level-1 aggregate). */

@@ -3,6 +3,8 @@ C-ABI library libmsp.so (include/msp.h).  Argument marshalling only: every step 
 solve path runs in the library's sm_100a kernels.  There is no CPU fallback: importing
 this package fails loudly when the native library is missing.
 """
-from ._binding import (MspError, MspSolver, HostSetup, Config, lib_path, STATUS)  # noqa: F401
+from ._binding import (MspError, MspSolver, DistSolver, HostSetup, Config, lib_path, STATUS,  # noqa: F401
+                       loopback_solve, nccl_unique_id)
 
-__all__ = ["MspSolver", "HostSetup", "MspError", "Config", "lib_path", "STATUS"]
+__all__ = ["MspSolver", "DistSolver", "HostSetup", "MspError", "Config", "lib_path", "STATUS",
+           "loopback_solve", "nccl_unique_id"]

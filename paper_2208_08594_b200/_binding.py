@@ -63,10 +63,13 @@ for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats",
            "msp_pgs_sweep", "msp_vcycle", "msp_bilu_apply", "msp_get_order", "msp_host_setup_run",
            "msp_host_setup_info", "msp_host_setup_level_dims", "msp_host_setup_level_csr",
            "msp_host_setup_level_colors", "msp_host_setup_level_agg", "msp_host_setup_weights",
-           "msp_host_setup_order", "msp_partition_owner"):
+           "msp_host_setup_order", "msp_partition_owner", "msp_nccl_unique_id", "msp_setup_dist",
+           "msp_dist_owned_cells", "msp_loopback_solve"):
     getattr(_lib, _n).restype = ctypes.c_int
 _lib.msp_destroy.argtypes = [ctypes.c_void_p]
 _lib.msp_time_kernel.restype = ctypes.c_int
+_lib.msp_dist_n_owned.restype = ctypes.c_int32
+_lib.msp_dist_n_owned.argtypes = [ctypes.c_void_p]
 _lib.msp_kernel_launches.restype = ctypes.c_int64
 _lib.msp_kernel_launches.argtypes = [ctypes.c_void_p]
 
@@ -251,6 +254,72 @@ class MspSolver:
                     bilu_colors=s.bilu_colors, level_n=list(s.level_n[:L + 1]),
                     level_nnz=list(s.level_nnz[:L + 1]), level_colors=list(s.level_colors[:L]),
                     device_bytes=s.device_bytes, kernels_per_iter=s.kernels_per_iter)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0); broadcast it to the other ranks."""
+    buf = (ctypes.c_char * 128)()
+    st = _lib.msp_nccl_unique_id(buf)
+    if st:
+        raise MspError(st, _lib.msp_last_error(None).decode())
+    return bytes(buf)
+
+
+class DistSolver(MspSolver):
+    """One rank of the z-slab distributed solver (msp_setup_dist, NCCL).  Vectors passed
+    to solve/apply are this rank's owned cells (ascending natural id: owned_cells())."""
+
+    def __init__(self, row_ptr, col, val, nc, rank, nranks, unique_id, owner=None, stream=None,
+                 torch_allocator=True, **cfg):
+        self.n_global = len(row_ptr) - 1
+        self.b = int(val.shape[-1])
+        self.nc = nc
+        self._keep_alloc = None
+        c = Config.make(**cfg)
+        if torch_allocator:
+            import torch
+            if torch.cuda.is_available():
+                self._keep_alloc = _TorchAllocator()
+                c.alloc = self._keep_alloc.alloc
+                c.free_fn = self._keep_alloc.free
+        self.cfg = c
+        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
+        A, keep = _bsr(rp, ci, v)
+        own = None if owner is None else _np(owner, np.int32)
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        h = ctypes.c_void_p()
+        st = _lib.msp_setup_dist(ctypes.byref(A), nc, ctypes.byref(c), _ptr(own) if own is not None else None,
+                                 uid, rank, nranks, ctypes.c_void_p(stream or 0), ctypes.byref(h))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        self._h = h
+        self.n = int(_lib.msp_dist_n_owned(h))
+        self.N = self.n * self.b
+
+    def owned_cells(self):
+        o = np.zeros(self.n, dtype=np.int32)
+        self._check(_lib.msp_dist_owned_cells(self._h, _ptr(o)))
+        return o
+
+
+def loopback_solve(row_ptr, col, val, nc, nranks, b, x0=None, owner=None, tol=1e-6, restart=30, maxit=1000,
+                   **cfg):
+    """Distributed path on ONE GPU: nranks virtual ranks (threads), event-ordered copies."""
+    c = Config.make(**cfg)
+    rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
+    A, keep = _bsr(rp, ci, v)
+    b = _np(b, np.float64)
+    x = np.zeros_like(b) if x0 is None else _np(x0, np.float64).copy()
+    own = None if owner is None else _np(owner, np.int32)
+    it = ctypes.c_int(0)
+    fr = ctypes.c_double(0)
+    info = np.zeros(4 * nranks, dtype=np.int32)
+    st = _lib.msp_loopback_solve(ctypes.byref(A), nc, ctypes.byref(c), _ptr(own) if own is not None else None,
+                                 nranks, _ptr(b), _ptr(x), ctypes.c_double(tol), restart, maxit,
+                                 ctypes.byref(it), ctypes.byref(fr), _ptr(info))
+    if st not in (0, 3):
+        raise MspError(st, _lib.msp_last_error(None).decode())
+    return dict(x=x, iters=it.value, final_rel=fr.value, status=st, rank_info=info.reshape(nranks, 4))
 
 
 class HostSetup:

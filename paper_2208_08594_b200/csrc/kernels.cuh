@@ -693,6 +693,34 @@ __global__ void refresh_values_kernel(int64_t nnzb, const int* __restrict__ src,
   if (c == 0) Pcol[e * B + r] = v;
 }
 
+// Distributed mode: scatter the allgathered level-1 right-hand side of every rank's owned
+// aggregates into the replicated level-1 vector (fused: first color of the level-1
+// pre-sweep from the zero guess when x1 != null).
+__global__ void scatter_l1_kernel(int count, const int* __restrict__ idx, const double* __restrict__ recv,
+                                  double* __restrict__ b1, double* __restrict__ x1, const double* __restrict__ d1,
+                                  int c1_end) {
+  PDL_ENTRY();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int I = ldg(idx + t);
+  if (I < 0) return;
+  const double v = recv[t];
+  b1[I] = v;
+  if (x1) x1[I] = (I < c1_end) ? v / ldg(d1 + I) : 0.0;
+}
+
+__global__ void add_vec_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
+                               double* __restrict__ out) {
+  PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] + b[i];
+}
+
+__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out) {
+  PDL_ENTRY();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = sqrt(in[0]);
+}
+
 // ---------------------------------------------------------------------------
 // a10 (K8): GMRES vector kernels with deterministic two-stage reductions.
 // multidot: part[blk][i] = sum over this block's elements of V_i . w, i = 0..nv-1.

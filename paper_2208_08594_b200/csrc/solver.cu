@@ -14,9 +14,11 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/msp.h"
+#include "comm.h"
 #include "coop.cuh"
 #include "setup.h"
 
@@ -130,6 +132,17 @@ struct msp_handle {
   int64_t nlaunch = 0;
   std::vector<int64_t> graph_kernels;
   double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
+  // distributed (z-slab) mode: owned cells [0, n), ghost cells after them
+  std::unique_ptr<msp::Comm> comm;   // null: single GPU
+  int rank = 0, nranks = 1;
+  int n_ghost = 0, n0_ghost = 0;     // cell-space / level-0 ghosts
+  msp::HaloPlan cell_halo;           // segments = BILU block colors
+  msp::HaloPlan l0_halo;             // segments = level-0 PGS-MC colors
+  int n_own_l1 = 0, l1_cmax = 0;     // owned level-1 rows (aggregates), max over ranks
+  int32_t *own_l1_pt = nullptr, *own_l1_idx = nullptr, *l1_scatter = nullptr;
+  double *l1_send = nullptr, *l1_recv = nullptr, *lred = nullptr;
+  std::vector<int32_t> owned_cells;  // natural ids of the owned cells, ascending
+  std::vector<int32_t> owner_in;     // caller partition (kept for rebuilds)
   // stats
   msp_stats st{};
   std::vector<int32_t> level_n;
@@ -170,6 +183,8 @@ struct msp_handle {
     lv.clear();
     V = nullptr;
     V_m = -1;
+    cell_halo = msp::HaloPlan();
+    l0_halo = msp::HaloPlan();
     if (hpin) { cudaFreeHost(hpin); hpin = nullptr; }
   }
 };
@@ -258,22 +273,18 @@ void transpose_blocks(const double* src, double* dst, size_t nblocks, int b) {
       for (int c = 0; c < b; ++c) dst[e * bb + c * b + r] = src[e * bb + r * b + c];
 }
 
-// Build SELL-32 device level from a natural-order CSR + coloring.
-void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolor,
-                  const std::vector<int32_t>& color, std::vector<int32_t>& perm_out) {
-  const int32_t n = A.n;
+// Build a SELL-32 device level from CSR rows that are already in their final (color-
+// major) order; color[i] non-decreasing.  Columns may reference ghost rows >= n (their
+// x values are received by halo exchanges); x is sized n_total = n + ghosts.
+void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, const std::vector<int32_t>& rp,
+                       const std::vector<int32_t>& ci, const std::vector<double>& v, int32_t ncolor,
+                       const std::vector<int32_t>& color) {
   L.n = n;
   L.ncolor = ncolor;
   std::vector<int32_t> cnt(ncolor + 1, 0);
   for (int32_t i = 0; i < n; ++i) cnt[color[i] + 1]++;
   for (int32_t c = 0; c < ncolor; ++c) cnt[c + 1] += cnt[c];
   L.color_row = cnt;
-  std::vector<int32_t> perm(n), inv(n);
-  {
-    std::vector<int32_t> f(cnt.begin(), cnt.end() - 1);
-    for (int32_t i = 0; i < n; ++i) { perm[i] = f[color[i]]++; inv[perm[i]] = i; }
-  }
-  // slices per color
   std::vector<int32_t> slice_row, slice_off;
   L.color_slice.assign(ncolor + 1, 0);
   for (int32_t c = 0; c < ncolor; ++c) {
@@ -286,10 +297,7 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
   for (int32_t s = 0; s < L.nslices; ++s) {
     int32_t r1 = std::min(slice_row[s] + kSell, slice_row[s + 1]);
     int32_t w = 0;
-    for (int32_t p = slice_row[s]; p < r1; ++p) {
-      const int32_t i = inv[p];
-      w = std::max(w, (int32_t)(A.rp[i + 1] - A.rp[i]) - 1);
-    }
+    for (int32_t p = slice_row[s]; p < r1; ++p) w = std::max(w, (int32_t)(rp[p + 1] - rp[p]) - 1);
     slice_off[s + 1] = slice_off[s] + std::max(w, 0) * kSell;
   }
   std::vector<int32_t> col(std::max<int32_t>(slice_off[L.nslices], 1));
@@ -301,11 +309,10 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
       const bool valid = p < slice_row[s + 1];
       int k = 0;
       if (valid) {
-        const int32_t i = inv[p];
-        for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
-          if (A.ci[e] == i) { diag[p] = A.v[e]; continue; }
-          col[slice_off[s] + k * kSell + l] = perm[A.ci[e]];
-          val[slice_off[s] + k * kSell + l] = A.v[e];
+        for (int32_t e = rp[p]; e < rp[p + 1]; ++e) {
+          if (ci[e] == p) { diag[p] = v[e]; continue; }
+          col[slice_off[s] + k * kSell + l] = ci[e];
+          val[slice_off[s] + k * kSell + l] = v[e];
           ++k;
         }
       }
@@ -317,11 +324,9 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
   }
   L.nnz_alloc = slice_off[L.nslices];
   {
-    const double avg = (double)A.nnz() / std::max<int32_t>(n, 1);
+    const double avg = (double)rp[n] / std::max<int32_t>(n, 1);
     L.lpr = (avg <= 8.0) ? 1 : (avg <= 20.0 ? 4 : 8);
     if (const char* e = std::getenv("MSP_LPR")) L.lpr = std::atoi(e);
-    // trailing colors whose rows fit one 1024-thread CTA pass each (rows * LPR <= 1024 per
-    // color and <= 2048 in total) run as one single-CTA kernel
     int tail_rows = 0, t = ncolor;
     const int lim_env = std::getenv("MSP_TAIL_ROWS") ? std::atoi(std::getenv("MSP_TAIL_ROWS")) : 2048;
     const int lim_col = std::getenv("MSP_TAIL_COLOR") ? std::atoi(std::getenv("MSP_TAIL_COLOR")) : 1024;
@@ -350,11 +355,36 @@ void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolo
   L.col = h->upload(col);
   L.val = h->upload(val);
   L.diag = h->upload(diag);
+  L.b = h->dalloc<double>(n);
+  L.x = h->dalloc<double>(n_total);
+  L.r = h->dalloc<double>(n);
+}
+
+// Build a SELL-32 device level from a natural-order CSR + coloring (rows permuted by
+// (color, natural index)).
+void upload_level(msp_handle* h, DevLevel& L, const msp::SpMat& A, int32_t ncolor,
+                  const std::vector<int32_t>& color, std::vector<int32_t>& perm_out) {
+  const int32_t n = A.n;
+  std::vector<int32_t> cnt(ncolor + 1, 0);
+  for (int32_t i = 0; i < n; ++i) cnt[color[i] + 1]++;
+  for (int32_t c = 0; c < ncolor; ++c) cnt[c + 1] += cnt[c];
+  std::vector<int32_t> perm(n), inv(n), pcolor(n);
+  {
+    std::vector<int32_t> f(cnt.begin(), cnt.end() - 1);
+    for (int32_t i = 0; i < n; ++i) { perm[i] = f[color[i]]++; inv[perm[i]] = i; }
+  }
+  std::vector<int32_t> rp(n + 1, 0), ci(A.ci.size());
+  std::vector<double> v(A.ci.size());
+  for (int32_t p = 0; p < n; ++p) {
+    const int32_t i = inv[p];
+    pcolor[p] = color[i];
+    rp[p + 1] = rp[p] + (A.rp[i + 1] - A.rp[i]);
+    int32_t q = rp[p];
+    for (int32_t e = A.rp[i]; e < A.rp[i + 1]; ++e, ++q) { ci[q] = perm[A.ci[e]]; v[q] = A.v[e]; }
+  }
+  upload_level_rows(h, L, n, n, rp, ci, v, ncolor, pcolor);
   L.perm = h->upload(perm);
   L.inv = h->upload(inv);
-  L.b = h->dalloc<double>(n);
-  L.x = h->dalloc<double>(n);
-  L.r = h->dalloc<double>(n);
   perm_out = perm;
 }
 
@@ -368,6 +398,28 @@ struct SetupTimer {
     t = n;
   }
 };
+
+// per-cell counts of external L / intra-block U entries (bilu_block_kernel), in global
+// positions
+std::vector<int32_t> block_counts(const msp::HostSetup& S, const std::vector<int32_t>& rp,
+                                  const std::vector<int32_t>& ci, const std::vector<int32_t>& dg) {
+  std::vector<int32_t> cnt(S.n, 0);
+  for (size_t k = 0; k + 1 < S.blk_ptr.size(); ++k) {
+    const int32_t c0 = S.blk_ptr[k], c1 = S.blk_ptr[k + 1];
+    for (int32_t i = c0; i < c1; ++i) {
+      int32_t next = 0, nint = 0;
+      for (int32_t e = rp[i]; e < dg[i]; ++e) if (ci[e] < c0) ++next;
+      for (int32_t e = dg[i] + 1; e < rp[i + 1]; ++e) if (ci[e] < c1) ++nint;
+      if (next > 255 || nint > 255) throw std::pair<int, std::string>(MSP_EINVAL, "BILU: row too long for the block kernel");
+      cnt[i] = next | (nint << 8);
+    }
+  }
+  return cnt;
+}
+
+void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
+                   const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
+                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms);
 
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
@@ -395,6 +447,63 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->src_entry = src;
   h->nat_rp = A.rp;
   h->nat_ci = A.ci;
+  h->bilu_ncolor = S.bilu_ncolor;
+  h->max_blk = 1;
+  for (size_t k = 0; k + 1 < S.blk_ptr.size(); ++k) h->max_blk = std::max(h->max_blk, S.blk_ptr[k + 1] - S.blk_ptr[k]);
+  h->n_ghost = 0;
+  h->n0_ghost = 0;
+  const int L = (int)S.lv.size();
+  // AMG levels: natural-order permutations of every level (the upload of level 0 is
+  // rank-local in distributed mode, levels >= 1 are replicated)
+  h->level_n.clear();
+  h->level_nnz.clear();
+  h->level_colors.clear();
+  h->lv.resize(L);
+  std::vector<std::vector<int32_t>> perms(L);
+  for (int l = 0; l < L; ++l) {
+    if (l > 0 || !h->comm) upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
+    else {
+      // permutation of level 0 only (upload done by dist_localize)
+      const auto& col = S.lv[0].color;
+      std::vector<int32_t> cnt(S.lv[0].ncolor + 1, 0);
+      for (int32_t c : col) cnt[c + 1]++;
+      for (int c = 0; c < S.lv[0].ncolor; ++c) cnt[c + 1] += cnt[c];
+      perms[0].resize(n);
+      for (int32_t i = 0; i < n; ++i) perms[0][i] = cnt[col[i]]++;
+    }
+    h->level_n.push_back(S.lv[l].A.n);
+    h->level_nnz.push_back(S.lv[l].A.nnz());
+    h->level_colors.push_back(S.lv[l].ncolor);
+  }
+  h->nL = S.Ac.n;
+  h->coarse_diag = S.coarse_diag;
+  h->level_n.push_back(S.Ac.n);
+  h->level_nnz.push_back(S.Ac.nnz());
+  h->level_colors.push_back(0);
+  for (int l = (h->comm ? 1 : 0); l < L; ++l) {
+    DevLevel& D = h->lv[l];
+    const auto& agg = S.lv[l].agg;
+    const int32_t nn = S.lv[l].n_next;
+    std::vector<int32_t> ap(D.n), inv(D.n);
+    for (int32_t i = 0; i < D.n; ++i) inv[perms[l][i]] = i;
+    for (int32_t p = 0; p < D.n; ++p) {
+      const int32_t I = agg[inv[p]];
+      ap[p] = (l + 1 < L) ? perms[l + 1][I] : I;
+    }
+    std::vector<int32_t> pp(nn + 1, 0), pi(D.n);
+    for (int32_t p = 0; p < D.n; ++p) pp[ap[p] + 1]++;
+    for (int32_t I = 0; I < nn; ++I) pp[I + 1] += pp[I];
+    {
+      std::vector<int32_t> f(pp.begin(), pp.end() - 1);
+      for (int32_t p = 0; p < D.n; ++p) pi[f[ap[p]]++] = p;
+    }
+    D.agg = h->upload(ap);
+    D.pt_ptr = h->upload(pp);
+    D.pt_idx = h->upload(pi);
+  }
+  if (h->comm) {
+    dist_localize(h, A, S, rp, ci, dg, src, F, perms);
+  } else {
   // BSR pattern + values (column-major blocks)
   h->rp = h->upload(rp);
   h->ci = h->upload(ci);
@@ -463,52 +572,14 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     }
     h->bcnt = h->upload(cnt);
   }
-  // AMG levels
-  h->level_n.clear();
-  h->level_nnz.clear();
-  h->level_colors.clear();
-  const int L = (int)S.lv.size();
-  h->lv.resize(L);
-  std::vector<std::vector<int32_t>> perms(L);
-  for (int l = 0; l < L; ++l) {
-    upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
-    h->level_n.push_back(S.lv[l].A.n);
-    h->level_nnz.push_back(S.lv[l].A.nnz());
-    h->level_colors.push_back(S.lv[l].ncolor);
-  }
-  h->nL = S.Ac.n;
-  h->coarse_diag = S.coarse_diag;
-  h->level_n.push_back(S.Ac.n);
-  h->level_nnz.push_back(S.Ac.nnz());
-  h->level_colors.push_back(0);
-  for (int l = 0; l < L; ++l) {
-    DevLevel& D = h->lv[l];
-    const auto& agg = S.lv[l].agg;
-    const int32_t nn = S.lv[l].n_next;
-    std::vector<int32_t> ap(D.n), inv(D.n);
-    for (int32_t i = 0; i < D.n; ++i) inv[perms[l][i]] = i;
-    for (int32_t p = 0; p < D.n; ++p) {
-      const int32_t I = agg[inv[p]];
-      ap[p] = (l + 1 < L) ? perms[l + 1][I] : I;
-    }
-    std::vector<int32_t> pp(nn + 1, 0), pi(D.n);
-    for (int32_t p = 0; p < D.n; ++p) pp[ap[p] + 1]++;
-    for (int32_t I = 0; I < nn; ++I) pp[I + 1] += pp[I];
     {
-      std::vector<int32_t> f(pp.begin(), pp.end() - 1);
-      for (int32_t p = 0; p < D.n; ++p) pi[f[ap[p]]++] = p;
+      std::vector<int32_t> l0(n);
+      for (int32_t p = 0; p < n; ++p) l0[p] = (L > 0) ? perms[0][S.order[p]] : S.order[p];
+      h->l0_of_cell = h->upload(l0);
+      std::vector<int32_t> inv(n);
+      for (int32_t p = 0; p < n; ++p) inv[l0[p]] = p;
+      h->cell_of_l0 = h->upload(inv);
     }
-    D.agg = h->upload(ap);
-    D.pt_ptr = h->upload(pp);
-    D.pt_idx = h->upload(pi);
-  }
-  {
-    std::vector<int32_t> l0(n);
-    for (int32_t p = 0; p < n; ++p) l0[p] = (L > 0) ? perms[0][S.order[p]] : S.order[p];
-    h->l0_of_cell = h->upload(l0);
-    std::vector<int32_t> inv(n);
-    for (int32_t p = 0; p < n; ++p) inv[l0[p]] = p;
-    h->cell_of_l0 = h->upload(inv);
   }
   T.mark("levels upload");
   // coarsest
@@ -554,14 +625,16 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     if (s2 != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnDgetrs"};
   }
   T.mark("coarsest inverse");
-  // work vectors
-  h->z = h->dalloc<double>(h->N);
-  h->r = h->dalloc<double>(h->N);
+  // work vectors (cell-space vectors read through ghost columns carry ghost slots)
+  const size_t Ng = (size_t)(h->n + h->n_ghost) * h->b;
+  h->z = h->dalloc<double>(Ng);
+  h->r = h->dalloc<double>(Ng);
   h->u = h->dalloc<double>(h->N);
-  h->xin = h->dalloc<double>(h->N);
+  h->xin = h->dalloc<double>(Ng);
   h->bin = h->dalloc<double>(h->N);
   h->io = h->dalloc<double>(h->N);
-  h->wp = h->dalloc<double>(n);
+  h->wp = h->dalloc<double>(h->n + h->n_ghost);
+  h->lred = h->dalloc<double>(kMaxV);
   h->part = h->dalloc<double>((size_t)kRedBlocks * kMaxV);
   h->dh1 = h->dalloc<double>(kMaxV);
   h->dh2 = h->dalloc<double>(kMaxV);
@@ -632,6 +705,295 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Distributed setup.  Every rank runs the same (deterministic) global
+// host setup, so colorings, aggregates, orderings and factors are those of 1 GPU; it
+// then keeps its owned rows.  Cell ownership follows the caller's partition (z-slabs),
+// with every ABMC block (= level-1 aggregate) assigned whole to the owner of its
+// lowest-index cell, so BILU blocks and level-1 aggregates are never split.
+//  cell space : owned cells in global ABMC position order, then ghosts grouped by
+//               (owner, block color, position) -> one contiguous receive per color;
+//  level 0    : owned rows in global level-0 order (color-major), then ghosts grouped
+//               by (owner, level-0 color, global row);
+//  levels >= 1 and the coarsest are replicated; the level-1 right-hand side is
+//  assembled by an allgather of every rank's owned aggregates.
+// ---------------------------------------------------------------------------
+static void build_halo(msp_handle* h, msp::HaloPlan& P, int nseg, int nranks, int me,
+                       const std::vector<std::vector<std::vector<int32_t>>>& sendl,   // [peer][seg] owned local idx
+                       const std::vector<std::vector<int32_t>>& recv_cnt) {          // [peer][seg]
+  P = msp::HaloPlan();
+  P.nseg = nseg;
+  std::vector<int32_t> idx;
+  int ghost = 0;
+  for (int q = 0; q < nranks; ++q) {
+    if (q == me) continue;
+    int ns = 0, nr = 0;
+    for (int sg = 0; sg < nseg; ++sg) { ns += (int)sendl[q][sg].size(); nr += recv_cnt[q][sg]; }
+    if (ns == 0 && nr == 0) continue;
+    P.peers.push_back(q);
+    P.send_base.push_back((int)idx.size());
+    P.recv_base.push_back(ghost);
+    std::vector<int> so(nseg + 1, 0), ro(nseg + 1, 0);
+    for (int sg = 0; sg < nseg; ++sg) {
+      so[sg + 1] = so[sg] + (int)sendl[q][sg].size();
+      ro[sg + 1] = ro[sg] + recv_cnt[q][sg];
+      idx.insert(idx.end(), sendl[q][sg].begin(), sendl[q][sg].end());
+    }
+    ghost += nr;
+    P.send_off.push_back(so);
+    P.recv_off.push_back(ro);
+  }
+  P.nsend = (int)idx.size();
+  P.nghost = ghost;
+  P.d_send_idx = h->upload(idx);
+  P.d_sendbuf = h->dalloc<double>((size_t)std::max(P.nsend, 1) * 8);
+}
+
+void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
+                   const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
+                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms) {
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b;
+  const int P = h->nranks, me = h->rank;
+  const int L = (int)S.lv.size();
+  if (L < 1) throw std::pair<int, std::string>(MSP_EINVAL, "distributed mode needs >= 1 AMG smoothing level (n > coarsest_max_dof)");
+  // effective owner of every global position: owner of the block's lowest natural cell
+  std::vector<int32_t> own_pos(n);
+  const int nb = (int)S.blk_ptr.size() - 1;
+  std::vector<int32_t> bcolor(nb), color_pos(n);
+  for (int c = 0; c < S.bilu_ncolor; ++c)
+    for (int k = S.color_blk_ptr[c]; k < S.color_blk_ptr[c + 1]; ++k) bcolor[k] = c;
+  for (int k = 0; k < nb; ++k) {
+    int32_t lowest = INT32_MAX;
+    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) lowest = std::min(lowest, S.order[p]);
+    const int32_t o = h->owner_in[lowest];
+    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) { own_pos[p] = o; color_pos[p] = bcolor[k]; }
+  }
+  std::vector<int32_t> own_cell(n);
+  for (int32_t p = 0; p < n; ++p) own_cell[S.order[p]] = own_pos[p];
+  // ---------------- cell space
+  std::vector<int32_t> loc(n, -1), posown;
+  for (int32_t p = 0; p < n; ++p)
+    if (own_pos[p] == me) { loc[p] = (int32_t)posown.size(); posown.push_back(p); }
+  const int32_t no = (int32_t)posown.size();
+  // needed[q] (per peer rank q): positions owned by `me` referenced by rows of q;
+  // ghosts of me: positions owned by others referenced by my rows
+  std::vector<std::vector<int32_t>> need(P);            // need[q]: my positions q needs
+  std::vector<int32_t> ghosts;
+  {
+    std::vector<int32_t> mark(n, -1);
+    for (int32_t p = 0; p < n; ++p) {
+      const int t = own_pos[p];
+      for (int32_t e = rp[p]; e < rp[p + 1]; ++e) {
+        const int32_t qpos = ci[e];
+        const int o = own_pos[qpos];
+        if (o == t) continue;
+        if (o == me) need[t].push_back(qpos);           // t's row reads my position
+        if (t == me && mark[qpos] < 0) { mark[qpos] = 1; ghosts.push_back(qpos); }
+      }
+    }
+    for (int q = 0; q < P; ++q) {
+      auto& v = need[q];
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) {
+        return color_pos[x] != color_pos[y] ? color_pos[x] < color_pos[y] : x < y;
+      });
+    }
+    std::sort(ghosts.begin(), ghosts.end(), [&](int32_t x, int32_t y) {
+      if (own_pos[x] != own_pos[y]) return own_pos[x] < own_pos[y];
+      if (color_pos[x] != color_pos[y]) return color_pos[x] < color_pos[y];
+      return x < y;
+    });
+  }
+  const int32_t ng = (int32_t)ghosts.size();
+  std::vector<int32_t> lcol(n, -1);                     // global position -> local column
+  for (int32_t l = 0; l < no; ++l) lcol[posown[l]] = l;
+  for (int32_t k = 0; k < ng; ++k) lcol[ghosts[k]] = no + k;
+  {
+    std::vector<std::vector<std::vector<int32_t>>> sendl(P, std::vector<std::vector<int32_t>>(S.bilu_ncolor));
+    std::vector<std::vector<int32_t>> rcnt(P, std::vector<int32_t>(S.bilu_ncolor, 0));
+    for (int q = 0; q < P; ++q)
+      for (int32_t pos : need[q]) sendl[q][color_pos[pos]].push_back(loc[pos]);
+    for (int32_t g : ghosts) rcnt[own_pos[g]][color_pos[g]]++;
+    build_halo(h, h->cell_halo, S.bilu_ncolor, P, me, sendl, rcnt);
+  }
+  // local BSR rows (entries keep the global position order: L | diag | U)
+  std::vector<int32_t> lrp(no + 1, 0), lci, ldg(no), lsrc;
+  std::vector<double> lF, lA, lPc, lW((size_t)no * b);
+  const std::vector<int32_t> gcnt = block_counts(S, rp, ci, dg);
+  std::vector<int32_t> lcnt(no);
+  for (int32_t l = 0; l < no; ++l) {
+    const int32_t p = posown[l];
+    for (int32_t e = rp[p]; e < rp[p + 1]; ++e) {
+      if (e == dg[p]) ldg[l] = (int32_t)lci.size();
+      lci.push_back(lcol[ci[e]]);
+      lsrc.push_back(src[e]);
+    }
+    lrp[l + 1] = (int32_t)lci.size();
+    lcnt[l] = gcnt[p];
+    std::memcpy(&lW[(size_t)l * b], &S.W[(size_t)S.order[p] * b], sizeof(double) * b);
+  }
+  const size_t ne = lci.size();
+  lF.resize(ne * bb);
+  lA.resize(ne * bb);
+  lPc.resize(ne * b);
+  {
+    size_t q = 0;
+    for (int32_t l = 0; l < no; ++l) {
+      const int32_t p = posown[l];
+      for (int32_t e = rp[p]; e < rp[p + 1]; ++e, ++q) {
+        for (int r = 0; r < b; ++r)
+          for (int c = 0; c < b; ++c) {
+            lF[q * bb + c * b + r] = F[(size_t)e * bb + r * b + c];                  // column-major
+            lA[q * bb + c * b + r] = A.v[(size_t)src[e] * bb + r * b + c];
+          }
+        for (int r = 0; r < b; ++r) lPc[q * b + r] = A.v[(size_t)src[e] * bb + r * b];
+      }
+    }
+  }
+  // owned blocks
+  std::vector<int32_t> lblk(1, 0), lcolor_blk(S.bilu_ncolor + 1, 0);
+  for (int c = 0; c < S.bilu_ncolor; ++c) {
+    for (int k = S.color_blk_ptr[c]; k < S.color_blk_ptr[c + 1]; ++k) {
+      if (own_pos[S.blk_ptr[k]] != me) continue;
+      lblk.push_back(lblk.back() + (S.blk_ptr[k + 1] - S.blk_ptr[k]));
+    }
+    lcolor_blk[c + 1] = (int32_t)lblk.size() - 1;
+  }
+  // natural order of the owned cells (the caller's b/x layout on this rank)
+  h->owned_cells.clear();
+  for (int32_t c = 0; c < n; ++c) if (own_cell[c] == me) h->owned_cells.push_back(c);
+  std::vector<int32_t> natloc(n, -1), lorder(no);
+  for (size_t k = 0; k < h->owned_cells.size(); ++k) natloc[h->owned_cells[k]] = (int32_t)k;
+  for (int32_t l = 0; l < no; ++l) lorder[l] = natloc[S.order[posown[l]]];
+  // upload cell space
+  h->n = no;
+  h->N = (size_t)no * b;
+  h->n_ghost = ng;
+  h->rp = h->upload(lrp);
+  h->ci = h->upload(lci);
+  h->dg = h->upload(ldg);
+  h->d_src = h->upload(lsrc);
+  h->src_entry = lsrc;
+  h->stage = nullptr;
+  h->d_order = h->upload(lorder);
+  h->order = lorder;
+  h->Fval = h->upload(lF);
+  h->Aval = h->upload(lA);
+  h->Pcol = h->upload(lPc);
+  h->W = h->upload(lW);
+  h->color_blk = lcolor_blk;
+  h->blk_ptr = h->upload(lblk);
+  h->bcnt = h->upload(lcnt);
+  h->nnzb = (int64_t)ne;
+  // ---------------- level 0
+  const msp::SpMat& A0 = S.lv[0].A;               // natural level-0 numbering = cells
+  const auto& col0 = S.lv[0].color;
+  const int g0 = S.lv[0].ncolor;
+  std::vector<int32_t> rows0;                     // owned natural cells by global level-0 row
+  for (int32_t c = 0; c < n; ++c) if (own_cell[c] == me) rows0.push_back(c);
+  std::sort(rows0.begin(), rows0.end(), [&](int32_t x, int32_t y) { return perms[0][x] < perms[0][y]; });
+  std::vector<int32_t> l0loc(n, -1), gh0;
+  for (size_t k = 0; k < rows0.size(); ++k) l0loc[rows0[k]] = (int32_t)k;
+  std::vector<std::vector<int32_t>> need0(P);
+  {
+    std::vector<int32_t> mark(n, -1);
+    for (int32_t c = 0; c < n; ++c) {
+      const int t = own_cell[c];
+      for (int32_t e = A0.rp[c]; e < A0.rp[c + 1]; ++e) {
+        const int32_t d = A0.ci[e];
+        const int o = own_cell[d];
+        if (o == t) continue;
+        if (o == me) need0[t].push_back(d);
+        if (t == me && mark[d] < 0) { mark[d] = 1; gh0.push_back(d); }
+      }
+    }
+    for (int q = 0; q < P; ++q) {
+      auto& v = need0[q];
+      std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) { return perms[0][x] < perms[0][y]; });
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+    std::sort(gh0.begin(), gh0.end(), [&](int32_t x, int32_t y) {
+      if (own_cell[x] != own_cell[y]) return own_cell[x] < own_cell[y];
+      return perms[0][x] < perms[0][y];                // color-major inside a peer
+    });
+  }
+  const int32_t no0 = (int32_t)rows0.size(), ng0 = (int32_t)gh0.size();
+  std::vector<int32_t> l0col(n, -1);
+  for (int32_t k = 0; k < no0; ++k) l0col[rows0[k]] = k;
+  for (int32_t k = 0; k < ng0; ++k) l0col[gh0[k]] = no0 + k;
+  {
+    std::vector<std::vector<std::vector<int32_t>>> sendl(P, std::vector<std::vector<int32_t>>(g0));
+    std::vector<std::vector<int32_t>> rcnt(P, std::vector<int32_t>(g0, 0));
+    for (int q = 0; q < P; ++q)
+      for (int32_t d : need0[q]) sendl[q][col0[d]].push_back(l0loc[d]);
+    for (int32_t d : gh0) rcnt[own_cell[d]][col0[d]]++;
+    build_halo(h, h->l0_halo, g0, P, me, sendl, rcnt);
+  }
+  {
+    std::vector<int32_t> r0(no0 + 1, 0), c0v, rc0(no0);
+    std::vector<double> v0;
+    for (int32_t k = 0; k < no0; ++k) {
+      const int32_t c = rows0[k];
+      // same entry order as upload_level: natural column order of the row
+      for (int32_t e = A0.rp[c]; e < A0.rp[c + 1]; ++e) { c0v.push_back(l0col[A0.ci[e]]); v0.push_back(A0.v[e]); }
+      r0[k + 1] = (int32_t)c0v.size();
+      rc0[k] = col0[c];
+    }
+    upload_level_rows(h, h->lv[0], no0, no0 + ng0, r0, c0v, v0, g0, rc0);
+    h->n0_ghost = ng0;
+  }
+  // level-0 -> level-1 (replicated) aggregate map and this rank's owned aggregates
+  {
+    const auto& agg0 = S.lv[0].agg;
+    auto l1row = [&](int32_t I) { return (L > 1) ? perms[1][I] : I; };
+    std::vector<int32_t> ap(no0);
+    for (int32_t k = 0; k < no0; ++k) ap[k] = l1row(agg0[rows0[k]]);
+    h->lv[0].agg = h->upload(ap);
+    const int32_t n1 = S.lv[0].n_next;
+    std::vector<int32_t> aown(n1, -1);
+    for (int32_t c = 0; c < n; ++c) aown[agg0[c]] = own_cell[c];     // whole aggregates per rank
+    std::vector<std::vector<int32_t>> ownl1(P);
+    for (int32_t I = 0; I < n1; ++I) ownl1[aown[I]].push_back(I);
+    for (int q = 0; q < P; ++q)
+      std::sort(ownl1[q].begin(), ownl1[q].end(), [&](int32_t x, int32_t y) { return l1row(x) < l1row(y); });
+    int cmax = 1;
+    for (int q = 0; q < P; ++q) cmax = std::max(cmax, (int)ownl1[q].size());
+    std::vector<int32_t> scat((size_t)P * cmax, -1);
+    for (int q = 0; q < P; ++q)
+      for (size_t k = 0; k < ownl1[q].size(); ++k) scat[(size_t)q * cmax + k] = l1row(ownl1[q][k]);
+    // member lists of my aggregates (local level-0 rows)
+    std::vector<int32_t> slot(n1, -1);
+    for (size_t k = 0; k < ownl1[me].size(); ++k) slot[ownl1[me][k]] = (int32_t)k;
+    const int32_t nm = (int32_t)ownl1[me].size();
+    std::vector<int32_t> pp(nm + 1, 0), pi(no0);
+    for (int32_t k = 0; k < no0; ++k) pp[slot[agg0[rows0[k]]] + 1]++;
+    for (int32_t k = 0; k < nm; ++k) pp[k + 1] += pp[k];
+    {
+      std::vector<int32_t> f(pp.begin(), pp.end() - 1);
+      for (int32_t k = 0; k < no0; ++k) pi[f[slot[agg0[rows0[k]]]]++] = k;
+    }
+    h->n_own_l1 = nm;
+    h->l1_cmax = cmax;
+    h->own_l1_pt = h->upload(pp);
+    h->own_l1_idx = h->upload(pi);
+    h->l1_scatter = h->upload(scat);
+    h->l1_send = h->dalloc<double>(cmax);
+    h->l1_recv = h->dalloc<double>((size_t)P * cmax);
+    CK(cudaMemsetAsync(h->l1_send, 0, sizeof(double) * cmax, h->s));
+  }
+  // cell <-> level-0 maps of the owned cells
+  {
+    std::vector<int32_t> l0(no), inv(no0);
+    for (int32_t l = 0; l < no; ++l) l0[l] = l0loc[S.order[posown[l]]];
+    for (int32_t l = 0; l < no; ++l) inv[l0[l]] = l;
+    h->l0_of_cell = h->upload(l0);
+    h->cell_of_l0 = h->upload(inv);
+  }
+  CK(cudaStreamSynchronize(h->s));
+}
+
 // ----------------------------------------------------------------- launches
 template <int B>
 void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, const int* ci, const double* val,
@@ -653,6 +1015,14 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
   }
 }
 
+// halo exchanges of the distributed mode (no-ops on a single GPU)
+void exch_cell(msp_handle* h, double* v, int width, int seg) {
+  if (h->comm) h->comm->halo(h->s, h->cell_halo, v, h->n, width, seg);
+}
+void exch_l0(msp_handle* h, double* x, int seg) {
+  if (h->comm) h->comm->halo(h->s, h->l0_halo, x, h->lv[0].n, 1, seg);
+}
+
 template <int B, int MAXC, bool WF = false>
 void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
@@ -669,9 +1039,12 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     else
       klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
   };
-  for (int c = 0; c < g - 1; ++c) run(c, 0);
+  // distributed: after each color phase, the ghost copies of that color's cells are
+  // refreshed (y after the forward phase, x after the backward phase)
+  for (int c = 0; c < g - 1; ++c) { run(c, 0); exch_cell(h, v, B, c); }
   run(g - 1, 2);
-  for (int c = g - 2; c >= 0; --c) run(c, 1);
+  if (g > 1) exch_cell(h, v, B, g - 1);
+  for (int c = g - 2; c >= 0; --c) { run(c, 1); if (c > 0) exch_cell(h, v, B, c); }
 }
 
 template <int B>
@@ -851,8 +1224,56 @@ void vcycle_any(msp_handle* h, bool init_done = false) {
 
 void msp_apply_npr(msp_handle* h, const double* g, double* z);
 
+// Distributed MSP (stages P, R): level 0 of the V-cycle is rank-local with halo
+// exchanges after every color; levels >= 1 and the coarsest are replicated (allgather
+// of the owned aggregates' right-hand side).
+void msp_apply_dist(msp_handle* h, const double* g, double* z) {
+  DevLevel& L0 = h->lv[0];
+  const int L = (int)h->lv.size();
+  CK(cudaMemsetAsync(L0.x + L0.n, 0, sizeof(double) * h->n0_ghost, h->s));    // zero guess of ghosts
+  launch_restrict_pressure(h, g, L0.b, true);                                // a3 + first color
+  exch_l0(h, L0.x, 0);
+  for (int c = 1; c < L0.ncolor; ++c) {
+    if (c == L0.ncolor - 1) sell_rows_any<true, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
+    else sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
+    exch_l0(h, L0.x, c);
+  }
+  if (L0.ncolor > 1) sell_rows_any<false, true>(h, L0, 0, L0.color_slice[L0.ncolor - 1]);
+  else sell_rows_any<false, true>(h, L0, 0, L0.nslices);
+  if (h->n_own_l1 > 0) {
+    klaunch(h->s, h->pdl, restrict_kernel, nblk(h->n_own_l1, 256), 256, h->n_own_l1, h->own_l1_pt, h->own_l1_idx,
+            (const double*)L0.r, h->l1_send, (double*)nullptr, (const double*)nullptr, 0);
+    ++h->nlaunch;
+  }
+  h->comm->allgather(h->s, h->l1_send, h->l1_recv, h->l1_cmax);
+  const bool init1 = L > 1 && h->prm.pre_sweeps > 0;
+  double* b1 = (L > 1) ? h->lv[1].b : h->bL;
+  double* x1 = (L > 1) ? h->lv[1].x : h->xL;
+  klaunch(h->s, h->pdl, scatter_l1_kernel, nblk((size_t)h->nranks * h->l1_cmax, 256), 256, h->nranks * h->l1_cmax,
+          (const int*)h->l1_scatter, (const double*)h->l1_recv, b1, init1 ? x1 : (double*)nullptr,
+          init1 ? (const double*)h->lv[1].diag : (const double*)nullptr, init1 ? h->lv[1].color_row[1] : 0);
+  ++h->nlaunch;
+  vcycle(h, 1, init1);
+  klaunch(h->s, h->pdl, prolong_kernel, nblk(L0.n, 256), 256, L0.n, (const int*)L0.agg, (const double*)x1, L0.x);
+  ++h->nlaunch;
+  exch_l0(h, L0.x, -1);
+  for (int c = L0.ncolor - 1; c >= 0; --c) {
+    sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
+    if (c > 0) exch_l0(h, L0.x, c);
+  }
+  klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, (const int*)h->l0_of_cell, (const double*)L0.x, h->wp);
+  ++h->nlaunch;
+  exch_cell(h, h->wp, 1, -1);
+  launch_spmv(h, 2, h->wp, g, h->r);                                         // a8 (owned rows)
+  launch_bilu(h, h->r, h->wp, z);                                            // a9 with per-color halos
+}
+
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
+  if (h->comm) {
+    msp_apply_dist(h, g, z);
+    return;
+  }
   if (h->prm.stages == 3) {
     msp_apply_npr(h, g, z);
     return;
@@ -935,8 +1356,18 @@ void reduce(msp_handle* h, int nv, double* out, const double* addend, double* ra
   klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, nv, h->part, out, addend, sqrt_index); ++h->nlaunch;
 }
 
+void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
+             double* raw, int sq);
+
 // ||w||^2 -> out[0] = ||w||
 void norm_dev(msp_handle* h, const double* w, double* out) {
+  if (h->comm) {
+    cgs_dot(h, 1, w, w, h->lred, nullptr, nullptr, -1);
+    h->comm->allreduce_sum(h->s, h->lred, 1);
+    klaunch(h->s, h->pdl, sqrt_kernel, 1, 32, (const double*)h->lred, out);
+    ++h->nlaunch;
+    return;
+  }
   multidot_t<4>(h, 1, w, w);
   klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, out, nullptr, 0); ++h->nlaunch;
 }
@@ -992,7 +1423,25 @@ void cgs_axpy(msp_handle* h, int nv, const double* V, const double* coef, double
 // CGS2 (R8) on w = V[nv] against V[0..nv): hcol[0..nv) = h1 + h2, hcol[nv] = ||w||,
 // V[nv] = w / ||w||.  Three passes over the basis:
 //   A: h1 = V^T w;  B: w -= V h1 and h2 = V^T w (fused);  C: w -= V h2 and ||w||^2.
+void cgs2_dist(msp_handle* h, int nv, double* w) {
+  // local partial sums, then sums over ranks; arithmetic per element as cgs2
+  cgs_dot(h, nv, h->V, w, h->dh1, nullptr, nullptr, -1);
+  h->comm->allreduce_sum(h->s, h->dh1, nv);
+  cgs_axpy<true>(h, nv, h->V, h->dh1, w, h->dh2, nullptr, nullptr, -1);
+  h->comm->allreduce_sum(h->s, h->dh2, nv);
+  klaunch(h->s, h->pdl, add_vec_kernel, 1, 64, nv, (const double*)h->dh1, (const double*)h->dh2, h->hcol);
+  cgs_axpy<false>(h, nv, h->V, h->dh2, w, h->lred, nullptr, nullptr, -1);
+  h->comm->allreduce_sum(h->s, h->lred, 1);
+  klaunch(h->s, h->pdl, sqrt_kernel, 1, 32, (const double*)h->lred, h->hcol + nv);
+  klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, h->N, (const double*)w, (const double*)(h->hcol + nv), w);
+  h->nlaunch += 3;
+}
+
 void cgs2(msp_handle* h, int nv, double* w) {
+  if (h->comm) {
+    cgs2_dist(h, nv, w);
+    return;
+  }
   cgs_dot(h, nv, h->V, w, h->dh1, nullptr, nullptr, -1);
   cgs_axpy<true>(h, nv, h->V, h->dh1, w, h->hcol, h->dh1, h->dh2, -1);
   cgs_axpy<false>(h, nv, h->V, h->dh2, w, h->hcol + nv, nullptr, nullptr, 0);
@@ -1007,6 +1456,7 @@ void arnoldi_step(msp_handle* h, int j) {
   double* vj = h->V + (size_t)j * N;
   double* w = h->V + (size_t)(j + 1) * N;
   msp_apply_dev(h, vj, h->z);
+  exch_cell(h, h->z, h->b, -1);
   launch_spmv(h, 0, h->z, nullptr, w);
   const int nv = j + 1;
   if (h->prm.orth == 0) {
@@ -1080,6 +1530,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
     if (hlen) *hlen = 0;
     return MSP_OK;
   }
+  exch_cell(h, h->xin, h->b, -1);
   launch_spmv(h, 1, h->xin, h->bin, h->r);                    // r = b - A x0
   norm_dev(h, h->r, h->hcol);
   CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
@@ -1128,6 +1579,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       maxpy(h, k, h->V, h->dh1, h->u, 1, nullptr);
       msp_apply_dev(h, h->u, h->z);
       klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->z, h->xin); ++h->nlaunch;
+      exch_cell(h, h->xin, h->b, -1);
       launch_spmv(h, 1, h->xin, h->bin, h->r);
       norm_dev(h, h->r, h->hcol);
       CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double), cudaMemcpyDeviceToHost, h->s));
@@ -1303,11 +1755,12 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
   // reuse: keep W, hierarchy and BILU factors; refresh A (SpMV, Alg. 1 residuals) on the GPU
   return guarded(h, [&]() -> msp_status {
     const int bb = h->b * h->b;
-    const size_t nv = (size_t)h->nnzb * bb;
+    const size_t nv = (size_t)h->nnzb * bb;                   // local entries to refresh
+    const size_t nglob = h->nat_ci.size() * (size_t)bb;        // caller's (global) values
     const double* nat = A_new->values;
     if (A_new->device < 0) {
-      if (!h->stage) h->stage = h->dalloc<double>(nv);
-      CK(cudaMemcpyAsync(h->stage, A_new->values, sizeof(double) * nv, cudaMemcpyHostToDevice, h->s));
+      if (!h->stage) h->stage = h->dalloc<double>(nglob);
+      CK(cudaMemcpyAsync(h->stage, A_new->values, sizeof(double) * nglob, cudaMemcpyHostToDevice, h->s));
       nat = h->stage;
     }
     switch (h->b) {
@@ -1540,6 +1993,145 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
     *bytes_per_launch = bytes;
     return MSP_OK;
   });
+}
+
+// ----------------------------------------------------------- distributed (§8(e))
+static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* cfg, const int32_t* owner,
+                                    std::unique_ptr<msp::Comm> comm, int rank, int nranks, void* cuda_stream,
+                                    msp_handle** out) {
+  if (!out) return fail(nullptr, MSP_EINVAL, "msp_setup_dist: out is NULL");
+  *out = nullptr;
+  msp_config c;
+  msp_config_default(&c);
+  if (cfg) c = *cfg;
+  if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth != 0)
+    return fail(nullptr, MSP_EINVAL, "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2");
+  c.use_graphs = 0;                 // collectives (and loopback host barriers) are not captured
+  c.use_coop = 0;
+  std::unique_ptr<msp_handle> h(new msp_handle);
+  h->cfg = c;
+  h->prm = params_of(&c);
+  msp::BlockMat M;
+  std::string err;
+  msp_status st = read_bsr(A, nc, M, err);
+  if (st) return fail(nullptr, st, err);
+  h->owner_in.resize(M.n);
+  for (int32_t i = 0; i < M.n; ++i) {
+    const int32_t o = owner ? owner[i] : (int32_t)(((int64_t)i * nranks) / M.n);
+    if (o < 0 || o >= nranks) return fail(nullptr, MSP_EINVAL, "msp_setup_dist: owner out of range");
+    h->owner_in[i] = o;
+  }
+  h->comm = std::move(comm);
+  h->rank = rank;
+  h->nranks = nranks;
+  st = guarded(h.get(), [&]() -> msp_status {
+    CK(cudaGetDevice(&h->device));
+    CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    if (cuda_stream) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, (cudaStream_t)cuda_stream));
+      CK(cudaStreamWaitEvent(h->s, e, 0));
+      cudaEventDestroy(e);
+    }
+    do_setup(h.get(), M);
+    return MSP_OK;
+  });
+  if (st) {
+    g_last_error = h->err;
+    h->free_all();
+    return st;
+  }
+  *out = h.release();
+  return MSP_OK;
+}
+
+msp_status msp_nccl_unique_id(void* id128) {
+  if (!id128) return MSP_EINVAL;
+  return msp::nccl_unique_id(id128) ? fail(nullptr, MSP_ENCCL, "ncclGetUniqueId failed") : MSP_OK;
+}
+
+msp_status msp_setup_dist(const msp_bsr* A, int nc, const msp_config* cfg, const int32_t* owner,
+                          const void* nccl_unique_id, int rank, int nranks, void* cuda_stream, msp_handle** out) {
+  if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, MSP_EINVAL, "msp_setup_dist: bad rank/id");
+  int e = 0;
+  auto comm = msp::make_nccl_comm(nccl_unique_id, rank, nranks, &e);
+  if (!comm) return fail(nullptr, MSP_ENCCL, "ncclCommInitRank failed: " + std::to_string(e));
+  return setup_dist_common(A, nc, cfg, owner, std::move(comm), rank, nranks, cuda_stream, out);
+}
+
+int32_t msp_dist_n_owned(const msp_handle* h) { return h ? h->n : 0; }
+
+msp_status msp_dist_owned_cells(const msp_handle* h, int32_t* cells) {
+  if (!h || !cells) return MSP_EINVAL;
+  if (!h->comm) {
+    for (int32_t i = 0; i < h->n; ++i) cells[i] = i;
+    return MSP_OK;
+  }
+  std::memcpy(cells, h->owned_cells.data(), sizeof(int32_t) * h->owned_cells.size());
+  return MSP_OK;
+}
+
+msp_status msp_loopback_solve(const msp_bsr* A, int nc, const msp_config* cfg, const int32_t* owner, int nranks,
+                              const double* b, double* x, double tol, int restart, int maxit, int* iterations,
+                              double* final_rel_res, int32_t* rank_info) {
+  if (!A || !b || !x || nranks < 1) return fail(nullptr, MSP_EINVAL, "msp_loopback_solve: bad arguments");
+  msp_config c;
+  msp_config_default(&c);
+  if (cfg) c = *cfg;
+  c.alloc = nullptr;                 // worker threads allocate with cudaMalloc
+  c.free_fn = nullptr;
+  auto grp = msp::make_loopback_group(nranks);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int b_ = A->block;
+  std::vector<msp_status> st(nranks, MSP_OK), sst(nranks, MSP_OK);
+  std::vector<int> its(nranks, 0);
+  std::vector<double> rel(nranks, 0.0);
+  std::vector<std::string> errs(nranks);
+  std::vector<int> fail_flag(nranks, 0);
+  std::vector<std::thread> th;
+  for (int r = 0; r < nranks; ++r)
+    th.emplace_back([&, r] {
+      cudaSetDevice(dev);
+      msp_handle* h = nullptr;
+      st[r] = setup_dist_common(A, nc, &c, owner, msp::make_loopback_comm(grp, r), r, nranks, nullptr, &h);
+      if (st[r]) { errs[r] = g_last_error; fail_flag[r] = 1; }
+      msp::loopback_barrier(*grp);
+      bool any = false;
+      for (int q = 0; q < nranks; ++q) any |= fail_flag[q] != 0;
+      if (!any) {
+        const int32_t no = h->n;
+        std::vector<double> bl((size_t)no * b_), xl((size_t)no * b_);
+        for (int32_t k = 0; k < no; ++k)
+          for (int q = 0; q < b_; ++q) {
+            bl[(size_t)k * b_ + q] = b[(size_t)h->owned_cells[k] * b_ + q];
+            xl[(size_t)k * b_ + q] = x[(size_t)h->owned_cells[k] * b_ + q];
+          }
+        sst[r] = msp_solve(h, bl.data(), xl.data(), tol, restart, maxit, &its[r], &rel[r], nullptr, 0, nullptr);
+        if (sst[r] != MSP_OK && sst[r] != MSP_ENOCONV) errs[r] = h->err;
+        for (int32_t k = 0; k < no; ++k)
+          for (int q = 0; q < b_; ++q) x[(size_t)h->owned_cells[k] * b_ + q] = xl[(size_t)k * b_ + q];
+        if (rank_info) {
+          rank_info[4 * r + 0] = h->n;
+          rank_info[4 * r + 1] = h->n_ghost;
+          rank_info[4 * r + 2] = h->lv.empty() ? 0 : h->lv[0].n;
+          rank_info[4 * r + 3] = h->n0_ghost;
+        }
+      }
+      if (h) msp_destroy(h);
+    });
+  for (auto& t : th) t.join();
+  for (int r = 0; r < nranks; ++r) {
+    if (st[r]) return fail(nullptr, st[r], "rank " + std::to_string(r) + ": " + errs[r]);
+    if (sst[r] != MSP_OK && sst[r] != MSP_ENOCONV) return fail(nullptr, sst[r], "rank " + std::to_string(r) + ": " + errs[r]);
+    if (its[r] != its[0]) return fail(nullptr, MSP_ECUDA, "loopback ranks disagree on the iteration count");
+  }
+  if (iterations) *iterations = its[0];
+  if (final_rel_res) *final_rel_res = rel[0];
+  return sst[0];
 }
 
 // ----------------------------------------------------------- host-setup introspection
