@@ -9,8 +9,10 @@ Setup (S1-S4) runs once before timing and is reported separately.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C3]
 
-Prints ONE JSON line (rank 0).  N>1 (torchrun, NCCL): every rank solves its own replica
-(DESIGN.md §7 "replicas" until the z-slab path lands); time = max over ranks.
+Prints ONE JSON line (rank 0).  N>1 (torchrun, NCCL): the system is partitioned into
+z-slabs over the ranks (msp_setup_dist: halo exchanges + allreduce + replicated coarse
+levels); one step = one solve of the whole system; time = max over ranks
+(strong scaling).
 """
 from __future__ import annotations
 
@@ -157,7 +159,7 @@ def run_reference(args, ws, rank):
               f"{setup_s:.1f}s excluded")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": workload_desc(args.config, p)},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -183,14 +185,22 @@ def main():
     import numpy as np
     import torch
     import gen
-    from paper_2208_08594_b200 import MspSolver
+    from paper_2208_08594_b200 import DistSolver, MspSolver, nccl_unique_id
 
     torch.cuda.set_device(local)
     p = gen.make_config(args.config)
-    N = p["n"] * p["b"]
-    s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"])
+    if ws > 1:
+        obj = [nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        s = DistSolver(p["row_ptr"], p["col"], p["val"], p["nc"], rank, ws, obj[0])
+        own = s.owned_cells()
+        rhs = np.ascontiguousarray(p["rhs"].reshape(-1, p["b"])[own].reshape(-1))
+    else:
+        s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"])
+        rhs = p["rhs"]
+    N = len(rhs)
     st0 = s.stats()
-    b_dev = torch.from_numpy(p["rhs"]).cuda()
+    b_dev = torch.from_numpy(rhs).cuda()
     x_dev = torch.zeros_like(b_dev)
 
     def one_solve():
@@ -226,11 +236,11 @@ def main():
         total = float(t.item())
         torch.distributed.barrier()
     ms_per_step = total / args.steps * 1e3
-    value = total / (args.steps * ws)            # seconds per system over the whole job
+    value = total / args.steps                   # seconds per system (one system per step)
 
     # ---- e2e: same solve through the C-ABI with pinned HOST buffers (H2D of b, x0 and
     # D2H of x inside the library's timed region)
-    b_host = torch.from_numpy(p["rhs"]).pin_memory()
+    b_host = torch.from_numpy(rhs).pin_memory()
     x_host = torch.zeros(N, dtype=torch.float64).pin_memory()
     e2e = []
     for k in range(args.warmup + args.steps):
@@ -243,13 +253,16 @@ def main():
     if ws > 1:
         t = torch.tensor([e2e_v], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_v = float(t.item()) / ws
+        e2e_v = float(t.item())
 
     # ---- per-kernel achieved bandwidth (CUDA events on the solver stream, L2 flushed)
     peak, peak_src = measured_peak()
     kernels = {}
-    for kind in ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
-                 "a10_multidot16", "a6_coarse_gemv", "msp_apply"):
+    kinds = ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
+             "a10_multidot16", "a6_coarse_gemv", "msp_apply")
+    if ws > 1:                                     # rank-local kernels only
+        kinds = ("a2_bsr_spmv", "a8_pcol_residual", "a10_multidot16")
+    for kind in kinds:
         try:
             ms, by = s.time_kernel(kind, reps=args.kernel_reps)
         except Exception as e:            # e.g. no AMG level 0 on small configs
@@ -262,7 +275,7 @@ def main():
     cyc = math.ceil(iters / RESTART)
     share = {
         "a2_bsr_spmv": kernels["a2_bsr_spmv"].get("ms", 0) * (iters + 2 * cyc + 1),
-        "a9_bilu_apply": kernels["a9_bilu_apply"].get("ms", 0) * (iters + cyc),
+        "a9_bilu_apply": kernels.get("a9_bilu_apply", {}).get("ms", 0) * (iters + cyc),
         "a8_pcol_residual": kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
         "a4_pgs_sweep_l0": kernels.get("a4_pgs_sweep_l0", {}).get("ms", 0) * 2 * (iters + cyc),
         "a10_multidot16": kernels["a10_multidot16"].get("ms", 0) * 2 * iters,
@@ -289,14 +302,15 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generator, SURVEY §8(d)); no datasets",
                "config": {"workload": workload_desc(args.config, p), "iterations": iters,
                           "iterations_per_step": its, "final_rel_res": max(rels),
                           "setup_s": st0["last_setup_seconds"], "levels": st0["level_n"],
                           "level_colors": st0["level_colors"], "bilu_colors": st0["bilu_colors"],
                           "l2": "inputs larger than L2 (A alone 1.0 GB); kernel timings flush L2",
-                          "parallelism": "replicas" if ws > 1 else "single GPU",
+                          "parallelism": (f"z-slab x{ws} (NCCL halo + allreduce, replicated coarse levels)"
+                                          if ws > 1 else "single GPU"),
                           "wall_s_timed_region": wall},
                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
                "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * N * 8,

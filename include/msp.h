@@ -223,6 +223,14 @@ msp_status msp_loopback_solve(const msp_bsr* A, int nc, const msp_config* cfg, c
  * the owner of the lowest-index cell of their level-1 aggregate). */
 msp_status msp_partition_owner(const msp_host_setup* s, int nx, int ny, int nz, int nranks,
                                int32_t* owner);
+/* Host-only halo plan of the cell space for `rank` (what msp_setup_dist builds; no GPU):
+ * owned_cells[n_own] natural ids in local order, ghost_cells[n_ghost] natural ids in
+ * receive order (grouped by source rank, then BILU color); send_cells (natural ids, size
+ * <= n*nranks) in send order per destination rank with offsets send_ptr[nranks+1];
+ * recv_ptr[nranks+1] ghost offsets per source rank.  owner NULL = index ranges. */
+msp_status msp_dist_plan(const msp_host_setup* s, const int32_t* owner, int rank, int nranks, int32_t* n_own,
+                         int32_t* owned_cells, int32_t* n_ghost, int32_t* ghost_cells, int32_t* send_ptr,
+                         int32_t* send_cells, int32_t* recv_ptr);
 
 #ifdef __cplusplus
 }

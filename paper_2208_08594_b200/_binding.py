@@ -64,7 +64,7 @@ for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats",
            "msp_host_setup_info", "msp_host_setup_level_dims", "msp_host_setup_level_csr",
            "msp_host_setup_level_colors", "msp_host_setup_level_agg", "msp_host_setup_weights",
            "msp_host_setup_order", "msp_partition_owner", "msp_nccl_unique_id", "msp_setup_dist",
-           "msp_dist_owned_cells", "msp_loopback_solve"):
+           "msp_dist_owned_cells", "msp_loopback_solve", "msp_dist_plan"):
     getattr(_lib, _n).restype = ctypes.c_int
 _lib.msp_destroy.argtypes = [ctypes.c_void_p]
 _lib.msp_time_kernel.restype = ctypes.c_int
@@ -383,6 +383,21 @@ class HostSetup:
         o = np.zeros(self.n, np.int32)
         _lib.msp_host_setup_order(self._h, _ptr(o))
         return o
+
+    def dist_plan(self, rank, nranks, owner=None):
+        """Host-only cell-space halo plan of `rank` (see msp_dist_plan)."""
+        n = self.n
+        no, ng = ctypes.c_int32(), ctypes.c_int32()
+        owned = np.zeros(n, np.int32); ghosts = np.zeros(n, np.int32)
+        sp_ = np.zeros(nranks + 1, np.int32); rp_ = np.zeros(nranks + 1, np.int32)
+        sc = np.zeros(max(n * nranks, 1), np.int32)
+        own = None if owner is None else _np(owner, np.int32)
+        st = _lib.msp_dist_plan(self._h, _ptr(own) if own is not None else None, rank, nranks, ctypes.byref(no),
+                                _ptr(owned), ctypes.byref(ng), _ptr(ghosts), _ptr(sp_), _ptr(sc), _ptr(rp_))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        return dict(owned=owned[:no.value].copy(), ghosts=ghosts[:ng.value].copy(), send_ptr=sp_,
+                    send_cells=sc[:sp_[-1]].copy(), recv_ptr=rp_)
 
     def partition_owner(self, nx, ny, nz, nranks):
         o = np.zeros(self.n, np.int32)

@@ -609,11 +609,9 @@ bool invert_block(int b, const double* D, double* Dinv) {
   return true;
 }
 
-int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp,
-                         std::vector<int32_t>& ci, std::vector<int32_t>& dg,
-                         std::vector<int32_t>& src, std::vector<double>& F, std::string& err) {
+int permuted_pattern(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp, std::vector<int32_t>& ci,
+                     std::vector<int32_t>& dg, std::vector<int32_t>& src, std::string& err) {
   const int32_t n = A.n;
-  const int b = A.b, bb = b * b;
   rp.assign(n + 1, 0);
   for (int32_t p = 0; p < n; ++p) {
     const int32_t c = S.order[p];
@@ -635,6 +633,16 @@ int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int3
     }
     if (dg[p] < 0) { err = "BILU: missing diagonal block at cell " + std::to_string(c); return 1; }
   }
+  return 0;
+}
+
+int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp,
+                         std::vector<int32_t>& ci, std::vector<int32_t>& dg,
+                         std::vector<int32_t>& src, std::vector<double>& F, std::string& err) {
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b;
+  int rc0 = permuted_pattern(S, A, rp, ci, dg, src, err);
+  if (rc0) return rc0;
   F.resize(A.v.size());
   for (size_t e = 0; e < src.size(); ++e)
     std::memcpy(&F[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);

@@ -69,6 +69,11 @@ int bilu_factor_permuted(const HostSetup& S, const BlockMat& A, std::vector<int3
                          std::vector<int32_t>& ci, std::vector<int32_t>& dg,
                          std::vector<int32_t>& src_entry, std::vector<double>& F, std::string& err);
 
+// Pattern of A in the ordering positions (rows/cols permuted, columns sorted), without
+// factorization; src[e] = natural entry of permuted entry e.
+int permuted_pattern(const HostSetup& S, const BlockMat& A, std::vector<int32_t>& rp, std::vector<int32_t>& ci,
+                     std::vector<int32_t>& dg, std::vector<int32_t>& src, std::string& err);
+
 // Building blocks (exposed for the host-setup introspection entry points / tests)
 Graph value_graph(const SpMat& A);
 Graph block_graph(const BlockMat& A);

@@ -749,6 +749,73 @@ static void build_halo(msp_handle* h, msp::HaloPlan& P, int nseg, int nranks, in
   P.d_sendbuf = h->dalloc<double>((size_t)std::max(P.nsend, 1) * 8);
 }
 
+// Host-side plan of the cell space for rank `me` (pure integer work, no GPU).
+struct CellPlan {
+  std::vector<int32_t> own_pos, color_pos;   // effective owner / block color of every position
+  std::vector<int32_t> posown, loc;          // owned positions (local order), position -> local
+  std::vector<int32_t> ghosts, lcol;         // ghost positions (receive order), position -> local col
+  std::vector<std::vector<std::vector<int32_t>>> sendl;   // [peer][color] owned local indices
+  std::vector<std::vector<int32_t>> rcnt;                 // [peer][color] ghost counts
+};
+
+CellPlan compute_cell_plan(const msp::HostSetup& S, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
+                           const std::vector<int32_t>& owner_in, int P, int me) {
+  const int32_t n = S.n;
+  CellPlan C;
+  C.own_pos.assign(n, 0);
+  C.color_pos.assign(n, 0);
+  const int nb = (int)S.blk_ptr.size() - 1;
+  std::vector<int32_t> bcolor(nb);
+  for (int c = 0; c < S.bilu_ncolor; ++c)
+    for (int k = S.color_blk_ptr[c]; k < S.color_blk_ptr[c + 1]; ++k) bcolor[k] = c;
+  for (int k = 0; k < nb; ++k) {
+    int32_t lowest = INT32_MAX;
+    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) lowest = std::min(lowest, S.order[p]);
+    const int32_t o = owner_in[lowest];
+    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) { C.own_pos[p] = o; C.color_pos[p] = bcolor[k]; }
+  }
+  C.loc.assign(n, -1);
+  for (int32_t p = 0; p < n; ++p)
+    if (C.own_pos[p] == me) { C.loc[p] = (int32_t)C.posown.size(); C.posown.push_back(p); }
+  std::vector<std::vector<int32_t>> need(P);
+  {
+    std::vector<int32_t> mark(n, -1);
+    for (int32_t p = 0; p < n; ++p) {
+      const int t = C.own_pos[p];
+      for (int32_t e = rp[p]; e < rp[p + 1]; ++e) {
+        const int32_t qpos = ci[e];
+        const int o = C.own_pos[qpos];
+        if (o == t) continue;
+        if (o == me) need[t].push_back(qpos);
+        if (t == me && mark[qpos] < 0) { mark[qpos] = 1; C.ghosts.push_back(qpos); }
+      }
+    }
+    for (int q = 0; q < P; ++q) {
+      auto& v = need[q];
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) {
+        return C.color_pos[x] != C.color_pos[y] ? C.color_pos[x] < C.color_pos[y] : x < y;
+      });
+    }
+    std::sort(C.ghosts.begin(), C.ghosts.end(), [&](int32_t x, int32_t y) {
+      if (C.own_pos[x] != C.own_pos[y]) return C.own_pos[x] < C.own_pos[y];
+      if (C.color_pos[x] != C.color_pos[y]) return C.color_pos[x] < C.color_pos[y];
+      return x < y;
+    });
+  }
+  const int32_t no = (int32_t)C.posown.size(), ng = (int32_t)C.ghosts.size();
+  C.lcol.assign(n, -1);
+  for (int32_t l = 0; l < no; ++l) C.lcol[C.posown[l]] = l;
+  for (int32_t k = 0; k < ng; ++k) C.lcol[C.ghosts[k]] = no + k;
+  C.sendl.assign(P, std::vector<std::vector<int32_t>>(S.bilu_ncolor));
+  C.rcnt.assign(P, std::vector<int32_t>(S.bilu_ncolor, 0));
+  for (int q = 0; q < P; ++q)
+    for (int32_t pos : need[q]) C.sendl[q][C.color_pos[pos]].push_back(C.loc[pos]);
+  for (int32_t g : C.ghosts) C.rcnt[C.own_pos[g]][C.color_pos[g]]++;
+  return C;
+}
+
 void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
                    const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms) {
@@ -757,67 +824,16 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
   const int P = h->nranks, me = h->rank;
   const int L = (int)S.lv.size();
   if (L < 1) throw std::pair<int, std::string>(MSP_EINVAL, "distributed mode needs >= 1 AMG smoothing level (n > coarsest_max_dof)");
-  // effective owner of every global position: owner of the block's lowest natural cell
-  std::vector<int32_t> own_pos(n);
-  const int nb = (int)S.blk_ptr.size() - 1;
-  std::vector<int32_t> bcolor(nb), color_pos(n);
-  for (int c = 0; c < S.bilu_ncolor; ++c)
-    for (int k = S.color_blk_ptr[c]; k < S.color_blk_ptr[c + 1]; ++k) bcolor[k] = c;
-  for (int k = 0; k < nb; ++k) {
-    int32_t lowest = INT32_MAX;
-    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) lowest = std::min(lowest, S.order[p]);
-    const int32_t o = h->owner_in[lowest];
-    for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) { own_pos[p] = o; color_pos[p] = bcolor[k]; }
-  }
+  // ---------------- cell space
+  CellPlan C = compute_cell_plan(S, rp, ci, h->owner_in, P, me);
+  const std::vector<int32_t>& own_pos = C.own_pos;
+  const std::vector<int32_t>& posown = C.posown;
+  const std::vector<int32_t>& lcol = C.lcol;
   std::vector<int32_t> own_cell(n);
   for (int32_t p = 0; p < n; ++p) own_cell[S.order[p]] = own_pos[p];
-  // ---------------- cell space
-  std::vector<int32_t> loc(n, -1), posown;
-  for (int32_t p = 0; p < n; ++p)
-    if (own_pos[p] == me) { loc[p] = (int32_t)posown.size(); posown.push_back(p); }
   const int32_t no = (int32_t)posown.size();
-  // needed[q] (per peer rank q): positions owned by `me` referenced by rows of q;
-  // ghosts of me: positions owned by others referenced by my rows
-  std::vector<std::vector<int32_t>> need(P);            // need[q]: my positions q needs
-  std::vector<int32_t> ghosts;
-  {
-    std::vector<int32_t> mark(n, -1);
-    for (int32_t p = 0; p < n; ++p) {
-      const int t = own_pos[p];
-      for (int32_t e = rp[p]; e < rp[p + 1]; ++e) {
-        const int32_t qpos = ci[e];
-        const int o = own_pos[qpos];
-        if (o == t) continue;
-        if (o == me) need[t].push_back(qpos);           // t's row reads my position
-        if (t == me && mark[qpos] < 0) { mark[qpos] = 1; ghosts.push_back(qpos); }
-      }
-    }
-    for (int q = 0; q < P; ++q) {
-      auto& v = need[q];
-      std::sort(v.begin(), v.end());
-      v.erase(std::unique(v.begin(), v.end()), v.end());
-      std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) {
-        return color_pos[x] != color_pos[y] ? color_pos[x] < color_pos[y] : x < y;
-      });
-    }
-    std::sort(ghosts.begin(), ghosts.end(), [&](int32_t x, int32_t y) {
-      if (own_pos[x] != own_pos[y]) return own_pos[x] < own_pos[y];
-      if (color_pos[x] != color_pos[y]) return color_pos[x] < color_pos[y];
-      return x < y;
-    });
-  }
-  const int32_t ng = (int32_t)ghosts.size();
-  std::vector<int32_t> lcol(n, -1);                     // global position -> local column
-  for (int32_t l = 0; l < no; ++l) lcol[posown[l]] = l;
-  for (int32_t k = 0; k < ng; ++k) lcol[ghosts[k]] = no + k;
-  {
-    std::vector<std::vector<std::vector<int32_t>>> sendl(P, std::vector<std::vector<int32_t>>(S.bilu_ncolor));
-    std::vector<std::vector<int32_t>> rcnt(P, std::vector<int32_t>(S.bilu_ncolor, 0));
-    for (int q = 0; q < P; ++q)
-      for (int32_t pos : need[q]) sendl[q][color_pos[pos]].push_back(loc[pos]);
-    for (int32_t g : ghosts) rcnt[own_pos[g]][color_pos[g]]++;
-    build_halo(h, h->cell_halo, S.bilu_ncolor, P, me, sendl, rcnt);
-  }
+  const int32_t ng = (int32_t)C.ghosts.size();
+  build_halo(h, h->cell_halo, S.bilu_ncolor, P, me, C.sendl, C.rcnt);
   // local BSR rows (entries keep the global position order: L | diag | U)
   std::vector<int32_t> lrp(no + 1, 0), lci, ldg(no), lsrc;
   std::vector<double> lF, lA, lPc, lW((size_t)no * b);
@@ -1896,6 +1912,8 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
   if (!h || reps < 1 || !ms_per_launch || !bytes_per_launch) return fail(h, MSP_EINVAL, "msp_time_kernel: bad args");
   const bool flush_l2 = (kind & 0x100) == 0;
   kind &= 0xff;
+  if (h->comm && kind != 0 && kind != 2 && kind != 4)
+    return fail(h, MSP_EINVAL, "msp_time_kernel: distributed handles time only rank-local kernels (0, 2, 4)");
   if ((kind == 1) && h->lv.empty()) return fail(h, MSP_EINVAL, "msp_time_kernel: no AMG level 0");
   return guarded(h, [&]() -> msp_status {
     const size_t kFlush = (size_t)256 << 20;
@@ -2211,6 +2229,40 @@ msp_status msp_host_setup_weights(const msp_host_setup* s, double* W) {
 msp_status msp_host_setup_order(const msp_host_setup* s, int32_t* order) {
   if (!s || !order) return MSP_EINVAL;
   std::memcpy(order, s->S.order.data(), sizeof(int32_t) * s->S.order.size());
+  return MSP_OK;
+}
+
+msp_status msp_dist_plan(const msp_host_setup* s, const int32_t* owner, int rank, int nranks, int32_t* n_own,
+                         int32_t* owned_cells, int32_t* n_ghost, int32_t* ghost_cells, int32_t* send_ptr,
+                         int32_t* send_cells, int32_t* recv_ptr) {
+  if (!s || nranks < 1 || rank < 0 || rank >= nranks || !n_own || !owned_cells || !n_ghost || !ghost_cells ||
+      !send_ptr || !send_cells || !recv_ptr)
+    return fail(nullptr, MSP_EINVAL, "msp_dist_plan: bad arguments");
+  const int32_t n = s->S.n;
+  std::vector<int32_t> own(n);
+  for (int32_t i = 0; i < n; ++i) {
+    own[i] = owner ? owner[i] : (int32_t)(((int64_t)i * nranks) / n);
+    if (own[i] < 0 || own[i] >= nranks) return fail(nullptr, MSP_EINVAL, "msp_dist_plan: owner out of range");
+  }
+  std::vector<int32_t> rp, ci, dg, src;
+  std::string err;
+  if (msp::permuted_pattern(s->S, s->M, rp, ci, dg, src, err)) return fail(nullptr, MSP_EINVAL, err);
+  CellPlan C = compute_cell_plan(s->S, rp, ci, own, nranks, rank);
+  *n_own = (int32_t)C.posown.size();
+  *n_ghost = (int32_t)C.ghosts.size();
+  for (size_t l = 0; l < C.posown.size(); ++l) owned_cells[l] = s->S.order[C.posown[l]];
+  for (size_t k = 0; k < C.ghosts.size(); ++k) ghost_cells[k] = s->S.order[C.ghosts[k]];
+  send_ptr[0] = 0;
+  recv_ptr[0] = 0;
+  for (int q = 0; q < nranks; ++q) {
+    int32_t ns = send_ptr[q], nr = 0;
+    for (size_t c = 0; c < C.sendl[q].size(); ++c) {
+      for (int32_t l : C.sendl[q][c]) send_cells[ns++] = s->S.order[C.posown[l]];
+      nr += C.rcnt[q][c];
+    }
+    send_ptr[q + 1] = ns;
+    recv_ptr[q + 1] = recv_ptr[q] + nr;
+  }
   return MSP_OK;
 }
 
