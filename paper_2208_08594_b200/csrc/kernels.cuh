@@ -84,6 +84,52 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
   }
 }
 
+// 4-lane reduce-scatter: lane q of a 4-lane group holds a[0..3] (partial sums of rows
+// 0..3); returns sum over the group of a[q] (fixed butterfly order: deterministic).
+// m4: mask of the (aligned) 4-lane group; xor offsets 1, 2 stay inside the group.
+__device__ __forceinline__ double reduce_scatter4(double a0, double a1, double a2, double a3, int q,
+                                                  unsigned m4) {
+  const bool hi = (q & 2) != 0;
+  const double s0 = hi ? a0 : a2, s1 = hi ? a1 : a3;
+  const double r0 = __shfl_xor_sync(m4, s0, 2), r1 = __shfl_xor_sync(m4, s1, 2);
+  const double k0 = (hi ? a2 : a0) + r0, k1 = (hi ? a3 : a1) + r1;
+  const bool odd = (q & 1) != 0;
+  const double r = __shfl_xor_sync(m4, odd ? k0 : k1, 1);
+  return (odd ? k1 : k0) + r;
+}
+
+// a2 for 4x4 blocks, column-per-lane: lane q loads block column q (two 16-byte loads,
+// column-major storage), multiplies by its own x_q (no broadcast), keeps 4 row partial
+// sums and reduce-scatters once per block row.  MODE 0: y = A x; MODE 1: y = g - A x.
+template <int MODE>
+__global__ void __launch_bounds__(256) bsr_spmv4c_kernel(int n, const int* __restrict__ rp,
+                                                         const int* __restrict__ ci,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ g,
+                                                         double* __restrict__ y) {
+  PDL_ENTRY();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gtid >> 2, q = threadIdx.x & 3;
+  if (row >= n) return;                       // whole 4-lane groups exit together
+  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 2
+  for (int e = e0; e < e1; ++e) {
+    const int c = ldg(ci + e);
+    const double xq = ldg(x + (size_t)c * 4 + q);
+    const double2* colp = reinterpret_cast<const double2*>(val + (size_t)e * 16 + q * 4);
+    const double2 lo = __ldg(colp), hi = __ldg(colp + 1);
+    a0 = fma(lo.x, xq, a0);
+    a1 = fma(lo.y, xq, a1);
+    a2 = fma(hi.x, xq, a2);
+    a3 = fma(hi.y, xq, a3);
+  }
+  const double acc = reduce_scatter4(a0, a1, a2, a3, q, 0xFu << ((threadIdx.x & 31) & ~3));
+  const size_t o = (size_t)row * 4 + q;
+  y[o] = (MODE == 0) ? acc : (g[o] - acc);
+}
+
 // ---------------------------------------------------------------------------
 // a3: pressure restriction with decoupling weights (R4): rp_l0[dst[c]] = sum_k
 // W[c][k] * g[c*B+k]; dst maps internal cell positions to level-0 rows.
@@ -506,15 +552,30 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     const int eext = e0 + (cn & 0xff);       // [e0, eext): external L; [eext, d): intra L
     int e = eext;
     double acc = 0.0;
+    if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 2
-    for (int ee = e0; ee < eext; ++ee) {    // external L part: columns before the block
-      const int k = ldg(ci + ee);
-      const double yq = (q < B) ? ldg(v + (size_t)k * B + q) : 0.0;
-      const double* blkF = F + (size_t)ee * BB;
+      for (int ee = e0; ee < eext; ++ee) {
+        const double yq = ldg(v + (size_t)ldg(ci + ee) * 4 + q);
+        const double2* cp = reinterpret_cast<const double2*>(F + (size_t)ee * 16 + q * 4);
+        const double2 lo = __ldg(cp), hi = __ldg(cp + 1);
+        a0 = fma(lo.x, yq, a0);
+        a1 = fma(lo.y, yq, a1);
+        a2 = fma(hi.x, yq, a2);
+        a3 = fma(hi.y, yq, a3);
+      }
+      acc = reduce_scatter4(a0, a1, a2, a3, q, cmask);
+    } else {
+#pragma unroll 2
+      for (int ee = e0; ee < eext; ++ee) {  // external L part: columns before the block
+        const int k = ldg(ci + ee);
+        const double yq = (q < B) ? ldg(v + (size_t)k * B + q) : 0.0;
+        const double* blkF = F + (size_t)ee * BB;
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const double yu = __shfl_sync(cmask, yq, cbase + u);
-        if (q < B) acc = fma(ldg(blkF + u * B + q), yu, acc);
+        for (int u = 0; u < B; ++u) {
+          const double yu = __shfl_sync(cmask, yq, cbase + u);
+          if (q < B) acc = fma(ldg(blkF + u * B + q), yu, acc);
+        }
       }
     }
     t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
@@ -541,15 +602,30 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     const int e1 = valid ? ldg(rp + i + 1) : 0;
     const int ei = d + 1 + (cn >> 8);        // (d, ei): intra U; [ei, e1): external U
     double acc = 0.0;
+    if constexpr (B == 4) {                  // column-per-lane (see the forward part)
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 2
-    for (int e = ei; e < e1; ++e) {          // external U part: columns after the block
-      const int j = ldg(ci + e);
-      const double xq = (q < B) ? ldg(v + (size_t)j * B + q) : 0.0;
-      const double* blkF = F + (size_t)e * BB;
+      for (int e = ei; e < e1; ++e) {
+        const double xq = ldg(v + (size_t)ldg(ci + e) * 4 + q);
+        const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
+        const double2 lo = __ldg(cp), hi = __ldg(cp + 1);
+        a0 = fma(lo.x, xq, a0);
+        a1 = fma(lo.y, xq, a1);
+        a2 = fma(hi.x, xq, a2);
+        a3 = fma(hi.y, xq, a3);
+      }
+      acc = reduce_scatter4(a0, a1, a2, a3, q, cmask);
+    } else {
+#pragma unroll 2
+      for (int e = ei; e < e1; ++e) {        // external U part: columns after the block
+        const int j = ldg(ci + e);
+        const double xq = (q < B) ? ldg(v + (size_t)j * B + q) : 0.0;
+        const double* blkF = F + (size_t)e * BB;
 #pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const double xu = __shfl_sync(cmask, xq, cbase + u);
-        if (q < B) acc = fma(ldg(blkF + u * B + q), xu, acc);
+        for (int u = 0; u < B; ++u) {
+          const double xu = __shfl_sync(cmask, xq, cbase + u);
+          if (q < B) acc = fma(ldg(blkF + u * B + q), xu, acc);
+        }
       }
     }
     t -= acc;

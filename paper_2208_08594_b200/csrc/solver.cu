@@ -1011,11 +1011,18 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
 }
 
 // ----------------------------------------------------------------- launches
+bool g_spmv4c = true;               // 4x4 blocks: column-per-lane SpMV (MSP_SPMV4C=0 to disable)
+
 template <int B>
 void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, const int* ci, const double* val,
                    const double* x, const double* g, double* y) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   const unsigned grid = nblk((size_t)n * TS, 256);
+  if (B == 4 && g_spmv4c && mode != 2) {
+    if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, grid, 256, n, rp, ci, val, x, g, y);
+    else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y);
+    return;
+  }
   if (mode == 0) klaunch(s, pdl, bsr_spmv_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
   else if (mode == 1) klaunch(s, pdl, bsr_spmv_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
   else klaunch(s, pdl, bsr_spmv_kernel<B, 2>, grid, 256, n, rp, ci, val, x, g, y);
@@ -1698,6 +1705,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
+  if (const char* e = std::getenv("MSP_SPMV4C")) g_spmv4c = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
