@@ -18,6 +18,15 @@ constexpr int kSell = 32;
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
 
+// Streaming (evict-first, ld.global.cs) loads for large single-use operands (matrix and
+// factor blocks), so that the gathered vectors stay L2-resident.  MSP_STREAM_HINT=0
+// equivalent: define MSP_NO_CS.
+#ifndef MSP_NO_CS
+__device__ __forceinline__ double2 ldstream2(const double2* p) { return __ldcs(p); }
+#else
+__device__ __forceinline__ double2 ldstream2(const double2* p) { return __ldg(p); }
+#endif
+
 // Programmatic dependent launch (PDL).  Every kernel is launched with programmatic
 // stream serialisation: it may start while its predecessor still runs, so it must
 // call pdl_wait() before touching anything a predecessor produced (vectors); only
@@ -119,7 +128,7 @@ __global__ void __launch_bounds__(256) bsr_spmv4c_kernel(int n, const int* __res
     const int c = ldg(ci + e);
     const double xq = ldg(x + (size_t)c * 4 + q);
     const double2* colp = reinterpret_cast<const double2*>(val + (size_t)e * 16 + q * 4);
-    const double2 lo = __ldg(colp), hi = __ldg(colp + 1);
+    const double2 lo = ldstream2(colp), hi = ldstream2(colp + 1);
     a0 = fma(lo.x, xq, a0);
     a1 = fma(lo.y, xq, a1);
     a2 = fma(hi.x, xq, a2);
@@ -558,7 +567,7 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
       for (int ee = e0; ee < eext; ++ee) {
         const double yq = ldg(v + (size_t)ldg(ci + ee) * 4 + q);
         const double2* cp = reinterpret_cast<const double2*>(F + (size_t)ee * 16 + q * 4);
-        const double2 lo = __ldg(cp), hi = __ldg(cp + 1);
+        const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
         a0 = fma(lo.x, yq, a0);
         a1 = fma(lo.y, yq, a1);
         a2 = fma(hi.x, yq, a2);
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
       for (int e = ei; e < e1; ++e) {
         const double xq = ldg(v + (size_t)ldg(ci + e) * 4 + q);
         const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
-        const double2 lo = __ldg(cp), hi = __ldg(cp + 1);
+        const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
         a0 = fma(lo.x, xq, a0);
         a1 = fma(lo.y, xq, a1);
         a2 = fma(hi.x, xq, a2);
