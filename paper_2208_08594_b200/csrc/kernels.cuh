@@ -14,6 +14,10 @@
 namespace mspk {
 
 constexpr int kSell = 32;
+#ifndef MSP_BILU_BATCH
+#define MSP_BILU_BATCH 0
+#endif
+constexpr bool kBiluBatch = MSP_BILU_BATCH != 0;
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
@@ -511,6 +515,41 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
   }
 }
 
+// External part of a 4x4 block-row product over entries [e0, e1), column-per-lane, with
+// up to 4 entries in flight (indices, then factor columns and vector components, then
+// FMAs): returns the 4 row partial sums of this lane's column contributions.
+__device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const int* __restrict__ ci,
+                                                 const double* __restrict__ F, const double* __restrict__ v,
+                                                 double& a0, double& a1, double& a2, double& a3) {
+  for (int base = e0; base < e1; base += 4) {
+    int k[4];
+    double2 lo[4], hi[4];
+    double vq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) k[u] = (base + u < e1) ? __ldg(ci + base + u) : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (k[u] >= 0) {
+        const double2* cp = reinterpret_cast<const double2*>(F + (size_t)(base + u) * 16 + q * 4);
+        lo[u] = ldstream2(cp);
+        hi[u] = ldstream2(cp + 1);
+        vq[u] = __ldg(v + (size_t)k[u] * 4 + q);
+      } else {
+        lo[u] = make_double2(0.0, 0.0);
+        hi[u] = lo[u];
+        vq[u] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fma(lo[u].x, vq[u], a0);
+      a1 = fma(lo[u].y, vq[u], a1);
+      a2 = fma(hi[u].x, vq[u], a2);
+      a3 = fma(hi[u].y, vq[u], a3);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // a9 v2: BILU(0) color phase with one lane group (TS lanes) per CELL of an aggregate
 // block (<= MAXC cells): team = MAXC*TS lanes.  Phase 1 gathers, for every cell of
@@ -563,6 +602,8 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     double acc = 0.0;
     if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (kBiluBatch) ext_sum4_batched(e0, eext, q, ci, F, v, a0, a1, a2, a3);
+      else
 #pragma unroll 2
       for (int ee = e0; ee < eext; ++ee) {
         const double yq = ldg(v + (size_t)ldg(ci + ee) * 4 + q);
@@ -613,6 +654,8 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     double acc = 0.0;
     if constexpr (B == 4) {                  // column-per-lane (see the forward part)
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (kBiluBatch) ext_sum4_batched(ei, e1, q, ci, F, v, a0, a1, a2, a3);
+      else
 #pragma unroll 2
       for (int e = ei; e < e1; ++e) {
         const double xq = ldg(v + (size_t)ldg(ci + e) * 4 + q);
