@@ -964,8 +964,9 @@ __global__ void __launch_bounds__(kRedThreads) multiaxpy_kernel(size_t N, int nv
 // raw[i] = sum (optional), sqrt applied to out[sqrt_index].  ticket is reset for the
 // next graph replay.
 // ---------------------------------------------------------------------------
+// partial sums of this CTA for vector slots [off, off + nv) -> part[blockIdx.x][off + i]
 template <int NV>
-__device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, double* part) {
+__device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, double* part, int off = 0) {
   __shared__ double sh[kRedThreads / 32][NV];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -980,17 +981,19 @@ __device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, 
   for (int i = threadIdx.x; i < nv; i += blockDim.x) {
     double a = 0.0;
     for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k][i];
-    part[(size_t)blockIdx.x * kMaxV + i] = a;
+    part[(size_t)blockIdx.x * kMaxV + off + i] = a;
   }
 }
 
+// The last CTA of the grid (all gridDim.x * gridDim.y CTAs) sums the partial rows
+// 0..gridDim.x-1 for slots [0, nv) in fixed order.
 __device__ __forceinline__ void finalize_partials(int nv, const double* part, double* out,
                                                   const double* addend, double* raw, int sqrt_index,
                                                   unsigned* ticket) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -1050,6 +1053,10 @@ __global__ void __launch_bounds__(kRedThreads, MINB) cgs_dot_kernel(size_t NE, i
                                                                  double* raw, int sqrt_index, unsigned* ticket) {
   PDL_ENTRY();
   using T = VecT<EW>;
+  // gridDim.y > 1: CTA row y handles vectors [y*NV, min(nv, (y+1)*NV))
+  const int vbase = blockIdx.y * NV;
+  const int nvl = min(NV, nv - vbase);
+  const double* Vb = V + (size_t)vbase * ldv;
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
@@ -1058,11 +1065,11 @@ __global__ void __launch_bounds__(kRedThreads, MINB) cgs_dot_kernel(size_t NE, i
     const T wt = T::ld(w, t);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      if (i < nv) acc[i] = vdot<EW>(T::ld(V + i * ldv, t), wt, acc[i]);
+      if (i < nvl) acc[i] = vdot<EW>(T::ld(Vb + i * ldv, t), wt, acc[i]);
       if (i % 16 == 15) asm volatile("" ::: "memory");   // <= 16 loads in flight (registers)
     }
   }
-  block_partials<NV>(acc, nv, part);
+  block_partials<NV>(acc, nvl, part, vbase);
   finalize_partials(nv, part, out, addend, raw, sqrt_index, ticket);
 }
 

@@ -1411,10 +1411,12 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
   if (nv <= 4) cgs_dot_t<4>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_dot_t<8>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_dot_t<16>(h, nv, V, w, out, addend, raw, sq);
-  else if (h->cgs_split) {                   // 16-vector halves, 16-byte loads
-    cgs_dot_t<16>(h, 16, V, w, out, addend, raw, -1);
-    cgs_dot(h, nv - 16, V + (size_t)16 * h->N, w, out + 16, addend ? addend + 16 : nullptr,
-            raw ? raw + 16 : nullptr, sq >= 16 ? sq - 16 : -1);
+  else if (h->cgs_split == 0) {
+    // 16 vectors per CTA row (gridDim.y = 2), 16-byte loads: full occupancy instead of
+    // 32 accumulators per thread
+    klaunch(h->s, h->pdl, cgs_dot_kernel<16, 2, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N / 2, nv, V,
+            h->N, w, h->part, out, addend, raw, sq, h->ticket);
+    ++h->nlaunch;
   } else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
 }
 template <int NV, bool DOT>
@@ -1432,14 +1434,11 @@ void cgs_axpy(msp_handle* h, int nv, const double* V, const double* coef, double
   if (nv <= 4) cgs_axpy_t<4, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_axpy_t<8, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_axpy_t<16, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
-  else if (DOT && h->cgs_split) {
-    // axpy over all nv vectors (16-byte loads, 16 in flight) with the dot over the first
-    // 16, then the dot of the remaining vectors as a separate pass
-    klaunch(h->s, h->pdl, cgs_axpy_kernel<32, 2, true, 16, 2>, kRedBlocks, kRedThreads, h->N / 2, nv, V, h->N,
-            coef, w, h->part, out, addend, raw, -1, h->ticket);
-    ++h->nlaunch;
-    cgs_dot(h, nv - 16, V + (size_t)16 * h->N, w, out + 16, addend ? addend + 16 : nullptr,
-            raw ? raw + 16 : nullptr, -1);
+  else if (DOT && h->cgs_split == 0) {
+    // nv > 16: the fused pass would need 32 accumulators per thread (25% occupancy);
+    // instead the (fast) 32-vector axpy, then the row-split dot of the updated w
+    cgs_axpy_t<32, false>(h, nv, V, coef, w, h->lred, nullptr, nullptr, -1);
+    cgs_dot(h, nv, V, w, out, addend, raw, sq);
   } else cgs_axpy_t<32, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
 }
 
