@@ -259,7 +259,7 @@ def main():
     peak, peak_src = measured_peak()
     kernels = {}
     kinds = ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
-             "a10_multidot16", "a6_coarse_gemv", "msp_apply")
+             "a10_multidot16", "cgs2_step15", "a6_coarse_gemv", "vcycle", "msp_apply")
     if ws > 1:                                     # rank-local kernels only
         kinds = ("a2_bsr_spmv", "a8_pcol_residual", "a10_multidot16")
     for kind in kinds:
@@ -271,14 +271,14 @@ def main():
         kernels[kind] = {"ms": ms, "alg_bytes": by,
                          "GBps": (by / (ms * 1e-3) / 1e9) if by else None,
                          "frac": (by / (ms * 1e-3) / 1e9 / peak) if by else None}
-    # per-solve share estimate: launches of each kernel per solve x its time
+    # estimated share of one solve of each HBM-bound kernel (launch counts per solve);
+    # the V-cycle (many latency-bound launches) is reported in `kernels`, not as a roofline
     cyc = math.ceil(iters / RESTART)
     share = {
         "a2_bsr_spmv": kernels["a2_bsr_spmv"].get("ms", 0) * (iters + 2 * cyc + 1),
         "a9_bilu_apply": kernels.get("a9_bilu_apply", {}).get("ms", 0) * (iters + cyc),
         "a8_pcol_residual": kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
-        "a4_pgs_sweep_l0": kernels.get("a4_pgs_sweep_l0", {}).get("ms", 0) * 2 * (iters + cyc),
-        "a10_multidot16": kernels["a10_multidot16"].get("ms", 0) * 2 * iters,
+        "cgs2_step15": kernels.get("cgs2_step15", {}).get("ms", 0) * iters,
     }
     dom = max(share, key=share.get)
     kd = kernels[dom]

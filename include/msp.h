@@ -155,10 +155,10 @@ msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x);
  * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory
  * traffic, each vector counted once).  kind: 0 a2 BSR SpMV; 1 a4 level-0 PGS-MC sweep
  * (all colors, descending = full work per color); 2 a8 pressure-column residual;
- * 3 a9 BILU(0) apply (all colors); 4 a10 CGS2 multidot over 16 basis vectors;
+ * 3 a9 BILU(0) apply (all colors); 4 a10 CGS2 pass A (dot) over 16 basis vectors;
  * 5 a6 coarsest dense-inverse GEMV; 6 one whole MSP application; 7 one V-cycle B_P;
- * 8 BILU apply; 9 one whole Arnoldi step (j = 15); 10 the CGS2 of step 15 (bytes = 0 for
- * kinds 6-10).  kind | 0x100: no L2 flush (warm caches).  Each piece is captured once
+ * 8 BILU apply; 9 one whole Arnoldi step (j = 15); 10 the CGS2 of step 15 (55 vectors);
+ * 11/12 Arnoldi step / CGS2 at j = 25 (bytes = 0 for kinds 6-9, 11, 12).  kind | 0x100: no L2 flush (warm caches).  Each piece is captured once
  * into a CUDA graph and replayed (as in the solve); the first replay is a warm-up.
  * Scratch contents of the handle are overwritten. */
 msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,

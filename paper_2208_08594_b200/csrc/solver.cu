@@ -1953,8 +1953,8 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
         bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
         break;
-      case 4:
-        fn = [&]() { multidot(h, 16, h->V, h->u); };
+      case 4:                                    // CGS2 pass A over 16 basis vectors
+        fn = [&]() { cgs_dot(h, 16, h->V, h->u, h->dh1, nullptr, nullptr, -1); };
         bytes = 17.0 * 8 * (double)N;
         break;
       case 5:
@@ -1979,7 +1979,8 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         break;
       case 10:                                   // CGS2 of step j=15 alone
         fn = [&]() { cgs2(h, 16, h->V + (size_t)16 * N); };
-        bytes = 0.0;
+        // pass A (16+1 vectors) + fused pass B (16 + 2) + pass C (16 + 2) + scale (2)
+        bytes = 55.0 * 8 * (double)N;
         break;
       case 11:
         fn = [&]() { arnoldi_step(h, 25); };

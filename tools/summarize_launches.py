@@ -33,7 +33,7 @@ with open(dst_txt, "w") as f:
         f.write(f"{t / T * 100:6.2f} {t / 1e6:9.3f} {cnt[n]:8d} {t / cnt[n] / 1e3:8.2f} "
                 f"{byt[n] / t if t else 0:9.1f} {byt[n] / cnt[n] / 1e6:12.2f}  {n}\n")
 pieces = {
-    "a2_bsr_spmv": lambda n: n.startswith("bsr_spmv_kernel<4, 0>"),
+    "a2_bsr_spmv": lambda n: n.startswith("bsr_spmv4c_kernel<0>") or n.startswith("bsr_spmv_kernel<4, 0>"),
     "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>"),
     "a9_bilu_apply": lambda n: n.startswith("bilu_block_kernel"),
 }
