@@ -40,9 +40,9 @@ pieces = {
 out = {}
 for key, pred in pieces.items():
     b = sum(byt[n] for n in byt if pred(n))
-    c = min((cnt[n] for n in cnt if pred(n) and ("0>" in n or "1, 1>" in n or key != "a9_bilu_apply")), default=0)
-    if key == "a9_bilu_apply":
-        c = max((cnt[n] for n in cnt if n.startswith("bilu_block_kernel") and n.endswith("1, 1>")), default=0)
+    c = sum(cnt[n] for n in cnt if pred(n))
+    if key == "a9_bilu_apply":            # one BILU apply per a8 launch (one per MSP apply)
+        c = sum(cnt[n] for n in cnt if n.startswith("bsr_spmv_kernel<4, 2>"))
     out[key] = b / c if c else None          # DRAM bytes per launch (per application)
 out["_source"] = src
 json.dump(out, open(dst_json, "w"), indent=1)
