@@ -111,6 +111,70 @@ __device__ __forceinline__ double reduce_scatter4(double a0, double a1, double a
   return (odd ? k1 : k0) + r;
 }
 
+// 8-lane reduce-scatter of a[0..7] (lane q of an aligned 8-lane group) -> sum of a[q]
+// over the group; 4 + 2 + 1 shuffles, fixed order.
+__device__ __forceinline__ double reduce_scatter8(const double (&a)[8], int q, unsigned m8) {
+  const bool b2 = (q & 4) != 0;
+  double k[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double send = b2 ? a[u] : a[u + 4];
+    const double keep = b2 ? a[u + 4] : a[u];
+    k[u] = keep + __shfl_xor_sync(m8, send, 4);
+  }
+  const bool b1 = (q & 2) != 0;
+  double l[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const double send = b1 ? k[u] : k[u + 2];
+    const double keep = b1 ? k[u + 2] : k[u];
+    l[u] = keep + __shfl_xor_sync(m8, send, 2);
+  }
+  const bool b0 = (q & 1) != 0;
+  const double send = b0 ? l[0] : l[1];
+  const double keep = b0 ? l[1] : l[0];
+  return keep + __shfl_xor_sync(m8, send, 1);
+}
+
+// column-per-lane partial sums for a B x B block (5 <= B <= 8, 8-lane group): lane q < B
+// adds column q of the column-major block times v_q into a[0..B-1]
+template <int B>
+__device__ __forceinline__ void col_accum8(const double* __restrict__ blk, double vq, int q, double (&a)[8]) {
+  if (q < B) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) a[r] = fma(__ldcs(blk + q * B + r), vq, a[r]);
+  }
+}
+
+// a2 for 5x5..8x8 blocks, column-per-lane (8 lanes per block row, lane 7 idle for B = 7)
+template <int B, int MODE>
+__global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __restrict__ rp,
+                                                         const int* __restrict__ ci,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ g,
+                                                         double* __restrict__ y) {
+  PDL_ENTRY();
+  constexpr int BB = B * B;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gtid >> 3, q = threadIdx.x & 7;
+  if (row >= n) return;
+  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  double a[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) a[r] = 0.0;
+  for (int e = e0; e < e1; ++e) {
+    const int c = ldg(ci + e);
+    const double xq = (q < B) ? ldg(x + (size_t)c * B + q) : 0.0;
+    col_accum8<B>(val + (size_t)e * BB, xq, q, a);
+  }
+  const double acc = reduce_scatter8(a, q, 0xFFu << ((threadIdx.x & 31) & ~7));
+  if (q < B) {
+    const size_t o = (size_t)row * B + q;
+    y[o] = (MODE == 0) ? acc : (g[o] - acc);
+  }
+}
+
 // a2 for 4x4 blocks, column-per-lane: lane q loads block column q (two 16-byte loads,
 // column-major storage), multiplies by its own x_q (no broadcast), keeps 4 row partial
 // sums and reduce-scatters once per block row.  MODE 0: y = A x; MODE 1: y = g - A x.
@@ -615,6 +679,15 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
         a3 = fma(hi.y, yq, a3);
       }
       acc = reduce_scatter4(a0, a1, a2, a3, q, cmask);
+    } else if constexpr (B >= 5) {          // 8-lane column-per-lane
+      double a8[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a8[r] = 0.0;
+      for (int ee = e0; ee < eext; ++ee) {
+        const double yq = (q < B) ? ldg(v + (size_t)ldg(ci + ee) * B + q) : 0.0;
+        col_accum8<B>(F + (size_t)ee * BB, yq, q, a8);
+      }
+      acc = reduce_scatter8(a8, q, cmask);
     } else {
 #pragma unroll 2
       for (int ee = e0; ee < eext; ++ee) {  // external L part: columns before the block
@@ -667,6 +740,15 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
         a3 = fma(hi.y, xq, a3);
       }
       acc = reduce_scatter4(a0, a1, a2, a3, q, cmask);
+    } else if constexpr (B >= 5) {           // 8-lane column-per-lane
+      double a8[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a8[r] = 0.0;
+      for (int e = ei; e < e1; ++e) {
+        const double xq = (q < B) ? ldg(v + (size_t)ldg(ci + e) * B + q) : 0.0;
+        col_accum8<B>(F + (size_t)e * BB, xq, q, a8);
+      }
+      acc = reduce_scatter8(a8, q, cmask);
     } else {
 #pragma unroll 2
       for (int e = ei; e < e1; ++e) {        // external U part: columns after the block

@@ -1023,6 +1023,13 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
     else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y);
     return;
   }
+  if constexpr (B >= 5) {
+    if (g_spmv4c && mode != 2) {
+      if (mode == 0) klaunch(s, pdl, bsr_spmv8c_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
+      else klaunch(s, pdl, bsr_spmv8c_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
+      return;
+    }
+  }
   if (mode == 0) klaunch(s, pdl, bsr_spmv_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
   else if (mode == 1) klaunch(s, pdl, bsr_spmv_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
   else klaunch(s, pdl, bsr_spmv_kernel<B, 2>, grid, 256, n, rp, ci, val, x, g, y);
