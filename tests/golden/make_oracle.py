@@ -1,5 +1,5 @@
-"""Writes tests/golden/oracle_c3.json: the CPU oracle's MSP-GMRES result on the full C3
-workload (SPE10-shaped 60x220x85, nc=3, tol 1e-6, GMRES(30)).  Calls only oracle/ and
+"""Writes tests/golden/oracle_<cfg>.json: the CPU oracle's MSP-GMRES result on a full-size
+workload (default C3: SPE10-shaped 60x220x85, nc=3; C4: nc=6), tol 1e-6, GMRES(30).  Calls only oracle/ and
 gen/ (seeded inputs).  Takes a few minutes single-threaded."""
 import json
 import os
@@ -11,14 +11,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import gen      # noqa: E402
 import oracle   # noqa: E402
 
-p = gen.make_config("C3")
+CFG = sys.argv[1] if len(sys.argv) > 1 else "C3"
+p = gen.make_config(CFG)
 t0 = time.time()
 M = oracle.Msp(p["row_ptr"], p["col"], p["val"])
 t1 = time.time()
 r = M.solve(p["rhs"], tol=1e-6, restart=30, maxit=1000)
 t2 = time.time()
-out = dict(config="C3", tol=1e-6, restart=30, iters=r["iters"], final_rel=r["final_rel"],
+out = dict(config=CFG, tol=1e-6, restart=30, iters=r["iters"], final_rel=r["final_rel"],
            hist=r["hist"].tolist(), status=r["status"], levels=M.info(),
            oracle_setup_s=t1 - t0, oracle_solve_s=t2 - t1, cores=1)
-json.dump(out, open(os.path.join(HERE, "oracle_c3.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(HERE, f"oracle_{CFG.lower()}.json"), "w"), indent=1)
 print(json.dumps({k: v for k, v in out.items() if k != "hist"}))

@@ -224,7 +224,7 @@ def test_asmsp_update_reuse_and_rebuild():
 def test_full_size_c3_spmv_sampled_and_solve():
     """C3 at full size in the bench's launch configuration: SpMV on sampled rows vs the
     oracle's definition, and the solve against the oracle's committed iteration count
-    (tests/golden/oracle_c3.json, written by tests/golden/make_oracle_c3.py)."""
+    (tests/golden/oracle_c3.json, written by tests/golden/make_oracle.py)."""
     p = gen.make_config("C3")
     s = solver(p)
     order = s.order()
