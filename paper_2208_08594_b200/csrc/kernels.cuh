@@ -18,6 +18,10 @@ constexpr int kSell = 32;
 #define MSP_BILU_BATCH 0
 #endif
 constexpr bool kBiluBatch = MSP_BILU_BATCH != 0;
+#ifndef MSP_BILU_PREFETCH
+#define MSP_BILU_PREFETCH 1
+#endif
+constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
@@ -623,7 +627,7 @@ __device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const in
 // vectors through register shuffles.  Same arithmetic as bilu_color_kernel, only
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
-template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false>
+template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch>
 __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
@@ -656,6 +660,34 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
   double t = 0.0;                           // working value of row q of cell i
   // cnt[i] = (#external L entries) | (#intra-block U entries << 8), from setup
   const int cn = valid ? ldg(cnt + i) : 0;
+  // PDL prologue (4x4 blocks): indices and factor columns of the first PFE external
+  // entries are immutable -> issued before the wait, overlapping the previous kernel
+  constexpr int PFE = (B == 4 && PF) ? 3 : 0;
+  int pk[PFE > 0 ? PFE : 1];
+  double2 plo[PFE > 0 ? PFE : 1], phi[PFE > 0 ? PFE : 1];
+  int px0 = 0, px1 = 0;
+  if constexpr (PFE > 0) {
+    if (FWD) {
+      px0 = valid ? ldg(rp + i) : 0;
+      px1 = px0 + (cn & 0xff);
+    } else {
+      px0 = (valid ? ldg(dg + i) : 0) + 1 + (cn >> 8);
+      px1 = valid ? ldg(rp + i + 1) : 0;
+    }
+#pragma unroll
+    for (int m = 0; m < PFE; ++m) {
+      const int e = px0 + m;
+      pk[m] = (e < px1) ? ldg(ci + e) : -1;
+      if (e < px1) {
+        const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
+        plo[m] = ldstream2(cp);
+        phi[m] = ldstream2(cp + 1);
+      } else {
+        plo[m] = make_double2(0.0, 0.0);
+        phi[m] = plo[m];
+      }
+    }
+  }
   pdl_wait();
   pdl_trigger();
   if (FWD) {
@@ -666,10 +698,23 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     double acc = 0.0;
     if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (kBiluBatch) ext_sum4_batched(e0, eext, q, ci, F, v, a0, a1, a2, a3);
+      int estart = e0;
+      if constexpr (PFE > 0) {
+#pragma unroll
+        for (int m = 0; m < PFE; ++m) {
+          if (pk[m] < 0) break;
+          const double yq = ldg(v + (size_t)pk[m] * 4 + q);
+          a0 = fma(plo[m].x, yq, a0);
+          a1 = fma(plo[m].y, yq, a1);
+          a2 = fma(phi[m].x, yq, a2);
+          a3 = fma(phi[m].y, yq, a3);
+        }
+        estart = min(eext, e0 + PFE);
+      }
+      if (kBiluBatch) ext_sum4_batched(estart, eext, q, ci, F, v, a0, a1, a2, a3);
       else
 #pragma unroll 2
-      for (int ee = e0; ee < eext; ++ee) {
+      for (int ee = estart; ee < eext; ++ee) {
         const double yq = ldg(v + (size_t)ldg(ci + ee) * 4 + q);
         const double2* cp = reinterpret_cast<const double2*>(F + (size_t)ee * 16 + q * 4);
         const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
@@ -727,10 +772,25 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
     double acc = 0.0;
     if constexpr (B == 4) {                  // column-per-lane (see the forward part)
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (kBiluBatch) ext_sum4_batched(ei, e1, q, ci, F, v, a0, a1, a2, a3);
+      int estart = ei;
+      if constexpr (PFE > 0) {
+        if (!FWD) {                              // (fused colors: no external U)
+#pragma unroll
+          for (int m = 0; m < PFE; ++m) {
+            if (pk[m] < 0) break;
+            const double xq = ldg(v + (size_t)pk[m] * 4 + q);
+            a0 = fma(plo[m].x, xq, a0);
+            a1 = fma(plo[m].y, xq, a1);
+            a2 = fma(phi[m].x, xq, a2);
+            a3 = fma(phi[m].y, xq, a3);
+          }
+          estart = min(e1, ei + PFE);
+        }
+      }
+      if (kBiluBatch) ext_sum4_batched(estart, e1, q, ci, F, v, a0, a1, a2, a3);
       else
 #pragma unroll 2
-      for (int e = ei; e < e1; ++e) {
+      for (int e = estart; e < e1; ++e) {
         const double xq = ldg(v + (size_t)ldg(ci + e) * 4 + q);
         const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
         const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);

@@ -105,7 +105,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0;
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, bilu_nopf = 0;
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1062,6 +1062,15 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
+    if (B == 4 && h->bilu_nopf) {            // A/B: no PDL-prologue prefetch
+      if (kind == 0)
+        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      else if (kind == 1)
+        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      else
+        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      return;
+    }
     if (kind == 0)
       klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
     else if (kind == 1)
@@ -1709,6 +1718,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_BILU_NOPF")) h->bilu_nopf = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
   if (const char* e = std::getenv("MSP_SPMV4C")) g_spmv4c = std::atoi(e) != 0;
