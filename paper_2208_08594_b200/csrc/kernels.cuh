@@ -211,6 +211,37 @@ __global__ void __launch_bounds__(256) bsr_spmv4c_kernel(int n, const int* __res
   y[o] = (MODE == 0) ? acc : (g[o] - acc);
 }
 
+// a8 for 4x4 blocks: r = g - A[:,P] x with the contiguous pressure columns Pcol (one
+// 32 B sector per block entry).  Entry-per-lane: lane q of the row's 4-lane group
+// takes entries e0+q, e0+q+4, ... (the group reads 128 contiguous bytes of Pcol and
+// 4 consecutive ci per round), accumulates all 4 rows, then one reduce-scatter.
+__global__ void __launch_bounds__(256) pcol_resid4_kernel(int n, const int* __restrict__ rp,
+                                                          const int* __restrict__ ci,
+                                                          const double* __restrict__ pcol,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ g,
+                                                          double* __restrict__ y) {
+  PDL_ENTRY();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gtid >> 2, q = threadIdx.x & 3;
+  if (row >= n) return;                       // whole 4-lane groups exit together
+  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 2
+  for (int e = e0 + q; e < e1; e += 4) {
+    const double xc = ldg(x + ldg(ci + e));
+    const double2* cp = reinterpret_cast<const double2*>(pcol + (size_t)e * 4);
+    const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
+    a0 = fma(lo.x, xc, a0);
+    a1 = fma(lo.y, xc, a1);
+    a2 = fma(hi.x, xc, a2);
+    a3 = fma(hi.y, xc, a3);
+  }
+  const double acc = reduce_scatter4(a0, a1, a2, a3, q, 0xFu << ((threadIdx.x & 31) & ~3));
+  const size_t o = (size_t)row * 4 + q;
+  y[o] = g[o] - acc;
+}
+
 // ---------------------------------------------------------------------------
 // a3: pressure restriction with decoupling weights (R4): rp_l0[dst[c]] = sum_k
 // W[c][k] * g[c*B+k]; dst maps internal cell positions to level-0 rows.

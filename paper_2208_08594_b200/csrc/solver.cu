@@ -105,7 +105,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, bilu_nopf = 0;
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, bilu_nopf = 0, pcol_rowwise = 0;
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1038,6 +1038,10 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
 void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
+  if (mode == 2 && h->b == 4 && !h->pcol_rowwise) {
+    klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)h->n * 4, 256), 256, h->n, h->rp, h->ci, val, x, g, y);
+    return;
+  }
   switch (h->b) {
 #define CASE(BV) case BV: launch_spmv_t<BV>(h->s, h->pdl, mode, h->n, h->rp, h->ci, val, x, g, y); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
@@ -1719,6 +1723,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_NOPF")) h->bilu_nopf = std::atoi(e);
+  if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
   if (const char* e = std::getenv("MSP_SPMV4C")) g_spmv4c = std::atoi(e) != 0;

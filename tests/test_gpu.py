@@ -250,3 +250,32 @@ def test_full_size_c3_spmv_sampled_and_solve():
     if os.path.exists(gold):
         ref = json.load(open(gold))
         assert abs(r["iters"] - ref["iters"]) <= 1, (r["iters"], ref["iters"])
+        _check_hist(r["hist"], ref["hist"])
+
+
+def _check_hist(h, ref, n_first=15, rtol=1e-9):
+    """Relative-residual history against the oracle's: the first n_first iterations
+    (before rounding differences amplify) agree to rtol."""
+    h = np.asarray(h)
+    ref = np.asarray(ref)
+    k = min(n_first, len(h), len(ref))
+    dev = np.abs(h[:k] - ref[:k]) / ref[:k]
+    print("hist max rel dev (first %d): %.3e" % (k, dev.max()))
+    assert dev.max() <= rtol, dev
+
+
+def test_full_size_c4_solve_vs_oracle_golden():
+    """C4 (SPE10-size, 6 components -> 7x7 blocks, the 8-lane kernel variants) at full
+    size: converged true residual, iteration count and early residual history against the
+    oracle's committed run (tests/golden/oracle_c4.json, make_oracle.py C4)."""
+    p = gen.make_config("C4")
+    s = solver(p)
+    r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-6)
+    b = p["b"]
+    A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * b,) * 2)
+    xs = r["x"].cpu().numpy()
+    assert np.linalg.norm(p["rhs"] - A @ xs) / np.linalg.norm(p["rhs"]) <= 1e-6
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_c4.json")))
+    assert s.stats()["levels"] == ref["levels"]["levels"]
+    assert abs(r["iters"] - ref["iters"]) <= 1, (r["iters"], ref["iters"])
+    _check_hist(r["hist"], ref["hist"])
