@@ -22,6 +22,12 @@ constexpr bool kBiluBatch = MSP_BILU_BATCH != 0;
 #define MSP_BILU_PREFETCH 1
 #endif
 constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
+#ifndef MSP_BILU_PFE
+#define MSP_BILU_PFE 2
+#endif
+#ifndef MSP_BILU_MINB
+#define MSP_BILU_MINB 12
+#endif
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 __device__ __forceinline__ int ldg(const int* p) { return __ldg(p); }
@@ -659,7 +665,7 @@ __device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const in
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
 template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch>
-__global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int b_first, int b_end,
+__global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
@@ -693,7 +699,7 @@ __global__ void __launch_bounds__(128, (B <= 4) ? 12 : 8) bilu_block_kernel(int 
   const int cn = valid ? ldg(cnt + i) : 0;
   // PDL prologue (4x4 blocks): indices and factor columns of the first PFE external
   // entries are immutable -> issued before the wait, overlapping the previous kernel
-  constexpr int PFE = (B == 4 && PF) ? 3 : 0;
+  constexpr int PFE = (B == 4 && PF) ? MSP_BILU_PFE : 0;
   int pk[PFE > 0 ? PFE : 1];
   double2 plo[PFE > 0 ? PFE : 1], phi[PFE > 0 ? PFE : 1];
   int px0 = 0, px1 = 0;
