@@ -20,6 +20,7 @@
 #include "../../include/msp.h"
 #include "comm.h"
 #include "coop.cuh"
+#include "cluster.cuh"
 #include "setup.h"
 
 using namespace mspk;
@@ -114,6 +115,9 @@ struct msp_handle {
   int32_t nL = 0, ldA = 0;
   VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
   int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
+  // cluster V-cycle legs (cluster.cuh): levels [cl_from, L) in one cl_size-CTA cluster
+  int cl_from = 0, cl_size = 16;             // opt-in (MSP_CLUSTER_FROM): measured slower
+  bool cl_on = false;
   bool pdl = true;                   // programmatic dependent launch for every kernel
   int cgs_split = 0;                 // nv > 16: 16-vector halves (see cgs_dot / cgs_axpy)
   bool coarse_diag = false;
@@ -421,6 +425,8 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
                    const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms);
 
+void setup_cluster(msp_handle* h);
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
   SetupTimer T;
@@ -651,6 +657,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->st.levels = L;
   h->st.n_coarsest = h->nL;
   h->st.bilu_colors = h->bilu_ncolor;
+  setup_cluster(h);
   // cooperative V-cycle parameters
   if (h->prm.use_coop && L <= kMaxLevels) {
     VParams vp;
@@ -1150,6 +1157,102 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool 
   ++h->nlaunch;
 }
 
+// Cluster V-cycle legs: usable when levels [cl_from, L) exist below level 0 and one
+// cluster of cl_size CTAs x 1024 threads fits (16 needs the non-portable size; else 8).
+void setup_cluster(msp_handle* h) {
+  h->cl_on = false;
+  const int L = (int)h->lv.size();
+  if (h->cl_from < 1 || h->cl_from >= L || L - h->cl_from > kClMaxLevels || h->prm.pre_sweeps < 1) return;
+  for (int cs : {h->cl_size, 8}) {
+    if (cs < 1 || cs > 16) continue;
+    const int np = cs > 8 ? 1 : 0;
+    CK(cudaFuncSetAttribute(vcycle_cluster_down_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, np));
+    CK(cudaFuncSetAttribute(vcycle_cluster_up_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, np));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kClThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int na = 0, nb = 0;
+    if (cudaOccupancyMaxActiveClusters(&na, vcycle_cluster_down_kernel, &cfg) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&nb, vcycle_cluster_up_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (na >= 1 && nb >= 1) {
+      h->cl_size = cs;
+      h->cl_on = true;
+      return;
+    }
+  }
+}
+
+ClParams cluster_params(msp_handle* h) {
+  ClParams P;
+  std::memset(&P, 0, sizeof(P));
+  const int L = (int)h->lv.size();
+  P.nlev = L - h->cl_from;
+  P.pre = h->prm.pre_sweeps;
+  P.post = h->prm.post_sweeps;
+  for (int l = h->cl_from; l < L; ++l) {
+    const DevLevel& D = h->lv[l];
+    ClLevel& E = P.lv[l - h->cl_from];
+    const bool last = (l + 1 == L);
+    E.n = D.n;
+    E.ncolor = D.ncolor;
+    E.lpr = D.lpr;
+    E.n_next = last ? h->nL : h->lv[l + 1].n;
+    E.c1_next = last ? 0 : h->lv[l + 1].color_row[1];
+    E.color_slice = D.d_color_slice;
+    E.slice_row = D.slice_row;
+    E.slice_off = D.slice_off;
+    E.col = D.col;
+    E.val = D.val;
+    E.diag = D.diag;
+    E.agg = D.agg;
+    E.pt_ptr = D.pt_ptr;
+    E.pt_idx = D.pt_idx;
+    E.b = D.b;
+    E.x = D.x;
+    E.r = D.r;
+    E.bn = last ? h->bL : h->lv[l + 1].b;
+    E.xn = last ? h->xL : h->lv[l + 1].x;
+    E.dn = last ? nullptr : h->lv[l + 1].diag;
+  }
+  return P;
+}
+
+void cluster_launch(msp_handle* h, void (*k)(const ClParams), const ClParams& P) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->cl_size);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.stream = h->s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = h->cl_size;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  CK(cudaLaunchKernelEx(&cfg, k, P));
+  ++h->nlaunch;
+}
+
+void coarsest_solve(msp_handle* h) {
+  ++h->nlaunch;
+  if (h->coarse_diag)
+    klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
+  else
+    klaunch(h->s, h->pdl, gemv4_kernel, nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+}
+
 template <int LPR, bool WR, bool RES>
 void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
   if (s1 <= s0) return;
@@ -1221,11 +1324,14 @@ void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool 
 // init_done: the zero-guess first color of level l was fused into b's producer.
 void vcycle(msp_handle* h, int l, bool init_done = false) {
   if (l == (int)h->lv.size()) {
-    ++h->nlaunch;
-    if (h->coarse_diag)
-      klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
-    else
-      klaunch(h->s, h->pdl, gemv4_kernel, nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+    coarsest_solve(h);
+    return;
+  }
+  if (h->cl_on && l == h->cl_from && init_done) {     // levels >= cl_from in one cluster
+    const ClParams P = cluster_params(h);
+    cluster_launch(h, vcycle_cluster_down_kernel, P);
+    coarsest_solve(h);
+    cluster_launch(h, vcycle_cluster_up_kernel, P);
     return;
   }
   DevLevel& L = h->lv[l];
@@ -1724,6 +1830,8 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_NOPF")) h->bilu_nopf = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
+  if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
+  if (const char* e = std::getenv("MSP_CLUSTER_SIZE")) h->cl_size = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
   if (const char* e = std::getenv("MSP_SPMV4C")) g_spmv4c = std::atoi(e) != 0;

@@ -116,6 +116,37 @@ def test_vcycle_parity(kw):
     assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("env,kw", [(dict(MSP_CLUSTER_FROM="2"), dict()),
+                                    (dict(MSP_CLUSTER_FROM="1"), dict()),
+                                    (dict(MSP_CLUSTER_FROM="1", MSP_CLUSTER_SIZE="8"), dict()),
+                                    (dict(MSP_CLUSTER_FROM="1"), dict(pre_sweeps=2, post_sweeps=2)),
+                                    (dict(MSP_CLUSTER_FROM="2"), dict(post_sweeps=0))])
+def test_cluster_vcycle_bit_identical(env, kw, monkeypatch):
+    """The coarse levels run as one thread-block cluster (cluster.cuh) must reproduce the
+    multi-launch V-cycle bit for bit (same per-row summation order), with fewer launches."""
+    p = gen.make_config("C2", nx=40, ny=30, nz=6)
+    monkeypatch.setenv("MSP_CLUSTER_FROM", "0")                     # multi-launch path
+    s0 = solver(p, coarsest_max_dof=60, **kw)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    s1 = solver(p, coarsest_max_dof=60, **kw)
+    assert s1.stats()["levels"] > int(env["MSP_CLUSTER_FROM"]) + 1
+    r = torch.from_numpy(gen.random_vector(p["n"], 7)).cuda()
+    out = []
+    for s in (s0, s1):
+        x = torch.zeros(p["n"], dtype=torch.float64, device="cuda")
+        k0 = s.kernel_launches()
+        s.vcycle(r, x)
+        out.append((x.cpu().numpy(), s.kernel_launches() - k0))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[1][1] < out[0][1], (out[0][1], out[1][1])
+    b = torch.from_numpy(p["rhs"]).cuda()
+    r0, r1 = s0.solve(b), s1.solve(b)
+    assert r0["iters"] == r1["iters"]
+    assert np.array_equal(r0["hist"], r1["hist"])
+    assert torch.equal(r0["x"], r1["x"])
+
+
 @pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0), dict(decoupling=1), dict(stages=3)])
 def test_bilu_and_msp_apply_parity(kw):
     p = gen.make_config("C2", nx=25, ny=20, nz=5)
