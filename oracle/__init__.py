@@ -63,13 +63,14 @@ def last_error() -> str:
 class Config(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int32) for k in ("coarsest_max_dof", "max_levels", "pre_sweeps",
                                               "post_sweeps", "pair_passes", "decoupling",
-                                              "bilu_order", "stages", "orth")]
+                                              "bilu_order", "stages", "orth", "smoother",
+                                              "gs_chunk")]
 
     @classmethod
     def make(cls, coarsest_max_dof=10000, max_levels=20, pre_sweeps=1, post_sweeps=1, pair_passes=2,
-             decoupling=2, bilu_order=1, stages=2, orth=0):
+             decoupling=2, bilu_order=1, stages=2, orth=0, smoother=0, gs_chunk=32):
         return cls(coarsest_max_dof, max_levels, pre_sweeps, post_sweeps, pair_passes, decoupling,
-                   bilu_order, stages, orth)
+                   bilu_order, stages, orth, smoother, gs_chunk)
 
 
 # ---------------------------------------------------------------- primitives
@@ -148,6 +149,25 @@ def pgs_mc(ptr, col, val, color, g, b, x, ascending=True):
     rc = lib().orc_pgs_mc(n, _p(_c(ptr, I32)), _p(_c(col, I32)), _p(_c(val, F64)),
                           _p(_c(color, I32)), g, _p(_c(b, F64)), _p(x), 1 if ascending else 0)
     if rc:
+        raise OracleError(last_error())
+    return x
+
+
+def jacobi_sweep(ptr, col, val, b, x):
+    """One PJAC-NO sweep (R13)."""
+    n = len(ptr) - 1
+    x = _c(x, F64).copy()
+    if lib().orc_jacobi(n, _p(_c(ptr, I32)), _p(_c(col, I32)), _p(_c(val, F64)), _p(_c(b, F64)), _p(x)):
+        raise OracleError(last_error())
+    return x
+
+
+def hybrid_gs_sweep(ptr, col, val, K, b, x, ascending=True):
+    """One PGS-NO sweep: chunks of K natural-order rows, GS inside, Jacobi across (R13)."""
+    n = len(ptr) - 1
+    x = _c(x, F64).copy()
+    if lib().orc_hybrid_gs(n, _p(_c(ptr, I32)), _p(_c(col, I32)), _p(_c(val, F64)), int(K),
+                           _p(_c(b, F64)), _p(x), 1 if ascending else 0):
         raise OracleError(last_error())
     return x
 

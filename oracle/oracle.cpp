@@ -217,6 +217,53 @@ static bool pgs_mc_sweep(const Csr& A, const std::vector<std::vector<int>>& grou
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-4 comparison smoothers (Table 2: "parallel GS and Jacobi methods based
+// on natural ordering, denoted as PGS-NO and PJAC-NO"; reading R13 in DESIGN.md).
+// PJAC-NO: one undamped Jacobi sweep, x_i <- (b_i - sum_{j != i} a_ij x_j^old) / a_ii.
+// PGS-NO: the hybrid Jacobi/GS of P:318 ("combines the Jacobi and GS methods"): the
+// natural-order rows are cut into chunks of K consecutive rows (one per parallel
+// worker); inside a chunk rows are relaxed in order (ascending for the pre-sweep,
+// descending for the post-sweep) with the newest values of the chunk, while every
+// coupling to another chunk uses the value from the start of the sweep.  K = 1 is
+// Jacobi, K >= n is sequential natural-order GS.
+// ---------------------------------------------------------------------------
+static bool jacobi_sweep(const Csr& A, const double* b, double* x) {
+  std::vector<double> xo(x, x + A.n);
+  for (int i = 0; i < A.n; ++i) {
+    double s = 0.0, d = 0.0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+      if (A.col[e] == i) d = A.val[e];
+      else s += A.val[e] * xo[A.col[e]];
+    }
+    if (d == 0.0) { g_err = "jacobi: zero diagonal at row " + std::to_string(i); return false; }
+    x[i] = (b[i] - s) / d;
+  }
+  return true;
+}
+
+static bool hybrid_gs_sweep(const Csr& A, int K, const double* b, double* x, bool ascending) {
+  if (K < 1) { g_err = "hybrid_gs: chunk < 1"; return false; }
+  std::vector<double> xo(x, x + A.n);       // values at the start of the sweep
+  const int nchunk = (A.n + K - 1) / K;
+  for (int c = 0; c < nchunk; ++c) {
+    const int q0 = c * K, q1 = std::min(A.n, q0 + K);
+    for (int t = 0; t < q1 - q0; ++t) {
+      const int i = ascending ? q0 + t : q1 - 1 - t;
+      double s = 0.0, d = 0.0;
+      for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+        const int j = A.col[e];
+        if (j == i) { d = A.val[e]; continue; }
+        const bool fresh = (j >= q0 && j < q1) && (ascending ? j < i : j > i);
+        s += A.val[e] * (fresh ? x[j] : xo[j]);
+      }
+      if (d == 0.0) { g_err = "hybrid_gs: zero diagonal at row " + std::to_string(i); return false; }
+      x[i] = (b[i] - s) / d;
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // c-5: NPAIR pairwise aggregation (P:459 names NPAIR [Napov-Notay] only; reading
 // from SPEC S:304/S:344, R3).  Neighbours from the c-3 graph; strength
 // via t_ij = a_ij + a_ji (s_ij = -t_ij/2).  Repeatedly take the unaggregated row
@@ -398,6 +445,8 @@ struct Config {
   int bilu_order = 1;            // 0 RB, 1 ABMC1 (R5)
   int stages = 2;                // 2 = PR (north_star), 3 = NPR (Eq. 21 full)
   int orth = 0;                  // 0 CGS2, 1 MGS (R8)
+  int smoother = 0;              // 0 PGS-MC (Alg. 4), 1 PJAC-NO, 2 PGS-NO (R13)
+  int gs_chunk = 32;             // PGS-NO chunk size K (R13)
 };
 
 // ---------------------------------------------------------------------------
@@ -560,6 +609,13 @@ static void coarse_solve(const Hierarchy& H, const double* b, double* x) {
   }
 }
 
+// one smoothing sweep of level L with the configured smoother (pre: ascending)
+static bool smooth(const Level& L, const Config& cfg, const double* b, double* x, bool pre) {
+  if (cfg.smoother == 1) return jacobi_sweep(L.A, b, x);
+  if (cfg.smoother == 2) return hybrid_gs_sweep(L.A, cfg.gs_chunk, b, x, pre);
+  return pgs_mc_sweep(L.A, L.groups, b, x, pre);
+}
+
 // c-7: V-cycle from zero initial guess: pre-smooth (colors ascending), restrict
 // r_{l+1} = P^T (b - A x), recurse, x += P e, post-smooth (colors descending).
 static bool vcycle(const Hierarchy& H, const Config& cfg, int l, const std::vector<double>& b,
@@ -573,7 +629,7 @@ static bool vcycle(const Hierarchy& H, const Config& cfg, int l, const std::vect
   const int n = L.A.n;
   x.assign(n, 0.0);
   for (int s = 0; s < cfg.pre_sweeps; ++s)
-    if (!pgs_mc_sweep(L.A, L.groups, b.data(), x.data(), true)) return false;
+    if (!smooth(L, cfg, b.data(), x.data(), true)) return false;
   std::vector<double> Ax(n);
   csr_spmv(L.A, x.data(), Ax.data());
   std::vector<double> bc(L.n_next, 0.0);
@@ -582,7 +638,7 @@ static bool vcycle(const Hierarchy& H, const Config& cfg, int l, const std::vect
   if (!vcycle(H, cfg, l + 1, bc, e)) return false;
   for (int i = 0; i < n; ++i) x[i] += e[L.agg[i]];
   for (int s = 0; s < cfg.post_sweeps; ++s)
-    if (!pgs_mc_sweep(L.A, L.groups, b.data(), x.data(), false)) return false;
+    if (!smooth(L, cfg, b.data(), x.data(), false)) return false;
   return true;
 }
 
@@ -956,7 +1012,7 @@ extern "C" {
 
 typedef struct {
   int32_t coarsest_max_dof, max_levels, pre_sweeps, post_sweeps, pair_passes, decoupling,
-      bilu_order, stages, orth;
+      bilu_order, stages, orth, smoother, gs_chunk;
 } orc_config;
 
 const char* orc_last_error() { return g_err.c_str(); }
@@ -997,6 +1053,8 @@ static Config mkcfg(const orc_config* c) {
   k.bilu_order = c->bilu_order;
   k.stages = c->stages;
   k.orth = c->orth;
+  k.smoother = c->smoother;
+  k.gs_chunk = c->gs_chunk;
   return k;
 }
 
@@ -1068,6 +1126,15 @@ int orc_pgs_mc(int n, const int* ptr, const int* col, const double* val, const i
   std::vector<std::vector<int>> groups(g);
   for (int i = 0; i < n; ++i) groups[color[i]].push_back(i);
   return pgs_mc_sweep(mkcsr(n, ptr, col, val), groups, b, x, ascending != 0) ? 0 : 2;
+}
+
+// one PJAC-NO / PGS-NO sweep (R13); returns 0 or 2
+int orc_jacobi(int n, const int* ptr, const int* col, const double* val, const double* b, double* x) {
+  return jacobi_sweep(mkcsr(n, ptr, col, val), b, x) ? 0 : 2;
+}
+int orc_hybrid_gs(int n, const int* ptr, const int* col, const double* val, int K, const double* b, double* x,
+                  int ascending) {
+  return hybrid_gs_sweep(mkcsr(n, ptr, col, val), K, b, x, ascending != 0) ? 0 : 2;
 }
 
 int orc_dense_lu_solve(int n, const double* M, const double* b, double* x) {

@@ -252,6 +252,69 @@ def test_pgs_mc_diagonal_exact_and_converges_to_solution():
     assert all(errs[i + 1] <= errs[i] * (1 + 1e-12) for i in range(len(errs) - 1))
 
 
+# ------------------------------------------------------------------ NEXT-4 smoothers (R13)
+def test_jacobi_closed_form_modes_and_fixed_point():
+    """PJAC-NO: on tridiag(-1, 2, -1) the sine modes are eigenvectors of the Jacobi
+    iteration matrix D^-1 (L + U) with eigenvalue cos(k pi / (n + 1)) (textbook closed form);
+    the exact solution is a fixed point."""
+    n = 15
+    ptr, col, val = csr_of(poisson1d(n))
+    i = np.arange(1, n + 1)
+    for k in (1, 4, 9, 15):
+        v = np.sin(k * np.pi * i / (n + 1))
+        x = oracle.jacobi_sweep(ptr, col, val, np.zeros(n), v)
+        assert np.allclose(x, np.cos(k * np.pi / (n + 1)) * v, rtol=0, atol=1e-14)
+        # K = 1: every coupling is to another chunk -> the same Jacobi mode factor
+        x1 = oracle.hybrid_gs_sweep(ptr, col, val, 1, np.zeros(n), v)
+        assert np.allclose(x1, np.cos(k * np.pi / (n + 1)) * v, rtol=0, atol=1e-14)
+    rng = np.random.default_rng(5)
+    A = rand_sparse(40, 0.1, rng)
+    ptr, col, val = csr_of(A)
+    b = rng.normal(size=40)
+    xs = np.linalg.solve(A, b)
+    assert np.allclose(oracle.jacobi_sweep(ptr, col, val, b, xs), xs, rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("K", [1, 3, 5, 8, 23, 100])
+def test_hybrid_gs_is_chunkwise_triangular_solve(K):
+    """PGS-NO (R13): one sweep is x' = M^-1 (b - (A - M) x) with M = D + the couplings to
+    earlier rows of the same chunk (descending: later rows), i.e. a sparse triangular
+    solve (scipy); K >= n is sequential natural-order forward / backward GS."""
+    from scipy.sparse.linalg import spsolve_triangular
+    rng = np.random.default_rng(11 + K)
+    n = 23
+    A = rand_sparse(n, 0.2, rng)
+    ptr, col, val = csr_of(A)
+    b, x0 = rng.normal(size=n), rng.normal(size=n)
+    chunk = np.arange(n) // K
+    same = chunk[:, None] == chunk[None, :]
+    for asc in (True, False):
+        tri = np.tril(A, -1) if asc else np.triu(A, 1)
+        M = np.diag(np.diag(A)) + np.where(same, tri, 0.0)
+        ref = spsolve_triangular(sp.csr_matrix(M), b - (A - M) @ x0, lower=asc)
+        x = oracle.hybrid_gs_sweep(ptr, col, val, K, b, x0, asc)
+        assert np.allclose(x, ref, rtol=1e-12, atol=1e-12)
+        if K >= n:                                          # plain sequential GS
+            ref2 = spsolve_triangular(sp.csr_matrix(np.tril(A) if asc else np.triu(A)),
+                                      b - (np.triu(A, 1) if asc else np.tril(A, -1)) @ x0, lower=asc)
+            assert np.allclose(x, ref2, rtol=1e-12, atol=1e-12)
+
+
+def test_smoothers_in_msp_gmres_converge_and_order():
+    """MSP-GMRES with each pressure smoother (Table 2 analog) reaches the
+    tolerance (true residual), and on this generated problem the iteration counts keep
+    the paper's order PGS-MC <= PGS-NO <= PJAC-NO (measured property, R13)."""
+    p = gen.make_config("C2", nx=24, ny=20, nz=4)
+    A = bsr_dense(p)
+    its = {}
+    for sm in (0, 2, 1):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=50, smoother=sm)
+        r = M.solve(p["rhs"], tol=1e-8)
+        assert np.linalg.norm(p["rhs"] - A @ r["x"]) <= 1.01e-8 * np.linalg.norm(p["rhs"])
+        its[sm] = r["iters"]
+    assert its[0] <= its[2] <= its[1], its
+
+
 # ------------------------------------------------------------------ c-5 NPAIR + Galerkin
 def poisson1d(n):
     return np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1)
