@@ -79,6 +79,10 @@ typedef struct {
   int32_t use_coop;          /* 0 (default): one graph node per PGS-MC color / transfer;
                                 1: whole V-cycle as one cooperative persistent kernel (measured
                                 slower on B200: grid.sync ~1.3 us vs ~1.2 us per graph node) */
+  int32_t smoother;          /* AMG smoother (NEXT-4, reading R13): 0 PGS-MC (Alg. 4,
+                                default), 1 PJAC-NO (Jacobi), 2 PGS-NO (hybrid Jacobi/GS:
+                                natural-order chunks of gs_chunk rows, GS inside a chunk) */
+  int32_t gs_chunk;          /* PGS-NO chunk size K (default 32) */
   msp_alloc_fn alloc;        /* optional device allocator */
   msp_free_fn free_fn;
   void* alloc_ctx;

@@ -33,7 +33,8 @@ class Config(ctypes.Structure):
                 ("pair_passes", ctypes.c_int32), ("decoupling", ctypes.c_int32),
                 ("bilu_order", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("orth", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("use_coop", ctypes.c_int32),
+                ("use_coop", ctypes.c_int32), ("smoother", ctypes.c_int32),
+                ("gs_chunk", ctypes.c_int32),
                 ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
 
     @classmethod

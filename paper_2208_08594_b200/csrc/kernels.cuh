@@ -308,6 +308,73 @@ __global__ void __launch_bounds__(128) pgs_color_kernel(int s_first, int s_end,
   x[row] = (ldg(b + row) - acc) / ldg(diag + row);
 }
 
+// NEXT-4 comparison smoothers (reading R13), on the color-permuted SELL layout.
+// PJAC-NO: x_i = (b_i - sum_{j != i} a_ij xo_j) / a_ii for every row (xo: the values at
+// the start of the sweep; LPR lanes per row as sell_row_kernel).
+template <int LPR>
+__global__ void __launch_bounds__(128) sell_jacobi_kernel(int s_first, int s_end,
+                                                          const int* __restrict__ slice_row,
+                                                          const int* __restrict__ slice_off,
+                                                          const int* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ diag,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ xo,
+                                                          double* __restrict__ x) {
+  PDL_ENTRY();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = s_first + t / (kSell * LPR);
+  if (s >= s_end) return;                      // whole warps (32*LPR threads per slice)
+  const int rem = t % (kSell * LPR);
+  const int l = rem / LPR, u = rem % LPR;
+  const int row = ldg(slice_row + s) + l;
+  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = u; k < w; k += LPR) {
+    const int o = o0 + k * kSell + l;
+    acc = fma(ldg(val + o), ldg(xo + ldg(col + o)), acc);
+  }
+#pragma unroll
+  for (int m = LPR / 2; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (u == 0 && row < ldg(slice_row + s + 1)) x[row] = (ldg(b + row) - acc) / ldg(diag + row);
+}
+
+// PGS-NO (hybrid Jacobi/GS): thread c relaxes the natural-order rows
+// [cK, cK+K) in order (descending for the post-sweep); a coupling to a row of the same
+// chunk that was already relaxed in this sweep uses its new value (x, written only by
+// this thread), every other coupling the start-of-sweep value xo.  perm/inv map natural
+// <-> permuted rows; row_start/row_width locate a row's SELL entries.
+__global__ void __launch_bounds__(128) hybrid_gs_kernel(int n, int K, int asc, const int* __restrict__ perm,
+                                                        const int* __restrict__ inv,
+                                                        const int* __restrict__ row_start,
+                                                        const int* __restrict__ row_width,
+                                                        const int* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ diag,
+                                                        const double* __restrict__ b,
+                                                        const double* __restrict__ xo, double* x) {
+  PDL_ENTRY();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q0 = c * K;
+  if (q0 >= n) return;
+  const int q1 = min(n, q0 + K);
+  for (int t = 0; t < q1 - q0; ++t) {
+    const int q = asc ? q0 + t : q1 - 1 - t;
+    const int p = ldg(perm + q);
+    const int o0 = ldg(row_start + p), w = ldg(row_width + p);
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+      const int o = o0 + k * kSell;
+      const int j = ldg(col + o);
+      const int qj = ldg(inv + j);
+      const bool fresh = qj >= q0 && qj < q1 && (asc ? qj < q : qj > q);
+      acc = fma(ldg(val + o), fresh ? x[j] : ldg(xo + j), acc);
+    }
+    x[p] = (ldg(b + p) - acc) / ldg(diag + p);
+  }
+}
+
 // First color of a pre-sweep from the zero initial guess: x_i = b_i / a_ii for the
 // rows of color 1 and x_i = 0 elsewhere (one pass over the whole level).
 __global__ void pgs_init_kernel(int n, int c1_end, const double* __restrict__ diag,

@@ -31,7 +31,7 @@ struct Graph {                       // symmetric adjacency, ascending neighbour
 struct Params {
   int32_t coarsest_max_dof = 10000, max_levels = 20, pre_sweeps = 1, post_sweeps = 1,
           pair_passes = 2, decoupling = 2, bilu_order = 1, stages = 2, orth = 0, use_graphs = 1,
-          use_coop = 1;
+          use_coop = 1, smoother = 0, gs_chunk = 32;
 };
 
 struct HostLevel {

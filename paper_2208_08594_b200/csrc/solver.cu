@@ -209,6 +209,8 @@ msp::Params params_of(const msp_config* c) {
   p.orth = c->orth;
   p.use_graphs = c->use_graphs;
   p.use_coop = c->use_coop;
+  p.smoother = c->smoother;
+  p.gs_chunk = c->gs_chunk;
   return p;
 }
 
@@ -1162,7 +1164,9 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool 
 void setup_cluster(msp_handle* h) {
   h->cl_on = false;
   const int L = (int)h->lv.size();
-  if (h->cl_from < 1 || h->cl_from >= L || L - h->cl_from > kClMaxLevels || h->prm.pre_sweeps < 1) return;
+  if (h->cl_from < 1 || h->cl_from >= L || L - h->cl_from > kClMaxLevels || h->prm.pre_sweeps < 1 ||
+      h->prm.smoother != 0)
+    return;
   for (int cs : {h->cl_size, 8}) {
     if (cs < 1 || cs > 16) continue;
     const int np = cs > 8 ? 1 : 0;
@@ -1282,12 +1286,41 @@ void sell_tail(msp_handle* h, DevLevel& L, int c0, int c1, bool asc, bool write_
   ++h->nlaunch;
 }
 
+// NEXT-4 comparison smoothers (R13): one PJAC-NO / PGS-NO sweep of level L.  The
+// values at the start of the sweep are snapshotted into L.r (free during a sweep; the
+// residual is written after the last pre-sweep), so neither kernel races with itself.
+void no_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool write_r) {
+  if (from_zero) CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
+  CK(cudaMemcpyAsync(L.r, L.x, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, h->s));
+  if (h->prm.smoother == 1) {
+    switch (L.lpr) {
+#define CASE(LP) case LP: klaunch(h->s, h->pdl, sell_jacobi_kernel<LP>, nblk((size_t)L.nslices * kSell * LP, 128), 128, \
+      0, L.nslices, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x); break;
+      CASE(2) CASE(4) CASE(8)
+      default: klaunch(h->s, h->pdl, sell_jacobi_kernel<1>, nblk((size_t)L.nslices * kSell, 128), 128, 0, L.nslices,
+                       L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x);
+#undef CASE
+    }
+  } else {
+    const int K = h->prm.gs_chunk;
+    const int nchunk = (L.n + K - 1) / K;
+    klaunch(h->s, h->pdl, hybrid_gs_kernel, nblk(nchunk, 128), 128, L.n, K, ascending ? 1 : 0, L.perm, L.inv,
+            L.row_start, L.row_width, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x);
+  }
+  ++h->nlaunch;
+  if (write_r) sell_rows_any<false, true>(h, L, 0, L.nslices);   // r = b - A x, every row
+}
+
 // One PGS-MC sweep of level L (Alg. 4).  write_r: the last color also writes the
 // residual of its rows (caller then computes the residual of the other colors).
 // from_zero: the first color starts from the zero guess; init_done: that first color was
 // already computed by the kernel that produced b (fused a3 / restriction).
 void pgs_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool write_r = false,
                bool init_done = false) {
+  if (h->prm.smoother != 0) {
+    no_sweep(h, L, ascending, from_zero, write_r);
+    return;
+  }
   if (ascending) {
     int c = 0;
     if (from_zero) {
@@ -1345,7 +1378,7 @@ void vcycle(msp_handle* h, int l, bool init_done = false) {
     CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.n, h->s));
     sell_rows_any<false, true>(h, L, 0, L.nslices);
   }
-  const bool fuse_next = !last && h->prm.pre_sweeps > 0;
+  const bool fuse_next = !last && h->prm.pre_sweeps > 0 && h->prm.smoother == 0;
   klaunch(h->s, h->pdl, restrict_kernel, nblk(nn, 256), 256, nn, L.pt_ptr, L.pt_idx, L.r, bn,
                                                    fuse_next ? h->lv[l + 1].x : nullptr,
                                                    fuse_next ? h->lv[l + 1].diag : nullptr,
@@ -1427,7 +1460,7 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
     msp_apply_npr(h, g, z);
     return;
   }
-  const bool fuse = !h->dvp;                                           // coop path inits itself
+  const bool fuse = !h->dvp && h->prm.smoother == 0;                  // coop path inits itself
   launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
   vcycle_any(h, fuse);                                                 // a4-a7: B_P
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
@@ -1465,8 +1498,9 @@ void launch_bgs(msp_handle* h, const double* r, double* w) {
 void msp_apply_npr(msp_handle* h, const double* g, double* z) {
   launch_bgs(h, g, h->wfull);                                          // line 2 (r = g)
   launch_spmv(h, 1, h->wfull, g, h->r1);                               // line 3: r = g - A w
-  launch_restrict_pressure(h, h->r1, level0_b(h), true);
-  vcycle(h, 0, true);                                                  // line 4
+  const bool fuse = h->prm.smoother == 0;
+  launch_restrict_pressure(h, h->r1, level0_b(h), fuse);
+  vcycle(h, 0, fuse);                                                  // line 4
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp);
   ++h->nlaunch;
   klaunch(h->s, h->pdl, set_pressure_kernel, nblk(h->n, 256), 256, h->n, h->b, h->wp, h->wfull);
@@ -1810,6 +1844,8 @@ void msp_config_default(msp_config* c) {
   c->orth = 0;
   c->use_graphs = 1;
   c->use_coop = 0;
+  c->smoother = 0;
+  c->gs_chunk = 32;
 }
 
 const char* msp_last_error(const msp_handle* h) { return h ? h->err.c_str() : g_last_error.c_str(); }
@@ -1821,8 +1857,10 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   msp_config_default(&c);
   if (cfg) c = *cfg;
   if (c.stages != 2 && c.stages != 3) return fail(nullptr, MSP_EINVAL, "msp_setup: stages must be 2 (P,R) or 3 (N,P,R)");
-  if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1)
+  if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1 ||
+      c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
+  if (c.smoother != 0) c.use_coop = 0;                 // the persistent V-cycle is PGS-MC only
   std::unique_ptr<msp_handle> h(new msp_handle);
   h->cfg = c;
   if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
@@ -2160,8 +2198,10 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   msp_config c;
   msp_config_default(&c);
   if (cfg) c = *cfg;
-  if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth != 0)
-    return fail(nullptr, MSP_EINVAL, "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2");
+  if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth != 0 ||
+      c.smoother != 0)
+    return fail(nullptr, MSP_EINVAL,
+                "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2, PGS-MC");
   c.use_graphs = 0;                 // collectives (and loopback host barriers) are not captured
   c.use_coop = 0;
   std::unique_ptr<msp_handle> h(new msp_handle);

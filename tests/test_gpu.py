@@ -100,6 +100,48 @@ def test_pgs_sweep_parity_every_level(asc):
         assert np.max(np.abs(x - ref)) <= 1e-12 * np.max(np.abs(ref)), l
 
 
+# ------------------------------------------------------------------ NEXT-4 smoothers (R13)
+@pytest.mark.parametrize("sm,K", [(1, 32), (2, 32), (2, 1), (2, 7), (2, 100000)])
+@pytest.mark.parametrize("asc", [True, False])
+def test_no_smoother_sweep_parity_every_level(sm, K, asc):
+    """One PJAC-NO / PGS-NO sweep per AMG level vs the oracle's definition (R13)."""
+    p = gen.make_config("C2", nx=40, ny=30, nz=6)
+    s = solver(p, coarsest_max_dof=200, smoother=sm, gs_chunk=K)
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=200)
+    L = O.info()["levels"]
+    assert L >= 2
+    for l in range(L):
+        ptr, col, val = O.level_csr(l)
+        n = len(ptr) - 1
+        b = gen.random_vector(n, 100 + l)
+        x0 = gen.random_vector(n, 200 + l)
+        if sm == 1:
+            ref = oracle.jacobi_sweep(ptr, col, val, b, x0)
+        else:
+            ref = oracle.hybrid_gs_sweep(ptr, col, val, K, b, x0, asc)
+        xd = torch.from_numpy(x0.copy()).cuda()
+        s.pgs_sweep(l, torch.from_numpy(b).cuda(), xd, asc)
+        x = xd.cpu().numpy()
+        assert np.max(np.abs(x - ref)) <= 1e-12 * np.max(np.abs(ref)), l
+
+
+@pytest.mark.parametrize("sm", [1, 2])
+def test_no_smoother_vcycle_and_solve_parity(sm):
+    """V-cycle and MSP-GMRES with the comparison smoothers vs the oracle (Table 2 analog)."""
+    p = gen.make_config("C2", nx=24, ny=20, nz=4)
+    s = solver(p, coarsest_max_dof=50, smoother=sm)
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=50, smoother=sm)
+    r = gen.random_vector(p["n"], 7)
+    ref = O.vcycle(r)
+    xd = torch.zeros(p["n"], dtype=torch.float64, device="cuda")
+    s.vcycle(torch.from_numpy(r).cuda(), xd)
+    assert np.linalg.norm(xd.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+    ro = O.solve(p["rhs"], tol=1e-8)
+    rg = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-8)
+    assert abs(rg["iters"] - ro["iters"]) <= 1, (rg["iters"], ro["iters"])
+    assert rg["final_rel"] <= 1e-8
+
+
 # ------------------------------------------------------------------ V-cycle, BILU, MSP
 @pytest.mark.parametrize("kw", [dict(coarsest_max_dof=200), dict(coarsest_max_dof=200, pair_passes=1),
                                 dict(), dict(coarsest_max_dof=200, use_coop=0),
