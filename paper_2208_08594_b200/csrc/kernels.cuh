@@ -340,12 +340,20 @@ __global__ void __launch_bounds__(128) sell_jacobi_kernel(int s_first, int s_end
   if (u == 0 && row < ldg(slice_row + s + 1)) x[row] = (ldg(b + row) - acc) / ldg(diag + row);
 }
 
-// PGS-NO (hybrid Jacobi/GS): thread c relaxes the natural-order rows
-// [cK, cK+K) in order (descending for the post-sweep); a coupling to a row of the same
-// chunk that was already relaxed in this sweep uses its new value (x, written only by
-// this thread), every other coupling the start-of-sweep value xo.  perm/inv map natural
-// <-> permuted rows; row_start/row_width locate a row's SELL entries.
-__global__ void __launch_bounds__(128) hybrid_gs_kernel(int n, int K, int asc, const int* __restrict__ perm,
+// PGS-NO (hybrid Jacobi/GS): one warp per chunk of K natural-order rows
+// [cK, cK+K), relaxed in order (descending for the post-sweep); a coupling to a row of
+// the same chunk relaxed earlier in this sweep uses its new value, every other coupling
+// the start-of-sweep value xo.  The chunk is processed in groups of 32 rows, lane l
+// holding the row at sweep position 32*g + l: each lane first sums, in parallel, its
+// couplings to start-of-sweep values and to rows finished in earlier groups, and writes
+// its couplings to earlier rows of the same group into a 32x32 shared tile; the group's
+// triangle is then resolved in 32 steps (lane t finishes, broadcasts x_t by shuffle,
+// later lanes add S[l][t] x_t).  perm/inv map natural <-> permuted rows;
+// row_start/row_width locate a row's SELL entries.
+// (K < 16: the thread-per-chunk variant below keeps the lanes busy.)
+constexpr int kHgsWarps = 4;
+__global__ void __launch_bounds__(32 * kHgsWarps) hybrid_gs_kernel(int n, int K, int asc,
+                                                        const int* __restrict__ perm,
                                                         const int* __restrict__ inv,
                                                         const int* __restrict__ row_start,
                                                         const int* __restrict__ row_width,
@@ -354,6 +362,64 @@ __global__ void __launch_bounds__(128) hybrid_gs_kernel(int n, int K, int asc, c
                                                         const double* __restrict__ diag,
                                                         const double* __restrict__ b,
                                                         const double* __restrict__ xo, double* x) {
+  __shared__ double S[kHgsWarps][32][33];
+  PDL_ENTRY();
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kHgsWarps + wi;
+  const int q0 = c * K;
+  if (q0 >= n) return;                                  // whole warp
+  const int q1 = min(n, q0 + K);
+  const int len = q1 - q0;
+  double* Sw = &S[wi][lane][0];
+  for (int g0 = 0; g0 < len; g0 += 32) {
+    const int pos = g0 + lane;
+    const bool active = pos < len;
+    const int q = asc ? q0 + pos : q1 - 1 - pos;
+#pragma unroll 4
+    for (int t = 0; t < 32; ++t) Sw[t] = 0.0;
+    double acc = 0.0, bv = 0.0, d = 1.0;
+    int p = 0;
+    if (active) {
+      p = ldg(perm + q);
+      const int o0 = ldg(row_start + p), w = ldg(row_width + p);
+      for (int k = 0; k < w; ++k) {
+        const int o = o0 + k * kSell;
+        const int j = ldg(col + o);
+        const int qj = ldg(inv + j);
+        const double a = ldg(val + o);
+        const int pj = asc ? qj - q0 : q1 - 1 - qj;     // sweep position of row j
+        if (qj >= q0 && qj < q1 && pj < pos) {           // relaxed earlier in this sweep
+          if (pj >= g0) Sw[pj - g0] = a;                 // same group: resolved below
+          else acc = fma(a, x[j], acc);                  // earlier group: final
+        } else {
+          acc = fma(a, ldg(xo + j), acc);
+        }
+      }
+      bv = ldg(b + p);
+      d = 1.0 / ldg(diag + p);                          // one division per row, outside the chain
+    }
+    __syncwarp();
+    double xi = 0.0;
+    for (int t = 0; t < 32; ++t) {
+      const double xt = __shfl_sync(0xffffffffu, (bv - acc) * d, t);
+      if (lane == t) xi = xt;
+      if (lane > t) acc = fma(Sw[t], xt, acc);
+    }
+    if (active) x[p] = xi;
+    __syncwarp();                                       // x of this group final for the next
+  }
+}
+
+// PGS-NO for small chunks (K < 16): one thread relaxes its chunk row by row.
+__global__ void __launch_bounds__(128) hybrid_gs_thread_kernel(int n, int K, int asc, const int* __restrict__ perm,
+                                                               const int* __restrict__ inv,
+                                                               const int* __restrict__ row_start,
+                                                               const int* __restrict__ row_width,
+                                                               const int* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ b,
+                                                               const double* __restrict__ xo, double* x) {
   PDL_ENTRY();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int q0 = c * K;

@@ -1304,8 +1304,12 @@ void no_sweep(msp_handle* h, DevLevel& L, bool ascending, bool from_zero, bool w
   } else {
     const int K = h->prm.gs_chunk;
     const int nchunk = (L.n + K - 1) / K;
-    klaunch(h->s, h->pdl, hybrid_gs_kernel, nblk(nchunk, 128), 128, L.n, K, ascending ? 1 : 0, L.perm, L.inv,
-            L.row_start, L.row_width, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x);
+    if (K < 16)
+      klaunch(h->s, h->pdl, hybrid_gs_thread_kernel, nblk(nchunk, 128), 128, L.n, K, ascending ? 1 : 0, L.perm,
+              L.inv, L.row_start, L.row_width, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x);
+    else
+      klaunch(h->s, h->pdl, hybrid_gs_kernel, nblk(nchunk, kHgsWarps), 32 * kHgsWarps, L.n, K, ascending ? 1 : 0,
+              L.perm, L.inv, L.row_start, L.row_width, L.col, L.val, L.diag, L.b, (const double*)L.r, L.x);
   }
   ++h->nlaunch;
   if (write_r) sell_rows_any<false, true>(h, L, 0, L.nslices);   // r = b - A x, every row

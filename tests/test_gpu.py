@@ -101,7 +101,7 @@ def test_pgs_sweep_parity_every_level(asc):
 
 
 # ------------------------------------------------------------------ NEXT-4 smoothers (R13)
-@pytest.mark.parametrize("sm,K", [(1, 32), (2, 32), (2, 1), (2, 7), (2, 100000)])
+@pytest.mark.parametrize("sm,K", [(1, 32), (2, 32), (2, 1), (2, 7), (2, 16), (2, 45), (2, 100000)])
 @pytest.mark.parametrize("asc", [True, False])
 def test_no_smoother_sweep_parity_every_level(sm, K, asc):
     """One PJAC-NO / PGS-NO sweep per AMG level vs the oracle's definition (R13)."""
@@ -335,6 +335,20 @@ def _check_hist(h, ref, n_first=15, rtol=1e-9):
     dev = np.abs(h[:k] - ref[:k]) / ref[:k]
     print("hist max rel dev (first %d): %.3e" % (k, dev.max()))
     assert dev.max() <= rtol, dev
+
+
+@pytest.mark.parametrize("sm", [1, 2])
+def test_full_size_c3_no_smoothers_vs_oracle_golden(sm):
+    """Table 2 analog at full C3 size (NEXT-4, R13): MSP-GMRES with PJAC-NO / PGS-NO (K=32)
+    against the oracle's committed runs (oracle_c3_sm<k>.json, make_oracle.py C3 <k>)."""
+    p = gen.make_config("C3")
+    s = solver(p, smoother=sm, gs_chunk=32)
+    r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-6)
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"oracle_c3_sm{sm}.json")))
+    assert ref["smoother"] == sm and ref["gs_chunk"] == 32
+    assert abs(r["iters"] - ref["iters"]) <= 1, (r["iters"], ref["iters"])
+    assert r["final_rel"] <= 1e-6
+    _check_hist(r["hist"], ref["hist"])
 
 
 def test_full_size_c4_solve_vs_oracle_golden():
