@@ -22,6 +22,9 @@ constexpr bool kBiluBatch = MSP_BILU_BATCH != 0;
 #define MSP_BILU_PREFETCH 1
 #endif
 constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
+#ifndef MSP_SELL_PF1
+#define MSP_SELL_PF1 6
+#endif
 #ifndef MSP_BILU_PFE
 #define MSP_BILU_PFE 2
 #endif
@@ -461,7 +464,7 @@ __global__ void pgs_init_kernel(int n, int c1_end, const double* __restrict__ di
 // the a5 residual, fused).  MODE_RES: residual only (rows of the other colors).
 // ---------------------------------------------------------------------------
 template <int LPR, bool WRITE_R, bool MODE_RES>
-__global__ void __launch_bounds__(128) sell_row_kernel(int s_first, int s_end,
+__global__ void __launch_bounds__(512) sell_row_kernel(int s_first, int s_end,
                                                        const int* __restrict__ slice_row,
                                                        const int* __restrict__ slice_off,
                                                        const int* __restrict__ col,
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(128) sell_row_kernel(int s_first, int s_end,
   const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
   // prologue (overlaps the predecessor kernel): the first PF matrix entries of this
   // lane and the diagonal are immutable
-  constexpr int PF = 4;
+  constexpr int PF = (LPR == 1) ? MSP_SELL_PF1 : 4;
   int pc[PF];
   double pv[PF];
 #pragma unroll

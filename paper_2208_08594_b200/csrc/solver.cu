@@ -116,6 +116,7 @@ struct msp_handle {
   VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
   int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
   // cluster V-cycle legs (cluster.cuh): levels [cl_from, L) in one cl_size-CTA cluster
+  int sell_tpb = 128;                        // CTA size of the LPR=1 (level-0) sweep kernels
   int cl_from = 0, cl_size = 16;             // opt-in (MSP_CLUSTER_FROM): measured slower
   bool cl_on = false;
   bool pdl = true;                   // programmatic dependent launch for every kernel
@@ -1260,7 +1261,8 @@ void coarsest_solve(msp_handle* h) {
 template <int LPR, bool WR, bool RES>
 void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
   if (s1 <= s0) return;
-  klaunch(h->s, h->pdl, sell_row_kernel<LPR, WR, RES>, nblk((size_t)(s1 - s0) * kSell * LPR, 128), 128, 
+  const int tpb = (LPR == 1) ? h->sell_tpb : 128;
+  klaunch(h->s, h->pdl, sell_row_kernel<LPR, WR, RES>, nblk((size_t)(s1 - s0) * kSell * LPR, tpb), tpb, 
       s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
   ++h->nlaunch;
 }
@@ -1873,6 +1875,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_BILU_NOPF")) h->bilu_nopf = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
+  if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_SIZE")) h->cl_size = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);

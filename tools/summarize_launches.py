@@ -34,7 +34,7 @@ with open(dst_txt, "w") as f:
                 f"{byt[n] / t if t else 0:9.1f} {byt[n] / cnt[n] / 1e6:12.2f}  {n}\n")
 pieces = {
     "a2_bsr_spmv": lambda n: n.startswith("bsr_spmv4c_kernel<0>") or n.startswith("bsr_spmv_kernel<4, 0>"),
-    "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>"),
+    "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>") or n.startswith("pcol_resid4_kernel"),
     "a9_bilu_apply": lambda n: n.startswith("bilu_block_kernel"),
 }
 out = {}
@@ -42,7 +42,7 @@ for key, pred in pieces.items():
     b = sum(byt[n] for n in byt if pred(n))
     c = sum(cnt[n] for n in cnt if pred(n))
     if key == "a9_bilu_apply":            # one BILU apply per a8 launch (one per MSP apply)
-        c = sum(cnt[n] for n in cnt if n.startswith("bsr_spmv_kernel<4, 2>"))
+        c = sum(cnt[n] for n in cnt if pieces["a8_pcol_residual"](n))
     out[key] = b / c if c else None          # DRAM bytes per launch (per application)
 out["_source"] = src
 json.dump(out, open(dst_json, "w"), indent=1)
