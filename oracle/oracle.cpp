@@ -926,10 +926,19 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
   if (out.final_rel <= tol) return out;
   std::vector<std::vector<double>> V(m + 1, std::vector<double>(N));
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gam(m + 1);
+  // DCGS2 state (orth == 2, R14): unrotated Hessenberg columns, the reorthogonalisation
+  // coefficients h2 of the provisional V[j] and its scalars nu (its normalisation) and
+  // rho (its norm after reorthogonalisation)
+  std::vector<double> Hraw((size_t)(m + 1) * m), h2p;
+  double nu = 1.0, rhop = 1.0;
   while (true) {
     for (size_t i = 0; i < N; ++i) V[0][i] = r[i] / beta;
     std::fill(gam.begin(), gam.end(), 0.0);
     gam[0] = beta;
+    h2p.clear();
+    nu = 1.0;                                           // V[0] is final
+    rhop = 1.0;
+    double next_scale = 0.0;
     int k = 0;
     for (int j = 0; j < m; ++j) {
       if (!Bop(V[j].data(), z.data())) { out.status = 2; return out; }
@@ -945,15 +954,64 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
             for (size_t q = 0; q < N; ++q) w[q] -= hh[i] * V[i][q];
           for (int i = 0; i <= j; ++i) h(i) += hh[i];
         }
-      } else {                                          // MGS
+      } else if (orth == 1) {                           // MGS
         for (int i = 0; i <= j; ++i) {
           double hi = dot(V[i], w);
           for (size_t q = 0; q < N; ++q) w[q] -= hi * V[i][q];
           h(i) = hi;
         }
       }
-      const double hn = nrm2(w);
-      h(j + 1) = hn;
+      double hn;
+      if (orth == 2) {
+        // DCGS2 (R14).  V[0..j) final; V[j] provisional = u_{j-1} / nu, whose second
+        // projection h2p = V[0..j)^T u_{j-1} is known; w = A B V[j].
+        // (1) a_i = V[i]^T w for i <= j (one pass)
+        std::vector<double> a(j + 1);
+        for (int i = 0; i <= j; ++i) a[i] = dot(V[i], w);
+        // (2) c_j = (final v_j)^T w = (nu a_j - h2p^T a_{0..j}) / rho
+        double cj = nu * a[j];
+        for (int i = 0; i < j; ++i) cj -= h2p[i] * a[i];
+        cj /= rhop;
+        // (3) finalise v_j = (nu V[j] - V[0..j) h2p) / rho and project w once onto the
+        //     final basis: u = w - V[0..j) a - v_j c_j (one pass)
+        for (size_t q = 0; q < N; ++q) {
+          double s1 = 0.0;
+          for (int i = 0; i < j; ++i) s1 += h2p[i] * V[i][q];
+          V[j][q] = (nu * V[j][q] - s1) / rhop;
+        }
+        for (size_t q = 0; q < N; ++q) {
+          double s2 = 0.0;
+          for (int i = 0; i < j; ++i) s2 += a[i] * V[i][q];
+          w[q] = w[q] - s2 - cj * V[j][q];
+        }
+        // (4) second-projection coefficients of u (used at the next step) and ||u||
+        std::vector<double> h2n(j + 1);
+        for (int i = 0; i <= j; ++i) h2n[i] = dot(V[i], w);
+        const double uu = dot(w, w);
+        double ss = 0.0;
+        for (int i = 0; i <= j; ++i) ss += h2n[i] * h2n[i];
+        const double nun = std::sqrt(uu);
+        const double rhon = std::sqrt(std::max(uu - ss, 0.0));
+        // (5) Hessenberg column j of the final basis:
+        //     A B v_j = (nu A B V[j] - sum_{l<j} h2p_l A B v_l) / rho,
+        //     A B V[j] = w = V[0..j] (c + h2n) + rhon v_{j+1}
+        for (int i = 0; i <= j + 1; ++i) {
+          double ci = (i < j) ? a[i] : (i == j ? cj : 0.0);
+          double v = (i <= j) ? nu * (ci + h2n[i]) : nu * rhon;
+          for (int l = 0; l < j; ++l) v -= h2p[l] * Hraw[(size_t)i * m + l];
+          Hraw[(size_t)i * m + j] = v / rhop;
+          h(i) = Hraw[(size_t)i * m + j];
+        }
+        hn = h(j + 1);
+        next_scale = nun;                                // V[j+1] provisional = u / ||u||
+        h2p = h2n;
+        nu = nun;
+        rhop = rhon;
+      } else {
+        hn = nrm2(w);
+        h(j + 1) = hn;
+        next_scale = hn;
+      }
       out.iters++;
       for (int i = 0; i < j; ++i) {                     // previous rotations
         double a = h(i), c = h(i + 1);
@@ -971,7 +1029,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       out.hist.push_back(est);
       k = j + 1;
       if (est <= tol || hn < 1e-14 * bnorm || out.iters >= maxit) break;
-      for (size_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / hn;
+      for (size_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / next_scale;
     }
     std::vector<double> y(k);
     for (int i = k - 1; i >= 0; --i) {

@@ -653,7 +653,7 @@ def test_gmres_exact_preconditioner_one_iteration():
     assert r["iters"] == 1
 
 
-@pytest.mark.parametrize("orth", [0, 1])
+@pytest.mark.parametrize("orth", [0, 1, 2])
 def test_gmres_vs_scipy_random30(orth):
     """Same Krylov method as scipy's GMRES (restart 30, identity preconditioner):
     iteration counts agree within 1 and solutions match the dense solve."""
@@ -670,6 +670,46 @@ def test_gmres_vs_scipy_random30(orth):
         assert abs(r["iters"] - cnt[0]) <= 1
         assert np.allclose(r["x"], np.linalg.solve(A, b), rtol=1e-6)
         assert abs(r["final_rel"] - np.linalg.norm(b - A @ r["x"]) / np.linalg.norm(b)) <= 1e-12
+
+
+@pytest.mark.parametrize("orth", [0, 1, 2])
+def test_gmres_residuals_are_krylov_minima(orth):
+    """Brute force: the k-th GMRES residual estimate equals min over x in K_k(A, b) of
+    ||b - A x|| / ||b|| (numpy least squares on a QR basis of [b, Ab, ...]); identity
+    preconditioner, no restart.  Checks CGS2, MGS and DCGS2 (R14) Arnoldi alike, including
+    the DCGS2 Hessenberg correction and its one-step-delayed reorthogonalisation."""
+    rng = np.random.default_rng(21)
+    n = 40
+    A = rng.normal(size=(n, n)) / np.sqrt(n) + 1.5 * np.eye(n)
+    b = rng.normal(size=n)
+    ptr, col, val = csr_of(A)
+    r = oracle.gmres_csr(ptr, col, val, b, tol=1e-13, m=40, maxit=40, orth=orth)
+    Q = (b / np.linalg.norm(b))[:, None]                  # orthonormal basis of K_k (Householder QR)
+    for k in range(1, 16):
+        y, *_ = np.linalg.lstsq(A @ Q, b, rcond=None)
+        ref = np.linalg.norm(b - A @ Q @ y) / np.linalg.norm(b)
+        assert abs(r["hist"][k - 1] - ref) <= 1e-9 * ref + 1e-15, (k, r["hist"][k - 1], ref)
+        Q, _ = np.linalg.qr(np.column_stack([Q, A @ Q[:, -1]]))
+
+
+@pytest.mark.parametrize("m", [5, 30])
+def test_dcgs2_restarted_matches_cgs2(m):
+    """DCGS2 (R14) computes the same Arnoldi basis as CGS2 in exact arithmetic: with
+    restarts, MSP preconditioning and a nonsymmetric system its residual history agrees
+    with the (scipy-pinned) CGS2 history to rounding level."""
+    p = gen.make_config("C2", nx=12, ny=10, nz=3)
+    out = []
+    for orth in (0, 2):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], orth=orth, coarsest_max_dof=40)
+        out.append(M.solve(p["rhs"], tol=1e-10, restart=m))
+    assert out[0]["iters"] == out[1]["iters"]
+    h0, h1 = out[0]["hist"], out[1]["hist"]
+    assert len(h0) == len(h1)
+    # rounding differences, amplified through restarts: relative 1e-7 plus 1e-13 of ||b||
+    assert np.all(np.abs(h0 - h1) <= 1e-7 * h0 + 1e-13)
+    k = min(m, out[0]["iters"])                                      # first-cycle estimates
+    assert np.max(np.abs(h0[:k] - h1[:k]) / h0[:k]) <= 1e-10
+    assert np.linalg.norm(out[0]["x"] - out[1]["x"]) <= 1e-8 * np.linalg.norm(out[0]["x"])
 
 
 def test_msp_gmres_3cube_vs_dense_lu():
@@ -693,10 +733,10 @@ def test_msp_gmres_3cube_vs_dense_lu():
 def test_cgs2_and_mgs_same_iterations_C1():
     p = gen.make_config("C1")
     its = []
-    for orth in (0, 1):
+    for orth in (0, 1, 2):
         M = oracle.Msp(p["row_ptr"], p["col"], p["val"], orth=orth, coarsest_max_dof=50)
         its.append(M.solve(p["rhs"])["iters"])
-    assert abs(its[0] - its[1]) <= 1
+    assert abs(its[0] - its[1]) <= 1 and abs(its[0] - its[2]) <= 1
 
 
 # ------------------------------------------------------------------ c-12 ASMSP
