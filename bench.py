@@ -259,7 +259,7 @@ def main():
     peak, peak_src = measured_peak()
     kernels = {}
     kinds = ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
-             "a10_multidot16", "cgs2_step15", "a6_coarse_gemv", "vcycle", "msp_apply")
+             "a10_multidot16", "orth_step15", "a6_coarse_gemv", "vcycle", "msp_apply")
     if ws > 1:                                     # rank-local kernels only
         kinds = ("a2_bsr_spmv", "a8_pcol_residual", "a10_multidot16")
     for kind in kinds:
@@ -278,7 +278,7 @@ def main():
         "a2_bsr_spmv": kernels["a2_bsr_spmv"].get("ms", 0) * (iters + 2 * cyc + 1),
         "a9_bilu_apply": kernels.get("a9_bilu_apply", {}).get("ms", 0) * (iters + cyc),
         "a8_pcol_residual": kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
-        "cgs2_step15": kernels.get("cgs2_step15", {}).get("ms", 0) * iters,
+        "orth_step15": kernels.get("orth_step15", {}).get("ms", 0) * iters,
     }
     dom = max(share, key=share.get)
     kd = kernels[dom]
@@ -308,6 +308,7 @@ def main():
                           "iterations_per_step": its, "final_rel_res": max(rels),
                           "setup_s": st0["last_setup_seconds"], "levels": st0["level_n"],
                           "level_colors": st0["level_colors"], "bilu_colors": st0["bilu_colors"],
+                          "orthogonalisation": "DCGS2 (msp_config default, R14)", "smoother": "PGS-MC",
                           "l2": "inputs larger than L2 (A alone 1.0 GB); kernel timings flush L2",
                           "parallelism": (f"z-slab x{ws} (NCCL halo + allreduce, replicated coarse levels)"
                                           if ws > 1 else "single GPU"),

@@ -74,7 +74,10 @@ typedef struct {
   int32_t decoupling;        /* 0 NONE (W = Π_P), 1 QI, 2 TI (default, R4) */
   int32_t bilu_order;        /* 0 RB (Alg. 2/3 cell colors), 1 ABMC1 (default, R5) */
   int32_t stages;            /* 2 = P,R (north_star, default); 3 = N,P,R (full Eq. 21) */
-  int32_t orth;              /* 0 CGS2 (default, R8); 1 MGS */
+  int32_t orth;              /* GMRES Arnoldi orthogonalisation: 2 DCGS2 (default, R14: CGS2's
+                                basis with the re-orthogonalisation delayed by one step, two
+                                passes over the basis per step instead of three); 0 CGS2 (R8);
+                                1 MGS */
   int32_t use_graphs;        /* 1: replay each Arnoldi step as a CUDA graph (default) */
   int32_t use_coop;          /* 0 (default): one graph node per PGS-MC color / transfer;
                                 1: whole V-cycle as one cooperative persistent kernel (measured

@@ -68,7 +68,7 @@ class Config(ctypes.Structure):
 
     @classmethod
     def make(cls, coarsest_max_dof=10000, max_levels=20, pre_sweeps=1, post_sweeps=1, pair_passes=2,
-             decoupling=2, bilu_order=1, stages=2, orth=0, smoother=0, gs_chunk=32):
+             decoupling=2, bilu_order=1, stages=2, orth=2, smoother=0, gs_chunk=32):
         return cls(coarsest_max_dof, max_levels, pre_sweeps, post_sweeps, pair_passes, decoupling,
                    bilu_order, stages, orth, smoother, gs_chunk)
 

@@ -444,7 +444,7 @@ struct Config {
   int decoupling = 2;            // 0 NONE, 1 QI, 2 TI (R4)
   int bilu_order = 1;            // 0 RB, 1 ABMC1 (R5)
   int stages = 2;                // 2 = PR (north_star), 3 = NPR (Eq. 21 full)
-  int orth = 0;                  // 0 CGS2, 1 MGS (R8)
+  int orth = 2;                  // 2 DCGS2 (R14, default), 0 CGS2, 1 MGS (R8)
   int smoother = 0;              // 0 PGS-MC (Alg. 4), 1 PJAC-NO, 2 PGS-NO (R13)
   int gs_chunk = 32;             // PGS-NO chunk size K (R13)
 };
@@ -963,8 +963,10 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       }
       double hn;
       if (orth == 2) {
-        // DCGS2 (R14).  V[0..j) final; V[j] provisional = u_{j-1} / nu, whose second
-        // projection h2p = V[0..j)^T u_{j-1} is known; w = A B V[j].
+        // DCGS2 (R14).  V[0..j) final; V[j] provisional = u_{j-1} / nu (the previous
+        // step's once-projected vector, stored unnormalised: nu = 1 for j >= 1, V[0] is
+        // final: nu = rho = 1), whose second projection h2p = V[0..j)^T V[j] and
+        // rho = ||V[j] - V[0..j) h2p|| are known; w = A B V[j].
         // (1) a_i = V[i]^T w for i <= j (one pass)
         std::vector<double> a(j + 1);
         for (int i = 0; i <= j; ++i) a[i] = dot(V[i], w);
@@ -990,7 +992,6 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
         const double uu = dot(w, w);
         double ss = 0.0;
         for (int i = 0; i <= j; ++i) ss += h2n[i] * h2n[i];
-        const double nun = std::sqrt(uu);
         const double rhon = std::sqrt(std::max(uu - ss, 0.0));
         // (5) Hessenberg column j of the final basis:
         //     A B v_j = (nu A B V[j] - sum_{l<j} h2p_l A B v_l) / rho,
@@ -1003,9 +1004,9 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
           h(i) = Hraw[(size_t)i * m + j];
         }
         hn = h(j + 1);
-        next_scale = nun;                                // V[j+1] provisional = u / ||u||
+        next_scale = 1.0;                                // V[j+1] provisional = u (unnormalised)
         h2p = h2n;
-        nu = nun;
+        nu = 1.0;
         rhop = rhon;
       } else {
         hn = nrm2(w);

@@ -77,7 +77,9 @@ _lib.msp_kernel_launches.argtypes = [ctypes.c_void_p]
 KERNEL_KINDS = {"a2_bsr_spmv": 0, "a4_pgs_sweep_l0": 1, "a8_pcol_residual": 2, "a9_bilu_apply": 3,
                 "a10_multidot16": 4, "a6_coarse_gemv": 5, "msp_apply": 6, "vcycle": 7,
                 "bilu": 8, "arnoldi_step15": 9, "cgs2_step15": 10, "arnoldi_step25": 11,
-                "cgs2_step25": 12}
+                "cgs2_step25": 12,
+                # the configured orthogonalisation (DCGS2 by default) at steps 15 / 25
+                "orth_step15": 10, "orth_step25": 12}
 _lib.msp_host_setup_free.argtypes = [ctypes.c_void_p]
 
 

@@ -1438,6 +1438,129 @@ __global__ void __launch_bounds__(kRedThreads, MINB) cgs_axpy_kernel(size_t NE, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// DCGS2 Arnoldi (orth = 2, reading R14): delayed re-orthogonalisation, two passes over
+// the basis per step instead of CGS2's three.  Step k holds V[0..k) final and V[k]
+// provisional = the previous step's once-projected vector u_{k-1}, stored UNnormalised
+// (the method only needs it up to a factor, so no scaling pass), with its second-
+// projection coefficients h2 = V[0..k)^T u_{k-1} and rho = ||u_{k-1} - V h2|| in the
+// state st: st[0..k) = h2, st[kMaxV] = nu = 1, st[kMaxV+1] = rho; k = 0: V[0] final,
+// nu = rho = 1.  w = A B V[k].
+// Pass 1 (cgs_dot): a = V[0..k]^T w.  Pass 2 (this kernel), per element:
+//   v_k = (nu V[k] - V[0..k) h2) / rho          (V[k] finalised in place)
+//   u   = w - V[0..k) a[0..k) - c_k v_k,  c_k = (nu a_k - h2^T a[0..k)) / rho
+// and, when DOT, the sums V[0..k)^T u, v_k^T u, u^T u (slots 0..k-1, k, k+1); without
+// DOT the caller gets them from cgs_dot over V[0..k+1] (u is stored in the slot V[k+1]).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dcgs_scalars(int k, const double* a, const double* st, double& nu, double& rho,
+                                             double& ck) {
+  nu = k ? st[kMaxV] : 1.0;
+  rho = k ? st[kMaxV + 1] : 1.0;
+  double c = nu * a[k];
+  for (int i = 0; i < k; ++i) c -= st[i] * a[i];
+  ck = c / rho;
+}
+
+#ifndef MSP_DCGS_MINB
+#define MSP_DCGS_MINB 4                  // 64 registers: 4 CTAs/SM (2: 128 regs, 18% slower)
+#endif
+#ifndef MSP_DCGS_GROUP
+#define MSP_DCGS_GROUP 16
+#endif
+template <int NV, int EW, bool DOT>
+__global__ void __launch_bounds__(kRedThreads, MSP_DCGS_MINB) dcgs_update_kernel(size_t NE, int k, const double* __restrict__ V,
+                                                                    size_t ldv, double* vk, double* w,
+                                                                    const double* __restrict__ a,
+                                                                    const double* __restrict__ st, double* part,
+                                                                    double* out, unsigned* ticket) {
+  PDL_ENTRY();
+  using T = VecT<EW>;
+  __shared__ double h2s[NV], as[NV], sc[4];
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) {
+    h2s[i] = (i < k) ? st[i] : 0.0;
+    as[i] = (i < k) ? a[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    dcgs_scalars(k, a, st, sc[0], sc[1], sc[2]);
+    sc[3] = 1.0 / sc[1];
+  }
+  __syncthreads();
+  const double nu = sc[0], rinv = sc[3], ck = sc[2];
+  double acc[DOT ? NV : 1];
+#pragma unroll
+  for (int i = 0; i < (DOT ? NV : 1); ++i) acc[i] = 0.0;
+  double accv = 0.0, accu = 0.0;
+  T* vT = reinterpret_cast<T*>(vk);
+  T* wT = reinterpret_cast<T*>(w);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < NE; t += stride) {
+    T vf = vT[t], u = wT[t];                           // issued before the basis loads
+    T s1, s2;
+    if constexpr (EW == 2) { s1 = {0.0, 0.0}; s2 = {0.0, 0.0}; } else { s1 = {0.0}; s2 = {0.0}; }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (i < k) {
+        const T vi = T::ld(V + i * ldv, t);
+        vaxpy<EW>(h2s[i], vi, s1);
+        vaxpy<EW>(as[i], vi, s2);
+      }
+      if (i % MSP_DCGS_GROUP == MSP_DCGS_GROUP - 1) asm volatile("" ::: "memory");
+    }
+    vf.x = (nu * vf.x - s1.x) * rinv;                   // (one division per CTA, not per element)
+    u.x = u.x - s2.x - ck * vf.x;
+    if constexpr (EW == 2) {
+      vf.y = (nu * vf.y - s1.y) * rinv;
+      u.y = u.y - s2.y - ck * vf.y;
+    }
+    vT[t] = vf;
+    wT[t] = u;
+    if constexpr (DOT) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        if (i < k) acc[i] = vdot<EW>(T::ldcg(V + i * ldv, t), u, acc[i]);
+        if (i % MSP_DCGS_GROUP == MSP_DCGS_GROUP - 1) asm volatile("" ::: "memory");
+      }
+      accv = vdot<EW>(vf, u, accv);
+      accu = vdot<EW>(u, u, accu);
+    }
+  }
+  if constexpr (DOT) {
+    block_partials<NV>(acc, k, part, 0);
+    const double tail[2] = {accv, accu};
+    block_partials<2>(tail, 2, part, k);
+    finalize_partials(k + 2, part, out, nullptr, nullptr, -1, ticket);
+  }
+}
+
+// One CTA: from a = V[0..k]^T w, the old state and the sums s (V[0..k)^T u, v_k^T u,
+// u^T u) -> new state (h2' = s[0..k], nu' = 1 (u kept unnormalised),
+// rho' = sqrt(u^T u - ||h2'||^2)) and the host record rec[0..k] = c + h2',
+// rec[k+1] = rho', rec[k+2] = nu', rec[k+3 .. 2k+3] = h2' (the host applies the
+// Hessenberg correction, R14).
+__global__ void dcgs_finish_kernel(int k, const double* __restrict__ a, const double* __restrict__ st_in,
+                                   const double* __restrict__ s, double* __restrict__ st_out,
+                                   double* __restrict__ rec) {
+  PDL_ENTRY();
+  if (threadIdx.x != 0) return;
+  double nu, rho, ck;
+  dcgs_scalars(k, a, st_in, nu, rho, ck);
+  const double uu = s[k + 1];
+  double ss = 0.0;
+  for (int i = 0; i <= k; ++i) ss += s[i] * s[i];
+  const double nun = 1.0;
+  const double rhon = sqrt(fmax(uu - ss, 0.0));
+  for (int i = 0; i <= k; ++i) {
+    const double ci = (i < k) ? a[i] : ck;
+    rec[i] = ci + s[i];
+    rec[k + 3 + i] = s[i];
+    st_out[i] = s[i];
+  }
+  rec[k + 1] = rhon;
+  rec[k + 2] = nun;
+  st_out[kMaxV] = nun;
+  st_out[kMaxV + 1] = rhon;
+}
+
 // v = w * (1/s[0])   (Arnoldi normalisation; s on device)
 __global__ void scale_kernel(size_t N, const double* __restrict__ w, const double* __restrict__ s,
                              double* __restrict__ v) {

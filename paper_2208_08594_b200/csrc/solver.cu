@@ -128,6 +128,7 @@ struct msp_handle {
   double *V = nullptr;
   int V_m = -1;
   double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
+  double *dst = nullptr, *dsum = nullptr;     // DCGS2 state (2 parities x (kMaxV+2)) and sums
   unsigned* ticket = nullptr;
   double* io = nullptr;              // staging for host<->device and natural-order vectors
   // graphs
@@ -647,10 +648,12 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->part = h->dalloc<double>((size_t)kRedBlocks * kMaxV);
   h->dh1 = h->dalloc<double>(kMaxV);
   h->dh2 = h->dalloc<double>(kMaxV);
-  h->hcol = h->dalloc<double>(kMaxV);
+  h->hcol = h->dalloc<double>(4 * kMaxV);
+  h->dst = h->dalloc<double>(2 * (kMaxV + 2));
+  h->dsum = h->dalloc<double>(kMaxV + 2);
   h->ticket = h->dalloc<unsigned>(4);
   CK(cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned), h->s));
-  CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 2));
+  CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 4));
   CK(cudaStreamSynchronize(h->s));
   auto t1 = std::chrono::steady_clock::now();
   const double secs = std::chrono::duration<double>(t1 - t0).count();
@@ -1563,13 +1566,20 @@ void norm_dev(msp_handle* h, const double* w, double* out) {
 
 constexpr bool kCgsWide32 = false;         // NV=32 basis kernels use 8-byte loads
 
+// 16-byte basis loads need an even vector length (N odd: 8-byte loads; V slots stay
+// N apart, so an odd N also breaks 16-byte alignment of V[1], V[3], ...)
+bool ew2_ok(const msp_handle* h) { return (h->N % 2) == 0; }
+
 template <int NV>
 void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
                double* raw, int sq) {
-  constexpr int EW = (NV <= 16 || kCgsWide32) ? 2 : 1;
   constexpr int MINB = 2;
-  klaunch(h->s, h->pdl, cgs_dot_kernel<NV, EW, MINB>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, w, h->part, out, addend, raw,
-                                                              sq, h->ticket);
+  if ((NV <= 16 || kCgsWide32) && ew2_ok(h))
+    klaunch(h->s, h->pdl, cgs_dot_kernel<NV, 2, MINB>, kRedBlocks, kRedThreads, h->N / 2, nv, V, h->N, w, h->part, out,
+            addend, raw, sq, h->ticket);
+  else
+    klaunch(h->s, h->pdl, cgs_dot_kernel<NV, 1, MINB>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, w, h->part, out,
+            addend, raw, sq, h->ticket);
   ++h->nlaunch;
 }
 void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
@@ -1580,18 +1590,25 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
   else if (h->cgs_split == 0) {
     // 16 vectors per CTA row (gridDim.y = 2), 16-byte loads: full occupancy instead of
     // 32 accumulators per thread
-    klaunch(h->s, h->pdl, cgs_dot_kernel<16, 2, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N / 2, nv, V,
-            h->N, w, h->part, out, addend, raw, sq, h->ticket);
+    if (ew2_ok(h))
+      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 2, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N / 2, nv, V,
+              h->N, w, h->part, out, addend, raw, sq, h->ticket);
+    else
+      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 1, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N, nv, V,
+              h->N, w, h->part, out, addend, raw, sq, h->ticket);
     ++h->nlaunch;
   } else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
 }
 template <int NV, bool DOT>
 void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
                 const double* addend, double* raw, int sq) {
-  constexpr int EW = (NV <= 16 || kCgsWide32) ? 2 : 1;
   constexpr int MINB = 2;
-  klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, EW, DOT, NV, MINB>, kRedBlocks, kRedThreads, h->N / EW, nv, V, h->N, coef, w, h->part, out,
-                                                                    addend, raw, sq, h->ticket);
+  if ((NV <= 16 || kCgsWide32) && ew2_ok(h))
+    klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, 2, DOT, NV, MINB>, kRedBlocks, kRedThreads, h->N / 2, nv, V, h->N, coef, w,
+            h->part, out, addend, raw, sq, h->ticket);
+  else
+    klaunch(h->s, h->pdl, cgs_axpy_kernel<NV, 1, DOT, NV, MINB>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, coef, w,
+            h->part, out, addend, raw, sq, h->ticket);
   ++h->nlaunch;
 }
 template <bool DOT>
@@ -1637,6 +1654,38 @@ void cgs2(msp_handle* h, int nv, double* w) {
   ++h->nlaunch;
 }
 
+// DCGS2 passes of step k (R14, kernels.cuh): w = V[k+1] = A B V[k] on entry; on exit
+// V[k] final, V[k+1] = u (provisional, unnormalised), hcol = the host record (2k+4 values).
+template <int NV>
+void dcgs_update_t(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
+  constexpr bool DOT = NV <= 16;
+  if (ew2_ok(h))
+    klaunch(h->s, h->pdl, dcgs_update_kernel<NV, 2, DOT>, kRedBlocks, kRedThreads, h->N / 2, k, (const double*)h->V,
+            h->N, vk, w, (const double*)h->dh1, st_in, h->part, h->dsum, h->ticket);
+  else
+    klaunch(h->s, h->pdl, dcgs_update_kernel<NV, 1, DOT>, kRedBlocks, kRedThreads, h->N, k, (const double*)h->V,
+            h->N, vk, w, (const double*)h->dh1, st_in, h->part, h->dsum, h->ticket);
+  ++h->nlaunch;
+  if (!DOT) cgs_dot(h, k + 2, h->V, w, h->dsum, nullptr, nullptr, -1);   // V[0..k]^T u and u^T u
+  if (h->comm) h->comm->allreduce_sum(h->s, h->dsum, k + 2);              // distributed: global sums
+}
+void dcgs2(msp_handle* h, int k) {
+  const size_t N = h->N;
+  double* vk = h->V + (size_t)k * N;
+  double* w = h->V + (size_t)(k + 1) * N;
+  const double* st_in = h->dst + (size_t)((k + 1) & 1) * (kMaxV + 2);
+  double* st_out = h->dst + (size_t)(k & 1) * (kMaxV + 2);
+  cgs_dot(h, k + 1, h->V, w, h->dh1, nullptr, nullptr, -1);                // pass 1: a
+  if (h->comm) h->comm->allreduce_sum(h->s, h->dh1, k + 1);
+  if (k <= 4) dcgs_update_t<4>(h, k, vk, w, st_in);                          // pass 2
+  else if (k <= 8) dcgs_update_t<8>(h, k, vk, w, st_in);
+  else if (k <= 16) dcgs_update_t<16>(h, k, vk, w, st_in);
+  else dcgs_update_t<32>(h, k, vk, w, st_in);
+  klaunch(h->s, h->pdl, dcgs_finish_kernel, 1, 32, k, (const double*)h->dh1, st_in, (const double*)h->dsum, st_out,
+          h->hcol);
+  ++h->nlaunch;
+}
+
 // One Arnoldi step j: z = B v_j; w = A z (into V[j+1]); orthogonalise (CGS2 or MGS);
 // hcol[0..j+1] = H(:, j); V[j+1] normalised; hcol copied to pinned host memory.
 void arnoldi_step(msp_handle* h, int j) {
@@ -1647,6 +1696,11 @@ void arnoldi_step(msp_handle* h, int j) {
   exch_cell(h, h->z, h->b, -1);
   launch_spmv(h, 0, h->z, nullptr, w);
   const int nv = j + 1;
+  if (h->prm.orth == 2) {
+    dcgs2(h, j);
+    CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (2 * j + 4), cudaMemcpyDeviceToHost, h->s));
+    return;
+  }
   if (h->prm.orth == 0) {
     cgs2(h, nv, w);
   } else {
@@ -1727,17 +1781,37 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
   double rel = beta / bnorm;
   msp_status status = MSP_OK;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gam(m + 1), y(m);
+  // DCGS2 (R14): unrotated Hessenberg columns and the previous step's h2, nu, rho
+  std::vector<double> Hraw((size_t)(m + 1) * m), h2p;
+  double nup = 1.0, rhop = 1.0;
   if (rel > tol) {
     while (true) {
       klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, h->r, h->hcol, h->V); ++h->nlaunch;   // v_0 = r / beta
       std::fill(gam.begin(), gam.end(), 0.0);
       gam[0] = beta;
+      h2p.clear();
+      nup = 1.0;
+      rhop = 1.0;
       int k = 0;
       for (int j = 0; j < m; ++j) {
         run_step(h, j, m);
         CK(cudaStreamSynchronize(h->s));
         auto Hc = [&](int i) -> double& { return H[(size_t)i * m + j]; };
-        for (int i = 0; i <= j + 1; ++i) Hc(i) = h->hpin[i];
+        if (h->prm.orth == 2) {
+          // column j of the final basis: (nu [c + h2'; rho'] - sum_l h2_l Hraw[:, l]) / rho
+          const double* rec = h->hpin;
+          for (int i = 0; i <= j + 1; ++i) {
+            double v = nup * ((i <= j) ? rec[i] : rec[j + 1]);
+            for (int l = 0; l < j; ++l) v -= h2p[l] * Hraw[(size_t)i * m + l];
+            Hraw[(size_t)i * m + j] = v / rhop;
+            Hc(i) = Hraw[(size_t)i * m + j];
+          }
+          h2p.assign(rec + j + 3, rec + 2 * j + 4);
+          nup = rec[j + 2];
+          rhop = rec[j + 1];
+        } else {
+          for (int i = 0; i <= j + 1; ++i) Hc(i) = h->hpin[i];
+        }
         const double hn = Hc(j + 1);
         ++it;
         for (int i = 0; i < j; ++i) {
@@ -1847,7 +1921,7 @@ void msp_config_default(msp_config* c) {
   c->decoupling = 2;
   c->bilu_order = 1;
   c->stages = 2;
-  c->orth = 0;
+  c->orth = 2;
   c->use_graphs = 1;
   c->use_coop = 0;
   c->smoother = 0;
@@ -1864,7 +1938,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (cfg) c = *cfg;
   if (c.stages != 2 && c.stages != 3) return fail(nullptr, MSP_EINVAL, "msp_setup: stages must be 2 (P,R) or 3 (N,P,R)");
   if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1 ||
-      c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1)
+      c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1 || c.orth < 0 || c.orth > 2)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
   if (c.smoother != 0) c.use_coop = 0;                 // the persistent V-cycle is PGS-MC only
   std::unique_ptr<msp_handle> h(new msp_handle);
@@ -2152,17 +2226,24 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         fn = [&]() { arnoldi_step(h, 15); };
         bytes = 0.0;
         break;
-      case 10:                                   // CGS2 of step j=15 alone
-        fn = [&]() { cgs2(h, 16, h->V + (size_t)16 * N); };
-        // pass A (16+1 vectors) + fused pass B (16 + 2) + pass C (16 + 2) + scale (2)
-        bytes = 55.0 * 8 * (double)N;
+      case 10:                                   // orthogonalisation of step j=15 alone
+        if (h->prm.orth == 2) {
+          fn = [&]() { dcgs2(h, 15); };
+          // pass 1 (16+1 vectors) + pass 2 (15 + 2 read, 2 written)
+          bytes = 36.0 * 8 * (double)N;
+        } else {
+          fn = [&]() { cgs2(h, 16, h->V + (size_t)16 * N); };
+          // pass A (16+1 vectors) + fused pass B (16 + 2) + pass C (16 + 2) + scale (2)
+          bytes = 55.0 * 8 * (double)N;
+        }
         break;
       case 11:
         fn = [&]() { arnoldi_step(h, 25); };
         bytes = 0.0;
         break;
       case 12:
-        fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
+        if (h->prm.orth == 2) fn = [&]() { dcgs2(h, 25); };
+        else fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
         bytes = 0.0;
         break;
       default:
@@ -2205,10 +2286,10 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   msp_config c;
   msp_config_default(&c);
   if (cfg) c = *cfg;
-  if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth != 0 ||
+  if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth == 1 ||
       c.smoother != 0)
     return fail(nullptr, MSP_EINVAL,
-                "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2, PGS-MC");
+                "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC");
   c.use_graphs = 0;                 // collectives (and loopback host barriers) are not captured
   c.use_coop = 0;
   std::unique_ptr<msp_handle> h(new msp_handle);

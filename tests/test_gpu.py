@@ -158,6 +158,23 @@ def test_vcycle_parity(kw):
     assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("nc,dims,orth", [(2, (13, 11, 3), 0), (4, (7, 5, 9), 0), (2, (13, 11, 3), 2),
+                                          (4, (7, 5, 9), 2), (2, (13, 11, 3), 1)])
+def test_solve_odd_vector_length(nc, dims, orth):
+    """N = n*b odd (b = 3, 5 with an odd cell count): the Krylov kernels' 16-byte paths
+    must not drop the last entry or misalign the basis slots."""
+    p = gen.make_config("C2", nx=dims[0], ny=dims[1], nz=dims[2], nc=nc)
+    assert (p["n"] * p["b"]) % 2 == 1
+    s = solver(p, coarsest_max_dof=60, orth=orth)
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=60, orth=orth)
+    ro = O.solve(p["rhs"], tol=1e-8)
+    rg = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-8)
+    assert abs(rg["iters"] - ro["iters"]) <= 1, (rg["iters"], ro["iters"])
+    A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * p["b"],) * 2)
+    xs = rg["x"].cpu().numpy()
+    assert np.linalg.norm(p["rhs"] - A @ xs) / np.linalg.norm(p["rhs"]) <= 1e-8
+
+
 @pytest.mark.parametrize("env,kw", [(dict(MSP_CLUSTER_FROM="2"), dict()),
                                     (dict(MSP_CLUSTER_FROM="1"), dict()),
                                     (dict(MSP_CLUSTER_FROM="1", MSP_CLUSTER_SIZE="8"), dict()),
@@ -241,6 +258,11 @@ def check_solve(p, tol=1e-6, restart=30, **kw):
     ("C1", {}, dict(coarsest_max_dof=50, stages=3)),
     ("C2", dict(nx=25, ny=20, nz=5), dict(coarsest_max_dof=100, stages=3)),
     ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100, stages=3)),
+    ("C1", {}, dict(coarsest_max_dof=50, orth=2)),
+    ("C1", {}, dict(coarsest_max_dof=50, orth=2, use_graphs=0)),
+    ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100, orth=2)),
+    ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100, orth=2)),
+    ("C3", dict(nx=12, ny=44, nz=17), dict(coarsest_max_dof=300, orth=2)),
 ])
 def test_solve_parity(name, gkw, kw):
     check_solve(gen.make_config(name, **gkw), **kw)
@@ -251,6 +273,9 @@ def test_solve_parity_restarts_and_mgs():
     r, o = check_solve(p, restart=5, coarsest_max_dof=100)
     assert r["iters"] > 5                                  # several restart cycles
     check_solve(p, coarsest_max_dof=100, orth=1)
+    r, o = check_solve(p, restart=5, coarsest_max_dof=100, orth=2)
+    r, o = check_solve(p, restart=30, coarsest_max_dof=100, orth=2, tol=1e-10)
+    assert r["iters"] > 17                                  # exercises the k > 16 (unfused) pass 2
 
 
 def test_solve_parity_C2_full():
@@ -346,6 +371,18 @@ def test_full_size_c3_no_smoothers_vs_oracle_golden(sm):
     r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-6)
     ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"oracle_c3_sm{sm}.json")))
     assert ref["smoother"] == sm and ref["gs_chunk"] == 32
+    assert abs(r["iters"] - ref["iters"]) <= 1, (r["iters"], ref["iters"])
+    assert r["final_rel"] <= 1e-6
+    _check_hist(r["hist"], ref["hist"])
+
+
+def test_full_size_c3_dcgs2_vs_oracle_golden():
+    """DCGS2 (orth=2, R14) at full C3 size against the oracle's CGS2 run: the same Arnoldi
+    basis in exact arithmetic -> same iterations, early history to rounding level."""
+    p = gen.make_config("C3")
+    s = solver(p, orth=2)
+    r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-6)
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_c3.json")))
     assert abs(r["iters"] - ref["iters"]) <= 1, (r["iters"], ref["iters"])
     assert r["final_rel"] <= 1e-6
     _check_hist(r["hist"], ref["hist"])

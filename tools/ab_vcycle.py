@@ -23,7 +23,10 @@ for tag, kw in variants:
     if "=" in tag:
         for kv in tag.split(","):
             k, v = kv.split("=")
-            os.environ[k] = v
+            if k.isupper():
+                os.environ[k] = v                      # MSP_* environment switch
+            else:
+                kw[k] = int(v)                         # msp_config field (e.g. orth=2)
     os.environ["MSP_BILU_V1"] = "1" if tag == "bilu_v1" else "0"
     os.environ["MSP_BILU_MODE"] = "0" if tag == "bilu_colors" else "1"
     s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], **kw)

@@ -15,9 +15,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--kernel", default=None, help="time_kernel kind instead of a solve")
+ap.add_argument("--orth", type=int, default=None, help="msp_config.orth (default: library default)")
 a = ap.parse_args()
 p = gen.make_config(a.config)
-s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"])
+s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"],
+              **({} if a.orth is None else dict(orth=a.orth)))
 b = torch.from_numpy(p["rhs"]).cuda()
 x = torch.zeros_like(b)
 r = s.solve(b, x)
