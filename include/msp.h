@@ -107,6 +107,7 @@ typedef struct {
   int32_t level_colors[24];  /* PGS-MC colors per smoothing level */
   int64_t device_bytes;      /* device memory held by the handle */
   int32_t kernels_per_iter;  /* kernel launches of one Arnoldi step */
+  int32_t fused_a8;          /* 1: the a8 residual runs inside the BILU forward kernels (4x4) */
 } msp_stats;
 
 void msp_config_default(msp_config* cfg);

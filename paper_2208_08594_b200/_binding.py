@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("n_coarsest", ctypes.c_int32), ("bilu_colors", ctypes.c_int32),
                 ("level_n", ctypes.c_int32 * 24), ("level_nnz", ctypes.c_int64 * 24),
                 ("level_colors", ctypes.c_int32 * 24), ("device_bytes", ctypes.c_int64),
-                ("kernels_per_iter", ctypes.c_int32)]
+                ("kernels_per_iter", ctypes.c_int32), ("fused_a8", ctypes.c_int32)]
 
 
 _lib.msp_last_error.restype = ctypes.c_char_p
@@ -256,7 +256,8 @@ class MspSolver:
                     solve_seconds=s.solve_seconds, levels=L, n_coarsest=s.n_coarsest,
                     bilu_colors=s.bilu_colors, level_n=list(s.level_n[:L + 1]),
                     level_nnz=list(s.level_nnz[:L + 1]), level_colors=list(s.level_colors[:L]),
-                    device_bytes=s.device_bytes, kernels_per_iter=s.kernels_per_iter)
+                    device_bytes=s.device_bytes, kernels_per_iter=s.kernels_per_iter,
+                    fused_a8=bool(s.fused_a8))
 
 
 def nccl_unique_id() -> bytes:

@@ -800,7 +800,11 @@ __device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const in
 // vectors through register shuffles.  Same arithmetic as bilu_color_kernel, only
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
-template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch>
+// FR (4x4 blocks, forward phases): the a8 residual of the pressure correction is fused
+// in: the cell's start value is r_i = g_i - sum_e Pcol_e wp[ci_e] over its whole row
+// (entry-per-lane, accumulated with the external-L sum before ONE reduce-scatter) instead
+// of a read of r written by a separate a8 launch.
+template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch, bool FR = false>
 __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
@@ -810,10 +814,13 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
                                                          const double* __restrict__ F,
                                                          double* v,
                                                          const double* __restrict__ wp,
-                                                         double* __restrict__ z) {
+                                                         double* __restrict__ z,
+                                                         const double* __restrict__ gf,
+                                                         const double* __restrict__ pcol) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int TM = MAXC * TS;
   static_assert(TM <= 32, "team must fit in a warp");
+  constexpr bool FR4 = FR && B == 4 && FWD;
   constexpr int BB = B * B;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int blk = b_first + gtid / TM;
@@ -871,6 +878,21 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
     double acc = 0.0;
     if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if constexpr (FR4) {                  // fused a8: pressure columns of the whole row
+        if (valid) {
+          const int r1 = ldg(rp + i + 1);
+#pragma unroll 2
+          for (int ee = e0 + q; ee < r1; ee += 4) {
+            const double xc = ldg(wp + ldg(ci + ee));
+            const double2* cp = reinterpret_cast<const double2*>(pcol + (size_t)ee * 4);
+            const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
+            a0 = fma(lo.x, xc, a0);
+            a1 = fma(lo.y, xc, a1);
+            a2 = fma(hi.x, xc, a2);
+            a3 = fma(hi.y, xc, a3);
+          }
+        }
+      }
       int estart = e0;
       if constexpr (PFE > 0) {
 #pragma unroll
@@ -919,7 +941,8 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
         }
       }
     }
-    t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
+    if constexpr (FR4) t = act ? (ldg(gf + (size_t)i * B + q) - acc) : 0.0;
+    else t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
     // intra-block triangle, cells in ascending order
 #pragma unroll
     for (int sidx = 0; sidx < MAXC - 1; ++sidx) {

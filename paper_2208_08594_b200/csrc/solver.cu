@@ -106,7 +106,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, bilu_nopf = 0, pcol_rowwise = 0;
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0;   // fuse_a8: measured slower
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1071,7 +1071,7 @@ void exch_l0(msp_handle* h, double* x, int seg) {
 }
 
 template <int B, int MAXC, bool WF = false>
-void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
+void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, const double* gf = nullptr) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
   const int g = h->bilu_ncolor;
   auto run = [&](int c, int kind) {
@@ -1079,21 +1079,24 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
-    if (B == 4 && h->bilu_nopf) {            // A/B: no PDL-prologue prefetch
-      if (kind == 0)
-        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
-      else if (kind == 1)
-        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
-      else
-        klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF, false>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
-      return;
+    const double* none = nullptr;
+    if constexpr (B == 4 && !WF) {
+      if (gf && kind != 1) {                   // forward phases with the fused a8 residual
+        if (kind == 0)
+          klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
+                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
+        else
+          klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
+                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
+        return;
+      }
     }
     if (kind == 0)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
     else if (kind == 1)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
     else
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
   };
   // distributed: after each color phase, the ghost copies of that color's cells are
   // refreshed (y after the forward phase, x after the backward phase)
@@ -1104,7 +1107,8 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z) {
 }
 
 template <int B>
-void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false) {
+void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
+                   const double* gf = nullptr) {
   if (wfull) {                                         // z = w (full vector) + R r
     if (h->max_blk <= 1) launch_bilu_block<B, 1, true>(h, v, wp, z);
     else if (h->max_blk <= 2) launch_bilu_block<B, 2, true>(h, v, wp, z);
@@ -1112,9 +1116,9 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool w
     return;
   }
   if (!h->bilu_v1 && h->max_blk <= 4) {
-    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z);
-    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z);
-    else launch_bilu_block<B, 4>(h, v, wp, z);
+    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z, gf);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z, gf);
+    else launch_bilu_block<B, 4>(h, v, wp, z, gf);
     return;
   }
   constexpr int TS = (B <= 4) ? 4 : 8;
@@ -1136,9 +1140,10 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool w
   for (int c = g - 2; c >= 0; --c) run(c, 1);
 }
 
-void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false) {
+void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
+                 const double* gf = nullptr) {
   switch (h->b) {
-#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull); break;
+#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull, gf); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -1460,6 +1465,8 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
 }
 
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
+bool a8_fused(const msp_handle* h) { return h->b == 4 && h->fuse_a8 && !h->bilu_v1 && h->max_blk <= 4; }
+
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
   if (h->comm) {
     msp_apply_dist(h, g, z);
@@ -1473,8 +1480,12 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
   launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
   vcycle_any(h, fuse);                                                 // a4-a7: B_P
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
-  launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
-  launch_bilu(h, h->r, h->wp, h->z == z ? z : z);                      // a9: z = Pi_P x_p + R r
+  if (a8_fused(h)) {
+    launch_bilu(h, h->r, h->wp, z, false, g);                          // a8 fused into a9's forward
+  } else {
+    launch_spmv(h, 2, h->wp, g, h->r);                                 // a8: r = g - A Pi_P x_p
+    launch_bilu(h, h->r, h->wp, z);                                    // a9: z = Pi_P x_p + R r
+  }
 }
 
 template <int B, int MAXC>
@@ -1946,7 +1957,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_BILU_NOPF")) h->bilu_nopf = std::atoi(e);
+  if (const char* e = std::getenv("MSP_FUSE_A8")) h->fuse_a8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
@@ -2149,6 +2160,7 @@ msp_status msp_get_stats(const msp_handle* h, msp_stats* out) {
   }
   out->device_bytes = h->bytes;
   out->kernels_per_iter = h->kernels_per_step;
+  out->fused_a8 = (!h->comm && a8_fused(h)) ? 1 : 0;
   return MSP_OK;
 }
 
@@ -2198,9 +2210,15 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         fn = [&]() { launch_spmv(h, 2, h->wp, h->bin, h->u); };
         bytes = nnzb * (8 * b + 4) + 4 * (n + 1) + 8 * n + 2 * 8 * (double)N;
         break;
-      case 3:
-        fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
-        bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
+      case 3:                                    // a9 as the solve runs it (a8 fused in for 4x4)
+        if (a8_fused(h)) {
+          fn = [&]() { launch_bilu(h, h->r, h->wp, h->z, false, h->bin); };
+          // + the pressure-column stream and the wp gather of the fused a8 (g replaces r)
+          bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N + nnzb * 8 * b + 8.0 * n;
+        } else {
+          fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
+          bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
+        }
         break;
       case 4:                                    // CGS2 pass A over 16 basis vectors
         fn = [&]() { cgs_dot(h, 16, h->V, h->u, h->dh1, nullptr, nullptr, -1); };

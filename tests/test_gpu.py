@@ -206,6 +206,24 @@ def test_cluster_vcycle_bit_identical(env, kw, monkeypatch):
     assert torch.equal(r0["x"], r1["x"])
 
 
+def test_msp_apply_with_fused_a8_parity(monkeypatch):
+    """Option MSP_FUSE_A8=1 (a8 inside the BILU forward kernels, 4x4 blocks): MSP apply and
+    solve vs the oracle."""
+    monkeypatch.setenv("MSP_FUSE_A8", "1")
+    p = gen.make_config("C2", nx=25, ny=20, nz=5)
+    s = solver(p, coarsest_max_dof=100)
+    assert s.stats()["fused_a8"]
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=100)
+    g = gen.random_vector(p["n"] * p["b"], 9)
+    out = torch.zeros(p["n"] * p["b"], dtype=torch.float64, device="cuda")
+    s.apply(torch.from_numpy(g).cuda(), out)
+    ref = O.apply(g)
+    assert np.linalg.norm(out.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
+    ro = O.solve(p["rhs"], tol=1e-8)
+    rg = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-8)
+    assert abs(rg["iters"] - ro["iters"]) <= 1
+
+
 @pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0), dict(decoupling=1), dict(stages=3)])
 def test_bilu_and_msp_apply_parity(kw):
     p = gen.make_config("C2", nx=25, ny=20, nz=5)

@@ -41,8 +41,8 @@ out = {}
 for key, pred in pieces.items():
     b = sum(byt[n] for n in byt if pred(n))
     c = sum(cnt[n] for n in cnt if pred(n))
-    if key == "a9_bilu_apply":            # one BILU apply per a8 launch (one per MSP apply)
-        c = sum(cnt[n] for n in cnt if pieces["a8_pcol_residual"](n))
+    if key == "a9_bilu_apply":            # one BILU apply per MSP apply (one a3 launch each)
+        c = sum(cnt[n] for n in cnt if n.startswith("restrict_pressure_kernel"))
     out[key] = b / c if c else None          # DRAM bytes per launch (per application)
 out["_source"] = src
 json.dump(out, open(dst_json, "w"), indent=1)
