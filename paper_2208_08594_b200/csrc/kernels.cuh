@@ -597,6 +597,57 @@ __global__ void __launch_bounds__(256) gemv4_kernel(int n, int ld, const double*
   if (lane == 0) x[row] = acc;
 }
 
+// coarsest GEMV, 8 independent 16-byte loads in flight per lane; the first 8 of the
+// (immutable) inverse are issued before the PDL wait, overlapping the previous kernel
+template <int U>
+__global__ void __launch_bounds__(256) gemv8_kernel(int n, int ld, const double* __restrict__ Ainv,
+                                                    const double* __restrict__ b, double* __restrict__ x) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const bool live = row < n;
+  const double2* a = reinterpret_cast<const double2*>(Ainv + (size_t)(live ? row : 0) * ld);
+  const double2* bb = reinterpret_cast<const double2*>(b);
+  const int n2 = n >> 1;                       // pairs
+  double2 pa[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = lane + 32 * u;
+    pa[u] = (live && j < n2) ? ldstream2(a + j) : make_double2(0.0, 0.0);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  for (int j0 = 0; j0 < n2; j0 += 32 * U) {
+    if (j0 > 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + lane + 32 * u;
+        pa[u] = (j < n2) ? ldstream2(a + j) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + lane + 32 * u;
+      if (j < n2) {
+        const double2 bv = __ldg(bb + j);
+        acc[u] = fma(pa[u].x, bv.x, fma(pa[u].y, bv.y, acc[u]));
+      }
+    }
+  }
+#pragma unroll
+  for (int w = U / 2; w; w >>= 1)
+#pragma unroll
+    for (int u = 0; u < w; ++u) acc[u] += acc[u + w];
+  double s = acc[0];
+  if ((n & 1) && lane == 0) s = fma(ldg(Ainv + (size_t)row * ld + n - 1), ldg(b + n - 1), s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[row] = s;
+}
+
 // a5 part 1: residual r = b - A x over all rows of the level (SELL-32 + diagonal).
 __global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
                                                             const int* __restrict__ slice_row,

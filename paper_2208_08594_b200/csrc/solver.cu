@@ -106,7 +106,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0;   // fuse_a8: measured slower
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1;   // fuse_a8: measured slower
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1263,7 +1263,8 @@ void coarsest_solve(msp_handle* h) {
   if (h->coarse_diag)
     klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
   else
-    klaunch(h->s, h->pdl, gemv4_kernel, nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+    klaunch(h->s, h->pdl, h->gemv8 == 16 ? gemv8_kernel<16> : h->gemv8 ? gemv8_kernel<8> : gemv4_kernel,
+            nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
 }
 
 template <int LPR, bool WR, bool RES>
@@ -1958,6 +1959,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_FUSE_A8")) h->fuse_a8 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_GEMV8")) h->gemv8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);

@@ -33,7 +33,7 @@ for tag, kw in variants:
     b = torch.from_numpy(p["rhs"]).cuda()
     r = s.solve(b)
     res = {}
-    for k in ("arnoldi_step15", "arnoldi_step25", "cgs2_step25", "msp_apply", "vcycle", "bilu", "cgs2_step15", "a2_bsr_spmv", "a8_pcol_residual", "a4_pgs_sweep_l0"):
+    for k in ("arnoldi_step15", "arnoldi_step25", "cgs2_step25", "msp_apply", "vcycle", "bilu", "cgs2_step15", "a2_bsr_spmv", "a8_pcol_residual", "a4_pgs_sweep_l0", "a6_coarse_gemv"):
         res[k + "_warm"] = s.time_kernel(k, reps=20, flush=False)[0]
         res[k + "_cold"] = s.time_kernel(k, reps=20, flush=True)[0]
     t0 = s.stats()["solve_seconds"]
