@@ -264,23 +264,32 @@ __global__ void restrict_pressure_kernel(int n, const double* __restrict__ W,
                                          const double* __restrict__ g, const int* __restrict__ src,
                                          double* __restrict__ rp, double* __restrict__ x0,
                                          const double* __restrict__ diag0, int c1_end) {
-  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int c = ldg(src + i);
+  const bool live = i < n;
+  // PDL prologue: the cell map, its weight row and the level-0 diagonal are immutable
+  const int c = live ? ldg(src + i) : 0;
+  double wk[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) wk[k] = live ? ldg(W + (size_t)c * B + k) : 0.0;
+  const double d = (live && x0 && i < c1_end) ? ldg(diag0 + i) : 1.0;
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < B; ++k) s = fma(ldg(W + (size_t)c * B + k), ldg(g + (size_t)c * B + k), s);
+  for (int k = 0; k < B; ++k) s = fma(wk[k], ldg(g + (size_t)c * B + k), s);
   rp[i] = s;
-  if (x0) x0[i] = (i < c1_end) ? s / ldg(diag0 + i) : 0.0;
+  if (x0) x0[i] = (i < c1_end) ? s / d : 0.0;
 }
 
 // gather of the level-0 correction into cell order: wp[c] = x0[dst[c]]
 __global__ void gather_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                               double* __restrict__ out) {
-  PDL_ENTRY();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n) out[c] = ldg(src + ldg(idx + c));
+  const int k = (c < n) ? ldg(idx + c) : 0;      // immutable map: before the PDL wait
+  pdl_wait();
+  pdl_trigger();
+  if (c < n) out[c] = ldg(src + k);
 }
 
 // ---------------------------------------------------------------------------
@@ -678,21 +687,34 @@ __global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
 __global__ void restrict_kernel(int nc, const int* __restrict__ pp, const int* __restrict__ pi,
                                 const double* __restrict__ r, double* __restrict__ bc,
                                 double* __restrict__ xc, const double* __restrict__ dc, int c1_end) {
-  PDL_ENTRY();
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= nc) return;
+  const bool live = I < nc;
+  // PDL prologue: member lists (<= 4 members for 2-pass NPAIR) and diagonal are immutable
+  const int e0 = live ? ldg(pp + I) : 0, e1 = live ? ldg(pp + I + 1) : 0;
+  int m[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) m[k] = (e0 + k < e1) ? ldg(pi + e0 + k) : -1;
+  const double d = (live && xc && I < c1_end) ? ldg(dc + I) : 1.0;
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
   double s = 0.0;
-  for (int e = ldg(pp + I); e < ldg(pp + I + 1); ++e) s += ldg(r + ldg(pi + e));
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (m[k] >= 0) s += ldg(r + m[k]);
+  for (int e = e0 + 4; e < e1; ++e) s += ldg(r + ldg(pi + e));
   bc[I] = s;
-  if (xc) xc[I] = (I < c1_end) ? s / ldg(dc + I) : 0.0;
+  if (xc) xc[I] = (I < c1_end) ? s / d : 0.0;
 }
 
 // a7: prolongation and correction x_i += e[agg(i)].
 __global__ void prolong_kernel(int n, const int* __restrict__ agg, const double* __restrict__ e,
                                double* __restrict__ x) {
-  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] += ldg(e + ldg(agg + i));
+  const int a = (i < n) ? ldg(agg + i) : 0;      // immutable map: before the PDL wait
+  pdl_wait();
+  pdl_trigger();
+  if (i < n) x[i] += ldg(e + a);
 }
 
 // a6 (K7): coarsest solve as a dense-inverse GEMV x = Ainv b (row-major).
