@@ -3,11 +3,11 @@
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?
-$NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv \
+$NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"mspk|sell_|bilu_|bsr_|cgs_|dcgs_|pcol_|gemv|restrict|prolong|gather|scale" -c 600 --csv --log-file gpurun_out/launches_bench.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 echo bench-launches rc $?
 python tools/profile_solve.py > gpurun_out/prof_plain.log 2>&1 && \
 $NCU --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size --clock-control none --csv --log-file gpurun_out/launches_solve.csv python tools/profile_solve.py > gpurun_out/ncu_l.log 2>&1
 echo launches rc $?
-$NCU --profile-from-start off --set full --clock-control none --import-source on -k regex:"bsr_spmv4c|pcol_resid4|bilu_block|cgs_dot|cgs_axpy|sell_row_kernel|gemv4" -c 12 -o gpurun_out/prof_full_r01 python tools/profile_solve.py --kernel arnoldi_step15 > gpurun_out/ncu_f.log 2>&1
+$NCU --profile-from-start off --set full --clock-control none --import-source on -k regex:"bsr_spmv4c|pcol_resid4|bilu_block|cgs_dot|dcgs_update|sell_row_kernel|gemv8" -c 14 -o gpurun_out/prof_full_r01 python tools/profile_solve.py --kernel arnoldi_step15 > gpurun_out/ncu_f.log 2>&1
 echo full rc $?

@@ -34,7 +34,7 @@ with open(dst_txt, "w") as f:
                 f"{byt[n] / t if t else 0:9.1f} {byt[n] / cnt[n] / 1e6:12.2f}  {n}\n")
 pieces = {
     "a2_bsr_spmv": lambda n: n.startswith("bsr_spmv4c_kernel<0>") or n.startswith("bsr_spmv_kernel<4, 0>"),
-    "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>") or n.startswith("pcol_resid4_kernel"),
+    "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>") or "pcol_resid4_kernel" in n,
     "a9_bilu_apply": lambda n: n.startswith("bilu_block_kernel"),
 }
 out = {}
