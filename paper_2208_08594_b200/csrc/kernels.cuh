@@ -1215,6 +1215,18 @@ __global__ void set_pressure_kernel(int n, int B, const double* __restrict__ wp,
   if (i < n) w[(size_t)i * B] = ldg(wp + i);
 }
 
+// setup upload: row-major b x b blocks -> column-major (out[e][c*B + r] = in[e][r*B + c])
+template <int B>
+__global__ void transpose_blocks_kernel(int64_t nnzb, const double* __restrict__ in, double* __restrict__ out) {
+  constexpr int BB = B * B;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnzb * BB) return;
+  const int64_t e = t / BB;
+  const int k = (int)(t - e * BB);
+  const int c = k / B, r = k - c * B;
+  out[t] = ldg(in + (size_t)e * BB + r * B + c);
+}
+
 // ASMSP reuse: refresh A in the internal layout from the caller's
 // natural-order row-major values: A_cm[e] = transpose(A_nat[src[e]]), Pcol[e] = column 0.
 template <int B>

@@ -273,14 +273,6 @@ msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err
 }
 
 // row-major b x b blocks -> column-major
-void transpose_blocks(const double* src, double* dst, size_t nblocks, int b) {
-  const int bb = b * b;
-#pragma omp parallel for schedule(static)
-  for (size_t e = 0; e < nblocks; ++e)
-    for (int r = 0; r < b; ++r)
-      for (int c = 0; c < b; ++c) dst[e * bb + c * b + r] = src[e * bb + r * b + c];
-}
-
 // Build a SELL-32 device level from CSR rows that are already in their final (color-
 // major) order; color[i] non-decreasing.  Columns may reference ghost rows >= n (their
 // x values are received by halo exchanges); x is sized n_total = n + ghosts.
@@ -522,18 +514,28 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->dg = h->upload(dg);
   h->d_order = h->upload(S.order);
   {
-    std::vector<double> tmp(F.size()), Ap(F.size());
-    transpose_blocks(F.data(), tmp.data(), ci.size(), b);
-    h->Fval = h->upload(tmp);
-#pragma omp parallel for schedule(static)
-    for (size_t e = 0; e < src.size(); ++e)
-      std::memcpy(&Ap[e * bb], &A.v[(size_t)src[e] * bb], sizeof(double) * bb);
-    transpose_blocks(Ap.data(), tmp.data(), ci.size(), b);
-    h->Aval = h->upload(tmp);
-    std::vector<double> pc(ci.size() * b);
-    for (size_t e = 0; e < ci.size(); ++e)
-      for (int q = 0; q < b; ++q) pc[e * b + q] = Ap[e * bb + q * b];
-    h->Pcol = h->upload(pc);
+    // raw row-major values through the ASMSP staging buffer, laid out on the device:
+    // F (internal order) -> column-major blocks; A (caller's natural order) -> permuted
+    // column-major blocks + pressure columns (the msp_update refresh kernel)
+    const size_t nv = ci.size() * (size_t)bb;
+    h->stage = h->dalloc<double>(std::max(nv, A.v.size()));
+    h->Fval = h->dalloc<double>(nv);
+    h->Aval = h->dalloc<double>(nv);
+    h->Pcol = h->dalloc<double>(ci.size() * (size_t)b);
+    CK(cudaMemcpyAsync(h->stage, F.data(), sizeof(double) * nv, cudaMemcpyHostToDevice, h->s));
+    switch (b) {
+#define CASE(BV) case BV: klaunch(h->s, false, transpose_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), \
+                                  (const double*)h->stage, h->Fval); break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    }
+    CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+    switch (b) {
+#define CASE(BV) case BV: klaunch(h->s, false, refresh_values_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), \
+                                  (const int*)h->d_src, (const double*)h->stage, h->Aval, h->Pcol); break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    }
     CK(cudaStreamSynchronize(h->s));
   }
   T.mark("A/F/Pcol transpose+upload");
@@ -1535,12 +1537,6 @@ template <int NV>
 void multidot_t(msp_handle* h, int nv, const double* V, const double* w) {
   klaunch(h->s, h->pdl, multidot_kernel<NV>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, w, h->part); ++h->nlaunch;
 }
-void multidot(msp_handle* h, int nv, const double* V, const double* w) {
-  if (nv <= 4) multidot_t<4>(h, nv, V, w);
-  else if (nv <= 8) multidot_t<8>(h, nv, V, w);
-  else if (nv <= 16) multidot_t<16>(h, nv, V, w);
-  else multidot_t<32>(h, nv, V, w);
-}
 template <int NV>
 void maxpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
   klaunch(h->s, h->pdl, multiaxpy_kernel<NV>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, coef, w, from_zero, part, 0); ++h->nlaunch;
@@ -1551,15 +1547,6 @@ void maxpy(msp_handle* h, int nv, const double* V, const double* coef, double* w
   else if (nv <= 16) maxpy_t<16>(h, nv, V, coef, w, from_zero, part);
   else maxpy_t<32>(h, nv, V, coef, w, from_zero, part);
 }
-void reduce(msp_handle* h, int nv, double* out, const double* addend, double* raw, int sqrt_index) {
-  // raw (optional) receives the plain sums, out = addend + sums
-  if (raw) {
-    klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, nv, h->part, raw, nullptr, sqrt_index);
-    ++h->nlaunch;
-  }
-  klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, nv, h->part, out, addend, sqrt_index); ++h->nlaunch;
-}
-
 void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
              double* raw, int sq);
 
