@@ -158,6 +158,11 @@ msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, i
 msp_status msp_vcycle(msp_handle* h, const double* r, double* x);
 /* R r: BILU(0) forward/backward substitution (natural order, device). */
 msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x);
+/* BILU(0) factors held by the handle (R5), for parity tests: F_out (HOST, nnzb*b*b doubles,
+ * caller-allocated) receives row-major blocks in the caller's natural entry order: the L
+ * and U blocks of the factorization, and D~_i^-1 in the diagonal slots.  Single-GPU
+ * handles only (MSP_EINVAL otherwise). */
+msp_status msp_bilu_factors(msp_handle* h, double* F_out);
 /* Times `reps` launches of one hot-path piece on the handle's stream with CUDA events,
  * flushing L2 (a 256 MB device write) before each launch.  Returns the mean device
  * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory

@@ -61,7 +61,7 @@ class Stats(ctypes.Structure):
 _lib.msp_last_error.restype = ctypes.c_char_p
 _lib.msp_last_error.argtypes = [ctypes.c_void_p]
 for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats", "msp_spmv",
-           "msp_pgs_sweep", "msp_vcycle", "msp_bilu_apply", "msp_get_order", "msp_host_setup_run",
+           "msp_pgs_sweep", "msp_vcycle", "msp_bilu_apply", "msp_bilu_factors", "msp_get_order", "msp_host_setup_run",
            "msp_host_setup_info", "msp_host_setup_level_dims", "msp_host_setup_level_csr",
            "msp_host_setup_level_colors", "msp_host_setup_level_agg", "msp_host_setup_weights",
            "msp_host_setup_order", "msp_partition_owner", "msp_nccl_unique_id", "msp_setup_dist",
@@ -139,6 +139,7 @@ class MspSolver:
     def __init__(self, row_ptr, col, val, nc, stream=None, torch_allocator=True, **cfg):
         self.n = len(row_ptr) - 1
         self.b = int(val.shape[-1])
+        self.nnzb = len(col)
         self.nc = nc
         self.N = self.n * self.b
         self._keep_alloc = None
@@ -227,6 +228,12 @@ class MspSolver:
     def bilu_apply(self, r, x):
         self._check(_lib.msp_bilu_apply(self._h, _ptr(r), _ptr(x)))
         return x
+
+    def bilu_factors(self):
+        """(nnzb, b, b) BILU(0) factors, natural entry order; diagonal slots hold D~^-1."""
+        F = np.zeros((self.nnzb, self.b, self.b))
+        self._check(_lib.msp_bilu_factors(self._h, _ptr(F)))
+        return F
 
     def order(self):
         o = np.zeros(self.n, dtype=np.int32)

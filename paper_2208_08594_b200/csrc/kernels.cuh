@@ -1215,6 +1215,97 @@ __global__ void set_pressure_kernel(int n, int B, const double* __restrict__ wp,
   if (i < n) w[(size_t)i * B] = ldg(wp + i);
 }
 
+// ---------------------------------------------------------------------------
+// SETUP on the GPU (NEXT-2): BILU(0) factorization (R5) of one ABMC block color, one
+// thread per aggregate block (its cells in order), on row-major blocks in the internal
+// order: for every L entry (i,k): A_ik <- A_ik D~_k^-1, then A_ij -= A_ik A_kj over the
+// U entries (k,j) of row k that lie in row i's pattern; finally D~_i^-1 replaces the
+// diagonal block (Gauss-Jordan, partial pivoting).  Exactly the host/oracle operation
+// order with explicitly rounded multiplies and adds (no FMA contraction), so the
+// factors are bit-identical to the host factorization (tests/test_gpu.py).
+// ---------------------------------------------------------------------------
+template <int B>
+__device__ bool gj_invert(double* D) {           // in place, row-major B x B
+  double a[B][B], r[B][B];
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < B; ++j) { a[i][j] = D[i * B + j]; r[i][j] = (i == j) ? 1.0 : 0.0; }
+  for (int k = 0; k < B; ++k) {
+    int p = k;
+    for (int i = k + 1; i < B; ++i) if (fabs(a[i][k]) > fabs(a[p][k])) p = i;
+    if (a[p][k] == 0.0) return false;
+    if (p != k)
+      for (int j = 0; j < B; ++j) {
+        const double t1 = a[k][j]; a[k][j] = a[p][j]; a[p][j] = t1;
+        const double t2 = r[k][j]; r[k][j] = r[p][j]; r[p][j] = t2;
+      }
+    const double piv = a[k][k];                   // row divided by the pivot (IEEE division)
+    for (int j = 0; j < B; ++j) { a[k][j] = __ddiv_rn(a[k][j], piv); r[k][j] = __ddiv_rn(r[k][j], piv); }
+    for (int i = 0; i < B; ++i) {
+      if (i == k) continue;
+      const double f = a[i][k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < B; ++j) {
+        a[i][j] = __dsub_rn(a[i][j], __dmul_rn(f, a[k][j]));
+        r[i][j] = __dsub_rn(r[i][j], __dmul_rn(f, r[k][j]));
+      }
+    }
+  }
+  for (int i = 0; i < B; ++i) for (int j = 0; j < B; ++j) D[i * B + j] = r[i][j];
+  return true;
+}
+
+template <int B>
+__global__ void bilu_factor_kernel(int b_first, int b_end, const int* __restrict__ blk_ptr,
+                                   const int* __restrict__ rp, const int* __restrict__ ci,
+                                   const int* __restrict__ dg, double* F, int* bad) {
+  constexpr int BB = B * B;
+  const int k = b_first + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= b_end) return;
+  double T[BB];
+  for (int i = blk_ptr[k]; i < blk_ptr[k + 1]; ++i) {
+    const int r0 = rp[i], r1 = rp[i + 1];
+    for (int e = r0; e < dg[i]; ++e) {
+      const int kk = ci[e];
+      double* Lik = F + (size_t)e * BB;
+      const double* Dk = F + (size_t)dg[kk] * BB;        // holds D~_k^-1
+      for (int r = 0; r < B; ++r)
+        for (int c = 0; c < B; ++c) {
+          double sum = 0.0;
+          for (int t = 0; t < B; ++t) sum = __dadd_rn(sum, __dmul_rn(Lik[r * B + t], Dk[t * B + c]));
+          T[r * B + c] = sum;
+        }
+      for (int t = 0; t < BB; ++t) Lik[t] = T[t];
+      int m = r0;                                         // row i's entries, ascending columns
+      for (int f = dg[kk] + 1; f < rp[kk + 1]; ++f) {
+        const int cj = ci[f];
+        while (m < r1 && ci[m] < cj) ++m;
+        if (m >= r1) break;
+        if (ci[m] != cj) continue;
+        const double* Ukj = F + (size_t)f * BB;
+        double* Aij = F + (size_t)m * BB;
+        for (int r = 0; r < B; ++r)
+          for (int c = 0; c < B; ++c) {
+            double sum = 0.0;
+            for (int t = 0; t < B; ++t) sum = __dadd_rn(sum, __dmul_rn(Lik[r * B + t], Ukj[t * B + c]));
+            Aij[r * B + c] = __dsub_rn(Aij[r * B + c], sum);
+          }
+      }
+    }
+    if (!gj_invert<B>(F + (size_t)dg[i] * BB)) atomicMax(bad, i);
+  }
+}
+
+// internal-order row-major blocks from the caller's natural order: out[e] = in[src[e]]
+template <int B>
+__global__ void gather_blocks_kernel(int64_t nnzb, const int* __restrict__ src, const double* __restrict__ in,
+                                     double* __restrict__ out) {
+  constexpr int BB = B * B;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnzb * BB) return;
+  const int64_t e = t / BB;
+  out[t] = ldg(in + (size_t)ldg(src + e) * BB + (t - e * BB));
+}
+
 // setup upload: row-major b x b blocks -> column-major (out[e][c*B + r] = in[e][r*B + c])
 template <int B>
 __global__ void transpose_blocks_kernel(int64_t nnzb, const double* __restrict__ in, double* __restrict__ out) {

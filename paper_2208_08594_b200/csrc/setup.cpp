@@ -596,8 +596,8 @@ bool invert_block(int b, const double* D, double* Dinv) {
     for (int i = k + 1; i < b; ++i) if (std::fabs(a[i][k]) > std::fabs(a[p][k])) p = i;
     if (a[p][k] == 0.0) return false;
     if (p != k) for (int j = 0; j < b; ++j) { std::swap(a[k][j], a[p][j]); std::swap(r[k][j], r[p][j]); }
-    const double inv = 1.0 / a[k][k];
-    for (int j = 0; j < b; ++j) { a[k][j] *= inv; r[k][j] *= inv; }
+    const double piv = a[k][k];                 // row divided by the pivot (R5)
+    for (int j = 0; j < b; ++j) { a[k][j] /= piv; r[k][j] /= piv; }
     for (int i = 0; i < b; ++i) {
       if (i == k) continue;
       const double f = a[i][k];

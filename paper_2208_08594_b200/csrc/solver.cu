@@ -433,9 +433,13 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   std::vector<int32_t> rp, ci, dg, src;
   std::vector<double> F;
   T.mark("host setup S1-S4");
-  rc = msp::bilu_factor_permuted(S, A, rp, ci, dg, src, F, err);
+  // BILU(0): on the GPU after the upload (single GPU), on the host for the distributed
+  // setup (every rank factorizes the global matrix) or when MSP_HOST_BILU=1
+  const bool gpu_bilu = !h->comm && !(std::getenv("MSP_HOST_BILU") && std::atoi(std::getenv("MSP_HOST_BILU")));
+  rc = gpu_bilu ? msp::permuted_pattern(S, A, rp, ci, dg, src, err)
+                : msp::bilu_factor_permuted(S, A, rp, ci, dg, src, F, err);
   if (rc) throw std::pair<int, std::string>(rc == 1 ? MSP_EINVAL : MSP_ESINGULAR, err);
-  T.mark("BILU factorization");
+  T.mark(gpu_bilu ? "BILU pattern (host)" : "BILU factorization (host)");
 
   h->free_all();
   const int32_t n = A.n;
@@ -515,28 +519,51 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->d_order = h->upload(S.order);
   {
     // raw row-major values through the ASMSP staging buffer, laid out on the device:
-    // F (internal order) -> column-major blocks; A (caller's natural order) -> permuted
-    // column-major blocks + pressure columns (the msp_update refresh kernel)
+    // A (caller's natural order) -> permuted column-major blocks + pressure columns (the
+    // msp_update refresh kernel); F = BILU factors, computed on the GPU per block color
+    // from the permuted row-major A (or uploaded from the host factorization), then
+    // transposed to column-major
     const size_t nv = ci.size() * (size_t)bb;
     h->stage = h->dalloc<double>(std::max(nv, A.v.size()));
     h->Fval = h->dalloc<double>(nv);
     h->Aval = h->dalloc<double>(nv);
     h->Pcol = h->dalloc<double>(ci.size() * (size_t)b);
-    CK(cudaMemcpyAsync(h->stage, F.data(), sizeof(double) * nv, cudaMemcpyHostToDevice, h->s));
-    switch (b) {
-#define CASE(BV) case BV: klaunch(h->s, false, transpose_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), \
-                                  (const double*)h->stage, h->Fval); break;
-      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-#undef CASE
-    }
     CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+    int* dbad = nullptr;
+    if (gpu_bilu) {
+      dbad = h->dalloc<int>(1);
+      CK(cudaMemsetAsync(dbad, 0xff, sizeof(int), h->s));               // -1
+    }
     switch (b) {
-#define CASE(BV) case BV: klaunch(h->s, false, refresh_values_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), \
-                                  (const int*)h->d_src, (const double*)h->stage, h->Aval, h->Pcol); break;
+#define CASE(BV) case BV: \
+      klaunch(h->s, false, refresh_values_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), (const int*)h->d_src, \
+              (const double*)h->stage, h->Aval, h->Pcol); \
+      if (gpu_bilu) { \
+        klaunch(h->s, false, gather_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), (const int*)h->d_src, \
+                (const double*)h->stage, h->Fval); \
+        const int32_t* bp = h->upload(S.blk_ptr); \
+        for (int col = 0; col + 1 < (int)S.color_blk_ptr.size(); ++col) { \
+          const int k0 = S.color_blk_ptr[col], k1 = S.color_blk_ptr[col + 1]; \
+          if (k1 > k0) klaunch(h->s, false, bilu_factor_kernel<BV>, nblk(k1 - k0, 64), 64, k0, k1, bp, \
+                               (const int*)h->rp, (const int*)h->ci, (const int*)h->dg, h->Fval, dbad); \
+        } \
+      } else { \
+        CK(cudaMemcpyAsync(h->Fval, F.data(), sizeof(double) * nv, cudaMemcpyHostToDevice, h->s)); \
+      } \
+      klaunch(h->s, false, transpose_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)ci.size(), \
+              (const double*)h->Fval, h->stage); \
+      std::swap(h->Fval, h->stage); \
+      break;
       CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     }
     CK(cudaStreamSynchronize(h->s));
+    if (gpu_bilu) {
+      int bad = -1;
+      CK(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
+      if (bad >= 0)
+        throw std::pair<int, std::string>(MSP_ESINGULAR, "BILU: singular pivot block at cell " + std::to_string(S.order[bad]));
+    }
   }
   T.mark("A/F/Pcol transpose+upload");
   if (h->prm.stages == 3) {
@@ -2100,6 +2127,23 @@ msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, i
     pgs_sweep(h, L, ascending != 0, false);
     klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, L.x, x, 0); ++h->nlaunch;
     CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_bilu_factors(msp_handle* h, double* F_out) {
+  if (!h || !F_out) return fail(h, MSP_EINVAL, "msp_bilu_factors: NULL argument");
+  if (h->comm) return fail(h, MSP_EINVAL, "msp_bilu_factors: single-GPU handles only");
+  return guarded(h, [&]() -> msp_status {
+    const int b = h->b, bb = b * b;
+    std::vector<double> cm((size_t)h->nnzb * bb);
+    CK(cudaStreamSynchronize(h->s));
+    CK(cudaMemcpy(cm.data(), h->Fval, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < h->nnzb; ++e) {
+      double* dst = F_out + (size_t)h->src_entry[e] * bb;
+      for (int r = 0; r < b; ++r)
+        for (int c = 0; c < b; ++c) dst[r * b + c] = cm[(size_t)e * bb + c * b + r];
+    }
     return MSP_OK;
   });
 }

@@ -206,6 +206,30 @@ def test_cluster_vcycle_bit_identical(env, kw, monkeypatch):
     assert torch.equal(r0["x"], r1["x"])
 
 
+@pytest.mark.parametrize("name,gkw,kw", [("C2", dict(nx=25, ny=20, nz=5), dict()),
+                                         ("C2", dict(nx=12, ny=10, nz=4, nc=6), dict()),
+                                         ("C2", dict(nx=13, ny=11, nz=3, nc=2), dict(bilu_order=0))])
+def test_gpu_bilu_factorization_bit_exact(name, gkw, kw, monkeypatch):
+    """NEXT-2: the BILU(0) factors computed on the GPU per block color are bit-identical to
+    the oracle's factorization (L/U blocks) and inverted pivot blocks D~^-1 (R5), and to
+    the product's host factorization (MSP_HOST_BILU=1)."""
+    p = gen.make_config(name, **gkw)
+    s = solver(p, coarsest_max_dof=100, **kw)
+    F = s.bilu_factors()
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=100, **kw)
+    Fo, Do = O.bilu_factors()
+    rp, col = p["row_ptr"], p["col"]
+    diag = np.zeros(len(col), bool)
+    for i in range(p["n"]):
+        for e in range(rp[i], rp[i + 1]):
+            if col[e] == i:
+                diag[e] = True
+                assert np.array_equal(F[e], Do[i]), i
+    assert np.array_equal(F[~diag], Fo[~diag])
+    monkeypatch.setenv("MSP_HOST_BILU", "1")
+    assert np.array_equal(solver(p, coarsest_max_dof=100, **kw).bilu_factors(), F)
+
+
 def test_msp_apply_with_fused_a8_parity(monkeypatch):
     """Option MSP_FUSE_A8=1 (a8 inside the BILU forward kernels, 4x4 blocks): MSP apply and
     solve vs the oracle."""
