@@ -9,5 +9,4 @@ echo bench-launches rc $?
 python tools/profile_solve.py > gpurun_out/prof_plain.log 2>&1 && \
 $NCU --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size --clock-control none --csv --log-file gpurun_out/launches_solve.csv python tools/profile_solve.py > gpurun_out/ncu_l.log 2>&1
 echo launches rc $?
-$NCU --profile-from-start off --set full --clock-control none --import-source on -k regex:"bsr_spmv4c|pcol_resid4|bilu_block|cgs_dot|dcgs_update|sell_row_kernel|gemv8" -c 14 -o gpurun_out/prof_full_r01 python tools/profile_solve.py --kernel arnoldi_step15 > gpurun_out/ncu_f.log 2>&1
-echo full rc $?
+# --set full captures: tools/gpu_full_caps.sh (separate calls: reports are large)
