@@ -525,6 +525,48 @@ __global__ void __launch_bounds__(512) sell_row_kernel(int s_first, int s_end,
   }
 }
 
+// Level-0 form of sell_row_kernel<1, ...> on a uniform-width SELL layout (every slice
+// W <= 8 wide): row = row_first + 32 (s - s_first) + l and entry k at s*32*W + 32 k + l are
+// arithmetic, so the PDL prologue loads all of the row's matrix entries and its diagonal
+// with no slice-metadata round trip.  Same per-row arithmetic and summation order.
+template <bool WRITE_R, bool MODE_RES>
+__global__ void __launch_bounds__(128) sell_row_uniform_kernel(int s_first, int s_end, int row_first, int row_end,
+                                                               int W, const int* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ x, double* __restrict__ r) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = s_first + t / kSell;
+  if (s >= s_end) return;
+  const int l = t % kSell;
+  const int row = row_first + (s - s_first) * kSell + l;
+  const size_t o0 = (size_t)s * kSell * W + l;
+  int pc[8];
+  double pv[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    pc[m] = (m < W) ? ldg(col + o0 + (size_t)m * kSell) : row;
+    pv[m] = (m < W) ? ldg(val + o0 + (size_t)m * kSell) : 0.0;
+  }
+  const bool valid = row < row_end;
+  const double d = valid ? ldg(diag + row) : 1.0;
+  pdl_wait();
+  pdl_trigger();
+  if (!valid) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) acc = fma(pv[m], x[pc[m]], acc);
+  if (MODE_RES) {
+    r[row] = ldg(b + row) - fma(d, x[row], acc);
+  } else {
+    const double bs = ldg(b + row) - acc;
+    const double xi = bs / d;
+    x[row] = xi;
+    if (WRITE_R) r[row] = fma(-d, xi, bs);
+  }
+}
+
 // Trailing colors c_first..c_last of one level in ONE CTA: every row of these colors is
 // owned by this CTA, so consecutive colors are separated by __syncthreads (global
 // writes of the CTA are visible to the CTA after the barrier) instead of kernel

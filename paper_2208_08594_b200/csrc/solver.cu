@@ -75,6 +75,7 @@ struct DevLevel {
   double *b = nullptr, *x = nullptr, *r = nullptr;
   int64_t nnz_alloc = 0;
   int lpr = 1;                       // lanes per row (coarse levels)
+  int uniform_w = 0;                 // > 0: every slice has this width (offsets arithmetic)
   int tail = 1 << 30;                // first color handled by the single-CTA tail kernel
   int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
 };
@@ -294,12 +295,25 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   L.nslices = (int32_t)slice_row.size();
   slice_row.push_back(n);
   slice_off.assign(L.nslices + 1, 0);
+  std::vector<int32_t> sw(L.nslices, 0);
+  int32_t wmax = 0;
+  int64_t tot = 0;
   for (int32_t s = 0; s < L.nslices; ++s) {
     int32_t r1 = std::min(slice_row[s] + kSell, slice_row[s + 1]);
     int32_t w = 0;
     for (int32_t p = slice_row[s]; p < r1; ++p) w = std::max(w, (int32_t)(rp[p + 1] - rp[p]) - 1);
-    slice_off[s + 1] = slice_off[s] + std::max(w, 0) * kSell;
+    sw[s] = std::max(w, 0);
+    wmax = std::max(wmax, sw[s]);
+    tot += sw[s];
   }
+  // narrow rows (one lane per row, <= 8 entries) with near-uniform slice widths: pad every
+  // slice to the widest so that slice offsets and row ranges are arithmetic (the level-0
+  // sweep kernel then needs no slice metadata loads); <= 5 % extra entries
+  const double avg_row = (double)rp[n] / std::max<int32_t>(n, 1);
+  const bool uniform = avg_row <= 8.0 && wmax > 0 && wmax <= 8 && (double)wmax * L.nslices <= 1.05 * (double)tot &&
+                       !(std::getenv("MSP_SELL_UNIFORM") && std::atoi(std::getenv("MSP_SELL_UNIFORM")) == 0);
+  for (int32_t s = 0; s < L.nslices; ++s) slice_off[s + 1] = slice_off[s] + (uniform ? wmax : sw[s]) * kSell;
+  L.uniform_w = uniform ? wmax : 0;
   std::vector<int32_t> col(std::max<int32_t>(slice_off[L.nslices], 1));
   std::vector<double> val(col.size(), 0.0), diag(n, 0.0);
   for (int32_t s = 0; s < L.nslices; ++s) {
@@ -1306,6 +1320,18 @@ void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
 }
 template <bool WR, bool RES>
 void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
+  if (L.lpr == 1 && L.uniform_w > 0 && s1 > s0) {
+    int c = 0;                                     // the color holding slice s0
+    while (c + 1 < L.ncolor && L.color_slice[c + 1] <= s0) ++c;
+    if (s1 <= L.color_slice[c + 1]) {              // range inside one color: uniform kernel
+      const int row_first = L.color_row[c] + (s0 - L.color_slice[c]) * kSell;
+      klaunch(h->s, h->pdl, sell_row_uniform_kernel<WR, RES>, nblk((size_t)(s1 - s0) * kSell, 128), 128, s0, s1,
+              row_first, L.color_row[c + 1], L.uniform_w, (const int*)L.col, (const double*)L.val,
+              (const double*)L.diag, (const double*)L.b, L.x, L.r);
+      ++h->nlaunch;
+      return;
+    }
+  }
   switch (L.lpr) {
     case 2: sell_rows<2, WR, RES>(h, L, s0, s1); break;
     case 4: sell_rows<4, WR, RES>(h, L, s0, s1); break;
