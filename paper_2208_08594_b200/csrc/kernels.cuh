@@ -926,6 +926,7 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
                                                          const int* __restrict__ ci,
                                                          const int* __restrict__ dg,
                                                          const int* __restrict__ cnt,
+                                                         const int4* __restrict__ islot,
                                                          const double* __restrict__ F,
                                                          double* v,
                                                          const double* __restrict__ wp,
@@ -955,6 +956,20 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
   double t = 0.0;                           // working value of row q of cell i
   // cnt[i] = (#external L entries) | (#intra-block U entries << 8), from setup
   const int cn = valid ? ldg(cnt + i) : 0;
+  // intra-block slots: entry of (i, c0 + s) (diagonal at s = cq), immutable: loaded and
+  // the needed factor blocks prefetched into L1 before the PDL wait, so the triangle
+  // steps below never wait on a column search
+  int sl[4] = {-1, -1, -1, -1};
+  if (MAXC > 1 && valid) {
+    const int4 s4 = __ldg(islot + i);
+    sl[0] = s4.x; sl[1] = s4.y; sl[2] = s4.z; sl[3] = s4.w;
+#pragma unroll
+    for (int sidx = 0; sidx < MAXC; ++sidx) {
+      const bool need = (FWD && sidx < cq) || (BWD && sidx >= cq);
+      if (need && sl[sidx] >= 0 && q * 4 < BB)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(F + (size_t)sl[sidx] * BB + q * 4));
+    }
+  }
   // PDL prologue (4x4 blocks): indices and factor columns of the first PFE external
   // entries are immutable -> issued before the wait, overlapping the previous kernel
   constexpr int PFE = (B == 4 && PF) ? MSP_BILU_PFE : 0;
@@ -989,7 +1004,6 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
     const int e0 = valid ? ldg(rp + i) : 0;
     const int d = valid ? ldg(dg + i) : 0;
     const int eext = e0 + (cn & 0xff);       // [e0, eext): external L; [eext, d): intra L
-    int e = eext;
     double acc = 0.0;
     if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -1063,14 +1077,14 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
     for (int sidx = 0; sidx < MAXC - 1; ++sidx) {
       // cell sidx is final: broadcast its vector, later cells subtract L_{i,sidx} y_sidx
       double contrib = 0.0;
-      const bool use = valid && cq > sidx && e < d && ldg(ci + e) == c0 + sidx;
-      const double* blkF = F + (size_t)e * BB;
+      const bool use = valid && cq > sidx && sl[sidx] >= 0;
+      const double* blkF = F + (size_t)(use ? sl[sidx] : 0) * BB;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const double yu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
         if (use && q < B) contrib = fma(ldg(blkF + u * B + q), yu, contrib);
       }
-      if (use) { t -= contrib; ++e; }
+      if (use) t -= contrib;
     }
     if (act) v[(size_t)i * B + q] = t;
     __syncwarp(tmask);
@@ -1134,7 +1148,6 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
       }
     }
     t -= acc;
-    int ep = ei - 1;                         // last intra U entry (descending consumption)
     const double* Dg = F + (size_t)(valid ? d : 0) * BB;
     double x = 0.0;
 #pragma unroll
@@ -1149,15 +1162,15 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
       if (cq == sidx) x = xs;
       if (sidx == 0) break;
       // earlier cells subtract U_{i,sidx} x_sidx
-      const bool use = valid && cq < sidx && ep > d && ldg(ci + ep) == c0 + sidx;
-      const double* blkF = F + (size_t)(use ? ep : 0) * BB;
+      const bool use = valid && cq < sidx && sl[sidx] >= 0;
+      const double* blkF = F + (size_t)(use ? sl[sidx] : 0) * BB;
       double contrib = 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const double xu = __shfl_sync(tmask, xs, tbase + sidx * TS + u);
         if (use && q < B) contrib = fma(ldg(blkF + u * B + q), xu, contrib);
       }
-      if (use) { t -= contrib; --ep; }
+      if (use) t -= contrib;
     }
     if (act) {
       v[(size_t)i * B + q] = x;
@@ -1573,11 +1586,25 @@ __device__ __forceinline__ void finalize_partials(int nv, const double* part, do
 template <int EW> struct VecT;
 template <> struct VecT<1> {
   double x;
+  __device__ static VecT ldre(const double* p, size_t t) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p + t));
+    return {v};
+  }
   __device__ static VecT ld(const double* p, size_t t) { return {__ldg(p + t)}; }
   __device__ static VecT ldcg(const double* p, size_t t) { return {__ldcg(p + t)}; }
 };
+__device__ __forceinline__ double2 ld_nc_v2_volatile(const double* p) {   // L1-cached, never merged
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
 template <> struct VecT<2> {
   double x, y;
+  __device__ static VecT ldre(const double* p, size_t t) {
+    const double2 v = ld_nc_v2_volatile(p + 2 * t);
+    return {v.x, v.y};
+  }
   __device__ static VecT ld(const double* p, size_t t) {
     const double2 v = __ldg(reinterpret_cast<const double2*>(p) + t);
     return {v.x, v.y};
@@ -1705,6 +1732,9 @@ __device__ __forceinline__ void dcgs_scalars(int k, const double* a, const doubl
 #ifndef MSP_DCGS_MINB
 #define MSP_DCGS_MINB 4                  // 64 registers: 4 CTAs/SM (2: 128 regs, 18% slower)
 #endif
+#ifndef MSP_DCGS_L1RE
+#define MSP_DCGS_L1RE 0
+#endif
 #ifndef MSP_DCGS_GROUP
 #define MSP_DCGS_GROUP 16
 #endif
@@ -1758,7 +1788,11 @@ __global__ void __launch_bounds__(kRedThreads, MSP_DCGS_MINB) dcgs_update_kernel
     if constexpr (DOT) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
+#if MSP_DCGS_L1RE
+        if (i < k) acc[i] = vdot<EW>(T::ldre(V + i * ldv, t), u, acc[i]);
+#else
         if (i < k) acc[i] = vdot<EW>(T::ldcg(V + i * ldv, t), u, acc[i]);
+#endif
         if (i % MSP_DCGS_GROUP == MSP_DCGS_GROUP - 1) asm volatile("" ::: "memory");
       }
       accv = vdot<EW>(vf, u, accv);

@@ -111,6 +111,7 @@ struct msp_handle {
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
+  int4* islot = nullptr;             // per cell: entry of (i, c0 + s) for the block's slots s (diag at its own)
   // AMG
   std::vector<DevLevel> lv;
   int32_t nL = 0, ldA = 0;
@@ -437,6 +438,26 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
 
 void setup_cluster(msp_handle* h);
 
+// BILU block kernels: per cell i of aggregate block [c0, c1) (<= 4 cells), the entry index
+// of (i, c0 + s) for every slot s of the block (-1: no coupling), with the diagonal entry
+// in the cell's own slot, so the intra-block triangle needs no column search.
+std::vector<int4> make_islot(int32_t n, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
+                             const std::vector<int32_t>& dg, const std::vector<int32_t>& blk_ptr) {
+  std::vector<int4> sl(n, make_int4(-1, -1, -1, -1));
+  for (size_t k = 0; k + 1 < blk_ptr.size(); ++k) {
+    const int32_t c0 = blk_ptr[k], c1 = blk_ptr[k + 1];
+    if (c1 - c0 > 4) continue;                          // (block kernels need <= 4 cells)
+    for (int32_t i = c0; i < c1; ++i) {
+      int v[4] = {-1, -1, -1, -1};
+      v[i - c0] = dg[i];
+      for (int32_t e = rp[i]; e < rp[i + 1]; ++e)
+        if (ci[e] >= c0 && ci[e] < c1 && ci[e] != i) v[ci[e] - c0] = e;
+      sl[i] = make_int4(v[0], v[1], v[2], v[3]);
+    }
+  }
+  return sl;
+}
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
   SetupTimer T;
@@ -624,6 +645,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
       }
     }
     h->bcnt = h->upload(cnt);
+    h->islot = h->upload(make_islot(n, rp, ci, dg, S.blk_ptr));
   }
     {
       std::vector<int32_t> l0(n);
@@ -958,6 +980,7 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
   h->color_blk = lcolor_blk;
   h->blk_ptr = h->upload(lblk);
   h->bcnt = h->upload(lcnt);
+  h->islot = h->upload(make_islot(no, lrp, lci, ldg, lblk));
   h->nnzb = (int64_t)ne;
   // ---------------- level 0
   const msp::SpMat& A0 = S.lv[0].A;               // natural level-0 numbering = cells
@@ -1127,19 +1150,19 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, co
       if (gf && kind != 1) {                   // forward phases with the fused a8 residual
         if (kind == 0)
           klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
-                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
+                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
         else
           klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
-                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
+                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
         return;
       }
     }
     if (kind == 0)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
     else if (kind == 1)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
     else
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
   };
   // distributed: after each color phase, the ghost copies of that color's cells are
   // refreshed (y after the forward phase, x after the backward phase)
