@@ -231,24 +231,68 @@ int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg) {
     }
   }
   for (int32_t i = 0; i < n; ++i) xadj[i + 1] += xadj[i];
+  // Selection order: the unaggregated row with the fewest unaggregated neighbours, lowest
+  // index on ties.  Counts are small integers, so a bucket queue does it exactly: one
+  // three-level bitset per count; the next row is the lowest set bit of the first
+  // non-empty bucket (same rows in the same order as a (count, index) min-heap).
   std::vector<int32_t> cnt(n);
-  using Key = std::pair<int32_t, int32_t>;
-  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> q;
-  for (int32_t i = 0; i < n; ++i) { cnt[i] = xadj[i + 1] - xadj[i]; q.push({cnt[i], i}); }
+  int32_t maxc = 0;
+  for (int32_t i = 0; i < n; ++i) { cnt[i] = xadj[i + 1] - xadj[i]; maxc = std::max(maxc, cnt[i]); }
+  const size_t w0 = ((size_t)n + 63) / 64, w1 = (w0 + 63) / 64, w2 = (w1 + 63) / 64;
+  struct Buckets {
+    size_t w0, w1, w2;
+    std::vector<uint64_t> b0, b1, b2;
+    std::vector<int32_t> size;
+    void init(int nb, size_t a, size_t b, size_t c) {
+      w0 = a; w1 = b; w2 = c;
+      b0.assign((size_t)nb * w0, 0); b1.assign((size_t)nb * w1, 0); b2.assign((size_t)nb * w2, 0);
+      size.assign(nb, 0);
+    }
+    void insert(int c, int32_t i) {
+      uint64_t* l0 = &b0[(size_t)c * w0]; uint64_t* l1 = &b1[(size_t)c * w1]; uint64_t* l2 = &b2[(size_t)c * w2];
+      const size_t k0 = (size_t)i >> 6, k1 = k0 >> 6, k2 = k1 >> 6;
+      l0[k0] |= 1ull << (i & 63);
+      l1[k1] |= 1ull << (k0 & 63);
+      l2[k2] |= 1ull << (k1 & 63);
+      ++size[c];
+    }
+    void erase(int c, int32_t i) {
+      uint64_t* l0 = &b0[(size_t)c * w0]; uint64_t* l1 = &b1[(size_t)c * w1]; uint64_t* l2 = &b2[(size_t)c * w2];
+      const size_t k0 = (size_t)i >> 6, k1 = k0 >> 6, k2 = k1 >> 6;
+      l0[k0] &= ~(1ull << (i & 63));
+      if (!l0[k0]) {
+        l1[k1] &= ~(1ull << (k0 & 63));
+        if (!l1[k1]) l2[k2] &= ~(1ull << (k1 & 63));
+      }
+      --size[c];
+    }
+    int32_t first(int c) const {
+      const uint64_t* l0 = &b0[(size_t)c * w0]; const uint64_t* l1 = &b1[(size_t)c * w1];
+      const uint64_t* l2 = &b2[(size_t)c * w2];
+      for (size_t k2 = 0; k2 < w2; ++k2)
+        if (l2[k2]) {
+          const size_t k1 = (k2 << 6) + __builtin_ctzll(l2[k2]);
+          const size_t k0 = (k1 << 6) + __builtin_ctzll(l1[k1]);
+          return (int32_t)((k0 << 6) + __builtin_ctzll(l0[k0]));
+        }
+      return -1;
+    }
+  } Q;
+  Q.init(maxc + 1, w0, w1, w2);
+  for (int32_t i = 0; i < n; ++i) Q.insert(cnt[i], i);
   std::vector<uint8_t> done(n, 0);
   agg.assign(n, -1);
   int32_t na = 0;
   auto release = [&](int32_t m) {
     for (int32_t e = xadj[m]; e < xadj[m + 1]; ++e) {
       const int32_t k = adj[e];
-      if (!done[k]) { --cnt[k]; q.push({cnt[k], k}); }
+      if (!done[k]) { Q.erase(cnt[k], k); --cnt[k]; Q.insert(cnt[k], k); }
     }
   };
-  while (!q.empty()) {
-    const Key top = q.top();
-    q.pop();
-    const int32_t i = top.second;
-    if (done[i] || top.first != cnt[i]) continue;
+  int c = 0;
+  for (int32_t left = n; left > 0;) {
+    while (Q.size[c] == 0) ++c;                       // counts only decrease: restart low
+    const int32_t i = Q.first(c);
     int32_t best = -1;
     double bt = 0.0;
     for (int32_t e = xadj[i]; e < xadj[i + 1]; ++e)
@@ -259,11 +303,19 @@ int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg) {
         if (!done[adj[e]] && std::fabs(tval[e]) > ba) { ba = std::fabs(tval[e]); best = adj[e]; }
     }
     done[i] = 1;
+    Q.erase(cnt[i], i);
+    --left;
     agg[i] = na;
-    if (best >= 0) { done[best] = 1; agg[best] = na; }
+    if (best >= 0) {
+      done[best] = 1;
+      Q.erase(cnt[best], best);
+      --left;
+      agg[best] = na;
+    }
     ++na;
     release(i);
     if (best >= 0) release(best);
+    c = 0;
   }
   return na;
 }
@@ -319,11 +371,18 @@ static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t
   comp.resize(A0.n);
   std::iota(comp.begin(), comp.end(), 0);
   int32_t na = A0.n;
+  const bool verbose = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
   for (int p = 0; p < passes; ++p) {
     std::vector<int32_t> a;
+    const auto t0 = std::chrono::steady_clock::now();
     na = pair_aggregate(cur, a);
     for (auto& c : comp) c = a[c];
+    const auto t1 = std::chrono::steady_clock::now();
     cur = galerkin_rap(cur, a, na);
+    if (verbose)
+      std::fprintf(stderr, "[msp setup]   pass %d: NPAIR %.3f s, Galerkin %.3f s (n %d -> %d)\n", p,
+                   std::chrono::duration<double>(t1 - t0).count(),
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count(), (int)cur.n, (int)na);
   }
   if (out) *out = std::move(cur);
   return na;
