@@ -43,6 +43,7 @@ class NcclComm : public Comm {
   }
   int rank() const override { return r; }
   int size() const override { return p; }
+  bool capturable() const override { return true; }   // NCCL operations are stream-capturable
   static void chk(ncclResult_t e, const char* what) {
     if (e != ncclSuccess) throw std::runtime_error(std::string("NCCL ") + what + ": " + ncclGetErrorString(e));
   }

@@ -42,6 +42,9 @@ class Comm {
   virtual void allreduce_sum(cudaStream_t s, double* buf, int count) = 0;
   // recv[r*count .. ) = send of rank r
   virtual void allgather(cudaStream_t s, const double* send, double* recv, int count) = 0;
+  // true if every call only enqueues work on s (no host synchronisation), so the
+  // Arnoldi steps that use it can be captured into CUDA graphs
+  virtual bool capturable() const { return false; }
 };
 
 // pack: sendbuf[k*width + w] = vec[idx[k]*width + w] for k in [k0, k1)

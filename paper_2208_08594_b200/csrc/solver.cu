@@ -2390,7 +2390,10 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
       c.smoother != 0)
     return fail(nullptr, MSP_EINVAL,
                 "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC");
-  c.use_graphs = 0;                 // collectives (and loopback host barriers) are not captured
+  // NCCL steps are replayed as CUDA graphs (halo send/recv groups and allreduces are
+  // captured with the kernels); the loopback backend synchronises host threads: direct
+  const char* ng = std::getenv("MSP_DIST_NOGRAPH");
+  c.use_graphs = (c.use_graphs && comm && comm->capturable() && !(ng && std::atoi(ng))) ? 1 : 0;
   c.use_coop = 0;
   std::unique_ptr<msp_handle> h(new msp_handle);
   h->cfg = c;

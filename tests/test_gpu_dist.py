@@ -57,16 +57,20 @@ def test_loopback_nc6_and_restarts():
     assert r1["iters"] > 6 and abs(rd["iters"] - r1["iters"]) <= 1
 
 
-def test_nccl_backend_single_rank_matches_single_gpu():
+@pytest.mark.parametrize("nograph", ["0", "1"])
+def test_nccl_backend_single_rank_matches_single_gpu(nograph, monkeypatch):
     """The NCCL communicator path (ncclCommInitRank, ncclAllReduce, ncclAllGather, empty
-    halos) at world size 1 reproduces the single-GPU solve."""
+    halos) at world size 1 reproduces the single-GPU solve, with the Arnoldi steps
+    captured as CUDA graphs (NCCL calls inside) and launched directly."""
     from paper_2208_08594_b200 import DistSolver, MspSolver, nccl_unique_id
+    monkeypatch.setenv("MSP_DIST_NOGRAPH", nograph)
     p = gen.make_config("C2", nx=20, ny=16, nz=6)
     uid = nccl_unique_id()
     d = DistSolver(p["row_ptr"], p["col"], p["val"], p["nc"], 0, 1, uid, coarsest_max_dof=80)
     own = d.owned_cells()
     assert np.array_equal(own, np.arange(p["n"]))
     rd = d.solve(torch.from_numpy(p["rhs"]).cuda())
+    assert (d.stats()["kernels_per_iter"] > 0) == (nograph == "0")      # graph captured or not
     s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], coarsest_max_dof=80)
     r1 = s.solve(torch.from_numpy(p["rhs"]).cuda())
     assert abs(rd["iters"] - r1["iters"]) <= 1
