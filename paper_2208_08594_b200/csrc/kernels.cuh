@@ -1547,9 +1547,10 @@ __device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, 
     if (lane == 0) sh[wid][i] = a;
   }
   __syncthreads();
+  const int nw = blockDim.x >> 5;               // (<= kRedThreads / 32 warps)
   for (int i = threadIdx.x; i < nv; i += blockDim.x) {
     double a = 0.0;
-    for (int k = 0; k < kRedThreads / 32; ++k) a += sh[k][i];
+    for (int k = 0; k < nw; ++k) a += sh[k][i];
     part[(size_t)blockIdx.x * kMaxV + off + i] = a;
   }
 }
@@ -1805,6 +1806,92 @@ __global__ void __launch_bounds__(kRedThreads, MSP_DCGS_MINB) dcgs_update_kernel
     block_partials<2>(tail, 2, part, k);
     finalize_partials(k + 2, part, out, nullptr, nullptr, -1, ticket);
   }
+}
+
+// DCGS2 pass 2, staged variant (DOT, 16-byte pairs, k <= NV): every thread streams its own
+// element pair of the k+2 vectors (V[0..k), V[k], w) into a private shared-memory slot
+// with cp.async, one tile ahead (double buffer), so up to 2 (k+2) 16-byte loads per
+// thread are in flight without holding registers, and the dot phase re-reads shared
+// memory instead of L2.  Each thread reads only the slots it filled: no block barriers in
+// the stream.  Same per-element arithmetic as dcgs_update_kernel.
+constexpr int kDcgsStThreads = 256;        // NV = 16 (k <= 16); NV = 32 runs 128 threads
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND)); }
+
+template <int NV, int TPB = kDcgsStThreads>
+__global__ void __launch_bounds__(TPB, 1) dcgs_update_staged_kernel(size_t NE, int k, const double* __restrict__ V,
+                                                                              size_t ldv, double* vk, double* w,
+                                                                              const double* __restrict__ a,
+                                                                              const double* __restrict__ st, double* part,
+                                                                              double* out, unsigned* ticket) {
+  extern __shared__ double2 stage[];            // [2][NV + 2][TPB]
+  __shared__ double h2s[NV], as[NV], sc[4];
+  PDL_ENTRY();
+  for (int i = threadIdx.x; i < NV; i += blockDim.x) {
+    h2s[i] = (i < k) ? st[i] : 0.0;
+    as[i] = (i < k) ? a[i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    dcgs_scalars(k, a, st, sc[0], sc[1], sc[2]);
+    sc[3] = 1.0 / sc[1];
+  }
+  __syncthreads();
+  const double nu = sc[0], rinv = sc[3], ck = sc[2];
+  const int nvec = k + 2;                        // V[0..k), V[k], w
+  auto slot = [&](int buf, int i) -> double2* { return stage + ((size_t)buf * (NV + 2) + i) * TPB + threadIdx.x; };
+  auto src = [&](int i, size_t t) -> const double2* {
+    const double* base = (i < k) ? V + (size_t)i * ldv : (i == k ? vk : w);
+    return reinterpret_cast<const double2*>(base) + t;
+  };
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < NE)
+    for (int i = 0; i < nvec; ++i) cp_async16(slot(0, i), src(i, t));
+  cp_async_commit();
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  double accv = 0.0, accu = 0.0;
+  int buf = 0;
+  for (; t < NE; t += stride, buf ^= 1) {
+    const size_t tn = t + stride;
+    if (tn < NE)
+      for (int i = 0; i < nvec; ++i) cp_async16(slot(buf ^ 1, i), src(i, tn));
+    cp_async_commit();
+    cp_async_wait<1>();                          // this tile's copies are complete
+    double2 s1 = make_double2(0.0, 0.0), s2 = s1;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < k) {
+        const double2 vi = *slot(buf, i);
+        s1.x = fma(h2s[i], vi.x, s1.x); s1.y = fma(h2s[i], vi.y, s1.y);
+        s2.x = fma(as[i], vi.x, s2.x); s2.y = fma(as[i], vi.y, s2.y);
+      }
+    double2 vf = *slot(buf, k), u = *slot(buf, k + 1);
+    vf.x = (nu * vf.x - s1.x) * rinv;
+    vf.y = (nu * vf.y - s1.y) * rinv;
+    u.x = u.x - s2.x - ck * vf.x;
+    u.y = u.y - s2.y - ck * vf.y;
+    reinterpret_cast<double2*>(vk)[t] = vf;
+    reinterpret_cast<double2*>(w)[t] = u;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < k) {
+        const double2 vi = *slot(buf, i);
+        acc[i] = fma(vi.x, u.x, fma(vi.y, u.y, acc[i]));
+      }
+    accv = fma(vf.x, u.x, fma(vf.y, u.y, accv));
+    accu = fma(u.x, u.x, fma(u.y, u.y, accu));
+  }
+  cp_async_wait<0>();
+  block_partials<NV>(acc, k, part, 0);
+  const double tail[2] = {accv, accu};
+  block_partials<2>(tail, 2, part, k);
+  finalize_partials(k + 2, part, out, nullptr, nullptr, -1, ticket);
 }
 
 // One CTA: from a = V[0..k]^T w, the old state and the sums s (V[0..k)^T u, v_k^T u,

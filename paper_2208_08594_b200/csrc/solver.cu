@@ -107,7 +107,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1;   // fuse_a8: measured slower
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1, dcgs_staged = 1;   // fuse_a8: measured slower
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1731,9 +1731,43 @@ void cgs2(msp_handle* h, int nv, double* w) {
 
 // DCGS2 passes of step k (R14, kernels.cuh): w = V[k+1] = A B V[k] on entry; on exit
 // V[k] final, V[k+1] = u (provisional, unnormalised), hcol = the host record (2k+4 values).
+template <int NV, int TPB>
+void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
+  constexpr size_t smem = sizeof(double2) * 2 * (NV + 2) * TPB;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(dcgs_update_staged_kernel<NV, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsm);                       // one CTA per SM, grid-stride over pairs
+  cfg.blockDim = dim3(TPB);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, dcgs_update_staged_kernel<NV, TPB>, h->N / 2, k, (const double*)h->V, h->N, vk, w,
+                        (const double*)h->dh1, st_in, h->part, h->dsum, h->ticket));
+  ++h->nlaunch;
+  if (h->comm) h->comm->allreduce_sum(h->s, h->dsum, k + 2);
+}
+
 template <int NV>
 void dcgs_update_t(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
   constexpr bool DOT = NV <= 16;
+  // staged (cp.async) pass 2 for 9 <= k <= 16 (measured: 9 % faster at k = 15; a 32-vector
+  // staged form at 128 threads per CTA was 15 % slower than the unfused k > 16 path)
+  if constexpr (NV == 16) {
+    if (ew2_ok(h) && h->dcgs_staged) {
+      dcgs_staged_launch<16, 256>(h, k, vk, w, st_in);
+      return;
+    }
+  }
   if (ew2_ok(h))
     klaunch(h->s, h->pdl, dcgs_update_kernel<NV, 2, DOT>, kRedBlocks, kRedThreads, h->N / 2, k, (const double*)h->V,
             h->N, vk, w, (const double*)h->dh1, st_in, h->part, h->dsum, h->ticket);
@@ -2023,6 +2057,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
   if (const char* e = std::getenv("MSP_FUSE_A8")) h->fuse_a8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_GEMV8")) h->gemv8 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_DCGS_STAGED")) h->dcgs_staged = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
