@@ -1536,7 +1536,7 @@ __global__ void __launch_bounds__(kRedThreads) multiaxpy_kernel(size_t N, int nv
 // partial sums of this CTA for vector slots [off, off + nv) -> part[blockIdx.x][off + i]
 template <int NV>
 __device__ __forceinline__ void block_partials(const double (&acc)[NV], int nv, double* part, int off = 0) {
-  __shared__ double sh[kRedThreads / 32][NV];
+  __shared__ double sh[32][NV];                  // up to 32 warps (1024-thread CTAs)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -1810,10 +1810,11 @@ __global__ void __launch_bounds__(kRedThreads, MSP_DCGS_MINB) dcgs_update_kernel
 
 // DCGS2 pass 2, staged variant (DOT, 16-byte pairs, k <= NV): every thread streams its own
 // element pair of the k+2 vectors (V[0..k), V[k], w) into a private shared-memory slot
-// with cp.async, one tile ahead (double buffer), so up to 2 (k+2) 16-byte loads per
-// thread are in flight without holding registers, and the dot phase re-reads shared
-// memory instead of L2.  Each thread reads only the slots it filled: no block barriers in
-// the stream.  Same per-element arithmetic as dcgs_update_kernel.
+// with cp.async (NBUF = 2: one tile ahead; NBUF = 1: the current tile), so k+2 16-byte
+// loads per thread are in flight without holding registers, and the dot phase re-reads
+// shared memory instead of L2.  Each thread reads only the slots it filled: no block
+// barriers in the stream.  Same per-element arithmetic as dcgs_update_kernel; also
+// covers k > 16 in ONE pass (the register kernel needs a separate dot pass there).
 constexpr int kDcgsStThreads = 256;        // NV = 16 (k <= 16); NV = 32 runs 128 threads
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
@@ -1822,13 +1823,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NPEND)); }
 
-template <int NV, int TPB = kDcgsStThreads>
+template <int NV, int TPB = kDcgsStThreads, int NBUF = 2>
 __global__ void __launch_bounds__(TPB, 1) dcgs_update_staged_kernel(size_t NE, int k, const double* __restrict__ V,
                                                                               size_t ldv, double* vk, double* w,
                                                                               const double* __restrict__ a,
                                                                               const double* __restrict__ st, double* part,
                                                                               double* out, unsigned* ticket) {
-  extern __shared__ double2 stage[];            // [2][NV + 2][TPB]
+  extern __shared__ double2 stage[];            // [NBUF][NV + 2][TPB]
   __shared__ double h2s[NV], as[NV], sc[4];
   PDL_ENTRY();
   for (int i = threadIdx.x; i < NV; i += blockDim.x) {
@@ -1849,20 +1850,26 @@ __global__ void __launch_bounds__(TPB, 1) dcgs_update_staged_kernel(size_t NE, i
   };
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < NE)
+  if (NBUF == 2 && t < NE)
     for (int i = 0; i < nvec; ++i) cp_async16(slot(0, i), src(i, t));
-  cp_async_commit();
+  if (NBUF == 2) cp_async_commit();
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
   double accv = 0.0, accu = 0.0;
   int buf = 0;
-  for (; t < NE; t += stride, buf ^= 1) {
-    const size_t tn = t + stride;
-    if (tn < NE)
-      for (int i = 0; i < nvec; ++i) cp_async16(slot(buf ^ 1, i), src(i, tn));
-    cp_async_commit();
-    cp_async_wait<1>();                          // this tile's copies are complete
+  for (; t < NE; t += stride, buf ^= (NBUF - 1)) {
+    if (NBUF == 2) {
+      const size_t tn = t + stride;
+      if (tn < NE)
+        for (int i = 0; i < nvec; ++i) cp_async16(slot(buf ^ 1, i), src(i, tn));
+      cp_async_commit();
+      cp_async_wait<1>();                        // this tile's copies are complete
+    } else {                                     // single buffer: this tile only
+      for (int i = 0; i < nvec; ++i) cp_async16(slot(0, i), src(i, t));
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
     double2 s1 = make_double2(0.0, 0.0), s2 = s1;
 #pragma unroll
     for (int i = 0; i < NV; ++i)

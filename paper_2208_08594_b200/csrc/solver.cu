@@ -107,7 +107,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1, dcgs_staged = 1;   // fuse_a8: measured slower
+  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1, dcgs_staged = 1, dcgs_staged32 = 1, dcgs_staged16 = 1, dcgs_staged8 = 1;   // fuse_a8: measured slower
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -1731,12 +1731,12 @@ void cgs2(msp_handle* h, int nv, double* w) {
 
 // DCGS2 passes of step k (R14, kernels.cuh): w = V[k+1] = A B V[k] on entry; on exit
 // V[k] final, V[k+1] = u (provisional, unnormalised), hcol = the host record (2k+4 values).
-template <int NV, int TPB>
+template <int NV, int TPB, int NBUF = 2>
 void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
-  constexpr size_t smem = sizeof(double2) * 2 * (NV + 2) * TPB;
+  constexpr size_t smem = sizeof(double2) * NBUF * (NV + 2) * TPB;
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(dcgs_update_staged_kernel<NV, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(dcgs_update_staged_kernel<NV, TPB, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   int nsm = 148;
@@ -1751,7 +1751,7 @@ void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const doubl
   at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, dcgs_update_staged_kernel<NV, TPB>, h->N / 2, k, (const double*)h->V, h->N, vk, w,
+  CK(cudaLaunchKernelEx(&cfg, dcgs_update_staged_kernel<NV, TPB, NBUF>, h->N / 2, k, (const double*)h->V, h->N, vk, w,
                         (const double*)h->dh1, st_in, h->part, h->dsum, h->ticket));
   ++h->nlaunch;
   if (h->comm) h->comm->allreduce_sum(h->s, h->dsum, k + 2);
@@ -1760,13 +1760,23 @@ void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const doubl
 template <int NV>
 void dcgs_update_t(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
   constexpr bool DOT = NV <= 16;
-  // staged (cp.async) pass 2 for 9 <= k <= 16 (measured: 9 % faster at k = 15; a 32-vector
-  // staged form at 128 threads per CTA was 15 % slower than the unfused k > 16 path)
+  // staged (cp.async) pass 2, one CTA per SM: k <= 8 at 1024 threads, 9 <= k <= 16 at 512
+  // and k > 16 at 256 threads, single-buffered (C3: orthogonalisation at k = 15 0.295 ->
+  // 0.255 ms, at k = 25 0.503 -> 0.457 ms); double-buffered forms kept as options
+  // (MSP_DCGS_STAGED16=0, MSP_DCGS_STAGED32=2: slower)
+  if constexpr (NV == 8) {
+    if (ew2_ok(h) && h->dcgs_staged8 == 1) { dcgs_staged_launch<8, 1024, 1>(h, k, vk, w, st_in); return; }
+  }
   if constexpr (NV == 16) {
     if (ew2_ok(h) && h->dcgs_staged) {
-      dcgs_staged_launch<16, 256>(h, k, vk, w, st_in);
+      if (h->dcgs_staged16 == 1) dcgs_staged_launch<16, 512, 1>(h, k, vk, w, st_in);
+      else dcgs_staged_launch<16, 256>(h, k, vk, w, st_in);
       return;
     }
+  }
+  if constexpr (NV == 32) {                       // fused staged pass 2 for k > 16
+    if (ew2_ok(h) && h->dcgs_staged32 == 1) { dcgs_staged_launch<32, 256, 1>(h, k, vk, w, st_in); return; }
+    if (ew2_ok(h) && h->dcgs_staged32 == 2) { dcgs_staged_launch<32, 128, 2>(h, k, vk, w, st_in); return; }
   }
   if (ew2_ok(h))
     klaunch(h->s, h->pdl, dcgs_update_kernel<NV, 2, DOT>, kRedBlocks, kRedThreads, h->N / 2, k, (const double*)h->V,
@@ -2058,6 +2068,9 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_FUSE_A8")) h->fuse_a8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_GEMV8")) h->gemv8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_DCGS_STAGED")) h->dcgs_staged = std::atoi(e);
+  if (const char* e = std::getenv("MSP_DCGS_STAGED32")) h->dcgs_staged32 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_DCGS_STAGED16")) h->dcgs_staged16 = std::atoi(e);
+  if (const char* e = std::getenv("MSP_DCGS_STAGED8")) h->dcgs_staged8 = std::atoi(e);
   if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
   if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
