@@ -135,8 +135,37 @@ int32_t color_groups(const Graph& G, std::vector<int32_t>& color) {
                    [&](int32_t a, int32_t b) { return G.deg(a) > G.deg(b); });
   std::vector<uint8_t> inV(n, 0), inFront(n, 0);
   std::vector<int32_t> stamp(n, -1);
-  using Key = std::pair<int32_t, int32_t>;  // (-deg, idx)
-  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> front;
+  // frontier: pop order (max static degree, lowest index) as a bucket queue over degrees,
+  // one bitset per degree (same sequence as a (-deg, index) min-heap with lazy removal)
+  int32_t maxd = 0;
+  for (int32_t v = 0; v < n; ++v) maxd = std::max(maxd, G.deg(v));
+  const size_t nw = ((size_t)n + 63) / 64;
+  std::vector<std::vector<uint64_t>> fb(maxd + 1);
+  std::vector<size_t> flo(maxd + 1, nw);           // lowest possibly non-zero word per degree
+  std::vector<int32_t> fcount(maxd + 1, 0), members;
+  int32_t ftop = -1;                                // highest degree with members (upper bound)
+  auto fpush = [&](int32_t u) {
+    const int d = G.deg(u);
+    if (fb[d].empty()) fb[d].assign(nw, 0);
+    const size_t w = (size_t)u >> 6;
+    fb[d][w] |= 1ull << (u & 63);
+    flo[d] = std::min(flo[d], w);
+    ++fcount[d];
+    ftop = std::max(ftop, d);
+    members.push_back(u);
+  };
+  auto fpop = [&]() -> int32_t {                    // best (max degree, min index) or -1
+    while (ftop >= 0 && fcount[ftop] == 0) --ftop;
+    if (ftop < 0) return -1;
+    std::vector<uint64_t>& b = fb[ftop];
+    size_t w = flo[ftop];
+    while (!b[w]) ++w;
+    flo[ftop] = w;
+    const int32_t u = (int32_t)((w << 6) + __builtin_ctzll(b[w]));
+    b[w] &= b[w] - 1;
+    --fcount[ftop];
+    return u;
+  };
   std::vector<int32_t> cur = bydeg, nxt;
   int32_t g = 0;
   while (!cur.empty()) {
@@ -144,11 +173,9 @@ int32_t color_groups(const Graph& G, std::vector<int32_t>& color) {
     size_t cursor = 0;
     while (true) {
       int32_t v = -1;
-      while (!front.empty()) {
-        int32_t t = front.top().second;
-        if (inV[t]) { v = t; front.pop(); inFront[t] = 0; break; }
-        front.pop();
+      for (int32_t t; (t = fpop()) >= 0;) {
         inFront[t] = 0;
+        if (inV[t]) { v = t; break; }
       }
       if (v < 0) {
         while (cursor < cur.size() && !inV[cur[cursor]]) ++cursor;
@@ -173,11 +200,19 @@ int32_t color_groups(const Graph& G, std::vector<int32_t>& color) {
           const int32_t u = G.adj[f];
           if (stamp[u] == v || !inV[u] || inFront[u]) continue;
           inFront[u] = 1;
-          front.push({-G.deg(u), u});
+          fpush(u);
         }
       }
     }
-    while (!front.empty()) { inFront[front.top().second] = 0; front.pop(); }
+    for (int32_t u : members) {                    // empty the frontier for the next color
+      const int d = G.deg(u);
+      const size_t w = (size_t)u >> 6;
+      if (fb[d][w] >> (u & 63) & 1ull) { fb[d][w] &= ~(1ull << (u & 63)); --fcount[d]; }
+      inFront[u] = 0;
+      flo[d] = nw;
+    }
+    members.clear();
+    ftop = -1;
     nxt.clear();
     for (int32_t v : cur)
       if (color[v] < 0) nxt.push_back(v);        // keeps degree order for the next call
