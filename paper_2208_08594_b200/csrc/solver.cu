@@ -1956,8 +1956,12 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         y[i] = (gam[i] - s) / H[(size_t)i * m + i];
       }
       // u = V_k y ; x += B u ; r = b - A x
+      // u = V y through the CGS axpy pass on a zeroed u with coefficients -y (the same
+      // fma(y_i, V_i, .) sequence as a plain V y, with the multi-vector pass's loads)
+      for (int i = 0; i < k; ++i) y[i] = -y[i];
       CK(cudaMemcpyAsync(h->dh1, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, h->s));
-      maxpy(h, k, h->V, h->dh1, h->u, 1, nullptr);
+      CK(cudaMemsetAsync(h->u, 0, sizeof(double) * N, h->s));
+      cgs_axpy<false>(h, k, h->V, h->dh1, h->u, h->lred, nullptr, nullptr, -1);
       msp_apply_dev(h, h->u, h->z);
       klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->z, h->xin); ++h->nlaunch;
       exch_cell(h, h->xin, h->b, -1);
