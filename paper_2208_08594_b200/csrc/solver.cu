@@ -1734,11 +1734,8 @@ void cgs2(msp_handle* h, int nv, double* w) {
 template <int NV, int TPB, int NBUF = 2>
 void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
   constexpr size_t smem = sizeof(double2) * NBUF * (NV + 2) * TPB;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(dcgs_update_staged_kernel<NV, TPB, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  // per device (cheap host call; inside a step it runs once, at graph capture)
+  CK(cudaFuncSetAttribute(dcgs_update_staged_kernel<NV, TPB, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nsm = 148;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
   cudaLaunchConfig_t cfg = {};
