@@ -692,6 +692,37 @@ def test_gmres_residuals_are_krylov_minima(orth):
         Q, _ = np.linalg.qr(np.column_stack([Q, A @ Q[:, -1]]))
 
 
+@pytest.mark.parametrize("orth", [0, 1, 2])
+def test_gmres_terminates_at_minimal_polynomial_degree(orth):
+    """Closed form (Krylov theory): unrestarted GMRES reaches the exact solution in
+    exactly deg(minimal polynomial of A w.r.t. b) steps.  (1) A = S diag(λ) S⁻¹, nonsymmetric,
+    with 4 distinct eigenvalues of multiplicity 5 each (n = 20): 4 iterations. (2) A Jordan
+    block I + N (N the upper shift) with b = e_n: the Krylov space grows one unit vector per
+    step, so exactly n iterations; before that the k-th relative residual is 1/sqrt(k+1):
+    A K_k ⊂ span(e_{n-k}..e_n), whose unit vector orthogonal to A K_k is the alternating
+    (±1, ..., ±1)/sqrt(k+1) (w_j + w_{j-1} = 0), and its e_n component is the residual."""
+    rng = np.random.default_rng(31)
+    n = 20
+    S = rng.normal(size=(n, n)) + 4 * np.eye(n)
+    lam = np.repeat([1.0, 2.0, 3.5, 5.0], 5)
+    A = S @ np.diag(lam) @ np.linalg.inv(S)
+    b = rng.normal(size=n)
+    ptr, col, val = csr_of(A)
+    r = oracle.gmres_csr(ptr, col, val, b, tol=1e-9, m=n, maxit=n, orth=orth)
+    assert r["iters"] == 4, r["iters"]
+    assert np.allclose(r["x"], np.linalg.solve(A, b), rtol=1e-7)
+    n = 8
+    J = np.eye(n) + np.eye(n, k=1)
+    e = np.zeros(n)
+    e[-1] = 1.0
+    ptr, col, val = csr_of(J)
+    r = oracle.gmres_csr(ptr, col, val, e, tol=1e-12, m=n, maxit=n, orth=orth)
+    assert r["iters"] == n, r["iters"]
+    assert np.allclose(r["x"], np.linalg.solve(J, e), rtol=1e-10)
+    for k in range(1, n):
+        assert abs(r["hist"][k - 1] - 1 / np.sqrt(k + 1)) <= 1e-12, (k, r["hist"][k - 1])
+
+
 @pytest.mark.parametrize("m", [5, 30])
 def test_dcgs2_restarted_matches_cgs2(m):
     """DCGS2 (R14) computes the same Arnoldi basis as CGS2 in exact arithmetic: with
