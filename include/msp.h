@@ -18,8 +18,12 @@
  *  - The caller owns every array it passes.  msp_setup deep-copies A; no caller
  *    pointer is retained after a call returns.
  *  - A handle is single-owner and not re-entrant; distinct handles are independent.
- *  - All GPU work is ordered after prior work on `cuda_stream` (0 = legacy default
+ *  - All GPU work of every call is ordered after prior work on the caller's stream (the
+ *    `cuda_stream` of msp_setup, changeable by msp_set_stream; 0 = legacy default
  *    stream) and the call returns after it has completed.
+ *  - A handle whose (re)SETUP failed (msp_update rebuild) is unusable: compute calls
+ *    return MSP_EINVAL until an msp_update rebuild succeeds.  The previous
+ *    preconditioner is not kept.
  *  - Sizes are element counts unless stated.  FP64 everywhere (R9).
  */
 #ifndef MSP_H_
@@ -38,7 +42,9 @@ typedef enum {
   MSP_ESINGULAR = 2,   /* zero A_PP diagonal, singular N-N block (decoupling), singular BILU pivot
                           block or singular coarsest matrix; index in msp_last_error */
   MSP_ENOCONV = 3,     /* maxit reached: x, history and final residual are still valid */
-  MSP_EBREAKDOWN = 4,  /* GMRES breakdown with the true residual above tol */
+  MSP_EBREAKDOWN = 4,  /* happy breakdown (h_{j+1,j} < 1e-14 ||b||, an invariant Krylov space)
+                          with the true residual still above tol: restarting cannot help;
+                          x, history and final residual are valid */
   MSP_ESTALL = 5,      /* AMG coarsening stalled above coarsest_max_dof on a non-diagonal level */
   MSP_ECUDA = 6,       /* CUDA runtime / cuSOLVER error (message in msp_last_error) */
   MSP_ENCCL = 7,       /* NCCL error (distributed entry points) */
@@ -163,6 +169,39 @@ msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x);
  * and U blocks of the factorization, and D~_i^-1 in the diagonal slots.  Single-GPU
  * handles only (MSP_EINVAL otherwise). */
 msp_status msp_bilu_factors(msp_handle* h, double* F_out);
+/* ---- Single steps of the hot path, for the per-kernel parity tests (device pointers,
+ * single-GPU handles; each call returns after its work completed).  Each runs the same
+ * kernel the solve runs for that step. ---- */
+/* a3 (R4; Π_P^T of Alg. 1 line 4, with the decoupling weights): rp = W^T g.
+ * g: n_cells*block doubles, natural cell order; rp: n_cells doubles, natural cell order. */
+msp_status msp_restrict_pressure(msp_handle* h, const double* g, double* rp);
+/* a5 (UA-AMG residual + restriction): bc = P_l^T (b - A_l x) on smoothing level l.
+ * b, x: level_n[l] doubles in the level's natural row numbering (the oracle's); bc:
+ * level_n[l+1] doubles in level l+1's natural numbering (aggregate creation order). */
+msp_status msp_residual_restrict(msp_handle* h, int level, const double* b, const double* x, double* bc);
+/* a7 (prolongation + correction): x += P_l e; e: level_n[l+1], x: level_n[l]
+ * (in/out), natural numberings as above. */
+msp_status msp_prolong(msp_handle* h, int level, const double* e, double* x);
+/* a8 (Alg. 1 line 5, with w = Π_P x_p): r = g - A Π_P x_p, reading only the pressure
+ * column of each block.  g, r: n_cells*block; xp: n_cells; natural cell order. */
+msp_status msp_pcol_residual(msp_handle* h, const double* g, const double* xp, double* r);
+/* a9 halves (Alg. 1 line 6; BILU(0) in ABMC order, R5): forward y = L^-1 r (all
+ * block colors ascending), backward x = U^-1 y (all colors descending, D~^-1 applied).
+ * Natural cell order, n_cells*block doubles. */
+msp_status msp_bilu_forward(msp_handle* h, const double* r, double* y);
+msp_status msp_bilu_backward(msp_handle* h, const double* y, double* x);
+/* a10 (Arnoldi orthogonalisation pass): out[i] = V_i^T w for i < k <= 32 with the
+ * multi-vector dot kernel.  V: k vectors of n_cells*block doubles, consecutive (device);
+ * w: device; out: HOST, k doubles. */
+msp_status msp_multidot(msp_handle* h, int k, const double* V, const double* w, double* out);
+/* Test hook: replace the handle's BILU factors by F (HOST, nnzb*block*block doubles,
+ * natural entry order, row-major blocks, D~_i^-1 in the diagonal slots -- the layout of
+ * msp_bilu_factors), e.g. with integer-valued factors for bit-exact substitution tests. */
+msp_status msp_bilu_set_factors(msp_handle* h, const double* F);
+/* The caller's stream: every entry point orders the handle's work after the work queued
+ * on it (default: the stream given to msp_setup; 0 = legacy default stream). */
+msp_status msp_set_stream(msp_handle* h, void* cuda_stream);
+
 /* Times `reps` launches of one hot-path piece on the handle's stream with CUDA events,
  * flushing L2 (a 256 MB device write) before each launch.  Returns the mean device
  * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory

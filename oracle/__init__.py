@@ -39,7 +39,10 @@ def lib():
         for name in ("orc_msp_update_values", "orc_msp_destroy", "orc_msp_info", "orc_msp_level_n",
                      "orc_msp_level_csr", "orc_msp_level_colors", "orc_msp_level_agg",
                      "orc_msp_weights", "orc_msp_order", "orc_msp_bilu_factors", "orc_msp_vcycle",
-                     "orc_msp_bilu_apply", "orc_msp_apply", "orc_msp_solve", "orc_msp_bgs_apply"):
+                     "orc_msp_bilu_apply", "orc_msp_apply", "orc_msp_solve", "orc_msp_bgs_apply",
+                     "orc_msp_restrict_pressure", "orc_msp_level_resid_restrict",
+                     "orc_msp_level_prolong", "orc_msp_bilu_forward", "orc_msp_bilu_backward",
+                     "orc_msp_bilu_apply_by_color", "orc_msp_bilu_blocks", "orc_msp_bilu_set_factors"):
             getattr(_lib, name).argtypes = None
     return _lib
 
@@ -68,7 +71,7 @@ class Config(ctypes.Structure):
 
     @classmethod
     def make(cls, coarsest_max_dof=10000, max_levels=20, pre_sweeps=1, post_sweeps=1, pair_passes=2,
-             decoupling=2, bilu_order=1, stages=2, orth=2, smoother=0, gs_chunk=32):
+             decoupling=2, bilu_order=1, stages=2, orth=0, smoother=0, gs_chunk=32):
         return cls(coarsest_max_dof, max_levels, pre_sweeps, post_sweeps, pair_passes, decoupling,
                    bilu_order, stages, orth, smoother, gs_chunk)
 
@@ -203,6 +206,15 @@ def gmres_csr(ptr, col, val, b, x0=None, tol=1e-6, m=30, maxit=1000, orth=0, Min
     return dict(x=x, iters=it.value, final_rel=fr.value, hist=hist[:hl.value].copy(), status=st)
 
 
+def dots(V, w):
+    """a10: V[i]^T w for the rows of V (k x N), plain index-ascending sums."""
+    V = _c(V, F64)
+    k, N = V.shape
+    out = np.zeros(k)
+    lib().orc_dots(ctypes.c_longlong(N), k, _p(V), _p(_c(w, F64)), _p(out))
+    return out
+
+
 def asmsp_decide(iota, last_it, mu, dims_changed=False):
     return bool(lib().orc_asmsp_decide(iota, last_it, mu, 1 if dims_changed else 0))
 
@@ -288,6 +300,53 @@ class Msp:
         x = np.zeros(self.n * self.b)
         lib().orc_msp_bilu_apply(self.h, _p(_c(r, F64)), _p(x))
         return x
+
+    def restrict_pressure(self, g):
+        """a3: r_p = W^T g (natural cell order)."""
+        rp = np.zeros(self.n)
+        lib().orc_msp_restrict_pressure(self.h, _p(_c(g, F64)), _p(rp))
+        return rp
+
+    def residual_restrict(self, l, b, x):
+        """a5 on level l: r_{l+1}[I] = sum_{i in I} (b - A_l x)_i."""
+        nn, _ = self.level_agg(l)
+        bc = np.zeros(nn)
+        if lib().orc_msp_level_resid_restrict(self.h, l, _p(_c(b, F64)), _p(_c(x, F64)), _p(bc)):
+            raise OracleError("bad level")
+        return bc
+
+    def prolong(self, l, e, x):
+        """a7 on level l: returns x + P e."""
+        x = _c(x, F64).copy()
+        if lib().orc_msp_level_prolong(self.h, l, _p(_c(e, F64)), _p(x)):
+            raise OracleError("bad level")
+        return x
+
+    def bilu_forward(self, r, absmode=False):
+        y = np.zeros(self.n * self.b)
+        lib().orc_msp_bilu_forward(self.h, _p(_c(r, F64)), _p(y), 1 if absmode else 0)
+        return y
+
+    def bilu_backward(self, y, absmode=False):
+        x = np.zeros(self.n * self.b)
+        lib().orc_msp_bilu_backward(self.h, _p(_c(y, F64)), _p(x), 1 if absmode else 0)
+        return x
+
+    def set_bilu_factors(self, F, Dinv):
+        """Test hook: replace the BILU factors (natural storage, row-major) and D~^-1."""
+        lib().orc_msp_bilu_set_factors(self.h, _p(_c(F, F64)), _p(_c(Dinv, F64)))
+
+    def bilu_apply_by_color(self, r):
+        x = np.zeros(self.n * self.b)
+        lib().orc_msp_bilu_apply_by_color(self.h, _p(_c(r, F64)), _p(x))
+        return x
+
+    def bilu_blocks(self):
+        """(g, color[n], blk[n]): ABMC block color and block (aggregate) id of every cell."""
+        color = np.zeros(self.n, dtype=I32)
+        blk = np.zeros(self.n, dtype=I32)
+        g = lib().orc_msp_bilu_blocks(self.h, _p(color), _p(blk))
+        return g, color, blk
 
     def bgs_apply(self, r):
         wN = np.zeros(self.n * (self.b - 1))

@@ -444,7 +444,7 @@ struct Config {
   int decoupling = 2;            // 0 NONE, 1 QI, 2 TI (R4)
   int bilu_order = 1;            // 0 RB, 1 ABMC1 (R5)
   int stages = 2;                // 2 = PR (north_star), 3 = NPR (Eq. 21 full)
-  int orth = 2;                  // 2 DCGS2 (R14, default), 0 CGS2, 1 MGS (R8)
+  int orth = 0;                  // 0 CGS2 (R8, default: the textbook reference), 1 MGS, 2 DCGS2 (R14)
   int smoother = 0;              // 0 PGS-MC (Alg. 4), 1 PJAC-NO, 2 PGS-NO (R13)
   int gs_chunk = 32;             // PGS-NO chunk size K (R13)
 };
@@ -616,6 +616,22 @@ static bool smooth(const Level& L, const Config& cfg, const double* b, double* x
   return pgs_mc_sweep(L.A, L.groups, b, x, pre);
 }
 
+// a5: residual and restriction r_{l+1}[I] = sum_{i in I} (b_i - (A_l x)_i) (P^T with the
+// piecewise-constant UA-AMG prolongation P): the residual of every row,
+// then the members of each aggregate summed in ascending row order (from +0.0).
+static void residual_restrict(const Level& L, const double* b, const double* x, double* bc) {
+  const int n = L.A.n;
+  std::vector<double> Ax(n);
+  csr_spmv(L.A, x, Ax.data());
+  for (int I = 0; I < L.n_next; ++I) bc[I] = 0.0;
+  for (int i = 0; i < n; ++i) bc[L.agg[i]] += b[i] - Ax[i];
+}
+
+// a7: prolongation and correction x_i += e[agg(i)] (P e, P piecewise constant).
+static void prolong_correct(const Level& L, const double* e, double* x) {
+  for (int i = 0; i < L.A.n; ++i) x[i] += e[L.agg[i]];
+}
+
 // c-7: V-cycle from zero initial guess: pre-smooth (colors ascending), restrict
 // r_{l+1} = P^T (b - A x), recurse, x += P e, post-smooth (colors descending).
 static bool vcycle(const Hierarchy& H, const Config& cfg, int l, const std::vector<double>& b,
@@ -630,13 +646,11 @@ static bool vcycle(const Hierarchy& H, const Config& cfg, int l, const std::vect
   x.assign(n, 0.0);
   for (int s = 0; s < cfg.pre_sweeps; ++s)
     if (!smooth(L, cfg, b.data(), x.data(), true)) return false;
-  std::vector<double> Ax(n);
-  csr_spmv(L.A, x.data(), Ax.data());
   std::vector<double> bc(L.n_next, 0.0);
-  for (int i = 0; i < n; ++i) bc[L.agg[i]] += b[i] - Ax[i];
+  residual_restrict(L, b.data(), x.data(), bc.data());
   std::vector<double> e;
   if (!vcycle(H, cfg, l + 1, bc, e)) return false;
-  for (int i = 0; i < n; ++i) x[i] += e[L.agg[i]];
+  prolong_correct(L, e.data(), x.data());
   for (int s = 0; s < cfg.post_sweeps; ++s)
     if (!smooth(L, cfg, b.data(), x.data(), false)) return false;
   return true;
@@ -665,10 +679,12 @@ static Csr cell_laplacian(const Graph& G) {
   return L;
 }
 
-static std::vector<int> bilu_ordering(const Bsr& A, const Csr& App, const Config& cfg) {
+static std::vector<int> bilu_ordering(const Bsr& A, const Csr& App, const Config& cfg,
+                                      std::vector<int>& color, std::vector<int>& blk) {
   const int n = A.n;
   Graph G = cell_graph(A);
-  std::vector<int> color(n), blk(n);
+  color.assign(n, 0);
+  blk.assign(n, 0);
   if (cfg.bilu_order == 0) {
     auto groups = vertices_grouping(G);
     for (size_t g = 0; g < groups.size(); ++g) for (int c : groups[g]) color[c] = (int)g;
@@ -701,6 +717,7 @@ static std::vector<int> bilu_ordering(const Bsr& A, const Csr& App, const Config
 
 struct Bilu {
   std::vector<int> order, pos;
+  std::vector<int> color, blk;  // block color and ABMC block (aggregate) of every cell
   Bsr F;                       // factors in A's (natural) storage: L_ik (k before i), U_ij (j after i)
   std::vector<double> Dinv;    // n * b*b
   std::vector<std::vector<int>> rowe;   // entries of row i sorted by position of column
@@ -752,11 +769,15 @@ static bool bilu_factor(const Bsr& A, const std::vector<int>& order, Bilu& R) {
   return true;
 }
 
-// forward y_i = r_i - sum_{k before i} L_ik y_k ; backward x_i = D~_i^-1 (y_i - sum_{j after i} U_ij x_j)
-static void bilu_apply(const Bilu& R, const double* r, double* x) {
+// Alg. 1 line 6 (R r) with the BILU(0) factors, sequentially in the elimination order:
+// forward  y_i = r_i - sum_{k before i} L_ik y_k                 (positions ascending)
+// backward x_i = D~_i^-1 (y_i - sum_{j after i} U_ij x_j)        (positions descending)
+// Sums run over row i's entries sorted by position, components ascending, from +0.0.
+// absmode: the same recurrences on |L|, |U|, |D~^-1| and |inputs| with every minus a
+// plus -- the componentwise magnitude bounds (I - |N|)^-1 |r| used by the parity tests.
+static void bilu_forward(const Bilu& R, const double* r, double* y, bool absmode = false) {
   const Bsr& F = R.F;
-  const int n = F.n, b = F.b, bb = b * b;
-  std::vector<double> y((size_t)n * b);
+  const int n = F.n, b = F.b;
   for (int p = 0; p < n; ++p) {
     const int i = R.order[p];
     for (int q = 0; q < b; ++q) {
@@ -764,11 +785,20 @@ static void bilu_apply(const Bilu& R, const double* r, double* x) {
       for (int e : R.rowe[i]) {
         const int k = F.col[e];
         if (R.pos[k] >= p) break;
-        for (int t = 0; t < b; ++t) s += F.blk(e)[q * b + t] * y[(size_t)k * b + t];
+        for (int t = 0; t < b; ++t) {
+          const double f = F.blk(e)[q * b + t];
+          s += (absmode ? std::fabs(f) : f) * y[(size_t)k * b + t];
+        }
       }
-      y[(size_t)i * b + q] = r[(size_t)i * b + q] - s;
+      const double ri = r[(size_t)i * b + q];
+      y[(size_t)i * b + q] = absmode ? std::fabs(ri) + s : ri - s;
     }
   }
+}
+
+static void bilu_backward(const Bilu& R, const double* y, double* x, bool absmode = false) {
+  const Bsr& F = R.F;
+  const int n = F.n, b = F.b, bb = b * b;
   std::vector<double> t(b);
   for (int p = n - 1; p >= 0; --p) {
     const int i = R.order[p];
@@ -777,16 +807,84 @@ static void bilu_apply(const Bilu& R, const double* r, double* x) {
       for (int e : R.rowe[i]) {
         const int j = F.col[e];
         if (R.pos[j] <= p) continue;
-        for (int u = 0; u < b; ++u) s += F.blk(e)[q * b + u] * x[(size_t)j * b + u];
+        for (int u = 0; u < b; ++u) {
+          const double f = F.blk(e)[q * b + u];
+          s += (absmode ? std::fabs(f) : f) * x[(size_t)j * b + u];
+        }
       }
-      t[q] = y[(size_t)i * b + q] - s;
+      const double yi = y[(size_t)i * b + q];
+      t[q] = absmode ? std::fabs(yi) + s : yi - s;
     }
     for (int q = 0; q < b; ++q) {
       double s = 0.0;
-      for (int u = 0; u < b; ++u) s += R.Dinv[(size_t)i * bb + q * b + u] * t[u];
+      for (int u = 0; u < b; ++u) {
+        const double d = R.Dinv[(size_t)i * bb + q * b + u];
+        s += (absmode ? std::fabs(d) : d) * t[u];
+      }
       x[(size_t)i * b + q] = s;
     }
   }
+}
+
+static void bilu_apply(const Bilu& R, const double* r, double* x) {
+  std::vector<double> y((size_t)R.F.n * R.F.b);
+  bilu_forward(R, r, y.data());
+  bilu_backward(R, y.data(), x);
+}
+
+// The same substitutions executed "in parallel by color" (P:258 with the block multicolor
+// reading R5, P:434's independence argument): every cell of block color c reads the
+// values of OTHER blocks from a snapshot taken before color c starts (colors < c final
+// in the forward phase, > c in the backward phase) and only its own block's cells
+// live, in order.  Identical summation order to bilu_forward/backward, so the result
+// is bit-identical to the sequential one exactly when same-color blocks are uncoupled.
+static void bilu_apply_by_color(const Bilu& R, const double* r, double* x) {
+  const Bsr& F = R.F;
+  const int n = F.n, b = F.b, bb = b * b;
+  int g = 0;
+  for (int c = 0; c < n; ++c) g = std::max(g, R.color[c] + 1);
+  std::vector<double> y((size_t)n * b, 0.0), snap;
+  for (int col = 0; col < g; ++col) {
+    snap = y;
+    for (int p = 0; p < n; ++p) {
+      const int i = R.order[p];
+      if (R.color[i] != col) continue;
+      for (int q = 0; q < b; ++q) {
+        double s = 0.0;
+        for (int e : R.rowe[i]) {
+          const int k = F.col[e];
+          if (R.pos[k] >= p) break;
+          const double* src = (R.blk[k] == R.blk[i]) ? y.data() : snap.data();
+          for (int t = 0; t < b; ++t) s += F.blk(e)[q * b + t] * src[(size_t)k * b + t];
+        }
+        y[(size_t)i * b + q] = r[(size_t)i * b + q] - s;
+      }
+    }
+  }
+  std::vector<double> xv((size_t)n * b, 0.0), t(b);
+  for (int col = g - 1; col >= 0; --col) {
+    snap = xv;
+    for (int p = n - 1; p >= 0; --p) {
+      const int i = R.order[p];
+      if (R.color[i] != col) continue;
+      for (int q = 0; q < b; ++q) {
+        double s = 0.0;
+        for (int e : R.rowe[i]) {
+          const int j = F.col[e];
+          if (R.pos[j] <= p) continue;
+          const double* src = (R.blk[j] == R.blk[i]) ? xv.data() : snap.data();
+          for (int u = 0; u < b; ++u) s += F.blk(e)[q * b + u] * src[(size_t)j * b + u];
+        }
+        t[q] = y[(size_t)i * b + q] - s;
+      }
+      for (int q = 0; q < b; ++q) {
+        double s = 0.0;
+        for (int u = 0; u < b; ++u) s += R.Dinv[(size_t)i * bb + q * b + u] * t[u];
+        xv[(size_t)i * b + q] = s;
+      }
+    }
+  }
+  std::copy(xv.begin(), xv.end(), x);
 }
 
 // ---------------------------------------------------------------------------
@@ -817,7 +915,13 @@ static int msp_setup(Msp& M) {
   M.App = extract_app(M.A, M.W);
   int rc = build_hierarchy(M.App, M.cfg, M.H);
   if (rc) return rc;
-  if (!bilu_factor(M.A, bilu_ordering(M.A, M.App, M.cfg), M.R)) return 2;
+  {
+    std::vector<int> color, blk;
+    std::vector<int> order = bilu_ordering(M.A, M.App, M.cfg, color, blk);
+    if (!bilu_factor(M.A, order, M.R)) return 2;
+    M.R.color = color;
+    M.R.blk = blk;
+  }
   if (M.cfg.stages == 3) {
     const int b = M.A.b, nc = b - 1;
     M.N.Dinv.assign((size_t)M.A.n * nc * nc, 0.0);
@@ -836,14 +940,21 @@ static int msp_setup(Msp& M) {
   return 0;
 }
 
-static bool pressure_stage(const Msp& M, const std::vector<double>& r, std::vector<double>& xp) {
-  const int n = M.A.n, b = M.A.b;
-  std::vector<double> rp(n);
-  for (int c = 0; c < n; ++c) {              // r_p = W^T r
+// a3: decoupled pressure restriction r_p = W^T r (R4; Π_P^T of Alg. 1 line 4, with
+// the decoupling weights in the middle factor): r_p[c] = sum_k w_c[k] r[c*b+k], k ascending.
+static void restrict_pressure(const Msp& M, const double* r, double* rp) {
+  const int b = M.A.b;
+  for (int c = 0; c < M.A.n; ++c) {
     double s = 0.0;
     for (int k = 0; k < b; ++k) s += M.W[(size_t)c * b + k] * r[(size_t)c * b + k];
     rp[c] = s;
   }
+}
+
+static bool pressure_stage(const Msp& M, const std::vector<double>& r, std::vector<double>& xp) {
+  const int n = M.A.n;
+  std::vector<double> rp(n);
+  restrict_pressure(M, r.data(), rp.data());
   return vcycle(M.H, M.cfg, 0, rp, xp);
 }
 
@@ -905,7 +1016,7 @@ static bool msp_apply(const Msp& M, const double* g, double* wout) {
 struct GmresOut {
   int iters = 0;
   double final_rel = 0.0;
-  int status = 0;    // 0 ok, 3 no convergence
+  int status = 0;    // 0 ok, 3 no convergence, 4 breakdown above tol
   std::vector<double> hist;
 };
 
@@ -940,6 +1051,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
     rhop = 1.0;
     double next_scale = 0.0;
     int k = 0;
+    bool broke = false;                                 // happy breakdown
     for (int j = 0; j < m; ++j) {
       if (!Bop(V[j].data(), z.data())) { out.status = 2; return out; }
       Aop(z.data(), t.data());
@@ -963,10 +1075,11 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       }
       double hn;
       if (orth == 2) {
-        // DCGS2 (R14).  V[0..j) final; V[j] provisional = u_{j-1} / nu (the previous
-        // step's once-projected vector, stored unnormalised: nu = 1 for j >= 1, V[0] is
-        // final: nu = rho = 1), whose second projection h2p = V[0..j)^T V[j] and
-        // rho = ||V[j] - V[0..j) h2p|| are known; w = A B V[j].
+        // DCGS2 (R14), textbook form with a NORMALISED provisional vector (the product
+        // stores it unnormalised; the two agree in exact arithmetic).  V[0..j) final;
+        // V[j] provisional = u_{j-1} / nu with nu = ||u_{j-1}|| (V[0] is final: nu = rho
+        // = 1); h2p = V[0..j)^T u_{j-1} and rho = ||u_{j-1} - V[0..j) h2p|| are known from
+        // the previous step; w = A B V[j].
         // (1) a_i = V[i]^T w for i <= j (one pass)
         std::vector<double> a(j + 1);
         for (int i = 0; i <= j; ++i) a[i] = dot(V[i], w);
@@ -992,6 +1105,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
         const double uu = dot(w, w);
         double ss = 0.0;
         for (int i = 0; i <= j; ++i) ss += h2n[i] * h2n[i];
+        const double nun = std::sqrt(uu);
         const double rhon = std::sqrt(std::max(uu - ss, 0.0));
         // (5) Hessenberg column j of the final basis:
         //     A B v_j = (nu A B V[j] - sum_{l<j} h2p_l A B v_l) / rho,
@@ -1004,9 +1118,9 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
           h(i) = Hraw[(size_t)i * m + j];
         }
         hn = h(j + 1);
-        next_scale = 1.0;                                // V[j+1] provisional = u (unnormalised)
+        next_scale = nun;                                // V[j+1] provisional = u / ||u||
         h2p = h2n;
-        nu = 1.0;
+        nu = nun;
         rhop = rhon;
       } else {
         hn = nrm2(w);
@@ -1029,7 +1143,8 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       const double est = std::fabs(gam[j + 1]) / bnorm;
       out.hist.push_back(est);
       k = j + 1;
-      if (est <= tol || hn < 1e-14 * bnorm || out.iters >= maxit) break;
+      broke = hn < 1e-14 * bnorm;
+      if (est <= tol || broke || out.iters >= maxit) break;
       for (size_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / next_scale;
     }
     std::vector<double> y(k);
@@ -1049,6 +1164,8 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
     out.final_rel = beta / bnorm;
     out.hist.push_back(out.final_rel);
     if (out.final_rel <= tol) return out;
+    // invariant Krylov space with the true residual above tol: MSP_EBREAKDOWN (4)
+    if (broke) { out.status = 4; return out; }
     if (out.iters >= maxit) { out.status = 3; return out; }
   }
 }
@@ -1320,6 +1437,65 @@ int orc_msp_bilu_apply(void* h, const double* r, double* x) {
   return 0;
 }
 int orc_msp_apply(void* h, const double* g, double* w) { return msp_apply(*(Msp*)h, g, w) ? 0 : 2; }
+
+// per-step entry points of the hot path (parity tests of the individual kernels)
+int orc_msp_restrict_pressure(void* h, const double* g, double* rp) {      // a3
+  restrict_pressure(*(Msp*)h, g, rp);
+  return 0;
+}
+int orc_msp_level_resid_restrict(void* h, int l, const double* b, const double* x, double* bc) {   // a5
+  Msp* M = (Msp*)h;
+  if (l < 0 || l >= (int)M->H.lv.size()) return 1;
+  residual_restrict(M->H.lv[l], b, x, bc);
+  return 0;
+}
+int orc_msp_level_prolong(void* h, int l, const double* e, double* x) {   // a7 (x updated in place)
+  Msp* M = (Msp*)h;
+  if (l < 0 || l >= (int)M->H.lv.size()) return 1;
+  prolong_correct(M->H.lv[l], e, x);
+  return 0;
+}
+int orc_msp_bilu_forward(void* h, const double* r, double* y, int absmode) {
+  bilu_forward(((Msp*)h)->R, r, y, absmode != 0);
+  return 0;
+}
+int orc_msp_bilu_backward(void* h, const double* y, double* x, int absmode) {
+  bilu_backward(((Msp*)h)->R, y, x, absmode != 0);
+  return 0;
+}
+int orc_msp_bilu_apply_by_color(void* h, const double* r, double* x) {
+  bilu_apply_by_color(((Msp*)h)->R, r, x);
+  return 0;
+}
+// test hook: replace the BILU factors (natural BSR storage, row-major blocks) and D~^-1,
+// e.g. by integer-valued factors for the bit-exact substitution tests
+int orc_msp_bilu_set_factors(void* h, const double* F, const double* Dinv) {
+  Msp* M = (Msp*)h;
+  std::copy(F, F + M->R.F.val.size(), M->R.F.val.begin());
+  std::copy(Dinv, Dinv + M->R.Dinv.size(), M->R.Dinv.begin());
+  return 0;
+}
+// block color and ABMC block id of every cell (natural numbering); returns #colors
+int orc_msp_bilu_blocks(void* h, int* color, int* blk) {
+  Msp* M = (Msp*)h;
+  int g = 0;
+  for (int c = 0; c < M->A.n; ++c) {
+    color[c] = M->R.color[c];
+    blk[c] = M->R.blk[c];
+    g = std::max(g, color[c] + 1);
+  }
+  return g;
+}
+// a10: out[i] = V[i]^T w for k vectors of length N stored consecutively (index-ascending
+// sums from +0.0, the plain definition)
+int orc_dots(long long N, int k, const double* V, const double* w, double* out) {
+  for (int i = 0; i < k; ++i) {
+    double s = 0.0;
+    for (long long q = 0; q < N; ++q) s += V[(size_t)i * N + q] * w[q];
+    out[i] = s;
+  }
+  return 0;
+}
 
 // B_N r (stages = 3 handles only): N-part of the result, n*nc doubles
 int orc_msp_bgs_apply(void* h, const double* r, double* wN) {

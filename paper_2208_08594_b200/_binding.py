@@ -65,7 +65,9 @@ for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats",
            "msp_host_setup_info", "msp_host_setup_level_dims", "msp_host_setup_level_csr",
            "msp_host_setup_level_colors", "msp_host_setup_level_agg", "msp_host_setup_weights",
            "msp_host_setup_order", "msp_partition_owner", "msp_nccl_unique_id", "msp_setup_dist",
-           "msp_dist_owned_cells", "msp_loopback_solve", "msp_dist_plan"):
+           "msp_dist_owned_cells", "msp_loopback_solve", "msp_dist_plan", "msp_restrict_pressure",
+           "msp_residual_restrict", "msp_prolong", "msp_pcol_residual", "msp_bilu_forward",
+           "msp_bilu_backward", "msp_multidot", "msp_bilu_set_factors", "msp_set_stream"):
     getattr(_lib, _n).restype = ctypes.c_int
 _lib.msp_destroy.argtypes = [ctypes.c_void_p]
 _lib.msp_time_kernel.restype = ctypes.c_int
@@ -131,6 +133,20 @@ class _TorchAllocator:
             pass
 
 
+def _caller_stream(stream):
+    """The stream the library orders its work after: the given one, else PyTorch's current
+    stream (so tensors written by torch are complete before the library reads them)."""
+    if stream:
+        return int(stream)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return int(torch.cuda.current_stream().cuda_stream)
+    except ImportError:
+        pass
+    return 0
+
+
 class MspSolver:
     """msp_setup / msp_solve handle.  A given as BSR arrays (natural cell order, row-major
     b x b blocks, unknown 0 = pressure).  Vectors may be numpy arrays (host) or torch
@@ -157,7 +173,7 @@ class MspSolver:
         rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
         A, keep = _bsr(rp, ci, v)
         h = ctypes.c_void_p()
-        st = _lib.msp_setup(ctypes.byref(A), nc, ctypes.byref(c), ctypes.c_void_p(stream or 0),
+        st = _lib.msp_setup(ctypes.byref(A), nc, ctypes.byref(c), ctypes.c_void_p(_caller_stream(stream)),
                             ctypes.byref(h))
         if st:
             raise MspError(st, _lib.msp_last_error(None).decode())
@@ -228,6 +244,52 @@ class MspSolver:
     def bilu_apply(self, r, x):
         self._check(_lib.msp_bilu_apply(self._h, _ptr(r), _ptr(x)))
         return x
+
+    # single hot-path steps (per-kernel parity tests); device tensors, natural order
+    def restrict_pressure(self, g, rp):
+        """a3: rp = W^T g."""
+        self._check(_lib.msp_restrict_pressure(self._h, _ptr(g), _ptr(rp)))
+        return rp
+
+    def residual_restrict(self, level, b, x, bc):
+        """a5 on AMG level `level`: bc = P^T (b - A x)."""
+        self._check(_lib.msp_residual_restrict(self._h, level, _ptr(b), _ptr(x), _ptr(bc)))
+        return bc
+
+    def prolong(self, level, e, x):
+        """a7: x += P e (in place)."""
+        self._check(_lib.msp_prolong(self._h, level, _ptr(e), _ptr(x)))
+        return x
+
+    def pcol_residual(self, g, xp, r):
+        """a8: r = g - A Pi_P xp."""
+        self._check(_lib.msp_pcol_residual(self._h, _ptr(g), _ptr(xp), _ptr(r)))
+        return r
+
+    def bilu_forward(self, r, y):
+        self._check(_lib.msp_bilu_forward(self._h, _ptr(r), _ptr(y)))
+        return y
+
+    def bilu_backward(self, y, x):
+        self._check(_lib.msp_bilu_backward(self._h, _ptr(y), _ptr(x)))
+        return x
+
+    def multidot(self, V, w):
+        """a10: V_i^T w for the k rows of V (k x N device tensor); returns numpy (k,)."""
+        k = int(V.shape[0])
+        out = np.zeros(k)
+        self._check(_lib.msp_multidot(self._h, k, _ptr(V), _ptr(w), _ptr(out)))
+        return out
+
+    def set_bilu_factors(self, F):
+        """Test hook: replace the BILU factors (natural entry order, row-major, D~^-1 on the
+        diagonal slots; the layout bilu_factors() returns)."""
+        F = _np(F, np.float64)
+        self._check(_lib.msp_bilu_set_factors(self._h, _ptr(F)))
+
+    def set_stream(self, stream):
+        """Order every later call after the work queued on `stream` (a cudaStream_t int)."""
+        self._check(_lib.msp_set_stream(self._h, ctypes.c_void_p(stream or 0)))
 
     def bilu_factors(self):
         """(nnzb, b, b) BILU(0) factors, natural entry order; diagonal slots hold D~^-1."""
@@ -300,7 +362,7 @@ class DistSolver(MspSolver):
         uid = ctypes.create_string_buffer(bytes(unique_id), 128)
         h = ctypes.c_void_p()
         st = _lib.msp_setup_dist(ctypes.byref(A), nc, ctypes.byref(c), _ptr(own) if own is not None else None,
-                                 uid, rank, nranks, ctypes.c_void_p(stream or 0), ctypes.byref(h))
+                                 uid, rank, nranks, ctypes.c_void_p(_caller_stream(stream)), ctypes.byref(h))
         if st:
             raise MspError(st, _lib.msp_last_error(None).decode())
         self._h = h

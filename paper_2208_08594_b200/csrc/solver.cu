@@ -140,6 +140,10 @@ struct msp_handle {
   int64_t nlaunch = 0;
   std::vector<int64_t> graph_kernels;
   double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
+  double* ftmp = nullptr;            // msp_bilu_set_factors scratch
+  cudaStream_t caller = nullptr;     // the caller's stream (msp_setup / msp_set_stream)
+  cudaEvent_t ev_in = nullptr;       // orders h->s after the caller's prior work
+  bool valid = false;                // false after a failed (re)SETUP: compute calls rejected
   // distributed (z-slab) mode: owned cells [0, n), ghost cells after them
   std::unique_ptr<msp::Comm> comm;   // null: single GPU
   int rank = 0, nranks = 1;
@@ -188,6 +192,8 @@ struct msp_handle {
     }
     allocs.clear();
     bytes = 0;
+    ftmp = nullptr;
+    flush = nullptr;
     lv.clear();
     V = nullptr;
     V_m = -1;
@@ -477,6 +483,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   T.mark(gpu_bilu ? "BILU pattern (host)" : "BILU factorization (host)");
 
   h->free_all();
+  h->valid = false;                  // until this SETUP completes (see msp_status docs)
   const int32_t n = A.n;
   const int b = A.b, bb = b * b;
   h->n = n;
@@ -781,6 +788,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   } else {
     h->dvp = nullptr;
   }
+  h->valid = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1136,8 +1144,11 @@ void exch_l0(msp_handle* h, double* x, int seg) {
   if (h->comm) h->comm->halo(h->s, h->l0_halo, x, h->lv[0].n, 1, seg);
 }
 
+// half: 0 both substitutions (the MSP apply), 1 forward only (v: r -> y), 2 backward only
+// (v: y -> x, z = x + wp) -- the halves exist for the per-kernel parity tests
 template <int B, int MAXC, bool WF = false>
-void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, const double* gf = nullptr) {
+void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, const double* gf = nullptr,
+                       int half = 0) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
   const int g = h->bilu_ncolor;
   auto run = [&](int c, int kind) {
@@ -1164,6 +1175,14 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, co
     else
       klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
   };
+  if (half == 1) {
+    for (int c = 0; c < g; ++c) run(c, 0);
+    return;
+  }
+  if (half == 2) {
+    for (int c = g - 1; c >= 0; --c) run(c, 1);
+    return;
+  }
   // distributed: after each color phase, the ghost copies of that color's cells are
   // refreshed (y after the forward phase, x after the backward phase)
   for (int c = 0; c < g - 1; ++c) { run(c, 0); exch_cell(h, v, B, c); }
@@ -1174,7 +1193,14 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, co
 
 template <int B>
 void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
-                   const double* gf = nullptr) {
+                   const double* gf = nullptr, int half = 0) {
+  if (half) {
+    if (h->max_blk > 4) throw std::pair<int, std::string>(MSP_EINVAL, "BILU halves need blocks of <= 4 cells");
+    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z, nullptr, half);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z, nullptr, half);
+    else launch_bilu_block<B, 4>(h, v, wp, z, nullptr, half);
+    return;
+  }
   if (wfull) {                                         // z = w (full vector) + R r
     if (h->max_blk <= 1) launch_bilu_block<B, 1, true>(h, v, wp, z);
     else if (h->max_blk <= 2) launch_bilu_block<B, 2, true>(h, v, wp, z);
@@ -1207,9 +1233,9 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool w
 }
 
 void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
-                 const double* gf = nullptr) {
+                 const double* gf = nullptr, int half = 0) {
   switch (h->b) {
-#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull, gf); break;
+#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull, gf, half); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -1909,6 +1935,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       nup = 1.0;
       rhop = 1.0;
       int k = 0;
+      bool broke = false;                    // happy breakdown: h_{j+1,j} < 1e-14 ||b||
       for (int j = 0; j < m; ++j) {
         run_step(h, j, m);
         CK(cudaStreamSynchronize(h->s));
@@ -1945,7 +1972,8 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         const double est = std::fabs(gam[j + 1]) / bnorm;
         push(est);
         k = j + 1;
-        if (est <= tol || hn < 1e-14 * bnorm || it >= maxit) break;
+        broke = hn < 1e-14 * bnorm;
+        if (est <= tol || broke || it >= maxit) break;
       }
       for (int i = k - 1; i >= 0; --i) {
         double s = 0.0;
@@ -1970,6 +1998,9 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       rel = beta / bnorm;
       push(rel);
       if (rel <= tol) break;
+      // the Krylov space became invariant yet the true residual is above tol: restarting
+      // cannot help (the preconditioned operator is singular on it)
+      if (broke) { status = MSP_EBREAKDOWN; break; }
       if (it >= maxit) { status = MSP_ENOCONV; break; }
     }
   }
@@ -1997,6 +2028,17 @@ msp_status guarded(msp_handle* h, F&& f) {
   } catch (const std::bad_alloc&) {
     return fail(h, MSP_ENOMEM, "host allocation failed");
   }
+}
+
+// Every entry point that reads caller buffers first orders the handle's (non-blocking)
+// stream after the work already queued on the caller's stream, so a buffer written there
+// (e.g. by PyTorch on the legacy default stream) is complete before any kernel reads it.
+// Rejects handles whose last SETUP failed.
+void sync_in(msp_handle* h) {
+  if (!h->valid) throw std::pair<int, std::string>(MSP_EINVAL, "handle unusable: its last SETUP failed");
+  if (!h->ev_in) CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  CK(cudaEventRecord(h->ev_in, h->caller));
+  CK(cudaStreamWaitEvent(h->s, h->ev_in, 0));
 }
 
 // copy a caller vector (host or device, natural order) into internal order (dst)
@@ -2090,10 +2132,11 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
     CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
-    if (cuda_stream) {
+    h->caller = (cudaStream_t)cuda_stream;
+    {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CK(cudaEventRecord(e, (cudaStream_t)cuda_stream));
+      CK(cudaEventRecord(e, h->caller));
       CK(cudaStreamWaitEvent(h->s, e, 0));
       cudaEventDestroy(e);
     }
@@ -2109,20 +2152,29 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   return MSP_OK;
 }
 
+msp_status msp_set_stream(msp_handle* h, void* cuda_stream) {
+  if (!h) return fail(nullptr, MSP_EINVAL, "msp_set_stream: NULL handle");
+  h->caller = (cudaStream_t)cuda_stream;
+  return MSP_OK;
+}
+
 msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_iterations, int mu,
                       int* did_setup) {
   if (!h) return fail(nullptr, MSP_EINVAL, "msp_update: NULL handle");
   if (!A_new || A_new->block != h->b || !A_new->row_ptr || !A_new->col_idx || !A_new->values)
     return fail(h, MSP_EINVAL, "msp_update: invalid matrix");
-  // Remark 2: the preconditioner must be regenerated when the size changed
-  bool same = (A_new->n_cells == h->n);
+  // Remark 2: the preconditioner must be regenerated when the size changed.  Sizes and
+  // patterns are compared GLOBALLY (the caller passes the global matrix on every rank of
+  // a distributed handle, whose h->n is the owned-cell count)
+  const int64_t n_glob = (int64_t)h->nat_rp.size() - 1;
+  bool same = h->valid && (A_new->n_cells == n_glob);
   if (same) {
-    std::vector<int32_t> rp(h->n + 1);
+    std::vector<int32_t> rp(n_glob + 1);
     if (A_new->device >= 0) {
-      if (cudaMemcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (h->n + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+      if (cudaMemcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (n_glob + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
         return fail(h, MSP_ECUDA, "msp_update: row_ptr copy failed");
     } else {
-      std::memcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (h->n + 1));
+      std::memcpy(rp.data(), A_new->row_ptr, sizeof(int32_t) * (n_glob + 1));
     }
     same = (rp == h->nat_rp);
     if (same) {
@@ -2151,6 +2203,7 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
   }
   // reuse: keep W, hierarchy and BILU factors; refresh A (SpMV, Alg. 1 residuals) on the GPU
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     const int bb = h->b * h->b;
     const size_t nv = (size_t)h->nnzb * bb;                   // local entries to refresh
     const size_t nglob = h->nat_ci.size() * (size_t)bb;        // caller's (global) values
@@ -2183,6 +2236,7 @@ msp_status msp_solve(msp_handle* h, const double* b, double* x, double tol, int 
   if (!iterations) iterations = &it_dummy;
   if (!final_rel_res) final_rel_res = &fr_dummy;
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     CK(cudaEventRecord(h->ev0, h->s));
     to_internal(h, b, h->bin, h->n, h->b);
     to_internal(h, x, h->xin, h->n, h->b);
@@ -2200,6 +2254,7 @@ msp_status msp_solve(msp_handle* h, const double* b, double* x, double tol, int 
 msp_status msp_apply(msp_handle* h, const double* g, double* w) {
   if (!h || !g || !w) return fail(h, MSP_EINVAL, "msp_apply: NULL argument");
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     to_internal(h, g, h->bin, h->n, h->b);
     msp_apply_dev(h, h->bin, h->z);
     from_internal(h, h->z, w, h->b);
@@ -2210,6 +2265,7 @@ msp_status msp_apply(msp_handle* h, const double* g, double* w) {
 msp_status msp_spmv(msp_handle* h, const double* x, double* y) {
   if (!h || !x || !y) return fail(h, MSP_EINVAL, "msp_spmv: NULL argument");
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     launch_spmv(h, 0, x, nullptr, y);
     CK(cudaStreamSynchronize(h->s));
     return MSP_OK;
@@ -2219,6 +2275,7 @@ msp_status msp_spmv(msp_handle* h, const double* x, double* y) {
 msp_status msp_pgs_sweep(msp_handle* h, int level, const double* b, double* x, int ascending) {
   if (!h || level < 0 || level >= (int)h->lv.size()) return fail(h, MSP_EINVAL, "msp_pgs_sweep: bad level");
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     DevLevel& L = h->lv[level];
     klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, b, L.b, 1); ++h->nlaunch;
     klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, x, L.x, 1); ++h->nlaunch;
@@ -2249,6 +2306,7 @@ msp_status msp_bilu_factors(msp_handle* h, double* F_out) {
 msp_status msp_vcycle(msp_handle* h, const double* r, double* x) {
   if (!h || !r || !x) return fail(h, MSP_EINVAL, "msp_vcycle: NULL argument");
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     if (h->lv.empty()) {
       CK(cudaMemcpyAsync(h->bL, r, sizeof(double) * h->nL, cudaMemcpyDeviceToDevice, h->s));
       vcycle_any(h);
@@ -2267,10 +2325,146 @@ msp_status msp_vcycle(msp_handle* h, const double* r, double* x) {
 msp_status msp_bilu_apply(msp_handle* h, const double* r, double* x) {
   if (!h || !r || !x) return fail(h, MSP_EINVAL, "msp_bilu_apply: NULL argument");
   return guarded(h, [&]() -> msp_status {
+    sync_in(h);
     to_internal(h, r, h->r, h->n, h->b);
     CK(cudaMemsetAsync(h->wp, 0, sizeof(double) * h->n, h->s));
     launch_bilu(h, h->r, h->wp, h->z);
     from_internal(h, h->z, x, h->b);
+    return MSP_OK;
+  });
+}
+
+// ---- per-kernel entry points (parity tests of single hot-path steps) ----
+msp_status msp_restrict_pressure(msp_handle* h, const double* g, double* rp) {
+  if (!h || !g || !rp || h->comm) return fail(h, MSP_EINVAL, "msp_restrict_pressure: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    to_internal(h, g, h->bin, h->n, h->b);
+    launch_restrict_pressure(h, h->bin, level0_b(h), false);
+    if (h->lv.empty()) {
+      CK(cudaMemcpyAsync(rp, h->bL, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->s));
+    } else {
+      DevLevel& L = h->lv[0];
+      klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, (const double*)L.b, rp, 0);
+      ++h->nlaunch;
+    }
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_residual_restrict(msp_handle* h, int level, const double* b, const double* x, double* bc) {
+  if (!h || !b || !x || !bc || level < 0 || level >= (int)h->lv.size() || (h->comm && level == 0))
+    return fail(h, MSP_EINVAL, "msp_residual_restrict: bad level/arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    DevLevel& L = h->lv[level];
+    const bool last = (level + 1 == (int)h->lv.size());
+    double* bn = last ? h->bL : h->lv[level + 1].b;
+    const int nn = last ? h->nL : h->lv[level + 1].n;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, b, L.b, 1); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, x, L.x, 1); ++h->nlaunch;
+    sell_rows_any<false, true>(h, L, 0, L.nslices);                     // r = b - A x, every row
+    klaunch(h->s, h->pdl, restrict_kernel, nblk(nn, 256), 256, nn, L.pt_ptr, L.pt_idx, (const double*)L.r, bn,
+            (double*)nullptr, (const double*)nullptr, 0);
+    ++h->nlaunch;
+    if (last) {
+      CK(cudaMemcpyAsync(bc, bn, sizeof(double) * nn, cudaMemcpyDeviceToDevice, h->s));
+    } else {
+      klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(nn, 256), 256, nn, h->lv[level + 1].perm, (const double*)bn, bc, 0);
+      ++h->nlaunch;
+    }
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_prolong(msp_handle* h, int level, const double* e, double* x) {
+  if (!h || !e || !x || level < 0 || level >= (int)h->lv.size() || (h->comm && level == 0))
+    return fail(h, MSP_EINVAL, "msp_prolong: bad level/arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    DevLevel& L = h->lv[level];
+    const bool last = (level + 1 == (int)h->lv.size());
+    double* xn = last ? h->xL : h->lv[level + 1].x;
+    const int nn = last ? h->nL : h->lv[level + 1].n;
+    if (last) CK(cudaMemcpyAsync(xn, e, sizeof(double) * nn, cudaMemcpyDeviceToDevice, h->s));
+    else { klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(nn, 256), 256, nn, h->lv[level + 1].perm, e, xn, 1); ++h->nlaunch; }
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, (const double*)x, L.x, 1); ++h->nlaunch;
+    klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, (const double*)xn, L.x); ++h->nlaunch;
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, (const double*)L.x, x, 0); ++h->nlaunch;
+    CK(cudaStreamSynchronize(h->s));
+    return MSP_OK;
+  });
+}
+
+msp_status msp_pcol_residual(msp_handle* h, const double* g, const double* xp, double* r) {
+  if (!h || !g || !xp || !r || h->comm) return fail(h, MSP_EINVAL, "msp_pcol_residual: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    to_internal(h, g, h->bin, h->n, h->b);
+    klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(h->n, 256), 256, h->n, h->d_order, xp, h->wp, 0);   // wp[p] = xp[order[p]]
+    ++h->nlaunch;
+    launch_spmv(h, 2, h->wp, h->bin, h->r);
+    from_internal(h, h->r, r, h->b);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_bilu_forward(msp_handle* h, const double* r, double* y) {
+  if (!h || !r || !y || h->comm) return fail(h, MSP_EINVAL, "msp_bilu_forward: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    to_internal(h, r, h->r, h->n, h->b);
+    launch_bilu(h, h->r, h->wp, h->z, false, nullptr, 1);
+    from_internal(h, h->r, y, h->b);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_bilu_backward(msp_handle* h, const double* y, double* x) {
+  if (!h || !y || !x || h->comm) return fail(h, MSP_EINVAL, "msp_bilu_backward: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    to_internal(h, y, h->r, h->n, h->b);
+    CK(cudaMemsetAsync(h->wp, 0, sizeof(double) * h->n, h->s));
+    launch_bilu(h, h->r, h->wp, h->z, false, nullptr, 2);
+    from_internal(h, h->z, x, h->b);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_multidot(msp_handle* h, int k, const double* V, const double* w, double* out) {
+  if (!h || !V || !w || !out || k < 1 || k > kMaxV || h->comm) return fail(h, MSP_EINVAL, "msp_multidot: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    sync_in(h);
+    cgs_dot(h, k, V, w, h->dh1, nullptr, nullptr, -1);                  // a10 pass-1 kernel
+    CK(cudaMemcpyAsync(h->hpin, h->dh1, sizeof(double) * k, cudaMemcpyDeviceToHost, h->s));
+    CK(cudaStreamSynchronize(h->s));
+    std::memcpy(out, h->hpin, sizeof(double) * k);
+    return MSP_OK;
+  });
+}
+
+msp_status msp_bilu_set_factors(msp_handle* h, const double* F) {
+  if (!h || !F || h->comm) return fail(h, MSP_EINVAL, "msp_bilu_set_factors: bad arguments");
+  return guarded(h, [&]() -> msp_status {
+    const int b = h->b, bb = b * b;
+    const size_t nv = (size_t)h->nnzb * bb;
+    if (!h->ftmp) h->ftmp = h->dalloc<double>(nv);
+    CK(cudaMemcpyAsync(h->stage, F, sizeof(double) * nv, cudaMemcpyHostToDevice, h->s));
+    switch (b) {
+#define CASE(BV) case BV: \
+      klaunch(h->s, false, gather_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)h->nnzb, (const int*)h->d_src, \
+              (const double*)h->stage, h->ftmp); \
+      klaunch(h->s, false, transpose_blocks_kernel<BV>, nblk(nv, 256), 256, (int64_t)h->nnzb, (const double*)h->ftmp, \
+              h->Fval); \
+      break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    }
+    h->nlaunch += 2;
+    CK(cudaStreamSynchronize(h->s));
     return MSP_OK;
   });
 }
@@ -2300,6 +2494,7 @@ void msp_destroy(msp_handle* h) {
   h->free_all();
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->s) cudaStreamDestroy(h->s);
   delete h;
 }
@@ -2465,10 +2660,11 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
     CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
-    if (cuda_stream) {
+    h->caller = (cudaStream_t)cuda_stream;
+    {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CK(cudaEventRecord(e, (cudaStream_t)cuda_stream));
+      CK(cudaEventRecord(e, h->caller));
       CK(cudaStreamWaitEvent(h->s, e, 0));
       cudaEventDestroy(e);
     }

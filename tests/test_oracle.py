@@ -774,3 +774,253 @@ def test_cgs2_and_mgs_same_iterations_C1():
 def test_asmsp_decisions_golden():
     for c in GOLD["asmsp"]["cases"]:
         assert oracle.asmsp_decide(c["iota"], c["last_it"], c["mu"], c["dims_changed"]) == c["setup"]
+
+
+# ------------------------------------------------------------------ round 2 pins
+# c-9 (R5): the ABMC ordering itself, the forward/backward halves of Alg. 1 line 6, and the
+# "parallel by color" equivalence.
+ABMC_CASES = [("C2", dict(nx=9, ny=7, nz=4), dict()),
+              ("C2", dict(nx=9, ny=7, nz=4), dict(pair_passes=1)),
+              ("C2", dict(nx=9, ny=7, nz=4), dict(bilu_order=0)),
+              ("C2", dict(nx=6, ny=5, nz=4, nc=2), dict(decoupling=1)),
+              ("C1", dict(nx=6, ny=5, nz=3), dict(decoupling=0)),      # A_PP diagonal: cell Laplacian
+              ("C3", dict(nx=6, ny=11, nz=6), dict())]
+
+
+def block_nonzero(p):
+    """Z[c, d] = block (c, d) stored with a nonzero entry (c != d), dense n x n."""
+    n = p["n"]
+    Z = np.zeros((n, n), bool)
+    for c in range(n):
+        for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+            d = p["col"][e]
+            if d != c and np.any(p["val"][e] != 0):
+                Z[c, d] = True
+    return Z | Z.T
+
+
+@pytest.mark.parametrize("name,gkw,kw", ABMC_CASES)
+def test_abmc_order_validity_bruteforce(name, gkw, kw):
+    """P:332-334 principles for the block coloring of R5, by O(n^2) brute force over all
+    cell pairs: (i) two cells of DIFFERENT blocks of the SAME color are never coupled;
+    (ii) every block of color c > 0 is coupled to some block of every earlier color (each
+    color class is a maximal independent set of the blocks left, Alg. 2); the order is
+    (color, block, cell) ascending; blocks are connected in the cell graph with <= 2^passes
+    cells."""
+    p = gen.make_config(name, **gkw)
+    n = p["n"]
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=30, **kw)
+    g, color, blk = M.bilu_blocks()
+    Z = block_nonzero(p)
+    same_color = color[:, None] == color[None, :]
+    diff_blk = blk[:, None] != blk[None, :]
+    assert not np.any(Z & same_color & diff_blk)
+    # maximality: block I of color c touches a block of every color c' < c
+    nb = blk.max() + 1
+    bcol = np.zeros(nb, int)
+    bcol[blk] = color
+    Q = np.zeros((nb, nb), bool)
+    cc, dd = np.nonzero(Z)
+    Q[blk[cc], blk[dd]] = True
+    np.fill_diagonal(Q, False)
+    for I in range(nb):
+        seen = set(bcol[np.flatnonzero(Q[I])].tolist())
+        assert all(c in seen for c in range(bcol[I])), I
+    order = M.order()
+    key = sorted(range(n), key=lambda c: (color[c], blk[c], c))
+    assert order.tolist() == key
+    passes = kw.get("pair_passes", 2)
+    for I in range(nb):
+        m = np.flatnonzero(blk == I)
+        assert 1 <= len(m) <= (1 if kw.get("bilu_order", 1) == 0 else 2 ** passes)
+        # connected inside the cell graph
+        reach = {m[0]}
+        stack = [m[0]]
+        while stack:
+            a = stack.pop()
+            for c in m:
+                if c not in reach and Z[a, c]:
+                    reach.add(c); stack.append(c)
+        assert len(reach) == len(m)
+    assert g == color.max() + 1
+
+
+@pytest.mark.parametrize("name,gkw,kw", ABMC_CASES)
+def test_bilu_parallel_by_color_equals_sequential(name, gkw, kw):
+    """Sequential-equivalent parallelism for the block smoother: the BILU
+    substitutions executed color by color (other blocks read from the snapshot before the
+    color phase) equal the sequential substitutions in the elimination order BIT FOR BIT."""
+    p = gen.make_config(name, **gkw)
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=30, **kw)
+    r = gen.random_vector(p["n"] * p["b"], 5)
+    assert np.array_equal(M.bilu_apply_by_color(r), M.bilu_apply(r))
+
+
+def test_bilu_coupled_cells_get_distinct_colors():
+    """Two coupled cells (RB): distinct colors, and the by-color substitution equals the
+    sequential one."""
+    rng = np.random.default_rng(2)
+    n, b = 2, 2
+    ptr = np.array([0, 2, 4]); col = np.array([0, 1, 0, 1])
+    val = rng.normal(size=(4, b, b)) + 5 * np.eye(b)
+    M = oracle.Msp(ptr, col, val, decoupling=0, bilu_order=0, coarsest_max_dof=100)
+    g, color, blk = M.bilu_blocks()
+    assert g == 2 and color[0] != color[1]             # coupled cells get different colors
+    r = rng.normal(size=n * b)
+    assert np.array_equal(M.bilu_apply_by_color(r), M.bilu_apply(r))
+
+
+def _lu_dense(M, p):
+    n, b = p["n"], p["b"]
+    F, Dinv = M.bilu_factors()
+    order = M.order()
+    pos = np.empty(n, int); pos[order] = np.arange(n)
+    L = np.eye(n * b); U = np.zeros((n * b, n * b))
+    for c in range(n):
+        for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+            d = p["col"][e]
+            sl = (slice(c * b, (c + 1) * b), slice(d * b, (d + 1) * b))
+            if pos[d] < pos[c]:
+                L[sl] = F[e]
+            elif pos[d] > pos[c]:
+                U[sl] = F[e]
+            else:
+                U[sl] = np.linalg.inv(Dinv[c])
+    return L, U
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0)])
+def test_bilu_forward_backward_are_triangular_solves(kw):
+    """Alg. 1 line 6 split in its two halves (R5): forward = (unit block-lower L)^-1 r,
+    backward = (block-upper U incl. D~)^-1 y, against dense scipy triangular solves in
+    natural numbering (L, U permuted by the elimination order); the abs-mode recurrences
+    bound |L^-1 r| and |U^-1 y| componentwise."""
+    p = gen.make_config("C2", nx=6, ny=5, nz=3, nc=2)
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=20, **kw)
+    L, U = _lu_dense(M, p)
+    r = gen.random_vector(p["n"] * p["b"], 8)
+    y = M.bilu_forward(r)
+    yref = np.linalg.solve(L, r)
+    assert np.max(np.abs(y - yref)) <= 1e-12 * np.max(np.abs(yref))
+    x = M.bilu_backward(y)
+    xref = np.linalg.solve(U, y)
+    assert np.max(np.abs(x - xref)) <= 1e-11 * np.max(np.abs(xref))
+    assert np.array_equal(M.bilu_backward(M.bilu_forward(r)), M.bilu_apply(r))
+    ya = M.bilu_forward(r, absmode=True)
+    assert np.all(ya >= np.abs(y) * (1 - 1e-14))
+    xa = M.bilu_backward(ya, absmode=True)
+    assert np.all(xa >= np.abs(x) * (1 - 1e-14))
+
+
+def test_vcycle_transfers_dense():
+    """a5 / a7 (P:459 UA-AMG): residual + restriction = P^T (b - A_l x) and
+    prolongation + correction = x + P e, against dense products with P from the aggregates."""
+    p = gen.make_config("C2", nx=12, ny=10, nz=3)
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=40)
+    L = M.info()["levels"]
+    assert L >= 2
+    for l in range(L):
+        ptr, col, val = M.level_csr(l)
+        n = len(ptr) - 1
+        A = sp.csr_matrix((val, col, ptr), shape=(n, n)).toarray()
+        nn, agg = M.level_agg(l)
+        P = np.zeros((n, nn)); P[np.arange(n), agg] = 1
+        b = gen.random_vector(n, 30 + l); x = gen.random_vector(n, 40 + l)
+        bc = M.residual_restrict(l, b, x)
+        ref = P.T @ (b - A @ x)
+        assert np.max(np.abs(bc - ref)) <= 1e-12 * (P.T @ (np.abs(b) + np.abs(A) @ np.abs(x))).max()
+        e = gen.random_vector(nn, 50 + l)
+        assert np.array_equal(M.prolong(l, e, x), x + P @ e)
+        # integer inputs: exact
+        bi = gen.integer_vector(n, 60 + l); xi = gen.integer_vector(n, 70 + l)
+        Ai = np.round(A)
+        if np.array_equal(Ai, A):
+            assert np.array_equal(M.residual_restrict(l, bi, xi), P.T @ (bi - A @ xi))
+
+
+def test_restrict_pressure_dense_and_dots():
+    """a3: r_p = W^T g (R4) against the dense block-row product of the weights; a10 dots
+    against numpy."""
+    p = gen.make_config("C1", nx=4, ny=3, nz=2)
+    n, b = p["n"], p["b"]
+    for mode in (0, 1, 2):
+        M = oracle.Msp(p["row_ptr"], p["col"], p["val"], decoupling=mode)
+        W = M.weights()
+        Wt = np.zeros((n, n * b))
+        for c in range(n):
+            Wt[c, c * b:(c + 1) * b] = W[c]
+        g = gen.random_vector(n * b, 3)
+        rp = M.restrict_pressure(g)
+        assert np.max(np.abs(rp - Wt @ g)) <= 1e-14 * (np.abs(Wt) @ np.abs(g)).max()
+        if mode == 0:
+            assert np.array_equal(rp, g[0::b])               # NONE: the pressure slots
+    rng = np.random.default_rng(0)
+    V = rng.normal(size=(7, 1001)); w = rng.normal(size=1001)
+    assert np.allclose(oracle.dots(V, w), V @ w, rtol=1e-13, atol=1e-13)
+    Vi = rng.integers(-20, 20, size=(5, 333)).astype(float); wi = rng.integers(-20, 20, size=333).astype(float)
+    assert np.array_equal(oracle.dots(Vi, wi), Vi @ wi)
+
+
+def test_qi_weights_closed_form():
+    """R4 QI: w_c = [1, y], D_NN^T y = -D_0N^T with D the diagonal block.  Diagonal blocks
+    built with D_NN = d I and D_0N = -d a (d a power of two) give y = a exactly; on random
+    blocks the defining equation holds to rounding (numpy solve of each nc x nc system)."""
+    p = gen.make_config("C2", nx=5, ny=4, nz=3)
+    n, b = p["n"], p["b"]
+    rng = np.random.default_rng(12)
+    val = p["val"].copy()
+    alpha = rng.uniform(0.5, 1.5, size=(n, b - 1))
+    for c in range(n):
+        for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+            if p["col"][e] == c:
+                d = 2.0 ** int(rng.integers(-4, 8))
+                val[e, 1:, 1:] = d * np.eye(b - 1)
+                val[e, 0, 1:] = -d * alpha[c]
+    M = oracle.Msp(p["row_ptr"], p["col"], val, decoupling=1, coarsest_max_dof=100000)
+    W = M.weights()
+    assert np.all(W[:, 0] == 1.0) and np.array_equal(W[:, 1:], alpha)
+    M2 = oracle.Msp(p["row_ptr"], p["col"], p["val"], decoupling=1, coarsest_max_dof=100000)
+    W2 = M2.weights()
+    for c in range(n):
+        e = [e for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]) if p["col"][e] == c][0]
+        D = p["val"][e]
+        y = np.linalg.solve(D[1:, 1:].T, -D[0, 1:])
+        assert np.allclose(W2[c, 1:], y, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("passes,expect", [(1, [[0, 1], [2, 3]]), (2, [[0, 1, 2, 3]])])
+def test_none_decoupling_cell_laplacian_blocks_chain(passes, expect):
+    """R5 with NONE decoupling on the Eq. 17 generator (A_PP diagonal): the ABMC blocks are
+    the NPAIR aggregates of the cell-graph Laplacian.  On a 4-cell chain the Laplacian is
+    [[1,-1],[-1,2,-1],[-1,2,-1],[-1,1]]: pass 1 pairs (0,1) (fewest neighbours, lowest
+    index) then (2,3); its Galerkin matrix [[1,-1],[-1,1]] pairs the two in pass 2."""
+    p = gen.make_config("C1", nx=4, ny=1, nz=1)
+    M = oracle.Msp(p["row_ptr"], p["col"], p["val"], decoupling=0, pair_passes=passes)
+    assert M.info()["coarse_diag"] or M.info()["levels"] == 0
+    ptr, col, val = M.level_csr(0)
+    A = sp.csr_matrix((val, col, ptr), shape=(4, 4)).toarray()
+    assert np.count_nonzero(A - np.diag(np.diag(A))) == 0          # A_PP diagonal (Eq. 17)
+    g, color, blk = M.bilu_blocks()
+    assert groups_of(blk.max() + 1, blk) == expect
+
+
+def test_stall_and_max_levels_give_estall():
+    """R11 stop rules ("coarsest ... 10000"): coarsening that keeps > 0.9 n on
+    a non-diagonal level -> MSP_ESTALL (5); reaching max_levels above coarsest_max_dof ->
+    MSP_ESTALL; a diagonal stalled level becomes the (exact, diagonal) coarsest."""
+    n = 100
+    A = np.diag(4.0 * np.ones(n))
+    A[0, 1] = A[1, 0] = -1.0                                 # one coupling: 99 aggregates
+    ptr, col, val = csr_of(A)
+    with pytest.raises(oracle.OracleError) as ei:
+        scalar_msp(ptr, col, val, coarsest_max_dof=10)
+    assert "(5)" in str(ei.value)
+    ptr, col, val = csr_of(poisson1d(64))
+    with pytest.raises(oracle.OracleError) as ei:
+        scalar_msp(ptr, col, val, coarsest_max_dof=1, max_levels=3)
+    assert "(5)" in str(ei.value)
+    ptr, col, val = csr_of(np.diag(np.arange(1.0, n + 1)))
+    M = scalar_msp(ptr, col, val, coarsest_max_dof=10)
+    assert M.info()["coarse_diag"]
+    r = gen.random_vector(n, 1)
+    assert np.allclose(M.vcycle(r), r / np.arange(1.0, n + 1), rtol=1e-15)
