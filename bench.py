@@ -287,14 +287,10 @@ def main():
     # estimated share of one solve of each HBM-bound kernel (launch counts per solve);
     # the V-cycle (many latency-bound launches) is reported in `kernels`, not as a roofline
     cyc = math.ceil(iters / RESTART)
-    fused_a8 = bool(st0.get("fused_a8"))      # a8 runs inside a9 (a9 timing/bytes include it)
-    if fused_a8 and "a9_bilu_apply" in kernels:
-        kernels["a9_bilu_apply"]["note"] = "a8 pressure-column residual fused into the forward phases"
-        kernels["a8_pcol_residual"]["note"] = "standalone kernel, not launched by the solve (fused into a9)"
     share = {
         "a2_bsr_spmv": kernels["a2_bsr_spmv"].get("ms", 0) * (iters + 2 * cyc + 1),
         "a9_bilu_apply": kernels.get("a9_bilu_apply", {}).get("ms", 0) * (iters + cyc),
-        "a8_pcol_residual": 0.0 if fused_a8 else kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
+        "a8_pcol_residual": kernels["a8_pcol_residual"].get("ms", 0) * (iters + cyc),
         "orth_step15": kernels.get("orth_step15", {}).get("ms", 0) * iters,
     }
     dom = max(share, key=share.get)

@@ -85,9 +85,8 @@ typedef struct {
                                 passes over the basis per step instead of three); 0 CGS2 (R8);
                                 1 MGS */
   int32_t use_graphs;        /* 1: replay each Arnoldi step as a CUDA graph (default) */
-  int32_t use_coop;          /* 0 (default): one graph node per PGS-MC color / transfer;
-                                1: whole V-cycle as one cooperative persistent kernel (measured
-                                slower on B200: grid.sync ~1.3 us vs ~1.2 us per graph node) */
+  int32_t use_coop;          /* must be 0 (a cooperative persistent V-cycle existed in round 1 and
+                                measured slower than graph replay: removed; 1 -> MSP_EINVAL) */
   int32_t smoother;          /* AMG smoother (NEXT-4, reading R13): 0 PGS-MC (Alg. 4,
                                 default), 1 PJAC-NO (Jacobi), 2 PGS-NO (hybrid Jacobi/GS:
                                 natural-order chunks of gs_chunk rows, GS inside a chunk) */
@@ -113,7 +112,7 @@ typedef struct {
   int32_t level_colors[24];  /* PGS-MC colors per smoothing level */
   int64_t device_bytes;      /* device memory held by the handle */
   int32_t kernels_per_iter;  /* kernel launches of one Arnoldi step */
-  int32_t fused_a8;          /* 1: the a8 residual runs inside the BILU forward kernels (4x4) */
+  int32_t fused_a8;          /* always 0 (the a8-in-BILU fusion measured slower and was removed) */
 } msp_stats;
 
 void msp_config_default(msp_config* cfg);

@@ -81,7 +81,8 @@ KERNEL_KINDS = {"a2_bsr_spmv": 0, "a4_pgs_sweep_l0": 1, "a8_pcol_residual": 2, "
                 "bilu": 8, "arnoldi_step15": 9, "cgs2_step15": 10, "arnoldi_step25": 11,
                 "cgs2_step25": 12,
                 # the configured orthogonalisation (DCGS2 by default) at steps 15 / 25
-                "orth_step15": 10, "orth_step25": 12}
+                "orth_step15": 10, "orth_step25": 12, "bilu_spmv": 13, "msp_apply_spmv": 14,
+                "spmv_orth15": 15}
 _lib.msp_host_setup_free.argtypes = [ctypes.c_void_p]
 
 

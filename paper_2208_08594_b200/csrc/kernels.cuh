@@ -14,10 +14,6 @@
 namespace mspk {
 
 constexpr int kSell = 32;
-#ifndef MSP_BILU_BATCH
-#define MSP_BILU_BATCH 0
-#endif
-constexpr bool kBiluBatch = MSP_BILU_BATCH != 0;
 #ifndef MSP_BILU_PREFETCH
 #define MSP_BILU_PREFETCH 1
 #endif
@@ -292,33 +288,6 @@ __global__ void gather_kernel(int n, const int* __restrict__ idx, const double* 
   if (c < n) out[c] = ldg(src + k);
 }
 
-// ---------------------------------------------------------------------------
-// a4 (K2): PGS-MC color sweep over SELL-32 (Alg. 4 line 5):
-// x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii for rows i of one color (independent,
-// P:434).  One thread per row; slice s_first.. of this color.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) pgs_color_kernel(int s_first, int s_end,
-                                                        const int* __restrict__ slice_row,
-                                                        const int* __restrict__ slice_off,
-                                                        const int* __restrict__ col,
-                                                        const double* __restrict__ val,
-                                                        const double* __restrict__ diag,
-                                                        const double* __restrict__ b,
-                                                        double* __restrict__ x) {
-  PDL_ENTRY();
-  const int s = s_first + (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
-  const int l = threadIdx.x % kSell;
-  if (s >= s_end) return;
-  const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
-  const int row = r0 + l;
-  if (row >= r1) return;
-  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
-  double acc = 0.0;
-  int o = o0 + l;
-#pragma unroll 4
-  for (int k = 0; k < w; ++k, o += kSell) acc = fma(ldg(val + o), x[ldg(col + o)], acc);
-  x[row] = (ldg(b + row) - acc) / ldg(diag + row);
-}
 
 // NEXT-4 comparison smoothers (reading R13), on the color-permuted SELL layout.
 // PJAC-NO: x_i = (b_i - sum_{j != i} a_ij xo_j) / a_ii for every row (xo: the values at
@@ -617,36 +586,6 @@ __global__ void __launch_bounds__(1024) sell_tail_kernel(int c_first, int c_last
   }
 }
 
-// coarsest GEMV, 4 independent 16-byte loads in flight per lane
-__global__ void __launch_bounds__(256) gemv4_kernel(int n, int ld, const double* __restrict__ Ainv,
-                                                    const double* __restrict__ b, double* __restrict__ x) {
-  PDL_ENTRY();
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  const double2* a = reinterpret_cast<const double2*>(Ainv + (size_t)row * ld);
-  const double2* bb = reinterpret_cast<const double2*>(b);
-  const int n2 = n >> 1;                       // pairs
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-  int j = lane;
-  for (; j + 96 < n2; j += 128) {
-    const double2 a0 = __ldg(a + j), a1 = __ldg(a + j + 32), a2 = __ldg(a + j + 64), a3 = __ldg(a + j + 96);
-    const double2 b0 = __ldg(bb + j), b1 = __ldg(bb + j + 32), b2 = __ldg(bb + j + 64), b3 = __ldg(bb + j + 96);
-    acc0 = fma(a0.x, b0.x, fma(a0.y, b0.y, acc0));
-    acc1 = fma(a1.x, b1.x, fma(a1.y, b1.y, acc1));
-    acc2 = fma(a2.x, b2.x, fma(a2.y, b2.y, acc2));
-    acc3 = fma(a3.x, b3.x, fma(a3.y, b3.y, acc3));
-  }
-  for (; j < n2; j += 32) {
-    const double2 a0 = __ldg(a + j), b0 = __ldg(bb + j);
-    acc0 = fma(a0.x, b0.x, fma(a0.y, b0.y, acc0));
-  }
-  double acc = (acc0 + acc1) + (acc2 + acc3);
-  if ((n & 1) && lane == 0) acc = fma(ldg(Ainv + (size_t)row * ld + n - 1), ldg(b + n - 1), acc);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) x[row] = acc;
-}
 
 // coarsest GEMV, 8 independent 16-byte loads in flight per lane; the first 8 of the
 // (immutable) inverse are issued before the PDL wait, overlapping the previous kernel
@@ -699,30 +638,6 @@ __global__ void __launch_bounds__(256) gemv8_kernel(int n, int ld, const double*
   if (lane == 0) x[row] = s;
 }
 
-// a5 part 1: residual r = b - A x over all rows of the level (SELL-32 + diagonal).
-__global__ void __launch_bounds__(128) sell_residual_kernel(int nslices,
-                                                            const int* __restrict__ slice_row,
-                                                            const int* __restrict__ slice_off,
-                                                            const int* __restrict__ col,
-                                                            const double* __restrict__ val,
-                                                            const double* __restrict__ diag,
-                                                            const double* __restrict__ b,
-                                                            const double* __restrict__ x,
-                                                            double* __restrict__ r) {
-  PDL_ENTRY();
-  const int s = (blockIdx.x * blockDim.x + threadIdx.x) / kSell;
-  const int l = threadIdx.x % kSell;
-  if (s >= nslices) return;
-  const int r0 = ldg(slice_row + s), r1 = ldg(slice_row + s + 1);
-  const int row = r0 + l;
-  if (row >= r1) return;
-  const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
-  double acc = ldg(diag + row) * ldg(x + row);
-  int o = o0 + l;
-#pragma unroll 4
-  for (int k = 0; k < w; ++k, o += kSell) acc = fma(ldg(val + o), ldg(x + ldg(col + o)), acc);
-  r[row] = ldg(b + row) - acc;
-}
 
 // a5 part 2: restriction b_{l+1}[I] = sum_{i in I} r_i (P^T, piecewise-constant P).
 // (fused: xc != null -> first color of the next level's pre-sweep from the zero guess)
@@ -759,28 +674,6 @@ __global__ void prolong_kernel(int n, const int* __restrict__ agg, const double*
   if (i < n) x[i] += ldg(e + a);
 }
 
-// a6 (K7): coarsest solve as a dense-inverse GEMV x = Ainv b (row-major).
-// One warp per row, 16-byte loads, warp-shuffle reduction.
-__global__ void __launch_bounds__(256) gemv_kernel(int n, int ld, const double* __restrict__ Ainv,
-                                                   const double* __restrict__ b,
-                                                   double* __restrict__ x) {
-  PDL_ENTRY();
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  const double* a = Ainv + (size_t)row * ld;   // ld: multiple of 32 (aligned rows)
-  double acc = 0.0;
-  const int n2 = n & ~1;
-  for (int j = 2 * lane; j < n2; j += 64) {
-    const double2 av = __ldg(reinterpret_cast<const double2*>(a + j));
-    acc = fma(av.x, ldg(b + j), acc);
-    acc = fma(av.y, ldg(b + j + 1), acc);
-  }
-  if ((n & 1) && lane == 0) acc = fma(ldg(a + n - 1), ldg(b + n - 1), acc);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) x[row] = acc;
-}
 
 __global__ void diag_solve_kernel(int n, const double* __restrict__ d, const double* __restrict__ b,
                                   double* __restrict__ x) {
@@ -789,8 +682,11 @@ __global__ void diag_solve_kernel(int n, const double* __restrict__ d, const dou
   if (i < n) x[i] = ldg(b + i) / ldg(d + i);
 }
 
+
+
 // ---------------------------------------------------------------------------
-// a9 (K4): BILU(0) substitution in ABMC order (R5).  One team of TS lanes per
+// a9 (K4), general form for aggregate blocks of any size (pair_passes >= 3): BILU(0)
+// substitution in ABMC order (R5).  One team of TS lanes per
 // aggregate block (blocks of one color are independent); the <= 4 cells of a block
 // are processed in order by the team.  Factors: rows in internal positions, L part
 // = entries [rp[i], dg[i]), U part = (dg[i], rp[i+1]), slot dg[i] holds D~_i^-1;
@@ -871,41 +767,6 @@ __global__ void __launch_bounds__(128) bilu_color_kernel(int b_first, int b_end,
   }
 }
 
-// External part of a 4x4 block-row product over entries [e0, e1), column-per-lane, with
-// up to 4 entries in flight (indices, then factor columns and vector components, then
-// FMAs): returns the 4 row partial sums of this lane's column contributions.
-__device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const int* __restrict__ ci,
-                                                 const double* __restrict__ F, const double* __restrict__ v,
-                                                 double& a0, double& a1, double& a2, double& a3) {
-  for (int base = e0; base < e1; base += 4) {
-    int k[4];
-    double2 lo[4], hi[4];
-    double vq[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) k[u] = (base + u < e1) ? __ldg(ci + base + u) : -1;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (k[u] >= 0) {
-        const double2* cp = reinterpret_cast<const double2*>(F + (size_t)(base + u) * 16 + q * 4);
-        lo[u] = ldstream2(cp);
-        hi[u] = ldstream2(cp + 1);
-        vq[u] = __ldg(v + (size_t)k[u] * 4 + q);
-      } else {
-        lo[u] = make_double2(0.0, 0.0);
-        hi[u] = lo[u];
-        vq[u] = 0.0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a0 = fma(lo[u].x, vq[u], a0);
-      a1 = fma(lo[u].y, vq[u], a1);
-      a2 = fma(hi[u].x, vq[u], a2);
-      a3 = fma(hi[u].y, vq[u], a3);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // a9 v2: BILU(0) color phase with one lane group (TS lanes) per CELL of an aggregate
 // block (<= MAXC cells): team = MAXC*TS lanes.  Phase 1 gathers, for every cell of
@@ -915,11 +776,7 @@ __device__ __forceinline__ void ext_sum4_batched(int e0, int e1, int q, const in
 // vectors through register shuffles.  Same arithmetic as bilu_color_kernel, only
 // the summation order differs (external before intra-block terms).
 // ---------------------------------------------------------------------------
-// FR (4x4 blocks, forward phases): the a8 residual of the pressure correction is fused
-// in: the cell's start value is r_i = g_i - sum_e Pcol_e wp[ci_e] over its whole row
-// (entry-per-lane, accumulated with the external-L sum before ONE reduce-scatter) instead
-// of a read of r written by a separate a8 launch.
-template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch, bool FR = false>
+template <int B, int MAXC, bool FWD, bool BWD, bool WFULL = false, bool PF = kBiluPrefetch>
 __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_kernel(int b_first, int b_end,
                                                          const int* __restrict__ blk_ptr,
                                                          const int* __restrict__ rp,
@@ -930,13 +787,10 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
                                                          const double* __restrict__ F,
                                                          double* v,
                                                          const double* __restrict__ wp,
-                                                         double* __restrict__ z,
-                                                         const double* __restrict__ gf,
-                                                         const double* __restrict__ pcol) {
+                                                         double* __restrict__ z) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int TM = MAXC * TS;
   static_assert(TM <= 32, "team must fit in a warp");
-  constexpr bool FR4 = FR && B == 4 && FWD;
   constexpr int BB = B * B;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int blk = b_first + gtid / TM;
@@ -1007,21 +861,6 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
     double acc = 0.0;
     if constexpr (B == 4) {                 // column-per-lane: 2 x 16 B loads, own y_q
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if constexpr (FR4) {                  // fused a8: pressure columns of the whole row
-        if (valid) {
-          const int r1 = ldg(rp + i + 1);
-#pragma unroll 2
-          for (int ee = e0 + q; ee < r1; ee += 4) {
-            const double xc = ldg(wp + ldg(ci + ee));
-            const double2* cp = reinterpret_cast<const double2*>(pcol + (size_t)ee * 4);
-            const double2 lo = ldstream2(cp), hi = ldstream2(cp + 1);
-            a0 = fma(lo.x, xc, a0);
-            a1 = fma(lo.y, xc, a1);
-            a2 = fma(hi.x, xc, a2);
-            a3 = fma(hi.y, xc, a3);
-          }
-        }
-      }
       int estart = e0;
       if constexpr (PFE > 0) {
 #pragma unroll
@@ -1035,8 +874,6 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
         }
         estart = min(eext, e0 + PFE);
       }
-      if (kBiluBatch) ext_sum4_batched(estart, eext, q, ci, F, v, a0, a1, a2, a3);
-      else
 #pragma unroll 2
       for (int ee = estart; ee < eext; ++ee) {
         const double yq = ldg(v + (size_t)ldg(ci + ee) * 4 + q);
@@ -1070,8 +907,7 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
         }
       }
     }
-    if constexpr (FR4) t = act ? (ldg(gf + (size_t)i * B + q) - acc) : 0.0;
-    else t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
+    t = act ? (v[(size_t)i * B + q] - acc) : 0.0;
     // intra-block triangle, cells in ascending order
 #pragma unroll
     for (int sidx = 0; sidx < MAXC - 1; ++sidx) {
@@ -1112,8 +948,6 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
           estart = min(e1, ei + PFE);
         }
       }
-      if (kBiluBatch) ext_sum4_batched(estart, e1, q, ci, F, v, a0, a1, a2, a3);
-      else
 #pragma unroll 2
       for (int e = estart; e < e1; ++e) {
         const double xq = ldg(v + (size_t)ldg(ci + e) * 4 + q);

@@ -19,9 +19,8 @@
 
 #include "../../include/msp.h"
 #include "comm.h"
-#include "coop.cuh"
-#include "cluster.cuh"
 #include "setup.h"
+#include "kernels.cuh"
 
 using namespace mspk;
 
@@ -107,7 +106,7 @@ struct msp_handle {
   int32_t* l0_of_cell = nullptr;
   int32_t* cell_of_l0 = nullptr;     // inverse map: level-0 row -> internal cell
   // ABMC blocks
-  int32_t bilu_ncolor = 0, max_blk = 1, bilu_v1 = 0, pcol_rowwise = 0, fuse_a8 = 0, gemv8 = 1, dcgs_staged = 1, dcgs_staged32 = 1, dcgs_staged16 = 1, dcgs_staged8 = 1;   // fuse_a8: measured slower
+  int32_t bilu_ncolor = 0, max_blk = 1;
   std::vector<int32_t> color_blk;    // host
   int32_t* blk_ptr = nullptr;
   int32_t* bcnt = nullptr;           // per cell: #external L | #intra U << 8
@@ -115,14 +114,8 @@ struct msp_handle {
   // AMG
   std::vector<DevLevel> lv;
   int32_t nL = 0, ldA = 0;
-  VParams* dvp = nullptr;            // device copy of the cooperative V-cycle parameters
-  int coop_grid = 0, coop_bps = 0, coop_tpb = 1024;
-  // cluster V-cycle legs (cluster.cuh): levels [cl_from, L) in one cl_size-CTA cluster
   int sell_tpb = 128;                        // CTA size of the LPR=1 (level-0) sweep kernels
-  int cl_from = 0, cl_size = 16;             // opt-in (MSP_CLUSTER_FROM): measured slower
-  bool cl_on = false;
   bool pdl = true;                   // programmatic dependent launch for every kernel
-  int cgs_split = 0;                 // nv > 16: 16-vector halves (see cgs_dot / cgs_axpy)
   bool coarse_diag = false;
   double *Ainv = nullptr, *cdiag = nullptr, *bL = nullptr, *xL = nullptr;
   // work vectors
@@ -318,7 +311,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   // sweep kernel then needs no slice metadata loads); <= 5 % extra entries
   const double avg_row = (double)rp[n] / std::max<int32_t>(n, 1);
   const bool uniform = avg_row <= 8.0 && wmax > 0 && wmax <= 8 && (double)wmax * L.nslices <= 1.05 * (double)tot &&
-                       !(std::getenv("MSP_SELL_UNIFORM") && std::atoi(std::getenv("MSP_SELL_UNIFORM")) == 0);
+                       true;
   for (int32_t s = 0; s < L.nslices; ++s) slice_off[s + 1] = slice_off[s] + (uniform ? wmax : sw[s]) * kSell;
   L.uniform_w = uniform ? wmax : 0;
   std::vector<int32_t> col(std::max<int32_t>(slice_off[L.nslices], 1));
@@ -442,7 +435,6 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
                    const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms);
 
-void setup_cluster(msp_handle* h);
 
 // BILU block kernels: per cell i of aggregate block [c0, c1) (<= 4 cells), the entry index
 // of (i, c0 + s) for every slot s of the block (-1: no coupling), with the diagonal entry
@@ -735,59 +727,6 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->st.levels = L;
   h->st.n_coarsest = h->nL;
   h->st.bilu_colors = h->bilu_ncolor;
-  setup_cluster(h);
-  // cooperative V-cycle parameters
-  if (h->prm.use_coop && L <= kMaxLevels) {
-    VParams vp;
-    std::memset(&vp, 0, sizeof(vp));
-    vp.L = L;
-    vp.pre = h->prm.pre_sweeps;
-    vp.post = h->prm.post_sweeps;
-    vp.nL = h->nL;
-    vp.ldA = h->ldA;
-    vp.coarse_diag = h->coarse_diag ? 1 : 0;
-    vp.Ainv = h->Ainv;
-    vp.cdiag = h->cdiag;
-    vp.bL = h->bL;
-    vp.xL = h->xL;
-    for (int l = 0; l < L; ++l) {
-      const DevLevel& D = h->lv[l];
-      LevelDev& E = vp.lv[l];
-      E.n = D.n;
-      E.ncolor = D.ncolor;
-      E.nslices = D.nslices;
-      E.fuse_rr = (l > 0) ? 1 : 0;
-      E.n_next = (l + 1 < L) ? h->lv[l + 1].n : h->nL;
-      E.color_row = D.d_color_row;
-      E.color_slice = D.d_color_slice;
-      E.slice_row = D.slice_row;
-      E.slice_off = D.slice_off;
-      E.col = D.col;
-      E.val = D.val;
-      E.diag = D.diag;
-      E.agg = D.agg;
-      E.pt_ptr = D.pt_ptr;
-      E.pt_idx = D.pt_idx;
-      E.row_start = D.row_start;
-      E.row_width = D.row_width;
-      E.b = D.b;
-      E.x = D.x;
-      E.r = D.r;
-    }
-    h->dvp = h->dalloc<VParams>(1);
-    CK(cudaMemcpyAsync(h->dvp, &vp, sizeof(vp), cudaMemcpyHostToDevice, h->s));
-    int nb = 0, nsm = 0;
-    h->coop_tpb = (h->coop_tpb == 256 || h->coop_tpb == 512) ? h->coop_tpb : 1024;
-    if (h->coop_tpb == 1024) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<1024>, 1024, 0));
-    else if (h->coop_tpb == 512) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<512>, 512, 0));
-    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vcycle_coop_kernel<256>, 256, 0));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
-    int bps = std::min(nb, h->coop_bps > 0 ? h->coop_bps : 1);
-    h->coop_grid = std::max(1, bps) * nsm;
-    CK(cudaStreamSynchronize(h->s));
-  } else {
-    h->dvp = nullptr;
-  }
   h->valid = true;
 }
 
@@ -1098,20 +1037,19 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
 }
 
 // ----------------------------------------------------------------- launches
-bool g_spmv4c = true;               // 4x4 blocks: column-per-lane SpMV (MSP_SPMV4C=0 to disable)
 
 template <int B>
 void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, const int* ci, const double* val,
                    const double* x, const double* g, double* y) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   const unsigned grid = nblk((size_t)n * TS, 256);
-  if (B == 4 && g_spmv4c && mode != 2) {
+  if (B == 4 && mode != 2) {
     if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, grid, 256, n, rp, ci, val, x, g, y);
     else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y);
     return;
   }
   if constexpr (B >= 5) {
-    if (g_spmv4c && mode != 2) {
+    if (mode != 2) {
       if (mode == 0) klaunch(s, pdl, bsr_spmv8c_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
       else klaunch(s, pdl, bsr_spmv8c_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
       return;
@@ -1125,7 +1063,7 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
 void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
-  if (mode == 2 && h->b == 4 && !h->pcol_rowwise) {
+  if (mode == 2 && h->b == 4) {
     klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)h->n * 4, 256), 256, h->n, h->rp, h->ci, val, x, g, y);
     return;
   }
@@ -1147,8 +1085,7 @@ void exch_l0(msp_handle* h, double* x, int seg) {
 // half: 0 both substitutions (the MSP apply), 1 forward only (v: r -> y), 2 backward only
 // (v: y -> x, z = x + wp) -- the halves exist for the per-kernel parity tests
 template <int B, int MAXC, bool WF = false>
-void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, const double* gf = nullptr,
-                       int half = 0) {
+void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, int half = 0) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
   const int g = h->bilu_ncolor;
   auto run = [&](int c, int kind) {
@@ -1156,24 +1093,12 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, co
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
-    const double* none = nullptr;
-    if constexpr (B == 4 && !WF) {
-      if (gf && kind != 1) {                   // forward phases with the fused a8 residual
-        if (kind == 0)
-          klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
-                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
-        else
-          klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF, kBiluPrefetch, true>, grid, 128, b0, b1,
-                  h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, gf, (const double*)h->Pcol);
-        return;
-      }
-    }
     if (kind == 0)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
     else if (kind == 1)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
     else
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, none, none);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
   };
   if (half == 1) {
     for (int c = 0; c < g; ++c) run(c, 0);
@@ -1192,13 +1117,12 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, co
 }
 
 template <int B>
-void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
-                   const double* gf = nullptr, int half = 0) {
+void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false, int half = 0) {
   if (half) {
     if (h->max_blk > 4) throw std::pair<int, std::string>(MSP_EINVAL, "BILU halves need blocks of <= 4 cells");
-    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z, nullptr, half);
-    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z, nullptr, half);
-    else launch_bilu_block<B, 4>(h, v, wp, z, nullptr, half);
+    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z, half);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z, half);
+    else launch_bilu_block<B, 4>(h, v, wp, z, half);
     return;
   }
   if (wfull) {                                         // z = w (full vector) + R r
@@ -1207,12 +1131,13 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool w
     else launch_bilu_block<B, 4, true>(h, v, wp, z);
     return;
   }
-  if (!h->bilu_v1 && h->max_blk <= 4) {
-    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z, gf);
-    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z, gf);
-    else launch_bilu_block<B, 4>(h, v, wp, z, gf);
+  if (h->max_blk <= 4) {
+    if (h->max_blk <= 1) launch_bilu_block<B, 1>(h, v, wp, z);
+    else if (h->max_blk <= 2) launch_bilu_block<B, 2>(h, v, wp, z);
+    else launch_bilu_block<B, 4>(h, v, wp, z);
     return;
   }
+  // aggregate blocks of more than 4 cells (pair_passes >= 3): one team per block
   constexpr int TS = (B <= 4) ? 4 : 8;
   const int g = h->bilu_ncolor;
   auto run = [&](int c, int kind) {
@@ -1232,10 +1157,9 @@ void launch_bilu_t(msp_handle* h, double* v, const double* wp, double* z, bool w
   for (int c = g - 2; c >= 0; --c) run(c, 1);
 }
 
-void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false,
-                 const double* gf = nullptr, int half = 0) {
+void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfull = false, int half = 0) {
   switch (h->b) {
-#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull, gf, half); break;
+#define CASE(BV) case BV: launch_bilu_t<BV>(h, v, wp, z, wfull, half); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -1260,102 +1184,12 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool 
   ++h->nlaunch;
 }
 
-// Cluster V-cycle legs: usable when levels [cl_from, L) exist below level 0 and one
-// cluster of cl_size CTAs x 1024 threads fits (16 needs the non-portable size; else 8).
-void setup_cluster(msp_handle* h) {
-  h->cl_on = false;
-  const int L = (int)h->lv.size();
-  if (h->cl_from < 1 || h->cl_from >= L || L - h->cl_from > kClMaxLevels || h->prm.pre_sweeps < 1 ||
-      h->prm.smoother != 0)
-    return;
-  for (int cs : {h->cl_size, 8}) {
-    if (cs < 1 || cs > 16) continue;
-    const int np = cs > 8 ? 1 : 0;
-    CK(cudaFuncSetAttribute(vcycle_cluster_down_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, np));
-    CK(cudaFuncSetAttribute(vcycle_cluster_up_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, np));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kClThreads);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int na = 0, nb = 0;
-    if (cudaOccupancyMaxActiveClusters(&na, vcycle_cluster_down_kernel, &cfg) != cudaSuccess ||
-        cudaOccupancyMaxActiveClusters(&nb, vcycle_cluster_up_kernel, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    if (na >= 1 && nb >= 1) {
-      h->cl_size = cs;
-      h->cl_on = true;
-      return;
-    }
-  }
-}
-
-ClParams cluster_params(msp_handle* h) {
-  ClParams P;
-  std::memset(&P, 0, sizeof(P));
-  const int L = (int)h->lv.size();
-  P.nlev = L - h->cl_from;
-  P.pre = h->prm.pre_sweeps;
-  P.post = h->prm.post_sweeps;
-  for (int l = h->cl_from; l < L; ++l) {
-    const DevLevel& D = h->lv[l];
-    ClLevel& E = P.lv[l - h->cl_from];
-    const bool last = (l + 1 == L);
-    E.n = D.n;
-    E.ncolor = D.ncolor;
-    E.lpr = D.lpr;
-    E.n_next = last ? h->nL : h->lv[l + 1].n;
-    E.c1_next = last ? 0 : h->lv[l + 1].color_row[1];
-    E.color_slice = D.d_color_slice;
-    E.slice_row = D.slice_row;
-    E.slice_off = D.slice_off;
-    E.col = D.col;
-    E.val = D.val;
-    E.diag = D.diag;
-    E.agg = D.agg;
-    E.pt_ptr = D.pt_ptr;
-    E.pt_idx = D.pt_idx;
-    E.b = D.b;
-    E.x = D.x;
-    E.r = D.r;
-    E.bn = last ? h->bL : h->lv[l + 1].b;
-    E.xn = last ? h->xL : h->lv[l + 1].x;
-    E.dn = last ? nullptr : h->lv[l + 1].diag;
-  }
-  return P;
-}
-
-void cluster_launch(msp_handle* h, void (*k)(const ClParams), const ClParams& P) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->cl_size);
-  cfg.blockDim = dim3(kClThreads);
-  cfg.stream = h->s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = h->cl_size;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  CK(cudaLaunchKernelEx(&cfg, k, P));
-  ++h->nlaunch;
-}
-
 void coarsest_solve(msp_handle* h) {
   ++h->nlaunch;
   if (h->coarse_diag)
     klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
   else
-    klaunch(h->s, h->pdl, h->gemv8 == 16 ? gemv8_kernel<16> : h->gemv8 ? gemv8_kernel<8> : gemv4_kernel,
+    klaunch(h->s, h->pdl, gemv8_kernel<8>,
             nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
 }
 
@@ -1479,13 +1313,6 @@ void vcycle(msp_handle* h, int l, bool init_done = false) {
     coarsest_solve(h);
     return;
   }
-  if (h->cl_on && l == h->cl_from && init_done) {     // levels >= cl_from in one cluster
-    const ClParams P = cluster_params(h);
-    cluster_launch(h, vcycle_cluster_down_kernel, P);
-    coarsest_solve(h);
-    cluster_launch(h, vcycle_cluster_up_kernel, P);
-    return;
-  }
   DevLevel& L = h->lv[l];
   const bool last = (l + 1 == (int)h->lv.size());
   double* bn = last ? h->bL : h->lv[l + 1].b;
@@ -1511,17 +1338,7 @@ void vcycle(msp_handle* h, int l, bool init_done = false) {
 double* level0_b(msp_handle* h) { return h->lv.empty() ? h->bL : h->lv[0].b; }
 double* level0_x(msp_handle* h) { return h->lv.empty() ? h->xL : h->lv[0].x; }
 
-void vcycle_any(msp_handle* h, bool init_done = false) {
-  if (h->dvp) {
-    void* args[] = {(void*)&h->dvp};
-    void* fn = (h->coop_tpb == 1024) ? (void*)vcycle_coop_kernel<1024>
-             : (h->coop_tpb == 512) ? (void*)vcycle_coop_kernel<512> : (void*)vcycle_coop_kernel<256>;
-    CK(cudaLaunchCooperativeKernel(fn, h->coop_grid, h->coop_tpb, args, 0, h->s));
-    ++h->nlaunch;
-  } else {
-    vcycle(h, 0, init_done);
-  }
-}
+void vcycle_any(msp_handle* h, bool init_done = false) { vcycle(h, 0, init_done); }
 
 void msp_apply_npr(msp_handle* h, const double* g, double* z);
 
@@ -1570,7 +1387,6 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
 }
 
 // z = B g (Alg. 1, stages P and R; internal order).  g must not alias z or h->r.
-bool a8_fused(const msp_handle* h) { return h->b == 4 && h->fuse_a8 && !h->bilu_v1 && h->max_blk <= 4; }
 
 void msp_apply_dev(msp_handle* h, const double* g, double* z) {
   if (h->comm) {
@@ -1581,16 +1397,12 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
     msp_apply_npr(h, g, z);
     return;
   }
-  const bool fuse = !h->dvp && h->prm.smoother == 0;                  // coop path inits itself
+  const bool fuse = h->prm.smoother == 0;
   launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
   vcycle_any(h, fuse);                                                 // a4-a7: B_P
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
-  if (a8_fused(h)) {
-    launch_bilu(h, h->r, h->wp, z, false, g);                          // a8 fused into a9's forward
-  } else {
-    launch_spmv(h, 2, h->wp, g, h->r);                                 // a8: r = g - A Pi_P x_p
-    launch_bilu(h, h->r, h->wp, z);                                    // a9: z = Pi_P x_p + R r
-  }
+  launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
+  launch_bilu(h, h->r, h->wp, z);                                      // a9: z = Pi_P x_p + R r
 }
 
 template <int B, int MAXC>
@@ -1643,12 +1455,6 @@ template <int NV>
 void maxpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
   klaunch(h->s, h->pdl, multiaxpy_kernel<NV>, kRedBlocks, kRedThreads, h->N, nv, V, h->N, coef, w, from_zero, part, 0); ++h->nlaunch;
 }
-void maxpy(msp_handle* h, int nv, const double* V, const double* coef, double* w, int from_zero, double* part) {
-  if (nv <= 4) maxpy_t<4>(h, nv, V, coef, w, from_zero, part);
-  else if (nv <= 8) maxpy_t<8>(h, nv, V, coef, w, from_zero, part);
-  else if (nv <= 16) maxpy_t<16>(h, nv, V, coef, w, from_zero, part);
-  else maxpy_t<32>(h, nv, V, coef, w, from_zero, part);
-}
 void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
              double* raw, int sq);
 
@@ -1688,7 +1494,7 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
   if (nv <= 4) cgs_dot_t<4>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_dot_t<8>(h, nv, V, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_dot_t<16>(h, nv, V, w, out, addend, raw, sq);
-  else if (h->cgs_split == 0) {
+  else {
     // 16 vectors per CTA row (gridDim.y = 2), 16-byte loads: full occupancy instead of
     // 32 accumulators per thread
     if (ew2_ok(h))
@@ -1698,7 +1504,7 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
       klaunch(h->s, h->pdl, cgs_dot_kernel<16, 1, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N, nv, V,
               h->N, w, h->part, out, addend, raw, sq, h->ticket);
     ++h->nlaunch;
-  } else cgs_dot_t<32>(h, nv, V, w, out, addend, raw, sq);
+  }
 }
 template <int NV, bool DOT>
 void cgs_axpy_t(msp_handle* h, int nv, const double* V, const double* coef, double* w, double* out,
@@ -1718,7 +1524,7 @@ void cgs_axpy(msp_handle* h, int nv, const double* V, const double* coef, double
   if (nv <= 4) cgs_axpy_t<4, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 8) cgs_axpy_t<8, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
   else if (nv <= 16) cgs_axpy_t<16, DOT>(h, nv, V, coef, w, out, addend, raw, sq);
-  else if (DOT && h->cgs_split == 0) {
+  else if (DOT) {
     // nv > 16: the fused pass would need 32 accumulators per thread (25% occupancy);
     // instead the (fast) 32-vector axpy, then the row-split dot of the updated w
     cgs_axpy_t<32, false>(h, nv, V, coef, w, h->lred, nullptr, nullptr, -1);
@@ -1785,21 +1591,15 @@ void dcgs_update_t(msp_handle* h, int k, double* vk, double* w, const double* st
   constexpr bool DOT = NV <= 16;
   // staged (cp.async) pass 2, one CTA per SM: k <= 8 at 1024 threads, 9 <= k <= 16 at 512
   // and k > 16 at 256 threads, single-buffered (C3: orthogonalisation at k = 15 0.295 ->
-  // 0.255 ms, at k = 25 0.503 -> 0.457 ms); double-buffered forms kept as options
-  // (MSP_DCGS_STAGED16=0, MSP_DCGS_STAGED32=2: slower)
+  // 0.255 ms, at k = 25 0.503 -> 0.457 ms; double-buffered forms measured slower, removed)
   if constexpr (NV == 8) {
-    if (ew2_ok(h) && h->dcgs_staged8 == 1) { dcgs_staged_launch<8, 1024, 1>(h, k, vk, w, st_in); return; }
+    if (ew2_ok(h)) { dcgs_staged_launch<8, 1024, 1>(h, k, vk, w, st_in); return; }
   }
   if constexpr (NV == 16) {
-    if (ew2_ok(h) && h->dcgs_staged) {
-      if (h->dcgs_staged16 == 1) dcgs_staged_launch<16, 512, 1>(h, k, vk, w, st_in);
-      else dcgs_staged_launch<16, 256>(h, k, vk, w, st_in);
-      return;
-    }
+    if (ew2_ok(h)) { dcgs_staged_launch<16, 512, 1>(h, k, vk, w, st_in); return; }
   }
   if constexpr (NV == 32) {                       // fused staged pass 2 for k > 16
-    if (ew2_ok(h) && h->dcgs_staged32 == 1) { dcgs_staged_launch<32, 256, 1>(h, k, vk, w, st_in); return; }
-    if (ew2_ok(h) && h->dcgs_staged32 == 2) { dcgs_staged_launch<32, 128, 2>(h, k, vk, w, st_in); return; }
+    if (ew2_ok(h)) { dcgs_staged_launch<32, 256, 1>(h, k, vk, w, st_in); return; }
   }
   if (ew2_ok(h))
     klaunch(h->s, h->pdl, dcgs_update_kernel<NV, 2, DOT>, kRedBlocks, kRedThreads, h->N / 2, k, (const double*)h->V,
@@ -2102,25 +1902,11 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1 ||
       c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1 || c.orth < 0 || c.orth > 2)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
-  if (c.smoother != 0) c.use_coop = 0;                 // the persistent V-cycle is PGS-MC only
+  if (c.use_coop != 0) return fail(nullptr, MSP_EINVAL, "msp_setup: use_coop (cooperative V-cycle) was removed: measured slower than graph replay");
   std::unique_ptr<msp_handle> h(new msp_handle);
   h->cfg = c;
-  if (const char* e = std::getenv("MSP_COOP_BPS")) h->coop_bps = std::atoi(e);
-  if (const char* e = std::getenv("MSP_COOP_TPB")) h->coop_tpb = std::atoi(e);
-  if (const char* e = std::getenv("MSP_BILU_V1")) h->bilu_v1 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_FUSE_A8")) h->fuse_a8 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_GEMV8")) h->gemv8 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_DCGS_STAGED")) h->dcgs_staged = std::atoi(e);
-  if (const char* e = std::getenv("MSP_DCGS_STAGED32")) h->dcgs_staged32 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_DCGS_STAGED16")) h->dcgs_staged16 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_DCGS_STAGED8")) h->dcgs_staged8 = std::atoi(e);
-  if (const char* e = std::getenv("MSP_PCOL_ROWWISE")) h->pcol_rowwise = std::atoi(e);
-  if (const char* e = std::getenv("MSP_CLUSTER_FROM")) h->cl_from = std::atoi(e);
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
-  if (const char* e = std::getenv("MSP_CLUSTER_SIZE")) h->cl_size = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
-  if (const char* e = std::getenv("MSP_CGS_SPLIT")) h->cgs_split = std::atoi(e);
-  if (const char* e = std::getenv("MSP_SPMV4C")) g_spmv4c = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
@@ -2416,7 +2202,7 @@ msp_status msp_bilu_forward(msp_handle* h, const double* r, double* y) {
   return guarded(h, [&]() -> msp_status {
     sync_in(h);
     to_internal(h, r, h->r, h->n, h->b);
-    launch_bilu(h, h->r, h->wp, h->z, false, nullptr, 1);
+    launch_bilu(h, h->r, h->wp, h->z, false, 1);
     from_internal(h, h->r, y, h->b);
     return MSP_OK;
   });
@@ -2428,7 +2214,7 @@ msp_status msp_bilu_backward(msp_handle* h, const double* y, double* x) {
     sync_in(h);
     to_internal(h, y, h->r, h->n, h->b);
     CK(cudaMemsetAsync(h->wp, 0, sizeof(double) * h->n, h->s));
-    launch_bilu(h, h->r, h->wp, h->z, false, nullptr, 2);
+    launch_bilu(h, h->r, h->wp, h->z, false, 2);
     from_internal(h, h->z, x, h->b);
     return MSP_OK;
   });
@@ -2485,7 +2271,7 @@ msp_status msp_get_stats(const msp_handle* h, msp_stats* out) {
   }
   out->device_bytes = h->bytes;
   out->kernels_per_iter = h->kernels_per_step;
-  out->fused_a8 = (!h->comm && a8_fused(h)) ? 1 : 0;
+  out->fused_a8 = 0;
   return MSP_OK;
 }
 
@@ -2536,15 +2322,9 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         fn = [&]() { launch_spmv(h, 2, h->wp, h->bin, h->u); };
         bytes = nnzb * (8 * b + 4) + 4 * (n + 1) + 8 * n + 2 * 8 * (double)N;
         break;
-      case 3:                                    // a9 as the solve runs it (a8 fused in for 4x4)
-        if (a8_fused(h)) {
-          fn = [&]() { launch_bilu(h, h->r, h->wp, h->z, false, h->bin); };
-          // + the pressure-column stream and the wp gather of the fused a8 (g replaces r)
-          bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N + nnzb * 8 * b + 8.0 * n;
-        } else {
-          fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
-          bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
-        }
+      case 3:                                    // a9 as the solve runs it
+        fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); };
+        bytes = (nnzb - n) * (8 * b * b + 4) + 8 * b * b * n + 8 * (n + 1) + 5 * 8 * (double)N;
         break;
       case 4:                                    // CGS2 pass A over 16 basis vectors
         fn = [&]() { cgs_dot(h, 16, h->V, h->u, h->dh1, nullptr, nullptr, -1); };
@@ -2588,6 +2368,21 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
       case 12:
         if (h->prm.orth == 2) fn = [&]() { dcgs2(h, 25); };
         else fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
+        bytes = 0.0;
+        break;
+      case 13:                                   // a9 followed by the Arnoldi SpMV
+        fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); launch_spmv(h, 0, h->z, nullptr, h->u); };
+        bytes = 0.0;
+        break;
+      case 14:                                   // MSP application followed by the SpMV
+        fn = [&]() { msp_apply_dev(h, h->bin, h->z); launch_spmv(h, 0, h->z, nullptr, h->u); };
+        bytes = 0.0;
+        break;
+      case 15:                                   // SpMV + orthogonalisation of step 15
+        fn = [&]() {
+          launch_spmv(h, 0, h->z, nullptr, h->V + (size_t)16 * N);
+          if (h->prm.orth == 2) dcgs2(h, 15); else cgs2(h, 16, h->V + (size_t)16 * N);
+        };
         bytes = 0.0;
         break;
       default:

@@ -145,12 +145,12 @@ def test_no_smoother_vcycle_and_solve_parity(sm):
 
 # ------------------------------------------------------------------ V-cycle, BILU, MSP
 @pytest.mark.parametrize("kw", [dict(coarsest_max_dof=200), dict(coarsest_max_dof=200, pair_passes=1),
-                                dict(), dict(coarsest_max_dof=200, use_coop=0),
+                                dict(), dict(coarsest_max_dof=200, use_graphs=0),
                                 dict(coarsest_max_dof=200, pre_sweeps=2, post_sweeps=2)])
 def test_vcycle_parity(kw):
     p = gen.make_config("C2", nx=40, ny=30, nz=6)
     s = solver(p, **kw)
-    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], **{k: v for k, v in kw.items() if k != "use_coop"})
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], **{k: v for k, v in kw.items() if k != "use_graphs"})
     r = gen.random_vector(p["n"], 7)
     ref = O.vcycle(r)
     xd = torch.zeros(p["n"], dtype=torch.float64, device="cuda")
@@ -174,37 +174,6 @@ def test_solve_odd_vector_length(nc, dims, orth):
     A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * p["b"],) * 2)
     xs = rg["x"].cpu().numpy()
     assert np.linalg.norm(p["rhs"] - A @ xs) / np.linalg.norm(p["rhs"]) <= 1e-8
-
-
-@pytest.mark.parametrize("env,kw", [(dict(MSP_CLUSTER_FROM="2"), dict()),
-                                    (dict(MSP_CLUSTER_FROM="1"), dict()),
-                                    (dict(MSP_CLUSTER_FROM="1", MSP_CLUSTER_SIZE="8"), dict()),
-                                    (dict(MSP_CLUSTER_FROM="1"), dict(pre_sweeps=2, post_sweeps=2)),
-                                    (dict(MSP_CLUSTER_FROM="2"), dict(post_sweeps=0))])
-def test_cluster_vcycle_bit_identical(env, kw, monkeypatch):
-    """The coarse levels run as one thread-block cluster (cluster.cuh) must reproduce the
-    multi-launch V-cycle bit for bit (same per-row summation order), with fewer launches."""
-    p = gen.make_config("C2", nx=40, ny=30, nz=6)
-    monkeypatch.setenv("MSP_CLUSTER_FROM", "0")                     # multi-launch path
-    s0 = solver(p, coarsest_max_dof=60, **kw)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    s1 = solver(p, coarsest_max_dof=60, **kw)
-    assert s1.stats()["levels"] > int(env["MSP_CLUSTER_FROM"]) + 1
-    r = torch.from_numpy(gen.random_vector(p["n"], 7)).cuda()
-    out = []
-    for s in (s0, s1):
-        x = torch.zeros(p["n"], dtype=torch.float64, device="cuda")
-        k0 = s.kernel_launches()
-        s.vcycle(r, x)
-        out.append((x.cpu().numpy(), s.kernel_launches() - k0))
-    assert np.array_equal(out[0][0], out[1][0])
-    assert out[1][1] < out[0][1], (out[0][1], out[1][1])
-    b = torch.from_numpy(p["rhs"]).cuda()
-    r0, r1 = s0.solve(b), s1.solve(b)
-    assert r0["iters"] == r1["iters"]
-    assert np.array_equal(r0["hist"], r1["hist"])
-    assert torch.equal(r0["x"], r1["x"])
 
 
 @pytest.mark.parametrize("name,gkw,kw", [("C2", dict(nx=25, ny=20, nz=5), dict()),
@@ -231,24 +200,6 @@ def test_gpu_bilu_factorization_bit_exact(name, gkw, kw, monkeypatch):
     assert np.array_equal(solver(p, coarsest_max_dof=100, **kw).bilu_factors(), F)
 
 
-def test_msp_apply_with_fused_a8_parity(monkeypatch):
-    """Option MSP_FUSE_A8=1 (a8 inside the BILU forward kernels, 4x4 blocks): MSP apply and
-    solve vs the oracle."""
-    monkeypatch.setenv("MSP_FUSE_A8", "1")
-    p = gen.make_config("C2", nx=25, ny=20, nz=5)
-    s = solver(p, coarsest_max_dof=100)
-    assert s.stats()["fused_a8"]
-    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=100)
-    g = gen.random_vector(p["n"] * p["b"], 9)
-    out = torch.zeros(p["n"] * p["b"], dtype=torch.float64, device="cuda")
-    s.apply(torch.from_numpy(g).cuda(), out)
-    ref = O.apply(g)
-    assert np.linalg.norm(out.cpu().numpy() - ref) <= 1e-10 * np.linalg.norm(ref)
-    ro = O.solve(p["rhs"], tol=1e-8)
-    rg = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=1e-8)
-    assert abs(rg["iters"] - ro["iters"]) <= 1
-
-
 @pytest.mark.parametrize("kw", [dict(), dict(bilu_order=0), dict(decoupling=1), dict(stages=3)])
 def test_bilu_and_msp_apply_parity(kw):
     p = gen.make_config("C2", nx=25, ny=20, nz=5)
@@ -273,7 +224,7 @@ def check_solve(p, tol=1e-6, restart=30, **kw):
     """GPU solve vs the oracle's TEXTBOOK orthogonalisation (CGS2, or MGS when asked): the
     product's DCGS2 (R14) builds the same basis in exact arithmetic."""
     s = solver(p, **kw)
-    okw = {k: v for k, v in kw.items() if k not in ("use_graphs", "use_coop", "orth")}
+    okw = {k: v for k, v in kw.items() if k not in ("use_graphs", "orth")}
     O = oracle.Msp(p["row_ptr"], p["col"], p["val"], orth=1 if kw.get("orth") == 1 else 0, **okw)
     o = O.solve(p["rhs"], tol=tol, restart=restart)
     r = s.solve(torch.from_numpy(p["rhs"]).cuda(), tol=tol, restart=restart)
@@ -293,8 +244,7 @@ def check_solve(p, tol=1e-6, restart=30, **kw):
     ("C1", {}, dict(coarsest_max_dof=50)),
     ("C1", {}, dict(coarsest_max_dof=50, bilu_order=0)),
     ("C1", {}, dict(coarsest_max_dof=50, use_graphs=0)),
-    ("C1", {}, dict(coarsest_max_dof=50, use_coop=0)),
-    ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100, use_coop=0)),
+    ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100, use_graphs=0)),
     ("C2", dict(nx=37, ny=23, nz=7), dict(coarsest_max_dof=100)),
     ("C2", dict(nx=20, ny=20, nz=5, nc=6), dict(coarsest_max_dof=100)),
     ("C3", dict(nx=12, ny=44, nz=17), dict(coarsest_max_dof=300)),

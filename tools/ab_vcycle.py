@@ -7,16 +7,10 @@ import gen  # noqa
 from paper_2208_08594_b200 import MspSolver  # noqa
 
 p = gen.make_config(sys.argv[1] if len(sys.argv) > 1 else "C3")
-variants = [("multi", dict(use_coop=0))]
+variants = [("default", dict())]
 for extra in sys.argv[2:]:
     if "=" in extra:
-        variants.append((extra, dict(use_coop=0)))
-if "bilu_v1" in sys.argv:
-    variants.append(("bilu_v1", dict(use_coop=0)))
-if "bilu_colors" in sys.argv:
-    variants.append(("bilu_colors", dict(use_coop=0)))
-if "coop" in sys.argv:
-    variants.append(("coop", dict(use_coop=1)))
+        variants.append((extra, dict()))
 base_env = dict(os.environ)
 for tag, kw in variants:
     os.environ.clear(); os.environ.update(base_env)
@@ -27,13 +21,11 @@ for tag, kw in variants:
                 os.environ[k] = v                      # MSP_* environment switch
             else:
                 kw[k] = int(v)                         # msp_config field (e.g. orth=2)
-    os.environ["MSP_BILU_V1"] = "1" if tag == "bilu_v1" else "0"
-    os.environ["MSP_BILU_MODE"] = "0" if tag == "bilu_colors" else "1"
     s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], **kw)
     b = torch.from_numpy(p["rhs"]).cuda()
     r = s.solve(b)
     res = {}
-    for k in ("arnoldi_step15", "arnoldi_step25", "cgs2_step25", "msp_apply", "vcycle", "bilu", "cgs2_step15", "a2_bsr_spmv", "a8_pcol_residual", "a4_pgs_sweep_l0", "a6_coarse_gemv"):
+    for k in ("arnoldi_step15", "arnoldi_step25", "cgs2_step25", "msp_apply", "vcycle", "bilu", "cgs2_step15", "a2_bsr_spmv", "a8_pcol_residual", "a4_pgs_sweep_l0", "a6_coarse_gemv", "bilu_spmv", "msp_apply_spmv", "spmv_orth15"):
         res[k + "_warm"] = s.time_kernel(k, reps=20, flush=False)[0]
         res[k + "_cold"] = s.time_kernel(k, reps=20, flush=True)[0]
     t0 = s.stats()["solve_seconds"]
