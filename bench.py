@@ -116,52 +116,77 @@ def dist_init():
     return ws, rank, local
 
 
-def oracle_sample(p, iters_full):
-    """The CPU oracle as it stands (1 thread) on a bounded sample of the same workload:
-    oracle SETUP once (not counted), then MSP-GMRES with maxit=2 from x0=0 (2 Arnoldi steps
-    + the cycle-end update: 3 MSP applications and 4 SpMVs).  Per-iteration cost = t/3;
-    s/system = that x (iterations + restart cycles) of a full solve."""
+def host_info():
+    """Core count and CPU model of the host the oracle runs on (nproc, lscpu)."""
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def oracle_full_solves(p, max_solves, budget_s, warmup=0):
+    """The CPU oracle as it stands (oracle/oracle.cpp, OpenMP timing mode on every host
+    core; bit-identical to its 1-thread mode) on the SAME workload: setup once (timed
+    separately), then FULL MSP-GMRES solves (x0 = 0, tol 1e-6, GMRES(30), CGS2) until
+    `max_solves` are timed or the next one would exceed `budget_s`."""
     import oracle
+    cores = oracle.set_threads(0)
     t0 = time.perf_counter()
     M = oracle.Msp(p["row_ptr"], p["col"], p["val"])
-    t1 = time.perf_counter()
-    r = M.solve(p["rhs"], tol=TOL, restart=RESTART, maxit=2)
-    t2 = time.perf_counter()
-    per_it = (t2 - t1) / 3.0
-    units = iters_full + math.ceil(iters_full / RESTART)
-    return dict(value=per_it * units, per_iteration_s=per_it, setup_s=t1 - t0, sample_s=t2 - t1,
-                sample_iters=r["iters"])
+    setup_s = time.perf_counter() - t0
+    times, iters = [], None
+    for k in range(warmup + max_solves):
+        t1 = time.perf_counter()
+        r = M.solve(p["rhs"], tol=TOL, restart=RESTART)
+        dt = time.perf_counter() - t1
+        iters = r["iters"]
+        if k >= warmup:
+            times.append(dt)
+        spent = sum(times)
+        if times and spent + dt > budget_s:
+            break
+    oracle.set_threads(1)
+    return dict(times=times, setup_s=setup_s, iters=iters, cores=cores)
+
+
+def seq_context(config):
+    """The oracle's 1-thread full solve recorded with the golden (tests/golden), if any."""
+    gold = os.path.join(ROOT, "tests", "golden", f"oracle_{config.lower()}.json")
+    if not os.path.exists(gold):
+        return None
+    g = json.load(open(gold))
+    return {"solve_s": g.get("oracle_solve_s"), "setup_s": g.get("oracle_setup_s"), "iters": g.get("iters"),
+            "cores": 1, "where": "tests/golden (written by make_oracle.py on the build container, not this host)"}
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the oracle (plain sequential C++), as it stands, on this arm's
-    config/metric.  Each step = the bounded sample of oracle_sample()."""
+    """--impl reference: the oracle (plain C++, OpenMP timing mode), as it stands, on this
+    arm's config/metric.  Each step = one FULL solve of the workload; the number of timed
+    steps is capped so the run ends within a few minutes (reported honestly as `steps`)."""
     if rank != 0:
         return
     import gen
     p = gen.make_config(args.config)
-    gold = os.path.join(ROOT, "tests", "golden", f"oracle_{args.config.lower()}.json")
-    iters_full = json.load(open(gold))["iters"] if os.path.exists(gold) else 30
-    import oracle
-    t0 = time.perf_counter()
-    M = oracle.Msp(p["row_ptr"], p["col"], p["val"])
-    setup_s = time.perf_counter() - t0
-    vals = []
-    for s in range(args.warmup + args.steps):
-        t1 = time.perf_counter()
-        M.solve(p["rhs"], tol=TOL, restart=RESTART, maxit=2)
-        dt = time.perf_counter() - t1
-        if s >= args.warmup:
-            vals.append(dt / 3.0 * (iters_full + math.ceil(iters_full / RESTART)))
-    v = statistics.mean(vals)
-    sample = (f"per step: oracle MSP-GMRES maxit=2 on {args.config} (3 MSP applications), scaled to "
-              f"{iters_full} iterations (oracle's own full-solve count, tests/golden); oracle setup "
-              f"{setup_s:.1f}s excluded")
+    o = oracle_full_solves(p, max_solves=args.steps, budget_s=float(os.environ.get("REF_BUDGET_S", "150")),
+                           warmup=min(args.warmup, 1))
+    v = statistics.mean(o["times"])
+    nproc, model = host_info()
+    sample = (f"per step: one full oracle MSP-GMRES solve of {args.config} ({o['iters']} iterations, CGS2) "
+              f"on {o['cores']} OpenMP threads ({model}, nproc {nproc}); oracle setup {o['setup_s']:.1f}s "
+              f"excluded; {len(o['times'])} of {args.steps} requested steps timed (time budget)")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": workload_desc(args.config, p)},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "steps": len(o["times"]), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+           "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "config": {"workload": workload_desc(args.config, p),
+                                                          "iterations": o["iters"]},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": o["cores"], "kind": "oracle", "sample": sample,
+                            "nproc": nproc, "cpu_model": model, "setup_s": o["setup_s"],
+                            "seq_1thread": seq_context(args.config)},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -305,12 +330,14 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        o = oracle_sample(p, iters)
-        cpu = {"value": o["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": (f"oracle (1 thread) MSP-GMRES maxit=2 on {args.config} after its setup "
-                          f"({o['setup_s']:.1f}s, excluded): {o['sample_s']:.2f}s for 3 MSP "
-                          f"applications -> {o['per_iteration_s']:.2f}s/iteration x "
-                          f"({iters} iterations + {cyc} cycle ends)")}
+        o = oracle_full_solves(p, max_solves=1, budget_s=1e9)
+        nproc, model = host_info()
+        cpu = {"value": o["times"][0], "unit": UNIT, "cores": o["cores"], "kind": "oracle",
+               "sample": (f"one full oracle MSP-GMRES solve of {args.config} (x0 = 0, tol {TOL:g}, "
+                          f"GMRES({RESTART}), CGS2: {o['iters']} iterations) on {o['cores']} OpenMP threads "
+                          f"(bit-identical to 1 thread); oracle setup {o['setup_s']:.1f}s excluded"),
+               "nproc": nproc, "cpu_model": model, "iterations": o["iters"], "setup_s": o["setup_s"],
+               "seq_1thread": seq_context(args.config)}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

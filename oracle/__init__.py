@@ -23,7 +23,7 @@ F64 = np.float64
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["g++", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-std=c++17",
-                               "-o", _LIB, _SRC])
+                               "-fopenmp", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -77,6 +77,12 @@ class Config(ctypes.Structure):
 
 
 # ---------------------------------------------------------------- primitives
+def set_threads(n: int) -> int:
+    """Timing switch: run the oracle's independent loops on n OpenMP threads (0 = all
+    cores); results are bit-identical for any n.  Returns the thread count in use."""
+    return int(lib().orc_set_threads(int(n)))
+
+
 def bsr_spmv(row_ptr, col, val, x):
     n = len(row_ptr) - 1
     b = val.shape[-1]

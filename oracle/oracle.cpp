@@ -17,6 +17,12 @@
 // FP64 throughout; compiled with -ffp-contract=off; every sum starts at +0.0
 // and runs in ascending index order unless stated.
 //
+// Timing switch (SURVEY §8(d) "Mode SEQ / Mode OMP"): orc_set_threads(n) runs the loops
+// whose per-element arithmetic is independent (SpMV rows, PGS-MC rows of one color, BILU
+// blocks of one color, vector updates, the CGS2 dots over basis vectors) on n OpenMP
+// threads.  Every sum keeps its sequential order, so results are BIT-IDENTICAL for any n
+// (tests/test_oracle.py::test_omp_mode_bit_identical).
+//
 // Parity status: every function is pinned by a -m "not gpu"
 // test except NPAIR's correspondence to the cited Napov-Notay scheme, which the
 // paper only names: "parity unpinned" w.r.t. the paper for NPAIR; the
@@ -34,7 +40,14 @@
 #include <utility>
 #include <vector>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 namespace orc {
+
+static int g_threads = 1;        // OMP timing mode (1 = SEQ)
+#define ORC_PAR _Pragma("omp parallel for schedule(static) num_threads(g_threads) if(g_threads > 1)")
 
 struct Csr {                  // scalar CSR, columns ascending per row
   int n = 0;
@@ -60,6 +73,7 @@ static std::string g_err;
 // ---------------------------------------------------------------------------
 static void bsr_spmv(const Bsr& A, const double* x, double* y) {
   const int b = A.b;
+  ORC_PAR
   for (int c = 0; c < A.n; ++c)
     for (int r = 0; r < b; ++r) {
       double s = 0.0;
@@ -73,6 +87,7 @@ static void bsr_spmv(const Bsr& A, const double* x, double* y) {
 }
 
 static void csr_spmv(const Csr& A, const double* x, double* y) {
+  ORC_PAR
   for (int i = 0; i < A.n; ++i) {
     double s = 0.0;
     for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) s += A.val[e] * x[A.col[e]];
@@ -203,15 +218,23 @@ static bool pgs_mc_sweep(const Csr& A, const std::vector<std::vector<int>>& grou
   const int g = (int)groups.size();
   for (int t = 0; t < g; ++t) {
     const std::vector<int>& Vl = groups[ascending ? t : g - 1 - t];
-    for (int i : Vl) {
+    int bad = -1;
+    ORC_PAR
+    for (size_t k = 0; k < Vl.size(); ++k) {        // rows of one color: independent
+      const int i = Vl[k];
       double s = 0.0, d = 0.0;
       for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
         if (A.col[e] == i) d = A.val[e];
         else s += A.val[e] * x[A.col[e]];
       }
-      if (d == 0.0) { g_err = "pgs_mc: zero diagonal at row " + std::to_string(i); return false; }
+      if (d == 0.0) {
+#pragma omp critical
+        bad = std::max(bad, i);
+        continue;
+      }
       x[i] = (b[i] - s) / d;
     }
+    if (bad >= 0) { g_err = "pgs_mc: zero diagonal at row " + std::to_string(bad); return false; }
   }
   return true;
 }
@@ -826,7 +849,10 @@ static void bilu_backward(const Bilu& R, const double* y, double* x, bool absmod
   }
 }
 
+static void bilu_apply_omp(const Bilu& R, const double* r, double* x);
+
 static void bilu_apply(const Bilu& R, const double* r, double* x) {
+  if (g_threads > 1) { bilu_apply_omp(R, r, x); return; }
   std::vector<double> y((size_t)R.F.n * R.F.b);
   bilu_forward(R, r, y.data());
   bilu_backward(R, y.data(), x);
@@ -887,6 +913,67 @@ static void bilu_apply_by_color(const Bilu& R, const double* r, double* x) {
   std::copy(xv.begin(), xv.end(), x);
 }
 
+// OMP timing mode of bilu_apply: the blocks of one color in parallel (their cells in
+// order), every sum in the sequential order -- bit-identical to bilu_forward/backward
+// because same-color blocks are uncoupled (ABMC validity, pinned by
+// test_abmc_order_validity_bruteforce / test_bilu_parallel_by_color_equals_sequential).
+static void bilu_apply_omp(const Bilu& R, const double* r, double* x) {
+  const Bsr& F = R.F;
+  const int n = F.n, b = F.b, bb = b * b;
+  std::vector<int> run;                      // position ranges of the blocks, in order
+  std::vector<int> color_run;                // first run of every color
+  for (int p = 0; p < n; ++p) {
+    const int i = R.order[p];
+    if (p == 0 || R.blk[i] != R.blk[R.order[p - 1]]) {
+      if (p == 0 || R.color[i] != R.color[R.order[p - 1]]) color_run.push_back((int)run.size());
+      run.push_back(p);
+    }
+  }
+  run.push_back(n);
+  color_run.push_back((int)run.size() - 1);
+  const int g = (int)color_run.size() - 1;
+  std::vector<double> y((size_t)n * b);
+  for (int c = 0; c < g; ++c) {
+    ORC_PAR
+    for (int k = color_run[c]; k < color_run[c + 1]; ++k)
+      for (int p = run[k]; p < run[k + 1]; ++p) {
+        const int i = R.order[p];
+        for (int q = 0; q < b; ++q) {
+          double s = 0.0;
+          for (int e : R.rowe[i]) {
+            const int kk = F.col[e];
+            if (R.pos[kk] >= p) break;
+            for (int t = 0; t < b; ++t) s += F.blk(e)[q * b + t] * y[(size_t)kk * b + t];
+          }
+          y[(size_t)i * b + q] = r[(size_t)i * b + q] - s;
+        }
+      }
+  }
+  for (int c = g - 1; c >= 0; --c) {
+    ORC_PAR
+    for (int k = color_run[c]; k < color_run[c + 1]; ++k) {
+      std::vector<double> t(b);
+      for (int p = run[k + 1] - 1; p >= run[k]; --p) {
+        const int i = R.order[p];
+        for (int q = 0; q < b; ++q) {
+          double s = 0.0;
+          for (int e : R.rowe[i]) {
+            const int j = F.col[e];
+            if (R.pos[j] <= p) continue;
+            for (int u = 0; u < b; ++u) s += F.blk(e)[q * b + u] * x[(size_t)j * b + u];
+          }
+          t[q] = y[(size_t)i * b + q] - s;
+        }
+        for (int q = 0; q < b; ++q) {
+          double s = 0.0;
+          for (int u = 0; u < b; ++u) s += R.Dinv[(size_t)i * bb + q * b + u] * t[u];
+          x[(size_t)i * b + q] = s;
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // NEXT-1: B_N = block GS on A_NN = Π_N^T A Π_N (R12): one forward
 // block Gauss-Seidel sweep from the zero guess over the nc x nc N-N blocks, in the
@@ -944,6 +1031,7 @@ static int msp_setup(Msp& M) {
 // the decoupling weights in the middle factor): r_p[c] = sum_k w_c[k] r[c*b+k], k ascending.
 static void restrict_pressure(const Msp& M, const double* r, double* rp) {
   const int b = M.A.b;
+  ORC_PAR
   for (int c = 0; c < M.A.n; ++c) {
     double s = 0.0;
     for (int k = 0; k < b; ++k) s += M.W[(size_t)c * b + k] * r[(size_t)c * b + k];
@@ -994,15 +1082,18 @@ static bool msp_apply(const Msp& M, const double* g, double* wout) {
     for (int c = 0; c < n; ++c)
       for (int i = 0; i < b - 1; ++i) w[(size_t)c * b + 1 + i] += wN[(size_t)c * (b - 1) + i];
     bsr_spmv(M.A, w.data(), Aw.data());                  // line 3
+    ORC_PAR
     for (size_t t = 0; t < N; ++t) r[t] = g[t] - Aw[t];
   }
   std::vector<double> xp;
   if (!pressure_stage(M, r, xp)) return false;         // line 4: w += Π_P B_P W^T r
   for (int c = 0; c < n; ++c) w[(size_t)c * b] += xp[c];
   bsr_spmv(M.A, w.data(), Aw.data());                  // line 5: r = g - A w
+  ORC_PAR
   for (size_t t = 0; t < N; ++t) r[t] = g[t] - Aw[t];
   std::vector<double> z(N);
   bilu_apply(M.R, r.data(), z.data());                 // line 6: w += R r
+  ORC_PAR
   for (size_t t = 0; t < N; ++t) wout[t] = w[t] + z[t];
   return true;
 }
@@ -1031,6 +1122,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
     return out;
   }
   Aop(x, t.data());
+  ORC_PAR
   for (size_t i = 0; i < N; ++i) r[i] = b[i] - t[i];
   double beta = nrm2(r);
   out.final_rel = beta / bnorm;
@@ -1043,6 +1135,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
   std::vector<double> Hraw((size_t)(m + 1) * m), h2p;
   double nu = 1.0, rhop = 1.0;
   while (true) {
+    ORC_PAR
     for (size_t i = 0; i < N; ++i) V[0][i] = r[i] / beta;
     std::fill(gam.begin(), gam.end(), 0.0);
     gam[0] = beta;
@@ -1061,9 +1154,12 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       if (orth == 0) {                                  // CGS2
         for (int pass = 0; pass < 2; ++pass) {
           std::vector<double> hh(j + 1);
+          ORC_PAR
           for (int i = 0; i <= j; ++i) hh[i] = dot(V[i], w);
-          for (int i = 0; i <= j; ++i)
-            for (size_t q = 0; q < N; ++q) w[q] -= hh[i] * V[i][q];
+          // w -= sum_i hh_i V_i: for every element the subtractions run in the order i = 0..j
+          ORC_PAR
+          for (size_t q = 0; q < N; ++q)
+            for (int i = 0; i <= j; ++i) w[q] -= hh[i] * V[i][q];
           for (int i = 0; i <= j; ++i) h(i) += hh[i];
         }
       } else if (orth == 1) {                           // MGS
@@ -1145,6 +1241,7 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       k = j + 1;
       broke = hn < 1e-14 * bnorm;
       if (est <= tol || broke || out.iters >= maxit) break;
+      ORC_PAR
       for (size_t q = 0; q < N; ++q) V[j + 1][q] = w[q] / next_scale;
     }
     std::vector<double> y(k);
@@ -1154,11 +1251,14 @@ static GmresOut gmres(size_t N, const std::function<void(const double*, double*)
       y[i] = (gam[i] - s) / H[(size_t)i * m + i];
     }
     std::vector<double> u(N, 0.0);
-    for (int i = 0; i < k; ++i)
-      for (size_t q = 0; q < N; ++q) u[q] += y[i] * V[i][q];
+    ORC_PAR
+    for (size_t q = 0; q < N; ++q)
+      for (int i = 0; i < k; ++i) u[q] += y[i] * V[i][q];
     if (!Bop(u.data(), z.data())) { out.status = 2; return out; }
+    ORC_PAR
     for (size_t q = 0; q < N; ++q) x[q] += z[q];
     Aop(x, t.data());
+    ORC_PAR
     for (size_t i = 0; i < N; ++i) r[i] = b[i] - t[i];
     beta = nrm2(r);
     out.final_rel = beta / bnorm;
@@ -1192,6 +1292,17 @@ typedef struct {
 } orc_config;
 
 const char* orc_last_error() { return g_err.c_str(); }
+
+// OMP timing mode (results bit-identical for any thread count); returns the count in use
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+  g_threads = n > 0 ? n : omp_get_max_threads();
+#else
+  (void)n;
+  g_threads = 1;
+#endif
+  return g_threads;
+}
 
 static Csr mkcsr(int n, const int* ptr, const int* col, const double* val) {
   Csr A;

@@ -1024,3 +1024,21 @@ def test_stall_and_max_levels_give_estall():
     assert M.info()["coarse_diag"]
     r = gen.random_vector(n, 1)
     assert np.allclose(M.vcycle(r), r / np.arange(1.0, n + 1), rtol=1e-15)
+
+
+def test_omp_mode_bit_identical():
+    """the oracle's OpenMP switch is for timing only -- a full MSP-GMRES
+    solve (PGS-MC, ABMC BILU, CGS2) gives bit-identical iterates with 1 and 4 threads."""
+    p = gen.make_config("C2", nx=24, ny=20, nz=5)
+    out = []
+    try:
+        for t in (1, 4):
+            assert oracle.set_threads(t) == t
+            M = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=60)
+            r = M.solve(p["rhs"], tol=1e-8)
+            out.append((r["iters"], r["hist"], r["x"]))
+    finally:
+        oracle.set_threads(1)
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2])
