@@ -21,6 +21,7 @@
 #include "comm.h"
 #include "setup.h"
 #include "kernels.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace mspk;
 
@@ -40,6 +41,15 @@ struct CudaError {
   } while (0)
 
 inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// NVTX range named after the SURVEY §8(a) row it covers (host-side: visible in profiles of
+// direct launches and of SETUP; graph replays show the graph launch)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // Launch with programmatic stream serialisation (PDL, see kernels.cuh) when enabled.
 template <typename... KArgs, typename... Args>
@@ -226,6 +236,27 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Host-side bounds checks of every index structure before it is uploaded (the kernels
+// index with these arrays unchecked; compute-sanitizer is not available on this pool).
+// A violation is a setup bug: MSP_EINVAL with the structure's name.
+void check_index(bool ok, const char* what) {
+  if (!ok) throw std::pair<int, std::string>(MSP_EINVAL, std::string("internal index check failed: ") + what);
+}
+void check_range(const std::vector<int32_t>& v, int64_t lo, int64_t hi, const char* what) {
+  for (int32_t x : v) check_index(x >= lo && x < hi, what);
+}
+void check_ptr(const std::vector<int32_t>& p, int64_t n, int64_t total, const char* what) {
+  check_index((int64_t)p.size() == n + 1 && p[0] == 0 && p[n] == total, what);
+  for (int64_t i = 0; i < n; ++i) check_index(p[i] <= p[i + 1], what);
+}
+void check_perm(const std::vector<int32_t>& v, const char* what) {
+  std::vector<char> seen(v.size(), 0);
+  for (int32_t x : v) {
+    check_index(x >= 0 && (size_t)x < v.size() && !seen[x], what);
+    seen[x] = 1;
+  }
+}
+
 // Copy the ABI's BSR into a host BlockMat (validating it).
 msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err) {
   if (!A || A->n_cells <= 0 || A->n_cells > INT32_MAX || A->block != nc + 1 || nc < 0 || nc > 7 ||
@@ -364,6 +395,8 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
     L.d_color_row = h->upload(L.color_row);
     L.d_color_slice = h->upload(L.color_slice);
   }
+  check_range(col, 0, n_total, "level SELL column");
+  check_index(slice_off[L.nslices] == (int32_t)L.nnz_alloc || L.nslices == 0, "level SELL slice offsets");
   L.slice_row = h->upload(slice_row);
   L.slice_off = h->upload(slice_off);
   L.col = h->upload(col);
@@ -461,7 +494,12 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   SetupTimer T;
   msp::HostSetup S;
   std::string err;
-  int rc = msp::run_host_setup(A, h->prm, S, err);
+  Nvtx nv_setup("S1-S4 SETUP");
+  int rc = 0;
+  {
+    Nvtx nv("S1-S4 host: weights, A_PP, NPAIR+Galerkin, colorings, ABMC order");
+    rc = msp::run_host_setup(A, h->prm, S, err);
+  }
   if (rc) throw std::pair<int, std::string>(rc, err);
   std::vector<int32_t> rp, ci, dg, src;
   std::vector<double> F;
@@ -537,6 +575,9 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
       std::vector<int32_t> f(pp.begin(), pp.end() - 1);
       for (int32_t p = 0; p < D.n; ++p) pi[f[ap[p]]++] = p;
     }
+    check_range(ap, 0, nn, "aggregate map");
+    check_ptr(pp, nn, D.n, "restriction pointers");
+    check_perm(pi, "restriction members");
     D.agg = h->upload(ap);
     D.pt_ptr = h->upload(pp);
     D.pt_idx = h->upload(pi);
@@ -545,6 +586,12 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     dist_localize(h, A, S, rp, ci, dg, src, F, perms);
   } else {
   // BSR pattern + values (column-major blocks)
+  check_ptr(rp, n, (int64_t)ci.size(), "BSR row pointers");
+  check_range(ci, 0, n, "BSR columns");
+  check_perm(src, "BSR entry permutation");
+  for (int32_t i = 0; i < n; ++i) check_index(dg[i] >= rp[i] && dg[i] < rp[i + 1] && ci[dg[i]] == i, "BSR diagonal");
+  check_perm(S.order, "ABMC cell order");
+  check_ptr(S.blk_ptr, (int64_t)S.blk_ptr.size() - 1, n, "ABMC block pointers");
   h->rp = h->upload(rp);
   h->ci = h->upload(ci);
   h->d_src = h->upload(src);
@@ -1398,10 +1445,20 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
     return;
   }
   const bool fuse = h->prm.smoother == 0;
-  launch_restrict_pressure(h, g, level0_b(h), fuse);                   // a3: r_p = W^T g
-  vcycle_any(h, fuse);                                                 // a4-a7: B_P
+  {
+    Nvtx nv("a3 pressure restriction");
+    launch_restrict_pressure(h, g, level0_b(h), fuse);                 // a3: r_p = W^T g
+  }
+  {
+    Nvtx nv("a4-a7 V-cycle (PGS-MC, transfers, coarsest)");
+    vcycle_any(h, fuse);                                               // a4-a7: B_P
+  }
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
-  launch_spmv(h, 2, h->wp, g, h->r);                                   // a8: r = g - A Pi_P x_p
+  {
+    Nvtx nv("a8 pressure-column residual");
+    launch_spmv(h, 2, h->wp, g, h->r);                                 // a8: r = g - A Pi_P x_p
+  }
+  Nvtx nv("a9 BILU(0) substitution");
   launch_bilu(h, h->r, h->wp, z);                                      // a9: z = Pi_P x_p + R r
 }
 
@@ -1636,7 +1693,11 @@ void arnoldi_step(msp_handle* h, int j) {
   double* w = h->V + (size_t)(j + 1) * N;
   msp_apply_dev(h, vj, h->z);
   exch_cell(h, h->z, h->b, -1);
-  launch_spmv(h, 0, h->z, nullptr, w);
+  {
+    Nvtx nvt("a2 BSR SpMV");
+    launch_spmv(h, 0, h->z, nullptr, w);
+  }
+  Nvtx nvt("a10 orthogonalisation");
   const int nv = j + 1;
   if (h->prm.orth == 2) {
     dcgs2(h, j);
@@ -1701,6 +1762,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
                  double* hist, int cap, int* hlen) {
   const size_t N = h->N;
   ensure_basis(h, m);
+  Nvtx nv_gmres("GMRES solve");
   int it = 0, hl = 0;
   auto push = [&](double v) { if (hist && hl < cap) hist[hl] = v; ++hl; };
   norm_dev(h, h->bin, h->hcol);
@@ -1780,6 +1842,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         for (int l = i + 1; l < k; ++l) s += H[(size_t)i * m + l] * y[l];
         y[i] = (gam[i] - s) / H[(size_t)i * m + i];
       }
+      Nvtx nv_end("a11 cycle end");
       // u = V_k y ; x += B u ; r = b - A x
       // u = V y through the CGS axpy pass on a zeroed u with coefficients -y (the same
       // fma(y_i, V_i, .) sequence as a plain V y, with the multi-vector pass's loads)
