@@ -197,6 +197,11 @@ msp_status msp_multidot(msp_handle* h, int k, const double* V, const double* w, 
  * natural entry order, row-major blocks, D~_i^-1 in the diagonal slots -- the layout of
  * msp_bilu_factors), e.g. with integer-valued factors for bit-exact substitution tests. */
 msp_status msp_bilu_set_factors(msp_handle* h, const double* F);
+/* SETUP step S1 as the handle computed it (NEXT-2: on the GPU unless MSP_HOST_SETUP=1):
+ * W[n_cells*block] decoupling weights and App[nnzb] the A_PP values in the caller's
+ * natural entry order (pattern = A's), both HOST buffers; *on_gpu = 1 if computed on the
+ * GPU.  For the bit-exact parity tests against the host setup and the oracle. */
+msp_status msp_get_s1(const msp_handle* h, double* W, double* App, int32_t* on_gpu);
 /* The caller's stream: every entry point orders the handle's work after the work queued
  * on it (default: the stream given to msp_setup; 0 = legacy default stream). */
 msp_status msp_set_stream(msp_handle* h, void* cuda_stream);

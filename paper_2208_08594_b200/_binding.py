@@ -67,7 +67,7 @@ for _n in ("msp_setup", "msp_update", "msp_solve", "msp_apply", "msp_get_stats",
            "msp_host_setup_order", "msp_partition_owner", "msp_nccl_unique_id", "msp_setup_dist",
            "msp_dist_owned_cells", "msp_loopback_solve", "msp_dist_plan", "msp_restrict_pressure",
            "msp_residual_restrict", "msp_prolong", "msp_pcol_residual", "msp_bilu_forward",
-           "msp_bilu_backward", "msp_multidot", "msp_bilu_set_factors", "msp_set_stream"):
+           "msp_bilu_backward", "msp_multidot", "msp_bilu_set_factors", "msp_set_stream", "msp_get_s1"):
     getattr(_lib, _n).restype = ctypes.c_int
 _lib.msp_destroy.argtypes = [ctypes.c_void_p]
 _lib.msp_time_kernel.restype = ctypes.c_int
@@ -287,6 +287,14 @@ class MspSolver:
         diagonal slots; the layout bilu_factors() returns)."""
         F = _np(F, np.float64)
         self._check(_lib.msp_bilu_set_factors(self._h, _ptr(F)))
+
+    def s1(self):
+        """(W (n, b), A_PP values (nnzb,), computed_on_gpu) of the last SETUP (natural order)."""
+        W = np.zeros((self.n, self.b))
+        App = np.zeros(self.nnzb)
+        g = ctypes.c_int32(0)
+        self._check(_lib.msp_get_s1(self._h, _ptr(W), _ptr(App), ctypes.byref(g)))
+        return W, App, bool(g.value)
 
     def set_stream(self, stream):
         """Order every later call after the work queued on `stream` (a cudaStream_t int)."""

@@ -401,7 +401,8 @@ static bool off_diagonal_zero(const SpMat& A) {
   return true;
 }
 
-static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t>& comp, SpMat* out) {
+static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t>& comp, SpMat* out,
+                                const RapFn* rap = nullptr) {
   SpMat cur = A0;
   comp.resize(A0.n);
   std::iota(comp.begin(), comp.end(), 0);
@@ -413,7 +414,9 @@ static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t
     na = pair_aggregate(cur, a);
     for (auto& c : comp) c = a[c];
     const auto t1 = std::chrono::steady_clock::now();
-    cur = galerkin_rap(cur, a, na);
+    SpMat nxt;
+    if (rap && *rap && (*rap)(cur, a, na, nxt) == 0) cur = std::move(nxt);
+    else cur = galerkin_rap(cur, a, na);
     if (verbose)
       std::fprintf(stderr, "[msp setup]   pass %d: NPAIR %.3f s, Galerkin %.3f s (n %d -> %d)\n", p,
                    std::chrono::duration<double>(t1 - t0).count(),
@@ -625,11 +628,13 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
   S.prm = prm;
   S.A = &A;
   S.n = A.n;
-  int rc = make_weights(A, prm.decoupling, S.W, err);
-  if (rc) return rc;
-  T.mark("decoupling weights");
-  S.App = pressure_matrix(A, S.W);
-  T.mark("A_PP");
+  if (!prm.s1_given) {                 // else: S.W and S.App computed on the GPU (NEXT-2)
+    int rc = make_weights(A, prm.decoupling, S.W, err);
+    if (rc) return rc;
+    T.mark("decoupling weights");
+    S.App = pressure_matrix(A, S.W);
+    T.mark("A_PP");
+  }
   S.lv.clear();
   S.coarse_diag = false;
   SpMat cur = S.App;
@@ -638,7 +643,7 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
     if (l + 1 >= prm.max_levels) { err = "AMG: max_levels reached above coarsest_max_dof"; return 5; }
     HostLevel L;
     SpMat nxt;
-    const int32_t nn = aggregate_passes(cur, prm.pair_passes, L.agg, &nxt);
+    const int32_t nn = aggregate_passes(cur, prm.pair_passes, L.agg, &nxt, &prm.rap);
     T.mark("NPAIR + Galerkin level");
     if ((double)nn > 0.9 * (double)cur.n) {
       if (off_diagonal_zero(cur)) { S.coarse_diag = true; break; }

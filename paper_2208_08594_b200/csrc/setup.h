@@ -6,6 +6,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <functional>
 #include <vector>
 
 namespace msp {
@@ -28,10 +29,16 @@ struct Graph {                       // symmetric adjacency, ascending neighbour
   int32_t deg(int32_t i) const { return xadj[i + 1] - xadj[i]; }
 };
 
+struct SpMat;
+// Galerkin product hook (GPU, NEXT-2): returns 0 and fills C, or nonzero -> host product
+using RapFn = std::function<int(const SpMat& A, const std::vector<int32_t>& agg, int32_t nagg, SpMat& C)>;
+
 struct Params {
   int32_t coarsest_max_dof = 10000, max_levels = 20, pre_sweeps = 1, post_sweeps = 1,
           pair_passes = 2, decoupling = 2, bilu_order = 1, stages = 2, orth = 0, use_graphs = 1,
           use_coop = 1, smoother = 0, gs_chunk = 32;
+  RapFn rap;                           // optional: S3 Galerkin products of the hierarchy
+  bool s1_given = false;               // S.W and S.App already computed (GPU S1)
 };
 
 struct HostLevel {

@@ -21,6 +21,7 @@
 #include "comm.h"
 #include "setup.h"
 #include "kernels.cuh"
+#include "setup_kernels.cuh"
 #include <nvtx3/nvToolsExt.h>
 
 using namespace mspk;
@@ -144,6 +145,9 @@ struct msp_handle {
   std::vector<int64_t> graph_kernels;
   double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
   double* ftmp = nullptr;            // msp_bilu_set_factors scratch
+  bool setup_on_gpu = true;          // NEXT-2: S1 + Galerkin on the GPU (MSP_HOST_SETUP=1: host)
+  bool gpu_s1 = false;               // the last SETUP computed S1 on the GPU
+  std::vector<double> W_nat, App_nat;  // S1 results of the last SETUP (natural order), for parity
   cudaStream_t caller = nullptr;     // the caller's stream (msp_setup / msp_set_stream)
   cudaEvent_t ev_in = nullptr;       // orders h->s after the caller's prior work
   bool valid = false;                // false after a failed (re)SETUP: compute calls rejected
@@ -489,6 +493,141 @@ std::vector<int4> make_islot(int32_t n, const std::vector<int32_t>& rp, const st
   return sl;
 }
 
+// Device scratch for the GPU SETUP steps (freed on scope exit, stream-ordered).
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DBuf(size_t bytes, cudaStream_t st) : s(st) { CK(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s)); }
+  ~DBuf() { cudaFreeAsync(p, s); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+template <class T>
+void h2d(cudaStream_t s, T* d, const std::vector<T>& v) {
+  if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+}
+
+// NEXT-2, S1 on the GPU (R4): block column sums (TI) or diagonal blocks (QI), the
+// decoupling weights and A_PP = W^T A Pi_P, explicitly rounded in the host/oracle order
+// (setup_kernels.cuh) -> bit-identical W and A_PP, returned to the host for the greedy
+// steps (NPAIR, colorings) that follow.
+void gpu_setup_s1(cudaStream_t s, int decoupling, const msp::BlockMat& A, msp::HostSetup& S) {
+  Nvtx nv("S1 weights + A_PP (GPU)");
+  const int32_t n = A.n;
+  const int b = A.b, bb = b * b;
+  const int64_t nnzb = (int64_t)A.ci.size();
+  DBuf dA((size_t)nnzb * bb * sizeof(double), s), dC((size_t)n * bb * sizeof(double), s);
+  DBuf dW((size_t)n * b * sizeof(double), s), dP((size_t)nnzb * sizeof(double), s);
+  DBuf drp((size_t)(n + 1) * 4, s), dbad(4, s);
+  CK(cudaMemcpyAsync(dA.p, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, s));
+  h2d(s, drp.as<int32_t>(), A.rp);
+  CK(cudaMemsetAsync(dbad.p, 0xff, 4, s));
+  std::unique_ptr<DBuf> dcp, dce;
+  if (decoupling == 2) {                        // CSC of the block pattern, rows ascending
+    std::vector<int32_t> cp(n + 1, 0), ce(nnzb);
+    for (int32_t c : A.ci) cp[c + 1]++;
+    for (int32_t c = 0; c < n; ++c) cp[c + 1] += cp[c];
+    std::vector<int32_t> f(cp.begin(), cp.end() - 1);
+    for (int32_t p = 0; p < n; ++p)
+      for (int32_t e = A.rp[p]; e < A.rp[p + 1]; ++e) ce[f[A.ci[e]]++] = e;
+    dcp.reset(new DBuf((size_t)(n + 1) * 4, s));
+    dce.reset(new DBuf((size_t)nnzb * 4, s));
+    h2d(s, dcp->as<int32_t>(), cp);
+    h2d(s, dce->as<int32_t>(), ce);
+  } else if (decoupling == 1) {
+    std::vector<int32_t> dg(n, -1);
+    for (int32_t c = 0; c < n; ++c)
+      for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) if (A.ci[e] == c) dg[c] = e;
+    dcp.reset(new DBuf((size_t)n * 4, s));
+    h2d(s, dcp->as<int32_t>(), dg);
+  }
+  const unsigned gC = nblk((size_t)n * bb, 256), gn = nblk(n, 128);
+  switch (b) {
+#define CASE(BV)                                                                                                  \
+  case BV:                                                                                                        \
+    if (decoupling == 2)                                                                                   \
+      klaunch(s, false, colsum_kernel<BV>, gC, 256, n, (const int*)dcp->p, (const int*)dce->p, (const double*)dA.p, \
+              dC.as<double>());                                                                                   \
+    else if (decoupling == 1)                                                                              \
+      klaunch(s, false, diagblock_kernel<BV>, gC, 256, n, (const int*)dcp->p, (const double*)dA.p, dC.as<double>()); \
+    if (decoupling != 0) klaunch(s, false, weights_kernel<BV>, gn, 128, n, (const double*)dC.p, dW.as<double>(), \
+                                        dbad.as<int>());                                                          \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  S.W.assign((size_t)n * b, 0.0);
+  if (decoupling == 0) {
+    for (int32_t c = 0; c < n; ++c) S.W[(size_t)c * b] = 1.0;
+    h2d(s, dW.as<double>(), S.W);
+  }
+  switch (b) {
+#define CASE(BV) case BV: klaunch(s, false, app_kernel<BV>, gn, 128, n, (const int*)drp.p, (const double*)dW.p, \
+                                  (const double*)dA.p, dP.as<double>()); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  int bad = -1;
+  S.App.n = n;
+  S.App.rp = A.rp;
+  S.App.ci = A.ci;
+  S.App.v.resize(nnzb);
+  CK(cudaMemcpyAsync(&bad, dbad.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(S.W.data(), dW.p, sizeof(double) * S.W.size(), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(S.App.v.data(), dP.p, sizeof(double) * nnzb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad >= 0) throw std::pair<int, std::string>(MSP_ESINGULAR, "decoupling: singular N-N block at cell " + std::to_string(bad));
+}
+
+// NEXT-2, S3 Galerkin product on the GPU (setup_kernels.cuh: pattern and values per
+// coarse row in the specified summation order -> bit-identical to the host product).
+// Returns nonzero (host fallback) when a coarse row has more than kRapMax candidates.
+int gpu_rap(cudaStream_t s, const msp::SpMat& A, const std::vector<int32_t>& agg, int32_t nagg, msp::SpMat& C) {
+  const int32_t n = A.n;
+  const int64_t nnz = (int64_t)A.ci.size();
+  std::vector<int32_t> mp(nagg + 1, 0), mi(n);
+  for (int32_t i = 0; i < n; ++i) mp[agg[i] + 1]++;
+  for (int32_t I = 0; I < nagg; ++I) mp[I + 1] += mp[I];
+  {
+    std::vector<int32_t> f(mp.begin(), mp.end() - 1);
+    for (int32_t i = 0; i < n; ++i) mi[f[agg[i]]++] = i;
+  }
+  DBuf drp((size_t)(n + 1) * 4, s), dci((size_t)nnz * 4, s), dv((size_t)nnz * 8, s), dagg((size_t)n * 4, s);
+  DBuf dmp((size_t)(nagg + 1) * 4, s), dmi((size_t)n * 4, s), dcnt((size_t)(nagg + 1) * 4, s), dov(4, s);
+  h2d(s, drp.as<int32_t>(), A.rp);
+  h2d(s, dci.as<int32_t>(), A.ci);
+  h2d(s, dv.as<double>(), A.v);
+  h2d(s, dagg.as<int32_t>(), agg);
+  h2d(s, dmp.as<int32_t>(), mp);
+  h2d(s, dmi.as<int32_t>(), mi);
+  CK(cudaMemsetAsync(dov.p, 0, 4, s));
+  const unsigned g = nblk(nagg, 128);
+  klaunch(s, false, rap_count_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)drp.p,
+          (const int*)dci.p, (const int*)dagg.p, dcnt.as<int>(), dov.as<int>());
+  std::vector<int32_t> cnt(nagg);
+  int ov = 0;
+  CK(cudaMemcpyAsync(cnt.data(), dcnt.p, sizeof(int32_t) * nagg, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&ov, dov.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ov) return 1;
+  C.n = nagg;
+  C.rp.assign(nagg + 1, 0);
+  for (int32_t I = 0; I < nagg; ++I) C.rp[I + 1] = C.rp[I] + cnt[I];
+  const int64_t cn = C.rp[nagg];
+  DBuf dcrp((size_t)(nagg + 1) * 4, s), dcci((size_t)cn * 4, s), dcv((size_t)cn * 8, s);
+  h2d(s, dcrp.as<int32_t>(), C.rp);
+  klaunch(s, false, rap_fill_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)drp.p,
+          (const int*)dci.p, (const double*)dv.p, (const int*)dagg.p, (const int*)dcrp.p, dcci.as<int>(),
+          dcv.as<double>());
+  C.ci.resize(cn);
+  C.v.resize(cn);
+  CK(cudaMemcpyAsync(C.ci.data(), dcci.p, sizeof(int32_t) * cn, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(C.v.data(), dcv.p, sizeof(double) * cn, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
   SetupTimer T;
@@ -496,14 +635,28 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   std::string err;
   Nvtx nv_setup("S1-S4 SETUP");
   int rc = 0;
+  h->gpu_s1 = false;
+  msp::Params prm = h->prm;
+  if (h->setup_on_gpu) {                 // NEXT-2: S1 and the Galerkin products on the GPU
+    gpu_setup_s1(h->s, h->prm.decoupling, A, S);
+    h->gpu_s1 = true;
+    prm.s1_given = true;
+    cudaStream_t st = h->s;
+    prm.rap = [st](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
+      return gpu_rap(st, Af, agg, na, C);
+    };
+  }
+  T.mark("S1 weights + A_PP (GPU)");
   {
-    Nvtx nv("S1-S4 host: weights, A_PP, NPAIR+Galerkin, colorings, ABMC order");
-    rc = msp::run_host_setup(A, h->prm, S, err);
+    Nvtx nv("S2-S4 host: NPAIR, colorings, ABMC order (Galerkin on the GPU)");
+    rc = msp::run_host_setup(A, prm, S, err);
   }
   if (rc) throw std::pair<int, std::string>(rc, err);
   std::vector<int32_t> rp, ci, dg, src;
   std::vector<double> F;
-  T.mark("host setup S1-S4");
+  T.mark("host setup S2-S4");
+  h->W_nat = S.W;
+  h->App_nat = S.App.v;
   // BILU(0): on the GPU after the upload (single GPU), on the host for the distributed
   // setup (every rank factorizes the global matrix) or when MSP_HOST_BILU=1
   const bool gpu_bilu = !h->comm && !(std::getenv("MSP_HOST_BILU") && std::atoi(std::getenv("MSP_HOST_BILU")));
@@ -1969,6 +2122,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   std::unique_ptr<msp_handle> h(new msp_handle);
   h->cfg = c;
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
+  if (const char* e = std::getenv("MSP_HOST_SETUP")) h->setup_on_gpu = std::atoi(e) == 0;
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;
@@ -2318,6 +2472,14 @@ msp_status msp_bilu_set_factors(msp_handle* h, const double* F) {
   });
 }
 
+msp_status msp_get_s1(const msp_handle* h, double* W, double* App, int32_t* on_gpu) {
+  if (!h || !W || !App || h->W_nat.empty()) return MSP_EINVAL;
+  std::memcpy(W, h->W_nat.data(), sizeof(double) * h->W_nat.size());
+  std::memcpy(App, h->App_nat.data(), sizeof(double) * h->App_nat.size());
+  if (on_gpu) *on_gpu = h->gpu_s1 ? 1 : 0;
+  return MSP_OK;
+}
+
 msp_status msp_get_order(const msp_handle* h, int32_t* order) {
   if (!h || !order) return MSP_EINVAL;
   std::memcpy(order, h->order.data(), sizeof(int32_t) * h->n);
@@ -2640,7 +2802,30 @@ msp_status msp_host_setup_run(const msp_bsr* A, int nc, const msp_config* cfg, m
   msp_config c;
   msp_config_default(&c);
   if (cfg) c = *cfg;
-  int rc = msp::run_host_setup(s->M, params_of(&c), s->S, err);
+  msp::Params prm = params_of(&c);
+  // MSP_HOST_SETUP_GPU=1: the GPU steps of NEXT-2 (S1, Galerkin) as msp_setup runs them,
+  // for the bit-exact comparison with the host path (needs a GPU)
+  const bool gpu = std::getenv("MSP_HOST_SETUP_GPU") && std::atoi(std::getenv("MSP_HOST_SETUP_GPU"));
+  msp_status gst = MSP_OK;
+  cudaStream_t stream = nullptr;
+  if (gpu) {
+    gst = guarded(nullptr, [&]() -> msp_status {
+      CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+      gpu_setup_s1(stream, prm.decoupling, s->M, s->S);
+      return MSP_OK;
+    });
+    if (gst) { if (stream) cudaStreamDestroy(stream); return gst; }
+    prm.s1_given = true;
+    prm.rap = [stream](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
+      try {
+        return gpu_rap(stream, Af, agg, na, C);
+      } catch (...) {
+        return 1;
+      }
+    };
+  }
+  int rc = msp::run_host_setup(s->M, prm, s->S, err);
+  if (stream) cudaStreamDestroy(stream);
   if (rc) return fail(nullptr, (msp_status)rc, err);
   *out = s.release();
   return MSP_OK;
