@@ -74,19 +74,23 @@ Graph value_graph(const SpMat& A) {
   return G;
 }
 
-Graph block_graph(const BlockMat& A) {
-  // nonzero flag per stored block, then symmetrise by merging each row with the
-  // transposed row (counting-sort transpose keeps both ascending)
+Graph block_graph(const BlockMat& A, const std::vector<uint8_t>* nz_given) {
+  // nonzero flag per stored block (or the flags computed on the GPU), then symmetrise by
+  // merging each row with the transposed row (counting-sort transpose keeps both ascending)
   const int bb = A.b * A.b;
   const int32_t n = A.n;
-  std::vector<uint8_t> nz(A.ci.size(), 0);
+  std::vector<uint8_t> nz_own;
+  if (!nz_given) {
+    nz_own.assign(A.ci.size(), 0);
 #pragma omp parallel for schedule(static)
-  for (int64_t e = 0; e < (int64_t)A.ci.size(); ++e) {
-    const double* B = &A.v[(size_t)e * bb];
-    bool f = false;
-    for (int t = 0; t < bb && !f; ++t) f = (B[t] != 0.0);
-    nz[e] = f;
+    for (int64_t e = 0; e < (int64_t)A.ci.size(); ++e) {
+      const double* B = &A.v[(size_t)e * bb];
+      bool f = false;
+      for (int t = 0; t < bb && !f; ++t) f = (B[t] != 0.0);
+      nz_own[e] = f;
+    }
   }
+  const std::vector<uint8_t>& nz = nz_given ? *nz_given : nz_own;
   std::vector<int32_t> tp(n + 1, 0), tc(A.ci.size());
   std::vector<uint8_t> tnz(A.ci.size());
   for (int32_t j : A.ci) tp[j + 1]++;
@@ -403,26 +407,27 @@ static bool off_diagonal_zero(const SpMat& A) {
 
 static int32_t aggregate_passes(const SpMat& A0, int passes, std::vector<int32_t>& comp, SpMat* out,
                                 const RapFn* rap = nullptr) {
-  SpMat cur = A0;
+  SpMat cur;                                   // product of the previous pass (pass 0 reads A0)
   comp.resize(A0.n);
   std::iota(comp.begin(), comp.end(), 0);
   int32_t na = A0.n;
   const bool verbose = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
   for (int p = 0; p < passes; ++p) {
+    const SpMat& in = (p == 0) ? A0 : cur;
     std::vector<int32_t> a;
     const auto t0 = std::chrono::steady_clock::now();
-    na = pair_aggregate(cur, a);
+    na = pair_aggregate(in, a);
     for (auto& c : comp) c = a[c];
     const auto t1 = std::chrono::steady_clock::now();
     SpMat nxt;
-    if (rap && *rap && (*rap)(cur, a, na, nxt) == 0) cur = std::move(nxt);
-    else cur = galerkin_rap(cur, a, na);
+    if (!(rap && *rap && (*rap)(in, a, na, nxt) == 0)) nxt = galerkin_rap(in, a, na);
+    cur = std::move(nxt);
     if (verbose)
       std::fprintf(stderr, "[msp setup]   pass %d: NPAIR %.3f s, Galerkin %.3f s (n %d -> %d)\n", p,
                    std::chrono::duration<double>(t1 - t0).count(),
                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count(), (int)cur.n, (int)na);
   }
-  if (out) *out = std::move(cur);
+  if (out) *out = (passes > 0) ? std::move(cur) : A0;
   return na;
 }
 
@@ -562,7 +567,7 @@ static SpMat graph_laplacian(const Graph& G) {
 static void make_ordering(HostSetup& S) {
   const BlockMat& A = *S.A;
   const int32_t n = A.n;
-  Graph G = block_graph(A);
+  Graph G = block_graph(A, S.block_nz.empty() ? nullptr : &S.block_nz);
   std::vector<int32_t> blk(n), bcol;
   int32_t nb;
   if (S.prm.bilu_order == 0) {
@@ -719,19 +724,25 @@ int permuted_pattern(const HostSetup& S, const BlockMat& A, std::vector<int32_t>
   ci.resize(A.ci.size());
   src.resize(A.ci.size());
   dg.assign(n, -1);
-  std::vector<std::pair<int32_t, int32_t>> tmp;
-  for (int32_t p = 0; p < n; ++p) {
-    const int32_t c = S.order[p];
-    tmp.clear();
-    for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) tmp.push_back({S.pos[A.ci[e]], e});
-    std::sort(tmp.begin(), tmp.end());
-    for (size_t t = 0; t < tmp.size(); ++t) {
-      ci[rp[p] + t] = tmp[t].first;
-      src[rp[p] + t] = tmp[t].second;
-      if (tmp[t].first == p) dg[p] = rp[p] + (int32_t)t;
+  int32_t bad = -1;
+#pragma omp parallel reduction(max : bad)
+  {
+    std::vector<std::pair<int32_t, int32_t>> tmp;   // rows are independent (disjoint output ranges)
+#pragma omp for schedule(static)
+    for (int32_t p = 0; p < n; ++p) {
+      const int32_t c = S.order[p];
+      tmp.clear();
+      for (int32_t e = A.rp[c]; e < A.rp[c + 1]; ++e) tmp.push_back({S.pos[A.ci[e]], e});
+      std::sort(tmp.begin(), tmp.end());
+      for (size_t t = 0; t < tmp.size(); ++t) {
+        ci[rp[p] + t] = tmp[t].first;
+        src[rp[p] + t] = tmp[t].second;
+        if (tmp[t].first == p) dg[p] = rp[p] + (int32_t)t;
+      }
+      if (dg[p] < 0) bad = std::max(bad, c);
     }
-    if (dg[p] < 0) { err = "BILU: missing diagonal block at cell " + std::to_string(c); return 1; }
   }
+  if (bad >= 0) { err = "BILU: missing diagonal block at cell " + std::to_string(bad); return 1; }
   return 0;
 }
 

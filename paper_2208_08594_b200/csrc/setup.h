@@ -64,6 +64,7 @@ struct HostSetup {
   std::vector<int32_t> blk_ptr;        // cell-position ranges of the ordering blocks
   std::vector<int32_t> color_blk_ptr;  // block ranges per block color
   std::vector<int32_t> level1_agg;     // ABMC blocks (cell -> block id)
+  std::vector<uint8_t> block_nz;       // optional: nonzero flag per stored block (GPU S1)
 };
 
 // status codes mirror msp_status
@@ -83,7 +84,7 @@ int permuted_pattern(const HostSetup& S, const BlockMat& A, std::vector<int32_t>
 
 // Building blocks (exposed for the host-setup introspection entry points / tests)
 Graph value_graph(const SpMat& A);
-Graph block_graph(const BlockMat& A);
+Graph block_graph(const BlockMat& A, const std::vector<uint8_t>* nz_given = nullptr);
 int32_t color_groups(const Graph& G, std::vector<int32_t>& color);
 int32_t pair_aggregate(const SpMat& A, std::vector<int32_t>& agg);
 SpMat galerkin_rap(const SpMat& A, const std::vector<int32_t>& agg, int32_t nagg);

@@ -206,4 +206,15 @@ __global__ void rap_fill_kernel(int nc, const int* __restrict__ mp, const int* _
   }
 }
 
+// Coarsest level (a6 setup): dense row-major A_L from its CSR and the identity right-hand
+// side (leading dimension ld) for the inverse; both outputs zeroed by the caller.
+__global__ void dense_identity_kernel(int m, int ld, const int* __restrict__ rp, const int* __restrict__ ci,
+                                      const double* __restrict__ v, double* __restrict__ dense,
+                                      double* __restrict__ ident) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (int e = rp[i]; e < rp[i + 1]; ++e) dense[(size_t)i * m + ci[e]] = v[e];
+  ident[(size_t)i * ld + i] = 1.0;
+}
+
 }  // namespace mspk

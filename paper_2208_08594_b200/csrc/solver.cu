@@ -146,6 +146,7 @@ struct msp_handle {
   double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
   double* ftmp = nullptr;            // msp_bilu_set_factors scratch
   bool setup_on_gpu = true;          // NEXT-2: S1 + Galerkin on the GPU (MSP_HOST_SETUP=1: host)
+  cusolverDnHandle_t cs = nullptr;   // coarsest inverse (created once, reused by rebuilds)
   bool gpu_s1 = false;               // the last SETUP computed S1 on the GPU
   std::vector<double> W_nat, App_nat;  // S1 results of the last SETUP (natural order), for parity
   cudaStream_t caller = nullptr;     // the caller's stream (msp_setup / msp_set_stream)
@@ -512,13 +513,20 @@ void h2d(cudaStream_t s, T* d, const std::vector<T>& v) {
 // decoupling weights and A_PP = W^T A Pi_P, explicitly rounded in the host/oracle order
 // (setup_kernels.cuh) -> bit-identical W and A_PP, returned to the host for the greedy
 // steps (NPAIR, colorings) that follow.
-void gpu_setup_s1(cudaStream_t s, int decoupling, const msp::BlockMat& A, msp::HostSetup& S) {
+std::unique_ptr<DBuf> gpu_setup_s1(cudaStream_t s, int decoupling, const msp::BlockMat& A, msp::HostSetup& S,
+                                   DBuf** dApp_out = nullptr) {
   Nvtx nv("S1 weights + A_PP (GPU)");
   const int32_t n = A.n;
   const int b = A.b, bb = b * b;
   const int64_t nnzb = (int64_t)A.ci.size();
-  DBuf dA((size_t)nnzb * bb * sizeof(double), s), dC((size_t)n * bb * sizeof(double), s);
-  DBuf dW((size_t)n * b * sizeof(double), s), dP((size_t)nnzb * sizeof(double), s);
+  std::unique_ptr<DBuf> dAp(new DBuf((size_t)nnzb * bb * sizeof(double), s));
+  DBuf& dA = *dAp;
+  DBuf dC((size_t)n * bb * sizeof(double), s), dW((size_t)n * b * sizeof(double), s);
+  DBuf* dPp = new DBuf((size_t)nnzb * sizeof(double), s);
+  std::unique_ptr<DBuf> dPown(dApp_out ? nullptr : dPp);
+  if (dApp_out) *dApp_out = dPp;
+  DBuf& dP = *dPp;
+  DBuf dnz((size_t)nnzb, s);
   DBuf drp((size_t)(n + 1) * 4, s), dbad(4, s);
   CK(cudaMemcpyAsync(dA.p, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, s));
   h2d(s, drp.as<int32_t>(), A.rp);
@@ -564,10 +572,14 @@ void gpu_setup_s1(cudaStream_t s, int decoupling, const msp::BlockMat& A, msp::H
   }
   switch (b) {
 #define CASE(BV) case BV: klaunch(s, false, app_kernel<BV>, gn, 128, n, (const int*)drp.p, (const double*)dW.p, \
-                                  (const double*)dA.p, dP.as<double>()); break;
+                                  (const double*)dA.p, dP.as<double>()); \
+                          klaunch(s, false, block_nonzero_kernel<BV>, nblk(nnzb, 256), 256, nnzb, (const double*)dA.p, \
+                                  dnz.as<uint8_t>()); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
+  S.block_nz.resize(nnzb);
+  CK(cudaMemcpyAsync(S.block_nz.data(), dnz.p, nnzb, cudaMemcpyDeviceToHost, s));
   int bad = -1;
   S.App.n = n;
   S.App.rp = A.rp;
@@ -578,14 +590,42 @@ void gpu_setup_s1(cudaStream_t s, int decoupling, const msp::BlockMat& A, msp::H
   CK(cudaMemcpyAsync(S.App.v.data(), dP.p, sizeof(double) * nnzb, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (bad >= 0) throw std::pair<int, std::string>(MSP_ESINGULAR, "decoupling: singular N-N block at cell " + std::to_string(bad));
+  return dAp;                                         // A's values on the device (natural order)
 }
+
+// Device-resident chain of the Galerkin products of one SETUP: the fine operand of the
+// next product is the previous product's result (or A_PP from S1) already on the device,
+// so only the aggregate map goes up and the coarse matrix (needed by the host NPAIR /
+// colorings) comes down.  Buffers grow on demand and live for the SETUP.
+struct RapChain {
+  cudaStream_t s = nullptr;
+  int32_t n = -1;                          // rows of the device-resident fine matrix (-1: none)
+  int64_t nnz = -1;
+  const double* host_v = nullptr;          // host buffer the device copy mirrors
+  std::vector<std::unique_ptr<DBuf>> keep;
+  int32_t *rp = nullptr, *ci = nullptr;
+  double* v = nullptr;
+};
 
 // NEXT-2, S3 Galerkin product on the GPU (setup_kernels.cuh: pattern and values per
 // coarse row in the specified summation order -> bit-identical to the host product).
 // Returns nonzero (host fallback) when a coarse row has more than kRapMax candidates.
-int gpu_rap(cudaStream_t s, const msp::SpMat& A, const std::vector<int32_t>& agg, int32_t nagg, msp::SpMat& C) {
+int gpu_rap(RapChain& ch, const msp::SpMat& A, const std::vector<int32_t>& agg, int32_t nagg, msp::SpMat& C) {
+  cudaStream_t s = ch.s;
   const int32_t n = A.n;
   const int64_t nnz = (int64_t)A.ci.size();
+  if (!(ch.n == n && ch.nnz == nnz && ch.host_v == A.v.data())) {     // fine matrix not resident
+    ch.keep.clear();
+    ch.keep.emplace_back(new DBuf((size_t)(n + 1) * 4, s));
+    ch.keep.emplace_back(new DBuf((size_t)nnz * 4, s));
+    ch.keep.emplace_back(new DBuf((size_t)nnz * 8, s));
+    ch.rp = ch.keep[0]->as<int32_t>();
+    ch.ci = ch.keep[1]->as<int32_t>();
+    ch.v = ch.keep[2]->as<double>();
+    h2d(s, ch.rp, A.rp);
+    h2d(s, ch.ci, A.ci);
+    h2d(s, ch.v, A.v);
+  }
   std::vector<int32_t> mp(nagg + 1, 0), mi(n);
   for (int32_t i = 0; i < n; ++i) mp[agg[i] + 1]++;
   for (int32_t I = 0; I < nagg; ++I) mp[I + 1] += mp[I];
@@ -593,18 +633,15 @@ int gpu_rap(cudaStream_t s, const msp::SpMat& A, const std::vector<int32_t>& agg
     std::vector<int32_t> f(mp.begin(), mp.end() - 1);
     for (int32_t i = 0; i < n; ++i) mi[f[agg[i]]++] = i;
   }
-  DBuf drp((size_t)(n + 1) * 4, s), dci((size_t)nnz * 4, s), dv((size_t)nnz * 8, s), dagg((size_t)n * 4, s);
+  DBuf dagg((size_t)n * 4, s);
   DBuf dmp((size_t)(nagg + 1) * 4, s), dmi((size_t)n * 4, s), dcnt((size_t)(nagg + 1) * 4, s), dov(4, s);
-  h2d(s, drp.as<int32_t>(), A.rp);
-  h2d(s, dci.as<int32_t>(), A.ci);
-  h2d(s, dv.as<double>(), A.v);
   h2d(s, dagg.as<int32_t>(), agg);
   h2d(s, dmp.as<int32_t>(), mp);
   h2d(s, dmi.as<int32_t>(), mi);
   CK(cudaMemsetAsync(dov.p, 0, 4, s));
   const unsigned g = nblk(nagg, 128);
-  klaunch(s, false, rap_count_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)drp.p,
-          (const int*)dci.p, (const int*)dagg.p, dcnt.as<int>(), dov.as<int>());
+  klaunch(s, false, rap_count_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)ch.rp,
+          (const int*)ch.ci, (const int*)dagg.p, dcnt.as<int>(), dov.as<int>());
   std::vector<int32_t> cnt(nagg);
   int ov = 0;
   CK(cudaMemcpyAsync(cnt.data(), dcnt.p, sizeof(int32_t) * nagg, cudaMemcpyDeviceToHost, s));
@@ -615,16 +652,28 @@ int gpu_rap(cudaStream_t s, const msp::SpMat& A, const std::vector<int32_t>& agg
   C.rp.assign(nagg + 1, 0);
   for (int32_t I = 0; I < nagg; ++I) C.rp[I + 1] = C.rp[I] + cnt[I];
   const int64_t cn = C.rp[nagg];
-  DBuf dcrp((size_t)(nagg + 1) * 4, s), dcci((size_t)cn * 4, s), dcv((size_t)cn * 8, s);
-  h2d(s, dcrp.as<int32_t>(), C.rp);
-  klaunch(s, false, rap_fill_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)drp.p,
-          (const int*)dci.p, (const double*)dv.p, (const int*)dagg.p, (const int*)dcrp.p, dcci.as<int>(),
-          dcv.as<double>());
+  std::unique_ptr<DBuf> dcrp(new DBuf((size_t)(nagg + 1) * 4, s)), dcci(new DBuf((size_t)cn * 4, s)),
+      dcv(new DBuf((size_t)cn * 8, s));
+  h2d(s, dcrp->as<int32_t>(), C.rp);
+  klaunch(s, false, rap_fill_kernel, g, 128, nagg, (const int*)dmp.p, (const int*)dmi.p, (const int*)ch.rp,
+          (const int*)ch.ci, (const double*)ch.v, (const int*)dagg.p, (const int*)dcrp->p, dcci->as<int>(),
+          dcv->as<double>());
   C.ci.resize(cn);
   C.v.resize(cn);
-  CK(cudaMemcpyAsync(C.ci.data(), dcci.p, sizeof(int32_t) * cn, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(C.v.data(), dcv.p, sizeof(double) * cn, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(C.ci.data(), dcci->p, sizeof(int32_t) * cn, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(C.v.data(), dcv->p, sizeof(double) * cn, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  // the product stays resident as the next fine operand (C is moved, its buffer kept)
+  ch.keep.clear();
+  ch.keep.push_back(std::move(dcrp));
+  ch.keep.push_back(std::move(dcci));
+  ch.keep.push_back(std::move(dcv));
+  ch.rp = ch.keep[0]->as<int32_t>();
+  ch.ci = ch.keep[1]->as<int32_t>();
+  ch.v = ch.keep[2]->as<double>();
+  ch.n = nagg;
+  ch.nnz = cn;
+  ch.host_v = C.v.data();
   return 0;
 }
 
@@ -637,13 +686,28 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   int rc = 0;
   h->gpu_s1 = false;
   msp::Params prm = h->prm;
+  std::unique_ptr<DBuf> dAvals;           // A's values on the device (S1 upload, reused for the stage)
+  RapChain chain;
+  chain.s = h->s;
   if (h->setup_on_gpu) {                 // NEXT-2: S1 and the Galerkin products on the GPU
-    gpu_setup_s1(h->s, h->prm.decoupling, A, S);
+    DBuf* dApp = nullptr;
+    dAvals = gpu_setup_s1(h->s, h->prm.decoupling, A, S, &dApp);
+    chain.keep.emplace_back(dApp);          // A_PP resident as the first fine operand
+    chain.v = dApp->as<double>();
+    chain.keep.emplace_back(new DBuf((size_t)(A.n + 1) * 4, h->s));
+    chain.keep.emplace_back(new DBuf(A.ci.size() * 4, h->s));
+    chain.rp = chain.keep[1]->as<int32_t>();
+    chain.ci = chain.keep[2]->as<int32_t>();
+    h2d(h->s, chain.rp, A.rp);
+    h2d(h->s, chain.ci, A.ci);
+    chain.n = A.n;
+    chain.nnz = (int64_t)A.ci.size();
+    chain.host_v = nullptr;                  // set below: the host copy the hierarchy starts from
     h->gpu_s1 = true;
     prm.s1_given = true;
-    cudaStream_t st = h->s;
-    prm.rap = [st](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
-      return gpu_rap(st, Af, agg, na, C);
+    prm.rap = [&chain](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
+      if (chain.host_v == nullptr && Af.n == chain.n && (int64_t)Af.ci.size() == chain.nnz) chain.host_v = Af.v.data();
+      return gpu_rap(chain, Af, agg, na, C);
     };
   }
   T.mark("S1 weights + A_PP (GPU)");
@@ -762,7 +826,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->Fval = h->dalloc<double>(nv);
     h->Aval = h->dalloc<double>(nv);
     h->Pcol = h->dalloc<double>(ci.size() * (size_t)b);
-    CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+    if (dAvals) CK(cudaMemcpyAsync(h->stage, dAvals->p, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
+    else CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
     int* dbad = nullptr;
     if (gpu_bilu) {
       dbad = h->dalloc<int>(1);
@@ -867,17 +932,24 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->cdiag = h->upload(d);
   } else {
     const int32_t m = h->nL;
-    std::vector<double> dense((size_t)m * m, 0.0);
-    for (int32_t i = 0; i < m; ++i)
-      for (int32_t e = S.Ac.rp[i]; e < S.Ac.rp[i + 1]; ++e) dense[(size_t)i * m + S.Ac.ci[e]] = S.Ac.v[e];
-    double* dA = h->upload(dense);           // row-major A == column-major A^T
+    // dense A_L and the identity right-hand side assembled on the device (no 2 x m^2 host
+    // uploads); inverse by LU (getrf) + m solves (getrs); the cuSOLVER handle is created
+    // once per msp_handle and reused by every rebuild
+    double* dA = h->dalloc<double>((size_t)m * m);           // row-major A == column-major A^T
     h->ldA = (m + 31) / 32 * 32;             // 256-byte aligned rows for the vector loads
     h->Ainv = h->dalloc<double>((size_t)m * h->ldA);
-    std::vector<double> I((size_t)m * h->ldA, 0.0);
-    for (int32_t i = 0; i < m; ++i) I[(size_t)i * h->ldA + i] = 1.0;
-    CK(cudaMemcpyAsync(h->Ainv, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, h->s));
-    cusolverDnHandle_t cs;
-    if (cusolverDnCreate(&cs) != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnCreate"};
+    {
+      const int32_t* crp = h->upload(S.Ac.rp);
+      const int32_t* cci = h->upload(S.Ac.ci);
+      const double* cv = h->upload(S.Ac.v);
+      CK(cudaMemsetAsync(dA, 0, sizeof(double) * (size_t)m * m, h->s));
+      CK(cudaMemsetAsync(h->Ainv, 0, sizeof(double) * (size_t)m * h->ldA, h->s));
+      klaunch(h->s, false, dense_identity_kernel, nblk(m, 128), 128, m, h->ldA, crp, cci, cv, dA, h->Ainv);
+    }
+    if (!h->cs) {
+      if (cusolverDnCreate(&h->cs) != CUSOLVER_STATUS_SUCCESS) { h->cs = nullptr; throw CudaError{cudaErrorUnknown, "cusolverDnCreate"}; }
+    }
+    cusolverDnHandle_t cs = h->cs;
     cusolverDnSetStream(cs, h->s);
     int lwork = 0;
     cusolverDnDgetrf_bufferSize(cs, m, m, dA, m, &lwork);
@@ -888,14 +960,11 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     int hinfo = 0;
     CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, h->s));
     CK(cudaStreamSynchronize(h->s));
-    if (s1 != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
-      cusolverDnDestroy(cs);
+    if (s1 != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
       throw std::pair<int, std::string>(MSP_ESINGULAR, "coarsest: singular dense matrix (getrf info " + std::to_string(hinfo) + ")");
-    }
     // (A^T) X = I  =>  X = A^-T column-major  ==  A^-1 row-major
     cusolverStatus_t s2 = cusolverDnDgetrs(cs, CUBLAS_OP_N, m, m, dA, m, ipiv, h->Ainv, h->ldA, info);
     CK(cudaStreamSynchronize(h->s));
-    cusolverDnDestroy(cs);
     if (s2 != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnDgetrs"};
   }
   T.mark("coarsest inverse");
@@ -2506,6 +2575,7 @@ void msp_destroy(msp_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->cs) cusolverDnDestroy(h->cs);
   if (h->s) cudaStreamDestroy(h->s);
   delete h;
 }
@@ -2816,15 +2886,19 @@ msp_status msp_host_setup_run(const msp_bsr* A, int nc, const msp_config* cfg, m
     });
     if (gst) { if (stream) cudaStreamDestroy(stream); return gst; }
     prm.s1_given = true;
-    prm.rap = [stream](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
+  }
+  RapChain chain;
+  chain.s = stream;
+  if (gpu)
+    prm.rap = [&chain](const msp::SpMat& Af, const std::vector<int32_t>& agg, int32_t na, msp::SpMat& C) {
       try {
-        return gpu_rap(stream, Af, agg, na, C);
+        return gpu_rap(chain, Af, agg, na, C);
       } catch (...) {
         return 1;
       }
     };
-  }
   int rc = msp::run_host_setup(s->M, prm, s->S, err);
+  chain.keep.clear();
   if (stream) cudaStreamDestroy(stream);
   if (rc) return fail(nullptr, (msp_status)rc, err);
   *out = s.release();
