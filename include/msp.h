@@ -94,6 +94,11 @@ typedef struct {
   msp_alloc_fn alloc;        /* optional device allocator */
   msp_free_fn free_fn;
   void* alloc_ctx;
+  int32_t coarse_mode;       /* distributed handles: 0 (default) levels >= 1 and the
+                                coarsest replicated on every rank (allgather of the level-1
+                                right-hand side); 1 ROOT: agglomerated onto rank 0, which runs them
+                                and broadcasts the level-1 correction (north_star's "coarse levels
+                                are agglomerated onto one GPU"; bit-identical iterates) */
 } msp_config;
 
 typedef struct msp_handle msp_handle;

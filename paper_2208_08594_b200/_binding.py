@@ -35,7 +35,8 @@ class Config(ctypes.Structure):
                 ("orth", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
                 ("use_coop", ctypes.c_int32), ("smoother", ctypes.c_int32),
                 ("gs_chunk", ctypes.c_int32),
-                ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
+                ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
+                ("coarse_mode", ctypes.c_int32)]
 
     @classmethod
     def make(cls, **kw):

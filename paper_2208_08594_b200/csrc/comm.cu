@@ -73,6 +73,9 @@ class NcclComm : public Comm {
   void allgather(cudaStream_t s, const double* send, double* recv, int count) override {
     chk(ncclAllGather(send, recv, count, ncclDouble, comm, s), "allgather");
   }
+  void broadcast(cudaStream_t s, double* buf, int count, int root) override {
+    chk(ncclBroadcast(buf, buf, count, ncclDouble, root, comm, s), "broadcast");
+  }
 };
 
 int nccl_unique_id(void* out) {
@@ -221,6 +224,19 @@ class LoopbackComm : public Comm {
     for (int q = 0; q < g->n; ++q) {
       if (q != r) cudaStreamWaitEvent(s, g->ready[q], 0);
       cudaMemcpyAsync(recv + (size_t)q * count, g->ptr[q], sizeof(double) * count, cudaMemcpyDeviceToDevice, s);
+    }
+    cudaEventRecord(g->done[r], s);
+    g->bar.arrive_and_wait();
+    wait_peers_done(s);          // later work on s may overwrite buffers peers read
+  }
+  void broadcast(cudaStream_t s, double* buf, int count, int root) override {
+    wait_peers_done(s);
+    cudaEventRecord(g->ready[r], s);
+    if (r == root) g->ptr[root] = buf;
+    g->bar.arrive_and_wait();
+    if (r != root) {
+      cudaStreamWaitEvent(s, g->ready[root], 0);
+      cudaMemcpyAsync(buf, g->ptr[root], sizeof(double) * count, cudaMemcpyDeviceToDevice, s);
     }
     cudaEventRecord(g->done[r], s);
     g->bar.arrive_and_wait();

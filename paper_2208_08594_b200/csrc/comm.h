@@ -42,6 +42,8 @@ class Comm {
   virtual void allreduce_sum(cudaStream_t s, double* buf, int count) = 0;
   // recv[r*count .. ) = send of rank r
   virtual void allgather(cudaStream_t s, const double* send, double* recv, int count) = 0;
+  // buf of every rank = buf of rank `root`
+  virtual void broadcast(cudaStream_t s, double* buf, int count, int root) = 0;
   // true if every call only enqueues work on s (no host synchronisation), so the
   // Arnoldi steps that use it can be captured into CUDA graphs
   virtual bool capturable() const { return false; }

@@ -229,6 +229,7 @@ msp::Params params_of(const msp_config* c) {
   p.use_coop = c->use_coop;
   p.smoother = c->smoother;
   p.gs_chunk = c->gs_chunk;
+  p.coarse_mode = c->coarse_mode;
   return p;
 }
 
@@ -1632,15 +1633,21 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
             (const double*)L0.r, h->l1_send, (double*)nullptr, (const double*)nullptr, 0);
     ++h->nlaunch;
   }
+  // level-1 right-hand side: every rank's owned aggregates (replicated: all ranks; ROOT:
+  // only rank 0 goes on with it)
   h->comm->allgather(h->s, h->l1_send, h->l1_recv, h->l1_cmax);
   const bool init1 = L > 1 && h->prm.pre_sweeps > 0;
   double* b1 = (L > 1) ? h->lv[1].b : h->bL;
   double* x1 = (L > 1) ? h->lv[1].x : h->xL;
-  klaunch(h->s, h->pdl, scatter_l1_kernel, nblk((size_t)h->nranks * h->l1_cmax, 256), 256, h->nranks * h->l1_cmax,
-          (const int*)h->l1_scatter, (const double*)h->l1_recv, b1, init1 ? x1 : (double*)nullptr,
-          init1 ? (const double*)h->lv[1].diag : (const double*)nullptr, init1 ? h->lv[1].color_row[1] : 0);
-  ++h->nlaunch;
-  vcycle(h, 1, init1);
+  const bool root_mode = h->prm.coarse_mode == 1;
+  if (!root_mode || h->rank == 0) {
+    klaunch(h->s, h->pdl, scatter_l1_kernel, nblk((size_t)h->nranks * h->l1_cmax, 256), 256, h->nranks * h->l1_cmax,
+            (const int*)h->l1_scatter, (const double*)h->l1_recv, b1, init1 ? x1 : (double*)nullptr,
+            init1 ? (const double*)h->lv[1].diag : (const double*)nullptr, init1 ? h->lv[1].color_row[1] : 0);
+    ++h->nlaunch;
+    vcycle(h, 1, init1);                                                     // levels >= 1 + coarsest
+  }
+  if (root_mode) h->comm->broadcast(h->s, x1, (L > 1) ? h->lv[1].n : h->nL, 0);   // level-1 correction
   klaunch(h->s, h->pdl, prolong_kernel, nblk(L0.n, 256), 256, L0.n, (const int*)L0.agg, (const double*)x1, L0.x);
   ++h->nlaunch;
   exch_l0(h, L0.x, -1);
@@ -2185,7 +2192,8 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (cfg) c = *cfg;
   if (c.stages != 2 && c.stages != 3) return fail(nullptr, MSP_EINVAL, "msp_setup: stages must be 2 (P,R) or 3 (N,P,R)");
   if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1 ||
-      c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1 || c.orth < 0 || c.orth > 2)
+      c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1 || c.orth < 0 || c.orth > 2 || c.coarse_mode < 0 ||
+      c.coarse_mode > 1)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
   if (c.use_coop != 0) return fail(nullptr, MSP_EINVAL, "msp_setup: use_coop (cooperative V-cycle) was removed: measured slower than graph replay");
   std::unique_ptr<msp_handle> h(new msp_handle);
@@ -2721,9 +2729,9 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   msp_config_default(&c);
   if (cfg) c = *cfg;
   if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth == 1 ||
-      c.smoother != 0)
+      c.smoother != 0 || c.coarse_mode < 0 || c.coarse_mode > 1)
     return fail(nullptr, MSP_EINVAL,
-                "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC");
+                "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC, coarse_mode 0/1");
   // NCCL steps are replayed as CUDA graphs (halo send/recv groups and allreduces are
   // captured with the kernels); the loopback backend synchronises host threads: direct
   const char* ng = std::getenv("MSP_DIST_NOGRAPH");

@@ -76,3 +76,51 @@ def test_nccl_backend_single_rank_matches_single_gpu(nograph, monkeypatch):
     assert abs(rd["iters"] - r1["iters"]) <= 1
     x1 = r1["x"].cpu().numpy()
     assert np.linalg.norm(rd["x"].cpu().numpy() - x1) <= 1e-8 * np.linalg.norm(x1)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_coarse_root_bit_identical(nranks):
+    """coarse_mode=1 (ROOT, north_star's "coarse levels agglomerated onto one GPU"): rank 0
+    runs levels >= 1 and the coarsest and broadcasts the level-1 correction; the iterates
+    are bit-identical to the replicated mode (same arithmetic on the same data)."""
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C2", nx=24, ny=20, nz=9)
+    owner = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"], coarsest_max_dof=100).partition_owner(
+        p["nx"], p["ny"], p["nz"], nranks)
+    r0 = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner,
+                        coarsest_max_dof=100)
+    r1 = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner,
+                        coarsest_max_dof=100, coarse_mode=1)
+    assert r0["iters"] == r1["iters"]
+    assert np.array_equal(r0["x"], r1["x"])
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_loopback_full_size_c3_zslabs_vs_oracle_golden(nranks):
+    """C3 at full size partitioned into z-slabs (§8(e): 85 layers over 2 / 4 ranks), on one
+    GPU through the loopback harness, against the ORACLE's committed solve
+    (tests/golden/oracle_c3.json): iterations within 1 and the converged true residual."""
+    import json
+    import os
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C3")
+    owner = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"]).partition_owner(p["nx"], p["ny"], p["nz"], nranks)
+    rd = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner,
+                        coarse_mode=1 if nranks == 4 else 0)
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_c3.json")))
+    assert abs(rd["iters"] - ref["iters"]) <= 1, (rd["iters"], ref["iters"])
+    A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * p["b"],) * 2)
+    assert np.linalg.norm(p["rhs"] - A @ rd["x"]) / np.linalg.norm(p["rhs"]) <= 1e-6
+    info = rd["rank_info"]
+    assert info[:, 0].sum() == p["n"] and (info[:, 1] > 0).all()
+
+
+def test_nccl_single_rank_coarse_root():
+    from paper_2208_08594_b200 import DistSolver, MspSolver, nccl_unique_id
+    p = gen.make_config("C2", nx=20, ny=16, nz=6)
+    d = DistSolver(p["row_ptr"], p["col"], p["val"], p["nc"], 0, 1, nccl_unique_id(), coarsest_max_dof=80,
+                   coarse_mode=1)
+    rd = d.solve(torch.from_numpy(p["rhs"]).cuda())
+    s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], coarsest_max_dof=80)
+    r1 = s.solve(torch.from_numpy(p["rhs"]).cuda())
+    assert abs(rd["iters"] - r1["iters"]) <= 1
