@@ -1810,4 +1810,78 @@ __global__ void scalar_perm_kernel(int n, const int* __restrict__ idx, const dou
   else dst[i] = ldg(src + ldg(idx + i));
 }
 
+// ---------------------------------------------------------------------------
+// a10/a11 on the device (one restart cycle = one CUDA graph): the Givens update of the
+// Hessenberg column of step j and the convergence test of the host loop in gmres(),
+// run by one thread after the step's kernels; it sets the conditional handle of step
+// j+1 when the cycle goes on (no host round trip per Arnoldi step).  Same operation
+// order as the host loop (explicitly rounded; hypot for the rotation).
+// State g (ld kGv = 32): H[33*32] rotated, Hraw[33*32] (DCGS2 unrotated columns),
+// cs[32], sn[32], gam[33], h2p[32], hist[32], scal[8] = {||b||, tol, nu, rho, k, broke,
+// it0, maxit}.
+constexpr int kGv = 32;
+constexpr int kGvH = 0, kGvHraw = kGvH + (kGv + 1) * kGv, kGvCs = kGvHraw + (kGv + 1) * kGv, kGvSn = kGvCs + kGv,
+              kGvGam = kGvSn + kGv, kGvH2 = kGvGam + kGv + 1, kGvHist = kGvH2 + kGv, kGvScal = kGvHist + kGv,
+              kGvSize = kGvScal + 8;
+
+__global__ void givens_init_kernel(double* g, const double* beta, double bnorm, double tol, double it0, double maxit) {
+  for (int i = threadIdx.x; i < kGvSize; i += blockDim.x) g[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g[kGvGam] = beta[0];
+    double* sc = g + kGvScal;
+    sc[0] = bnorm; sc[1] = tol; sc[2] = 1.0; sc[3] = 1.0; sc[4] = 0.0; sc[5] = 0.0; sc[6] = it0; sc[7] = maxit;
+  }
+}
+
+template <bool DCGS>
+__global__ void givens_kernel(int j, int m, const double* __restrict__ rec, double* g,
+                              cudaGraphConditionalHandle next, int has_next) {
+  if (threadIdx.x != 0) return;
+  pdl_wait();
+  double* H = g + kGvH;
+  double* Hraw = g + kGvHraw;
+  double* cs = g + kGvCs;
+  double* sn = g + kGvSn;
+  double* gam = g + kGvGam;
+  double* h2p = g + kGvH2;
+  double* sc = g + kGvScal;
+  auto Hc = [&](int i) -> double& { return H[i * kGv + j]; };
+  if (DCGS) {
+    const double nup = sc[2], rhop = sc[3];
+    for (int i = 0; i <= j + 1; ++i) {
+      double v = __dmul_rn(nup, (i <= j) ? rec[i] : rec[j + 1]);
+      for (int l = 0; l < j; ++l) v = __dsub_rn(v, __dmul_rn(h2p[l], Hraw[i * kGv + l]));
+      Hraw[i * kGv + j] = __ddiv_rn(v, rhop);
+      Hc(i) = Hraw[i * kGv + j];
+    }
+    for (int l = 0; l <= j; ++l) h2p[l] = rec[j + 3 + l];
+    sc[2] = rec[j + 2];
+    sc[3] = rec[j + 1];
+  } else {
+    for (int i = 0; i <= j + 1; ++i) Hc(i) = rec[i];
+  }
+  const double hn = Hc(j + 1);
+  for (int i = 0; i < j; ++i) {
+    const double a = Hc(i), c = Hc(i + 1);
+    Hc(i) = __dadd_rn(__dmul_rn(cs[i], a), __dmul_rn(sn[i], c));
+    Hc(i + 1) = __dadd_rn(__dmul_rn(-sn[i], a), __dmul_rn(cs[i], c));
+  }
+  const double rho = hypot(Hc(j), Hc(j + 1));
+  cs[j] = __ddiv_rn(Hc(j), rho);
+  sn[j] = __ddiv_rn(Hc(j + 1), rho);
+  Hc(j) = rho;
+  Hc(j + 1) = 0.0;
+  gam[j + 1] = __dmul_rn(-sn[j], gam[j]);
+  gam[j] = __dmul_rn(cs[j], gam[j]);
+  const double bnorm = sc[0];
+  const double est = __ddiv_rn(fabs(gam[j + 1]), bnorm);
+  g[kGvHist + j] = est;
+  sc[4] = (double)(j + 1);
+  const bool broke = hn < __dmul_rn(1e-14, bnorm);
+  sc[5] = broke ? 1.0 : 0.0;
+  const bool stop = est <= sc[1] || broke || sc[6] + (double)(j + 1) >= sc[7];
+  if (!stop && has_next && j + 1 < m) cudaGraphSetConditional(next, 1);
+}
+
 }  // namespace mspk

@@ -134,6 +134,11 @@ struct msp_handle {
   double *V = nullptr;
   int V_m = -1;
   double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
+  double *gv = nullptr, *hgv = nullptr;        // device Givens state / its pinned host copy
+  cudaGraphExec_t cycle_exec = nullptr;        // one restart cycle as ONE graph (conditional steps)
+  int cycle_m = -1;
+  std::vector<int64_t> cycle_kernels;          // kernels of step j inside the cycle graph
+  bool cycle_graphs = false;                   // MSP_CYCLE_GRAPH=1: one graph per restart cycle (measured: no gain)
   double *dst = nullptr, *dsum = nullptr;     // DCGS2 state (2 parities x (kMaxV+2)) and sums
   unsigned* ticket = nullptr;
   double* io = nullptr;              // staging for host<->device and natural-order vectors
@@ -208,6 +213,10 @@ struct msp_handle {
     cell_halo = msp::HaloPlan();
     l0_halo = msp::HaloPlan();
     if (hpin) { cudaFreeHost(hpin); hpin = nullptr; }
+    if (hgv) { cudaFreeHost(hgv); hgv = nullptr; }
+    if (cycle_exec) { cudaGraphExecDestroy(cycle_exec); cycle_exec = nullptr; }
+    cycle_m = -1;
+    gv = nullptr;
   }
 };
 
@@ -988,6 +997,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->ticket = h->dalloc<unsigned>(4);
   CK(cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned), h->s));
   CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 4));
+  CK(cudaMallocHost(&h->hgv, sizeof(double) * kGvSize));
+  h->gv = h->dalloc<double>(kGvSize);
   CK(cudaStreamSynchronize(h->s));
   auto t1 = std::chrono::steady_clock::now();
   const double secs = std::chrono::duration<double>(t1 - t0).count();
@@ -1916,7 +1927,7 @@ void dcgs2(msp_handle* h, int k) {
 
 // One Arnoldi step j: z = B v_j; w = A z (into V[j+1]); orthogonalise (CGS2 or MGS);
 // hcol[0..j+1] = H(:, j); V[j+1] normalised; hcol copied to pinned host memory.
-void arnoldi_step(msp_handle* h, int j) {
+void arnoldi_step(msp_handle* h, int j, bool record_to_host = true) {
   const size_t N = h->N;
   double* vj = h->V + (size_t)j * N;
   double* w = h->V + (size_t)(j + 1) * N;
@@ -1930,7 +1941,7 @@ void arnoldi_step(msp_handle* h, int j) {
   const int nv = j + 1;
   if (h->prm.orth == 2) {
     dcgs2(h, j);
-    CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (2 * j + 4), cudaMemcpyDeviceToHost, h->s));
+    if (record_to_host) CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (2 * j + 4), cudaMemcpyDeviceToHost, h->s));
     return;
   }
   if (h->prm.orth == 0) {
@@ -1944,7 +1955,50 @@ void arnoldi_step(msp_handle* h, int j) {
     klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
     klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, w, h->hcol + nv, w); ++h->nlaunch;
   }
-  CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
+  if (record_to_host) CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
+}
+
+// One restart cycle of GMRES(m) as ONE executable graph: a chain of m conditional (IF)
+// nodes; body j = the kernels of Arnoldi step j (captured into the body) followed by
+// givens_kernel, which performs the Givens update and convergence test on the device and
+// enables body j+1 (its handle is reset to 0 at every launch).  The host synchronises once
+// per cycle instead of once per step.  Single-GPU, CGS2 / DCGS2.
+void build_cycle_graph(msp_handle* h, int m) {
+  if (h->cycle_exec) { cudaGraphExecDestroy(h->cycle_exec); h->cycle_exec = nullptr; }
+  cudaGraph_t root;
+  CK(cudaGraphCreate(&root, 0));
+  std::vector<cudaGraphConditionalHandle> hd(m);
+  for (int j = 0; j < m; ++j)
+    CK(cudaGraphConditionalHandleCreate(&hd[j], root, j == 0 ? 1u : 0u, cudaGraphCondAssignDefault));
+  h->cycle_kernels.assign(m, 0);
+  cudaGraphNode_t prev = nullptr;
+  for (int j = 0; j < m; ++j) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hd[j];
+    np.conditional.type = cudaGraphCondTypeIf;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, root, prev ? &prev : nullptr, prev ? 1 : 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int64_t before = h->nlaunch;
+    CK(cudaStreamBeginCaptureToGraph(h->s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    arnoldi_step(h, j, false);
+    const cudaGraphConditionalHandle nx = (j + 1 < m) ? hd[j + 1] : hd[j];
+    if (h->prm.orth == 2)
+      klaunch(h->s, h->pdl, givens_kernel<true>, 1, 32, j, m, (const double*)h->hcol, h->gv, nx, (j + 1 < m) ? 1 : 0);
+    else
+      klaunch(h->s, h->pdl, givens_kernel<false>, 1, 32, j, m, (const double*)h->hcol, h->gv, nx, (j + 1 < m) ? 1 : 0);
+    cudaGraph_t out;
+    CK(cudaStreamEndCapture(h->s, &out));
+    h->cycle_kernels[j] = h->nlaunch - before;
+    h->nlaunch = before;
+    prev = node;
+  }
+  CK(cudaGraphInstantiate(&h->cycle_exec, root, 0));
+  cudaGraphDestroy(root);
+  h->cycle_m = m;
+  h->kernels_per_step = (int)(h->cycle_kernels.empty() ? 0 : h->cycle_kernels[0]);
 }
 
 void ensure_basis(msp_handle* h, int m) {
@@ -1954,6 +2008,8 @@ void ensure_basis(msp_handle* h, int m) {
   for (auto g : h->graphs) if (g) cudaGraphExecDestroy(g);
   h->graphs.clear();
   h->graphs_m = -1;
+  if (h->cycle_exec) { cudaGraphExecDestroy(h->cycle_exec); h->cycle_exec = nullptr; }
+  h->cycle_m = -1;
 }
 
 void run_step(msp_handle* h, int j, int m) {
@@ -2027,7 +2083,28 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       rhop = 1.0;
       int k = 0;
       bool broke = false;                    // happy breakdown: h_{j+1,j} < 1e-14 ||b||
-      for (int j = 0; j < m; ++j) {
+      const bool cyc = h->prm.use_graphs && h->cycle_graphs && !h->comm && h->prm.orth != 1;
+      if (cyc) {
+        // the whole cycle on the device: givens_kernel replaces the host loop below
+        if (h->cycle_m != m) build_cycle_graph(h, m);
+        klaunch(h->s, false, givens_init_kernel, 1, 256, h->gv, (const double*)h->hcol, bnorm, tol, (double)it,
+                (double)maxit);
+        ++h->nlaunch;
+        CK(cudaGraphLaunch(h->cycle_exec, h->s));
+        CK(cudaMemcpyAsync(h->hgv, h->gv, sizeof(double) * kGvSize, cudaMemcpyDeviceToHost, h->s));
+        CK(cudaStreamSynchronize(h->s));
+        const double* g = h->hgv;
+        k = (int)g[kGvScal + 4];
+        broke = g[kGvScal + 5] != 0.0;
+        for (int j = 0; j < k; ++j) {
+          push(g[kGvHist + j]);
+          h->nlaunch += h->cycle_kernels[j];
+          for (int i = 0; i <= j + 1; ++i) H[(size_t)i * m + j] = g[kGvH + i * kGv + j];
+        }
+        for (int i = 0; i <= k; ++i) gam[i] = g[kGvGam + i];
+        it += k;
+      }
+      for (int j = 0; j < m && !cyc; ++j) {
         run_step(h, j, m);
         CK(cudaStreamSynchronize(h->s));
         auto Hc = [&](int i) -> double& { return H[(size_t)i * m + j]; };
@@ -2200,6 +2277,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   h->cfg = c;
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_HOST_SETUP")) h->setup_on_gpu = std::atoi(e) == 0;
+  if (const char* e = std::getenv("MSP_CYCLE_GRAPH")) h->cycle_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;

@@ -430,3 +430,21 @@ def test_full_size_c5_solve_vs_oracle_golden():
     xs = r["x"].cpu().numpy()
     assert np.linalg.norm(p["rhs"] - A @ xs) / np.linalg.norm(p["rhs"]) <= 1e-6
     _check_hist(r["hist"], ref["hist"], iters=r["iters"], ref_iters=ref["iters"])
+
+
+@pytest.mark.parametrize("orth", [0, 2])
+def test_cycle_graph_matches_per_step_graphs(orth, monkeypatch):
+    """MSP_CYCLE_GRAPH=1: each restart cycle runs as ONE graph of conditional Arnoldi steps
+    with the Givens update / convergence test on the device (givens_kernel); same
+    iterations, history and solution as the per-step graphs with the host loop."""
+    p = gen.make_config("C2", nx=30, ny=30, nz=6)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("MSP_CYCLE_GRAPH", v)
+        s = solver(p, coarsest_max_dof=100, orth=orth)
+        r = s.solve(torch.from_numpy(p["rhs"]).cuda(), restart=7, tol=1e-9)
+        out.append(r)
+    assert out[0]["iters"] == out[1]["iters"] and out[0]["iters"] > 7
+    assert np.allclose(out[0]["hist"], out[1]["hist"], rtol=1e-9, atol=0)
+    x0, x1 = out[0]["x"].cpu().numpy(), out[1]["x"].cpu().numpy()
+    assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x0)
