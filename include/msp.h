@@ -99,6 +99,12 @@ typedef struct {
                                 right-hand side); 1 ROOT: agglomerated onto rank 0, which runs them
                                 and broadcasts the level-1 correction (north_star's "coarse levels
                                 are agglomerated onto one GPU"; bit-identical iterates) */
+  int32_t bilu_local;        /* distributed handles: 0 (default) BILU(0) of the whole matrix (the
+                                single-GPU preconditioner; halo exchanges after every color
+                                phase); 1 rank-local BILU: couplings between cells of different
+                                ranks removed before the factorization (block Jacobi across the
+                                slabs; no exchange in the substitutions; the preconditioner then
+                                depends on the partition).  Single-GPU handles: must be 0. */
 } msp_config;
 
 typedef struct msp_handle msp_handle;

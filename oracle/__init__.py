@@ -42,7 +42,7 @@ def lib():
                      "orc_msp_bilu_apply", "orc_msp_apply", "orc_msp_solve", "orc_msp_bgs_apply",
                      "orc_msp_restrict_pressure", "orc_msp_level_resid_restrict",
                      "orc_msp_level_prolong", "orc_msp_bilu_forward", "orc_msp_bilu_backward",
-                     "orc_msp_bilu_apply_by_color", "orc_msp_bilu_blocks", "orc_msp_bilu_set_factors"):
+                     "orc_msp_bilu_apply_by_color", "orc_msp_bilu_blocks", "orc_msp_bilu_set_factors", "orc_msp_bilu_refactor"):
             getattr(_lib, name).argtypes = None
     return _lib
 
@@ -341,6 +341,11 @@ class Msp:
     def set_bilu_factors(self, F, Dinv):
         """Test hook: replace the BILU factors (natural storage, row-major) and D~^-1."""
         lib().orc_msp_bilu_set_factors(self.h, _p(_c(F, F64)), _p(_c(Dinv, F64)))
+
+    def bilu_refactor(self, val):
+        """Test hook: refactorize BILU(0) in the same order from other values (natural BSR)."""
+        if lib().orc_msp_bilu_refactor(self.h, _p(_c(val, F64))):
+            raise OracleError(last_error())
 
     def bilu_apply_by_color(self, r):
         x = np.zeros(self.n * self.b)

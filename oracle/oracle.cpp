@@ -1586,6 +1586,19 @@ int orc_msp_bilu_set_factors(void* h, const double* F, const double* Dinv) {
   std::copy(Dinv, Dinv + M->R.Dinv.size(), M->R.Dinv.begin());
   return 0;
 }
+// test hook: refactorize the BILU(0) in the SAME elimination order from the given values
+// (e.g. A with the couplings between ranks removed: the rank-local BILU of the distributed
+// product); the hierarchy and W stay those of the setup matrix
+int orc_msp_bilu_refactor(void* h, const double* vals) {
+  Msp* M = (Msp*)h;
+  Bsr B = M->A;
+  std::copy(vals, vals + B.val.size(), B.val.begin());
+  std::vector<int> color = M->R.color, blk = M->R.blk, order = M->R.order;
+  if (!bilu_factor(B, order, M->R)) return 2;
+  M->R.color = color;
+  M->R.blk = blk;
+  return 0;
+}
 // block color and ABMC block id of every cell (natural numbering); returns #colors
 int orc_msp_bilu_blocks(void* h, int* color, int* blk) {
   Msp* M = (Msp*)h;

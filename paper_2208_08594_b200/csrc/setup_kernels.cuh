@@ -206,6 +206,15 @@ __global__ void rap_fill_kernel(int nc, const int* __restrict__ mp, const int* _
   }
 }
 
+// Rank-local BILU (NEXT-3 option): zero the blocks of the couplings between cells of
+// different owners before the factorization (list of entries, bb doubles each).
+__global__ void zero_blocks_kernel(int64_t count, int bb, const int* __restrict__ idx, double* __restrict__ F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * bb) return;
+  const int64_t q = t / bb;
+  F[(size_t)idx[q] * bb + (t - q * bb)] = 0.0;
+}
+
 // Coarsest level (a6 setup): dense row-major A_L from its CSR and the identity right-hand
 // side (leading dimension ld) for the inverse; both outputs zeroed by the caller.
 __global__ void dense_identity_kernel(int m, int ld, const int* __restrict__ rp, const int* __restrict__ ci,

@@ -239,6 +239,7 @@ msp::Params params_of(const msp_config* c) {
   p.smoother = c->smoother;
   p.gs_chunk = c->gs_chunk;
   p.coarse_mode = c->coarse_mode;
+  p.bilu_local = c->bilu_local;
   return p;
 }
 
@@ -481,7 +482,8 @@ std::vector<int32_t> block_counts(const msp::HostSetup& S, const std::vector<int
 
 void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
-                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms);
+                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms,
+                   const double* dF = nullptr, const double* dAnat = nullptr);
 
 
 // BILU block kernels: per cell i of aggregate block [c0, c1) (<= 4 cells), the entry index
@@ -687,6 +689,54 @@ int gpu_rap(RapChain& ch, const msp::SpMat& A, const std::vector<int32_t>& agg, 
   return 0;
 }
 
+// Global BILU(0) factorization on the GPU (distributed handles): every rank factorizes the
+// whole matrix per block color exactly as the single-GPU setup does (bit-identical
+// factors), then dist_localize keeps its rows.  Returns the factors, row-major blocks in
+// the global permuted entry order.
+std::unique_ptr<DBuf> gpu_bilu_global(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S,
+                                      const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
+                                      const std::vector<int32_t>& dg, const std::vector<int32_t>& src, const DBuf& dAnat,
+                                      const std::vector<int32_t>& masked) {
+  Nvtx nv("S4 BILU(0) factorization (GPU, global)");
+  cudaStream_t s = h->s;
+  const int b = A.b, bb = b * b;
+  const size_t ne = ci.size();
+  std::unique_ptr<DBuf> F(new DBuf(ne * bb * sizeof(double), s));
+  DBuf drp(rp.size() * 4, s), dci(ne * 4, s), ddg(dg.size() * 4, s), dsrc(ne * 4, s), dbp(S.blk_ptr.size() * 4, s),
+      dbad(4, s);
+  h2d(s, drp.as<int32_t>(), rp);
+  h2d(s, dci.as<int32_t>(), ci);
+  h2d(s, ddg.as<int32_t>(), dg);
+  h2d(s, dsrc.as<int32_t>(), src);
+  h2d(s, dbp.as<int32_t>(), S.blk_ptr);
+  CK(cudaMemsetAsync(dbad.p, 0xff, 4, s));
+  std::unique_ptr<DBuf> dmask;                        // rank-local BILU: couplings across owners
+  if (!masked.empty()) {
+    dmask.reset(new DBuf(masked.size() * 4, s));
+    h2d(s, dmask->as<int32_t>(), masked);
+  }
+  switch (b) {
+#define CASE(BV) case BV: \
+    klaunch(s, false, gather_blocks_kernel<BV>, nblk(ne * bb, 256), 256, (int64_t)ne, (const int*)dsrc.p, \
+            (const double*)dAnat.p, F->as<double>()); \
+    if (dmask) klaunch(s, false, zero_blocks_kernel, nblk(masked.size() * bb, 256), 256, (int64_t)masked.size(), bb, \
+                       (const int*)dmask->p, F->as<double>()); \
+    for (int col = 0; col + 1 < (int)S.color_blk_ptr.size(); ++col) { \
+      const int k0 = S.color_blk_ptr[col], k1 = S.color_blk_ptr[col + 1]; \
+      if (k1 > k0) klaunch(s, false, bilu_factor_kernel<BV>, nblk(k1 - k0, 64), 64, k0, k1, (const int*)dbp.p, \
+                           (const int*)drp.p, (const int*)dci.p, (const int*)ddg.p, F->as<double>(), dbad.as<int>()); \
+    } \
+    break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+  }
+  int bad = -1;
+  CK(cudaMemcpyAsync(&bad, dbad.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad >= 0) throw std::pair<int, std::string>(MSP_ESINGULAR, "BILU: singular pivot block at cell " + std::to_string(S.order[bad]));
+  return F;
+}
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
   SetupTimer T;
@@ -733,7 +783,11 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->App_nat = S.App.v;
   // BILU(0): on the GPU after the upload (single GPU), on the host for the distributed
   // setup (every rank factorizes the global matrix) or when MSP_HOST_BILU=1
-  const bool gpu_bilu = !h->comm && !(std::getenv("MSP_HOST_BILU") && std::atoi(std::getenv("MSP_HOST_BILU")));
+  const bool host_bilu_env = std::getenv("MSP_HOST_BILU") && std::atoi(std::getenv("MSP_HOST_BILU"));
+  // distributed handles factorize the GLOBAL matrix on the GPU too (every rank holds A's
+  // values on its device after S1) and keep their rows; host factorization only without
+  // the GPU setup steps
+  const bool gpu_bilu = !host_bilu_env && (!h->comm || dAvals);
   rc = gpu_bilu ? msp::permuted_pattern(S, A, rp, ci, dg, src, err)
                 : msp::bilu_factor_permuted(S, A, rp, ci, dg, src, F, err);
   if (rc) throw std::pair<int, std::string>(rc == 1 ? MSP_EINVAL : MSP_ESINGULAR, err);
@@ -810,7 +864,27 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     D.pt_idx = h->upload(pi);
   }
   if (h->comm) {
-    dist_localize(h, A, S, rp, ci, dg, src, F, perms);
+    std::unique_ptr<DBuf> Fglob;
+    std::vector<int32_t> masked;
+    if (h->prm.bilu_local) {
+      // rank-local BILU (NEXT-3 option): ILU(0) of the matrix with every coupling between
+      // cells of different owners removed (block Jacobi across slabs) -- no halo exchange
+      // in the substitutions, a preconditioner that depends on the partition
+      const int nb = (int)S.blk_ptr.size() - 1;
+      std::vector<int32_t> opos(A.n);
+      for (int k = 0; k < nb; ++k) {
+        int32_t lowest = INT32_MAX;
+        for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) lowest = std::min(lowest, S.order[p]);
+        for (int32_t p = S.blk_ptr[k]; p < S.blk_ptr[k + 1]; ++p) opos[p] = h->owner_in[lowest];
+      }
+      for (int32_t p = 0; p < A.n; ++p)
+        for (int32_t e = rp[p]; e < rp[p + 1]; ++e)
+          if (opos[p] != opos[ci[e]]) masked.push_back(e);
+    }
+    if (gpu_bilu) Fglob = gpu_bilu_global(h, A, S, rp, ci, dg, src, *dAvals, masked);
+    else if (!masked.empty()) throw std::pair<int, std::string>(MSP_EINVAL, "bilu_local needs the GPU setup path");
+    dist_localize(h, A, S, rp, ci, dg, src, F, perms, Fglob ? Fglob->as<double>() : nullptr,
+                  dAvals ? dAvals->as<double>() : nullptr);
   } else {
   // BSR pattern + values (column-major blocks)
   check_ptr(rp, n, (int64_t)ci.size(), "BSR row pointers");
@@ -982,6 +1056,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   const size_t Ng = (size_t)(h->n + h->n_ghost) * h->b;
   h->z = h->dalloc<double>(Ng);
   h->r = h->dalloc<double>(Ng);
+  CK(cudaMemsetAsync(h->r, 0, sizeof(double) * Ng, h->s));   // ghost slots finite (rank-local BILU reads 0 x them)
   h->u = h->dalloc<double>(h->N);
   h->xin = h->dalloc<double>(Ng);
   h->bin = h->dalloc<double>(h->N);
@@ -1124,7 +1199,8 @@ CellPlan compute_cell_plan(const msp::HostSetup& S, const std::vector<int32_t>& 
 
 void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
-                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms) {
+                   const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms,
+                   const double* dF, const double* dAnat) {
   const int32_t n = A.n;
   const int b = A.b, bb = b * b;
   const int P = h->nranks, me = h->rank;
@@ -1157,10 +1233,17 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
     std::memcpy(&lW[(size_t)l * b], &S.W[(size_t)S.order[p] * b], sizeof(double) * b);
   }
   const size_t ne = lci.size();
+  std::vector<int32_t> lent;                      // global (permuted) entry of every local entry
+  if (dF) {
+    lent.reserve(ne);
+    for (int32_t l = 0; l < no; ++l)
+      for (int32_t e = rp[posown[l]]; e < rp[posown[l] + 1]; ++e) lent.push_back(e);
+  } else {
   lF.resize(ne * bb);
   lA.resize(ne * bb);
   lPc.resize(ne * b);
-  {
+  }
+  if (!dF) {
     size_t q = 0;
     for (int32_t l = 0; l < no; ++l) {
       const int32_t p = posown[l];
@@ -1201,9 +1284,30 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
   h->stage = nullptr;
   h->d_order = h->upload(lorder);
   h->order = lorder;
-  h->Fval = h->upload(lF);
-  h->Aval = h->upload(lA);
-  h->Pcol = h->upload(lPc);
+  if (dF) {
+    // factors and values laid out on the device from the global GPU factorization and A's
+    // natural values (no host copies of the local blocks)
+    h->Fval = h->dalloc<double>(ne * bb);
+    h->Aval = h->dalloc<double>(ne * bb);
+    h->Pcol = h->dalloc<double>(ne * b);
+    double* tmp = h->dalloc<double>(ne * bb);
+    const int32_t* d_lent = h->upload(lent);
+    switch (b) {
+#define CASE(BV) case BV: \
+      klaunch(h->s, false, gather_blocks_kernel<BV>, nblk(ne * bb, 256), 256, (int64_t)ne, d_lent, dF, tmp); \
+      klaunch(h->s, false, transpose_blocks_kernel<BV>, nblk(ne * bb, 256), 256, (int64_t)ne, (const double*)tmp, h->Fval); \
+      klaunch(h->s, false, refresh_values_kernel<BV>, nblk(ne * bb, 256), 256, (int64_t)ne, (const int*)h->d_src, dAnat, \
+              h->Aval, h->Pcol); \
+      break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    }
+    CK(cudaStreamSynchronize(h->s));
+  } else {
+    h->Fval = h->upload(lF);
+    h->Aval = h->upload(lA);
+    h->Pcol = h->upload(lPc);
+  }
   h->W = h->upload(lW);
   h->color_blk = lcolor_blk;
   h->blk_ptr = h->upload(lblk);
@@ -1391,10 +1495,13 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
   }
   // distributed: after each color phase, the ghost copies of that color's cells are
   // refreshed (y after the forward phase, x after the backward phase)
-  for (int c = 0; c < g - 1; ++c) { run(c, 0); exch_cell(h, v, B, c); }
+  // rank-local BILU: the factor blocks of couplings to other ranks are zero, ghost slots of v
+  // are never read with a nonzero factor -> no exchange
+  const bool ex = !h->prm.bilu_local;
+  for (int c = 0; c < g - 1; ++c) { run(c, 0); if (ex) exch_cell(h, v, B, c); }
   run(g - 1, 2);
-  if (g > 1) exch_cell(h, v, B, g - 1);
-  for (int c = g - 2; c >= 0; --c) { run(c, 1); if (c > 0) exch_cell(h, v, B, c); }
+  if (g > 1 && ex) exch_cell(h, v, B, g - 1);
+  for (int c = g - 2; c >= 0; --c) { run(c, 1); if (c > 0 && ex) exch_cell(h, v, B, c); }
 }
 
 template <int B>
@@ -2270,7 +2377,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (c.stages != 2 && c.stages != 3) return fail(nullptr, MSP_EINVAL, "msp_setup: stages must be 2 (P,R) or 3 (N,P,R)");
   if (c.pre_sweeps < 1 || c.post_sweeps < 0 || c.pair_passes < 1 || c.coarsest_max_dof < 1 ||
       c.smoother < 0 || c.smoother > 2 || c.gs_chunk < 1 || c.orth < 0 || c.orth > 2 || c.coarse_mode < 0 ||
-      c.coarse_mode > 1)
+      c.coarse_mode > 1 || c.bilu_local != 0)
     return fail(nullptr, MSP_EINVAL, "msp_setup: invalid config");
   if (c.use_coop != 0) return fail(nullptr, MSP_EINVAL, "msp_setup: use_coop (cooperative V-cycle) was removed: measured slower than graph replay");
   std::unique_ptr<msp_handle> h(new msp_handle);
@@ -2807,7 +2914,7 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   msp_config_default(&c);
   if (cfg) c = *cfg;
   if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth == 1 ||
-      c.smoother != 0 || c.coarse_mode < 0 || c.coarse_mode > 1)
+      c.smoother != 0 || c.coarse_mode < 0 || c.coarse_mode > 1 || c.bilu_local < 0 || c.bilu_local > 1)
     return fail(nullptr, MSP_EINVAL,
                 "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC, coarse_mode 0/1");
   // NCCL steps are replayed as CUDA graphs (halo send/recv groups and allreduces are

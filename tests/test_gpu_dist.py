@@ -124,3 +124,47 @@ def test_nccl_single_rank_coarse_root():
     s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], coarsest_max_dof=80)
     r1 = s.solve(torch.from_numpy(p["rhs"]).cuda())
     assert abs(rd["iters"] - r1["iters"]) <= 1
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_rank_local_bilu_vs_oracle(nranks):
+    """bilu_local=1 (NEXT-3): BILU(0) of A with the couplings between ranks removed (block
+    Jacobi across the z-slabs), no halo exchange in the substitutions.  Against the oracle's
+    MSP whose BILU is refactorized from the same masked values in the same order
+    (orc_msp_bilu_refactor): iterations within 1."""
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C2", nx=24, ny=20, nz=9)
+    H = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"], coarsest_max_dof=100)
+    owner_in = H.partition_owner(p["nx"], p["ny"], p["nz"], nranks)
+    owner = np.empty(p["n"], np.int32)
+    for r in range(nranks):
+        owner[H.dist_plan(r, nranks, owner_in)["owned"]] = r
+    val = p["val"].copy()
+    for c in range(p["n"]):
+        for e in range(p["row_ptr"][c], p["row_ptr"][c + 1]):
+            if owner[p["col"][e]] != owner[c]:
+                val[e] = 0.0
+    O = oracle.Msp(p["row_ptr"], p["col"], p["val"], coarsest_max_dof=100)
+    O.bilu_refactor(val)
+    o = O.solve(p["rhs"])
+    rd = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner_in,
+                        coarsest_max_dof=100, bilu_local=1)
+    assert abs(rd["iters"] - o["iters"]) <= 1, (rd["iters"], o["iters"])
+    A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * p["b"],) * 2)
+    assert np.linalg.norm(p["rhs"] - A @ rd["x"]) / np.linalg.norm(p["rhs"]) <= 1e-6
+    full = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner_in,
+                          coarsest_max_dof=100)
+    print("iterations: global BILU", full["iters"], "rank-local BILU", rd["iters"])
+
+
+def test_loopback_gpu_factorization_bit_identical_to_single_gpu():
+    """The distributed setup factorizes the GLOBAL matrix on the GPU (like msp_setup) and
+    keeps its rows: the loopback solve at 1 rank reproduces the single-GPU solve."""
+    from paper_2208_08594_b200 import loopback_solve, MspSolver
+    p = gen.make_config("C2", nx=20, ny=16, nz=6)
+    rd = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], 1, p["rhs"], coarsest_max_dof=80)
+    s = MspSolver(p["row_ptr"], p["col"], p["val"], nc=p["nc"], coarsest_max_dof=80)
+    r1 = s.solve(torch.from_numpy(p["rhs"]).cuda())
+    assert rd["iters"] == r1["iters"]
+    x1 = r1["x"].cpu().numpy()
+    assert np.linalg.norm(rd["x"] - x1) <= 1e-9 * np.linalg.norm(x1)
