@@ -188,16 +188,20 @@ __global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __res
 // column-major storage), multiplies by its own x_q (no broadcast), keeps 4 row partial
 // sums and reduce-scatters once per block row.  MODE 0: y = A x; MODE 1: y = g - A x.
 template <int MODE>
+// rows != null: process only the n rows listed (distributed mode: the slab-interior rows
+// while the z halo is in flight, then the boundary rows)
 __global__ void __launch_bounds__(256) bsr_spmv4c_kernel(int n, const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ g,
-                                                         double* __restrict__ y) {
+                                                         double* __restrict__ y,
+                                                         const int* __restrict__ rows = nullptr) {
   PDL_ENTRY();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = gtid >> 2, q = threadIdx.x & 3;
-  if (row >= n) return;                       // whole 4-lane groups exit together
+  const int slot = gtid >> 2, q = threadIdx.x & 3;
+  if (slot >= n) return;                      // whole 4-lane groups exit together
+  const int row = rows ? ldg(rows + slot) : slot;
   const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 2
@@ -225,11 +229,13 @@ __global__ void __launch_bounds__(256) pcol_resid4_kernel(int n, const int* __re
                                                           const double* __restrict__ pcol,
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ g,
-                                                          double* __restrict__ y) {
+                                                          double* __restrict__ y,
+                                                          const int* __restrict__ rows = nullptr) {
   PDL_ENTRY();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = gtid >> 2, q = threadIdx.x & 3;
-  if (row >= n) return;                       // whole 4-lane groups exit together
+  const int slot = gtid >> 2, q = threadIdx.x & 3;
+  if (slot >= n) return;                      // whole 4-lane groups exit together
+  const int row = rows ? ldg(rows + slot) : slot;
   const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 2

@@ -159,6 +159,11 @@ struct msp_handle {
   bool valid = false;                // false after a failed (re)SETUP: compute calls rejected
   // distributed (z-slab) mode: owned cells [0, n), ghost cells after them
   std::unique_ptr<msp::Comm> comm;   // null: single GPU
+  cudaStream_t s2 = nullptr;         // side stream of the overlapped halo (distributed)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int32_t *rows_in = nullptr, *rows_bd = nullptr;   // slab-interior / boundary rows (cell space)
+  int n_rows_in = 0, n_rows_bd = 0;
+  bool overlap_halo = true;          // MSP_DIST_OVERLAP=0: exchange, then the whole SpMV
   int rank = 0, nranks = 1;
   int n_ghost = 0, n0_ghost = 0;     // cell-space / level-0 ghosts
   msp::HaloPlan cell_halo;           // segments = BILU block colors
@@ -1314,6 +1319,18 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
   h->bcnt = h->upload(lcnt);
   h->islot = h->upload(make_islot(no, lrp, lci, ldg, lblk));
   h->nnzb = (int64_t)ne;
+  {
+    std::vector<int32_t> rin, rbd;                // rows without / with a ghost column
+    for (int32_t l = 0; l < no; ++l) {
+      bool gh = false;
+      for (int32_t e = lrp[l]; e < lrp[l + 1]; ++e) gh = gh || lci[e] >= no;
+      (gh ? rbd : rin).push_back(l);
+    }
+    h->n_rows_in = (int)rin.size();
+    h->n_rows_bd = (int)rbd.size();
+    h->rows_in = h->upload(rin);
+    h->rows_bd = h->upload(rbd);
+  }
   // ---------------- level 0
   const msp::SpMat& A0 = S.lv[0].A;               // natural level-0 numbering = cells
   const auto& col0 = S.lv[0].color;
@@ -1429,8 +1446,9 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
   constexpr int TS = (B <= 4) ? 4 : 8;
   const unsigned grid = nblk((size_t)n * TS, 256);
   if (B == 4 && mode != 2) {
-    if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, grid, 256, n, rp, ci, val, x, g, y);
-    else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y);
+    const int* none = nullptr;
+    if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, grid, 256, n, rp, ci, val, x, g, y, none);
+    else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y, none);
     return;
   }
   if constexpr (B >= 5) {
@@ -1449,7 +1467,8 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
   if (mode == 2 && h->b == 4) {
-    klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)h->n * 4, 256), 256, h->n, h->rp, h->ci, val, x, g, y);
+    klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)h->n * 4, 256), 256, h->n, h->rp, h->ci, val, x, g, y,
+            (const int*)nullptr);
     return;
   }
   switch (h->b) {
@@ -1458,6 +1477,31 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
 #undef CASE
   }
 }
+
+// Distributed mode, 4x4 blocks: y = A x (mode 0) or r = g - A[:,P] x_p (mode 2) with the z
+// halo of x overlapped: the exchange runs on a side stream (fork/join by events; NCCL calls
+// are captured into the step graph like the kernels) while the slab-interior rows (no
+// ghost column) are computed, then the boundary rows.
+void spmv_overlapped(msp_handle* h, int mode, double* x, int width, const double* g, double* y) {
+  CK(cudaEventRecord(h->ev_fork, h->s));
+  CK(cudaStreamWaitEvent(h->s2, h->ev_fork, 0));
+  h->comm->halo(h->s2, h->cell_halo, x, h->n, width, -1);
+  CK(cudaEventRecord(h->ev_join, h->s2));
+  auto part = [&](const int32_t* rows, int nr) {
+    if (nr <= 0) return;
+    ++h->nlaunch;
+    if (mode == 2)
+      klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)nr * 4, 256), 256, nr, (const int*)h->rp,
+              (const int*)h->ci, (const double*)h->Pcol, (const double*)x, g, y, (const int*)rows);
+    else
+      klaunch(h->s, h->pdl, bsr_spmv4c_kernel<0>, nblk((size_t)nr * 4, 256), 256, nr, (const int*)h->rp,
+              (const int*)h->ci, (const double*)h->Aval, (const double*)x, g, y, (const int*)rows);
+  };
+  part(h->rows_in, h->n_rows_in);
+  CK(cudaStreamWaitEvent(h->s, h->ev_join, 0));
+  part(h->rows_bd, h->n_rows_bd);
+}
+bool overlap_ok(const msp_handle* h) { return h->comm && h->b == 4 && h->s2 && h->overlap_halo; }
 
 // halo exchanges of the distributed mode (no-ops on a single GPU)
 void exch_cell(msp_handle* h, double* v, int width, int seg) {
@@ -1775,8 +1819,12 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
   }
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, (const int*)h->l0_of_cell, (const double*)L0.x, h->wp);
   ++h->nlaunch;
-  exch_cell(h, h->wp, 1, -1);
-  launch_spmv(h, 2, h->wp, g, h->r);                                         // a8 (owned rows)
+  if (overlap_ok(h)) {
+    spmv_overlapped(h, 2, h->wp, 1, g, h->r);                                // a8, halo overlapped
+  } else {
+    exch_cell(h, h->wp, 1, -1);
+    launch_spmv(h, 2, h->wp, g, h->r);                                       // a8 (owned rows)
+  }
   launch_bilu(h, h->r, h->wp, z);                                            // a9 with per-color halos
 }
 
@@ -2039,10 +2087,14 @@ void arnoldi_step(msp_handle* h, int j, bool record_to_host = true) {
   double* vj = h->V + (size_t)j * N;
   double* w = h->V + (size_t)(j + 1) * N;
   msp_apply_dev(h, vj, h->z);
-  exch_cell(h, h->z, h->b, -1);
   {
     Nvtx nvt("a2 BSR SpMV");
-    launch_spmv(h, 0, h->z, nullptr, w);
+    if (overlap_ok(h)) {
+      spmv_overlapped(h, 0, h->z, h->b, nullptr, w);
+    } else {
+      exch_cell(h, h->z, h->b, -1);
+      launch_spmv(h, 0, h->z, nullptr, w);
+    }
   }
   Nvtx nvt("a10 orthogonalisation");
   const int nv = j + 1;
@@ -2768,6 +2820,9 @@ void msp_destroy(msp_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->s2) cudaStreamDestroy(h->s2);
   if (h->cs) cusolverDnDestroy(h->cs);
   if (h->s) cudaStreamDestroy(h->s);
   delete h;
@@ -2941,6 +2996,10 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   st = guarded(h.get(), [&]() -> msp_status {
     CK(cudaGetDevice(&h->device));
     CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    if (const char* e = std::getenv("MSP_DIST_OVERLAP")) h->overlap_halo = std::atoi(e) != 0;
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     h->caller = (cudaStream_t)cuda_stream;
