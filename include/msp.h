@@ -218,7 +218,8 @@ msp_status msp_get_s1(const msp_handle* h, double* W, double* App, int32_t* on_g
 msp_status msp_set_stream(msp_handle* h, void* cuda_stream);
 
 /* Times `reps` launches of one hot-path piece on the handle's stream with CUDA events,
- * flushing L2 (a 256 MB device write) before each launch.  Returns the mean device
+ * flushing L2 before each launch by READING a 256 MB buffer (clean lines: no write-back of
+ * unrelated dirty data inside the timed launch).  Returns the mean device
  * milliseconds per launch and the ALGORITHMIC bytes per launch (compulsory
  * traffic, each vector counted once).  kind: 0 a2 BSR SpMV; 1 a4 level-0 PGS-MC sweep
  * (all colors, descending = full work per color); 2 a8 pressure-column residual;

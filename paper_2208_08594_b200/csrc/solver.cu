@@ -164,6 +164,7 @@ struct msp_handle {
   int32_t *rows_in = nullptr, *rows_bd = nullptr;   // slab-interior / boundary rows (cell space)
   int n_rows_in = 0, n_rows_bd = 0;
   bool overlap_halo = true;          // MSP_DIST_OVERLAP=0: exchange, then the whole SpMV
+  bool setup_rank0 = true;           // MSP_DIST_SETUP_ALL=1: every rank runs the host setup
   int rank = 0, nranks = 1;
   int n_ghost = 0, n0_ghost = 0;     // cell-space / level-0 ghosts
   msp::HaloPlan cell_halo;           // segments = BILU block colors
@@ -694,6 +695,76 @@ int gpu_rap(RapChain& ch, const msp::SpMat& A, const std::vector<int32_t>& agg, 
   return 0;
 }
 
+// ---- rank-0 SETUP of the distributed path: the result of S1-S4 (weights, A_PP, levels,
+// colorings, aggregates, ABMC order) serialised on rank 0 and broadcast to the other ranks
+// through the handle's Comm (NCCL broadcast / loopback copy), instead of every rank
+// running the same host setup on the whole matrix.
+struct SetupBlob {
+  std::vector<char> b;
+  size_t rd = 0;
+  void put(const void* p, size_t n) { const char* c = (const char*)p; b.insert(b.end(), c, c + n); }
+  void get(void* p, size_t n) {
+    if (rd + n > b.size()) throw std::pair<int, std::string>(MSP_ECUDA, "setup broadcast: truncated");
+    std::memcpy(p, b.data() + rd, n);
+    rd += n;
+  }
+  template <class T> void vec(const std::vector<T>& v) { const uint64_t n = v.size(); put(&n, 8); put(v.data(), n * sizeof(T)); }
+  template <class T> void vec(std::vector<T>& v, bool) { uint64_t n = 0; get(&n, 8); v.resize(n); get(v.data(), n * sizeof(T)); }
+  template <class T> void val(const T& x) { put(&x, sizeof(T)); }
+  template <class T> void val(T& x, bool) { get(&x, sizeof(T)); }
+  void mat(const msp::SpMat& m) { val(m.n); vec(m.rp); vec(m.ci); vec(m.v); }
+  void mat(msp::SpMat& m, bool) { val(m.n, true); vec(m.rp, true); vec(m.ci, true); vec(m.v, true); }
+};
+
+void pack_setup(const msp::HostSetup& S, SetupBlob& o) {
+  o.val(S.n); o.vec(S.W); o.mat(S.App);
+  const int32_t L = (int32_t)S.lv.size();
+  o.val(L);
+  for (const auto& l : S.lv) { o.mat(l.A); o.val(l.ncolor); o.vec(l.color); o.vec(l.agg); o.val(l.n_next); }
+  o.mat(S.Ac); o.val(S.coarse_diag); o.vec(S.order); o.vec(S.pos); o.val(S.bilu_ncolor);
+  o.vec(S.blk_ptr); o.vec(S.color_blk_ptr); o.vec(S.level1_agg);
+}
+
+void unpack_setup(SetupBlob& o, msp::HostSetup& S) {
+  o.val(S.n, true); o.vec(S.W, true); o.mat(S.App, true);
+  int32_t L = 0;
+  o.val(L, true);
+  S.lv.resize(L);
+  for (auto& l : S.lv) { o.mat(l.A, true); o.val(l.ncolor, true); o.vec(l.color, true); o.vec(l.agg, true); o.val(l.n_next, true); }
+  o.mat(S.Ac, true); o.val(S.coarse_diag, true); o.vec(S.order, true); o.vec(S.pos, true); o.val(S.bilu_ncolor, true);
+  o.vec(S.blk_ptr, true); o.vec(S.color_blk_ptr, true); o.vec(S.level1_agg, true);
+}
+
+// Collective: rank 0 broadcasts {status, bytes} and then the blob (as doubles).
+void bcast_setup(msp_handle* h, int& status, std::string& err, SetupBlob& blob) {
+  cudaStream_t s = h->s;
+  DBuf hdr(16, s);
+  double hv[2] = {(double)status, (double)blob.b.size()};
+  if (h->rank == 0) CK(cudaMemcpyAsync(hdr.p, hv, 16, cudaMemcpyHostToDevice, s));
+  h->comm->broadcast(s, hdr.as<double>(), 2, 0);
+  CK(cudaMemcpyAsync(hv, hdr.p, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  status = (int)hv[0];
+  if (status) {
+    if (h->rank != 0) err = "setup failed on rank 0 (status " + std::to_string(status) + ")";
+    return;
+  }
+  const size_t bytes = (size_t)hv[1], nd = (bytes + 7) / 8;
+  DBuf dev(nd * 8, s);
+  if (h->rank == 0) {
+    blob.b.resize(nd * 8, 0);
+    CK(cudaMemcpyAsync(dev.p, blob.b.data(), nd * 8, cudaMemcpyHostToDevice, s));
+  }
+  h->comm->broadcast(s, dev.as<double>(), (int)nd, 0);
+  if (h->rank != 0) {
+    blob.b.resize(nd * 8);
+    CK(cudaMemcpyAsync(blob.b.data(), dev.p, nd * 8, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  blob.b.resize(bytes);
+  blob.rd = 0;
+}
+
 // Global BILU(0) factorization on the GPU (distributed handles): every rank factorizes the
 // whole matrix per block color exactly as the single-GPU setup does (bit-identical
 // factors), then dist_localize keeps its rows.  Returns the factors, row-major blocks in
@@ -754,7 +825,15 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   std::unique_ptr<DBuf> dAvals;           // A's values on the device (S1 upload, reused for the stage)
   RapChain chain;
   chain.s = h->s;
-  if (h->setup_on_gpu) {                 // NEXT-2: S1 and the Galerkin products on the GPU
+  // distributed: only rank 0 runs S1-S4, the others receive the result (MSP_DIST_SETUP_ALL=1:
+  // every rank runs it)
+  const bool rank0_setup = h->comm && h->nranks > 1 && h->setup_rank0;
+  const bool run_here = !rank0_setup || h->rank == 0;
+  if (rank0_setup && h->rank != 0 && h->setup_on_gpu) {
+    dAvals.reset(new DBuf(A.v.size() * sizeof(double), h->s));
+    CK(cudaMemcpyAsync(dAvals->p, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+  }
+  if (h->setup_on_gpu && run_here) {     // NEXT-2: S1 and the Galerkin products on the GPU
     DBuf* dApp = nullptr;
     dAvals = gpu_setup_s1(h->s, h->prm.decoupling, A, S, &dApp);
     chain.keep.emplace_back(dApp);          // A_PP resident as the first fine operand
@@ -776,9 +855,31 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     };
   }
   T.mark("S1 weights + A_PP (GPU)");
-  {
+  if (run_here) {
     Nvtx nv("S2-S4 host: NPAIR, colorings, ABMC order (Galerkin on the GPU)");
-    rc = msp::run_host_setup(A, prm, S, err);
+    try {
+      rc = msp::run_host_setup(A, prm, S, err);
+    } catch (const std::pair<int, std::string>& e) {
+      if (!rank0_setup) throw;
+      rc = e.first;
+      err = e.second;
+    } catch (const CudaError& e) {        // rank 0 must still reach the broadcast
+      if (!rank0_setup) throw;
+      rc = MSP_ECUDA;
+      err = std::string("CUDA: ") + cudaGetErrorString(e.e) + " in " + e.where;
+    }
+  }
+  if (rank0_setup) {
+    Nvtx nv("S1-S4 result broadcast from rank 0");
+    SetupBlob blob;
+    if (h->rank == 0 && rc == 0) pack_setup(S, blob);
+    bcast_setup(h, rc, err, blob);
+    if (rc == 0 && h->rank != 0) {
+      unpack_setup(blob, S);
+      S.prm = prm;
+      S.A = &A;
+    }
+    T.mark("setup broadcast");
   }
   if (rc) throw std::pair<int, std::string>(rc, err);
   std::vector<int32_t> rp, ci, dg, src;
@@ -2840,7 +2941,11 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
   if ((kind == 1) && h->lv.empty()) return fail(h, MSP_EINVAL, "msp_time_kernel: no AMG level 0");
   return guarded(h, [&]() -> msp_status {
     const size_t kFlush = (size_t)256 << 20;
-    if (!h->flush) h->flush = h->dalloc<double>(kFlush / sizeof(double));
+    if (!h->flush) {
+      h->flush = h->dalloc<double>(kFlush / sizeof(double) + 1);
+      CK(cudaMemsetAsync(h->flush, 0, kFlush + sizeof(double), h->s));
+      CK(cudaStreamSynchronize(h->s));
+    }
     ensure_basis(h, 30);
     const size_t N = h->N;
     const double n = h->n, b = h->b, nnzb = (double)h->nnzb;
@@ -2943,7 +3048,11 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
     cudaGraphDestroy(graph);
     double total = 0.0;
     for (int r = 0; r < reps + 1; ++r) {
-      if (flush_l2) CK(cudaMemsetAsync(h->flush, r & 0xff, kFlush, h->s));
+      // flush L2 by READING 256 MB (2x L2): the cache is left holding clean lines, so the
+      // timed kernel pays no write-back of unrelated dirty data
+      if (flush_l2)
+        klaunch(h->s, false, flush_read_kernel, 4 * 148, 512, kFlush / sizeof(double), (const double*)h->flush,
+                h->flush + kFlush / sizeof(double));
       CK(cudaEventRecord(h->ev0, h->s));
       CK(cudaGraphLaunch(gexec, h->s));
       CK(cudaEventRecord(h->ev1, h->s));
@@ -3000,6 +3109,7 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     if (const char* e = std::getenv("MSP_DIST_OVERLAP")) h->overlap_halo = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSP_DIST_SETUP_ALL")) h->setup_rank0 = std::atoi(e) == 0;
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     h->caller = (cudaStream_t)cuda_stream;

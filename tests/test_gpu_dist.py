@@ -185,3 +185,31 @@ def test_loopback_halo_overlap_bit_identical(nranks, monkeypatch):
                                   coarsest_max_dof=100))
     assert out[0]["iters"] == out[1]["iters"]
     assert np.array_equal(out[0]["x"], out[1]["x"])
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_rank0_setup_broadcast_identical(nranks, monkeypatch):
+    """Only rank 0 runs S1-S4 and broadcasts the result (default) vs every rank running the
+    host setup (MSP_DIST_SETUP_ALL=1): identical plans -> bit-identical iterates."""
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C2", nx=24, ny=20, nz=9)
+    owner = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"], coarsest_max_dof=100).partition_owner(
+        p["nx"], p["ny"], p["nz"], nranks)
+    out = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("MSP_DIST_SETUP_ALL", v)
+        out.append(loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner,
+                                  coarsest_max_dof=100))
+    assert out[0]["iters"] == out[1]["iters"]
+    assert np.array_equal(out[0]["x"], out[1]["x"])
+    assert np.array_equal(out[0]["rank_info"], out[1]["rank_info"])
+
+
+def test_loopback_rank0_setup_error_propagates():
+    """A setup error on rank 0 (coarsening stall -> MSP_ESTALL there) reaches every rank
+    through the broadcast status instead of leaving the others waiting."""
+    from paper_2208_08594_b200 import loopback_solve
+    from paper_2208_08594_b200._binding import MspError
+    p = gen.make_config("C2", nx=12, ny=10, nz=4)
+    with pytest.raises(MspError):
+        loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], 2, p["rhs"], coarsest_max_dof=1, max_levels=2)
