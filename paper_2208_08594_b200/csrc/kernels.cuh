@@ -593,57 +593,61 @@ __global__ void __launch_bounds__(1024) sell_tail_kernel(int c_first, int c_last
 }
 
 
-// coarsest GEMV, 8 independent 16-byte loads in flight per lane; the first 8 of the
-// (immutable) inverse are issued before the PDL wait, overlapping the previous kernel
-template <int U>
-__global__ void __launch_bounds__(256) gemv8_kernel(int n, int ld, const double* __restrict__ Ainv,
-                                                    const double* __restrict__ b, double* __restrict__ x) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const bool live = row < n;
-  const double2* a = reinterpret_cast<const double2*>(Ainv + (size_t)(live ? row : 0) * ld);
+
+
+// a6 coarsest GEMV with W warps per row (one CTA per row): the row's 16-byte pairs are
+// spread over 32*W lanes (stride 32*W, U pairs in flight per lane; the first U issued
+// before the PDL wait), so the 4.4k-row inverse keeps every SM busy with ~4x more loads
+// in flight than warp-per-row; warp sums, then the W partial sums added in warp order
+// through shared memory (deterministic).
+template <int W, int U>
+__global__ void __launch_bounds__(32 * W) gemv_row_kernel(int n, int ld, const double* __restrict__ Ainv,
+                                                          const double* __restrict__ b, double* __restrict__ x) {
+  __shared__ double part[W];
+  const int row = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const double2* a = reinterpret_cast<const double2*>(Ainv + (size_t)row * ld);
   const double2* bb = reinterpret_cast<const double2*>(b);
-  const int n2 = n >> 1;                       // pairs
+  const int n2 = n >> 1;
+  constexpr int S = 32 * W;
   double2 pa[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int j = lane + 32 * u;
-    pa[u] = (live && j < n2) ? ldstream2(a + j) : make_double2(0.0, 0.0);
+    const int j = t + S * u;
+    pa[u] = (j < n2) ? ldstream2(a + j) : make_double2(0.0, 0.0);
   }
   pdl_wait();
   pdl_trigger();
-  if (!live) return;
-  double acc[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) acc[u] = 0.0;
-  for (int j0 = 0; j0 < n2; j0 += 32 * U) {
+  double acc = 0.0;
+  for (int j0 = 0; j0 < n2; j0 += S * U) {
     if (j0 > 0) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int j = j0 + lane + 32 * u;
+        const int j = j0 + t + S * u;
         pa[u] = (j < n2) ? ldstream2(a + j) : make_double2(0.0, 0.0);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = j0 + lane + 32 * u;
+      const int j = j0 + t + S * u;
       if (j < n2) {
         const double2 bv = __ldg(bb + j);
-        acc[u] = fma(pa[u].x, bv.x, fma(pa[u].y, bv.y, acc[u]));
+        acc = fma(pa[u].x, bv.x, fma(pa[u].y, bv.y, acc));
       }
     }
   }
+  if ((n & 1) && t == 0) acc = fma(ldg(Ainv + (size_t)row * ld + n - 1), ldg(b + n - 1), acc);
 #pragma unroll
-  for (int w = U / 2; w; w >>= 1)
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) part[w] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
 #pragma unroll
-    for (int u = 0; u < w; ++u) acc[u] += acc[u + w];
-  double s = acc[0];
-  if ((n & 1) && lane == 0) s = fma(ldg(Ainv + (size_t)row * ld + n - 1), ldg(b + n - 1), s);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) x[row] = s;
+    for (int k = 0; k < W; ++k) s += part[k];
+    x[row] = s;
+  }
 }
-
 
 // a5 part 2: restriction b_{l+1}[I] = sum_{i in I} r_i (P^T, piecewise-constant P).
 // (fused: xc != null -> first color of the next level's pre-sweep from the zero guess)

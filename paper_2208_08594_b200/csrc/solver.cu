@@ -1722,8 +1722,9 @@ void coarsest_solve(msp_handle* h) {
   if (h->coarse_diag)
     klaunch(h->s, h->pdl, diag_solve_kernel, nblk(h->nL, 256), 256, h->nL, h->cdiag, h->bL, h->xL);
   else
-    klaunch(h->s, h->pdl, gemv8_kernel<8>,
-            nblk((size_t)h->nL * 32, 256), 256, h->nL, h->ldA, h->Ainv, h->bL, h->xL);
+    // 4 warps per row (C3: 30.8 vs 34.3 us for warp-per-row, which was removed)
+    klaunch(h->s, h->pdl, gemv_row_kernel<4, 4>, h->nL, 128, h->nL, h->ldA, (const double*)h->Ainv,
+            (const double*)h->bL, h->xL);
 }
 
 template <int LPR, bool WR, bool RES>
