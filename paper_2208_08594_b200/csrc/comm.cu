@@ -47,8 +47,8 @@ class NcclComm : public Comm {
   static void chk(ncclResult_t e, const char* what) {
     if (e != ncclSuccess) throw std::runtime_error(std::string("NCCL ") + what + ": " + ncclGetErrorString(e));
   }
-  void halo(cudaStream_t s, const HaloPlan& P, double* vec, int n_own, int width, int seg) override {
-    for (size_t pi = 0; pi < P.peers.size(); ++pi) {
+  void halo(cudaStream_t s, const HaloPlan& P, double* vec, int n_own, int width, int seg, bool packed) override {
+    for (size_t pi = 0; pi < P.peers.size() && !packed; ++pi) {
       int a, b;
       seg_range(P, (int)pi, seg, true, a, b);
       launch_pack(s, P.d_send_idx, vec, P.d_sendbuf, P.send_base[pi] + a, P.send_base[pi] + b, width);
@@ -172,9 +172,9 @@ class LoopbackComm : public Comm {
     for (int q = 0; q < g->n; ++q)
       if (q != r) cudaStreamWaitEvent(s, g->done[q], 0);
   }
-  void halo(cudaStream_t s, const HaloPlan& P, double* vec, int n_own, int width, int seg) override {
+  void halo(cudaStream_t s, const HaloPlan& P, double* vec, int n_own, int width, int seg, bool packed) override {
     wait_peers_done(s);
-    for (size_t pi = 0; pi < P.peers.size(); ++pi) {
+    for (size_t pi = 0; pi < P.peers.size() && !packed; ++pi) {
       int a, b;
       seg_range(P, (int)pi, seg, true, a, b);
       launch_pack(s, P.d_send_idx, vec, P.d_sendbuf, P.send_base[pi] + a, P.send_base[pi] + b, width);

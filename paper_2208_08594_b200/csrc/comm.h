@@ -29,6 +29,9 @@ struct HaloPlan {
   int nsend = 0, nghost = 0;
   int32_t* d_send_idx = nullptr;             // device: owned local index of every send entry
   double* d_sendbuf = nullptr;               // device: nsend * max_width
+  int2* d_slots = nullptr;                   // device, per owned entry: its (<= 2) send positions
+                                             // (-1 none) -- producer kernels write the send buffer
+                                             // themselves (null: a row is sent more than twice)
 };
 
 class Comm {
@@ -37,7 +40,9 @@ class Comm {
   virtual int rank() const = 0;
   virtual int size() const = 0;
   // ghost values of vec (width doubles per entry): segment seg of every peer (-1: all)
-  virtual void halo(cudaStream_t s, const HaloPlan& plan, double* vec, int n_own, int width, int seg) = 0;
+  // packed: the producer kernel already wrote the send buffer (no pack kernel)
+  virtual void halo(cudaStream_t s, const HaloPlan& plan, double* vec, int n_own, int width, int seg,
+                    bool packed = false) = 0;
   // in-place sum over ranks (identical result on every rank)
   virtual void allreduce_sum(cudaStream_t s, double* buf, int count) = 0;
   // recv[r*count .. ) = send of rank r

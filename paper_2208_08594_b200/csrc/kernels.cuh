@@ -50,6 +50,20 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 #define PDL_ENTRY() do { pdl_wait(); pdl_trigger(); } while (0)
 
+// Distributed mode: the producer of a halo-exchanged vector also writes each of its rows'
+// values to their (<= 2) positions in the send buffer (HaloPlan::d_slots), so no separate
+// pack kernel runs before the exchange.  slots == null: nothing to pack.
+struct HaloPack {
+  const int2* slots;
+  double* buf;
+};
+__device__ __forceinline__ void halo_pack(const HaloPack& pk, int row, double v) {
+  if (!pk.slots) return;
+  const int2 q = __ldg(pk.slots + row);
+  if (q.x >= 0) pk.buf[q.x] = v;
+  if (q.y >= 0) pk.buf[q.y] = v;
+}
+
 // ---------------------------------------------------------------------------
 // a2 (K1): BSR SpMV.  One team of TS lanes per block row (TS = 4 for b=4, 8 for b=7);
 // lane q < B owns output row q of the cell.  Each block column-major: lane q reads
@@ -265,7 +279,7 @@ template <int B>
 __global__ void restrict_pressure_kernel(int n, const double* __restrict__ W,
                                          const double* __restrict__ g, const int* __restrict__ src,
                                          double* __restrict__ rp, double* __restrict__ x0,
-                                         const double* __restrict__ diag0, int c1_end) {
+                                         const double* __restrict__ diag0, int c1_end, HaloPack pk) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < n;
   // PDL prologue: the cell map, its weight row and the level-0 diagonal are immutable
@@ -281,7 +295,11 @@ __global__ void restrict_pressure_kernel(int n, const double* __restrict__ W,
 #pragma unroll
   for (int k = 0; k < B; ++k) s = fma(wk[k], ldg(g + (size_t)c * B + k), s);
   rp[i] = s;
-  if (x0) x0[i] = (i < c1_end) ? s / d : 0.0;
+  if (x0) {
+    const double xv = (i < c1_end) ? s / d : 0.0;
+    x0[i] = xv;
+    halo_pack(pk, i, xv);
+  }
 }
 
 // gather of the level-0 correction into cell order: wp[c] = x0[dst[c]]
@@ -510,7 +528,8 @@ __global__ void __launch_bounds__(128) sell_row_uniform_kernel(int s_first, int 
                                                                const double* __restrict__ val,
                                                                const double* __restrict__ diag,
                                                                const double* __restrict__ b,
-                                                               double* __restrict__ x, double* __restrict__ r) {
+                                                               double* __restrict__ x, double* __restrict__ r,
+                                                               HaloPack pk) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = s_first + t / kSell;
   if (s >= s_end) return;
@@ -538,6 +557,7 @@ __global__ void __launch_bounds__(128) sell_row_uniform_kernel(int s_first, int 
     const double bs = ldg(b + row) - acc;
     const double xi = bs / d;
     x[row] = xi;
+    halo_pack(pk, row, xi);
     if (WRITE_R) r[row] = fma(-d, xi, bs);
   }
 }
@@ -676,12 +696,16 @@ __global__ void restrict_kernel(int nc, const int* __restrict__ pp, const int* _
 
 // a7: prolongation and correction x_i += e[agg(i)].
 __global__ void prolong_kernel(int n, const int* __restrict__ agg, const double* __restrict__ e,
-                               double* __restrict__ x) {
+                               double* __restrict__ x, HaloPack pk) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int a = (i < n) ? ldg(agg + i) : 0;      // immutable map: before the PDL wait
   pdl_wait();
   pdl_trigger();
-  if (i < n) x[i] += ldg(e + a);
+  if (i < n) {
+    const double xv = x[i] + ldg(e + a);
+    x[i] = xv;
+    halo_pack(pk, i, xv);
+  }
 }
 
 
@@ -797,7 +821,9 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
                                                          const double* __restrict__ F,
                                                          double* v,
                                                          const double* __restrict__ wp,
-                                                         double* __restrict__ z) {
+                                                         double* __restrict__ z,
+                                                         const int2* __restrict__ slots,
+                                                         double* __restrict__ sbuf) {
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int TM = MAXC * TS;
   static_assert(TM <= 32, "team must fit in a warp");
@@ -834,6 +860,9 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
         asm volatile("prefetch.global.L1 [%0];" ::"l"(F + (size_t)sl[sidx] * BB + q * 4));
     }
   }
+  // distributed mode: send positions of this cell (the halo of this color phase is packed
+  // here, not by a separate kernel)
+  const int2 sl2 = (slots && valid) ? __ldg(slots + i) : make_int2(-1, -1);
   // PDL prologue (4x4 blocks): indices and factor columns of the first PFE external
   // entries are immutable -> issued before the wait, overlapping the previous kernel
   constexpr int PFE = (B == 4 && PF) ? MSP_BILU_PFE : 0;
@@ -932,7 +961,13 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
       }
       if (use) t -= contrib;
     }
-    if (act) v[(size_t)i * B + q] = t;
+    if (act) {
+      v[(size_t)i * B + q] = t;
+      if (!BWD) {
+        if (sl2.x >= 0) sbuf[(size_t)sl2.x * B + q] = t;
+        if (sl2.y >= 0) sbuf[(size_t)sl2.y * B + q] = t;
+      }
+    }
     __syncwarp(tmask);
   }
   if (BWD) {
@@ -1018,6 +1053,8 @@ __global__ void __launch_bounds__(128, (B <= 4) ? MSP_BILU_MINB : 8) bilu_block_
     }
     if (act) {
       v[(size_t)i * B + q] = x;
+      if (sl2.x >= 0) sbuf[(size_t)sl2.x * B + q] = x;
+      if (sl2.y >= 0) sbuf[(size_t)sl2.y * B + q] = x;
       // z = w + R r: WFULL -> w is a full cell vector (stages NPR), else only the
       // pressure correction wp (stages PR)
       z[(size_t)i * B + q] = x + (WFULL ? ldg(wp + (size_t)i * B + q) : ((q == 0) ? ldg(wp + i) : 0.0));

@@ -165,6 +165,7 @@ struct msp_handle {
   int n_rows_in = 0, n_rows_bd = 0;
   bool overlap_halo = true;          // MSP_DIST_OVERLAP=0: exchange, then the whole SpMV
   bool setup_rank0 = true;           // MSP_DIST_SETUP_ALL=1: every rank runs the host setup
+  bool fuse_halo = true;             // MSP_DIST_FUSE_PACK=0: separate pack kernel per exchange
   int rank = 0, nranks = 1;
   int n_ghost = 0, n0_ghost = 0;     // cell-space / level-0 ghosts
   msp::HaloPlan cell_halo;           // segments = BILU block colors
@@ -1207,7 +1208,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
 // ---------------------------------------------------------------------------
 static void build_halo(msp_handle* h, msp::HaloPlan& P, int nseg, int nranks, int me,
                        const std::vector<std::vector<std::vector<int32_t>>>& sendl,   // [peer][seg] owned local idx
-                       const std::vector<std::vector<int32_t>>& recv_cnt) {          // [peer][seg]
+                       const std::vector<std::vector<int32_t>>& recv_cnt,            // [peer][seg]
+                       int n_own = -1) {
   P = msp::HaloPlan();
   P.nseg = nseg;
   std::vector<int32_t> idx;
@@ -1234,6 +1236,17 @@ static void build_halo(msp_handle* h, msp::HaloPlan& P, int nseg, int nranks, in
   P.nghost = ghost;
   P.d_send_idx = h->upload(idx);
   P.d_sendbuf = h->dalloc<double>((size_t)std::max(P.nsend, 1) * 8);
+  if (n_own >= 0) {                               // send positions per owned entry (<= 2)
+    std::vector<int2> sl(std::max(n_own, 1), make_int2(-1, -1));
+    bool ok = true;
+    for (int k = 0; k < (int)idx.size() && ok; ++k) {
+      int2& e = sl[idx[k]];
+      if (e.x < 0) e.x = k;
+      else if (e.y < 0) e.y = k;
+      else ok = false;
+    }
+    P.d_slots = ok ? h->upload(sl) : nullptr;
+  }
 }
 
 // Host-side plan of the cell space for rank `me` (pure integer work, no GPU).
@@ -1321,7 +1334,7 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
   for (int32_t p = 0; p < n; ++p) own_cell[S.order[p]] = own_pos[p];
   const int32_t no = (int32_t)posown.size();
   const int32_t ng = (int32_t)C.ghosts.size();
-  build_halo(h, h->cell_halo, S.bilu_ncolor, P, me, C.sendl, C.rcnt);
+  build_halo(h, h->cell_halo, S.bilu_ncolor, P, me, C.sendl, C.rcnt, (int)C.posown.size());
   // local BSR rows (entries keep the global position order: L | diag | U)
   std::vector<int32_t> lrp(no + 1, 0), lci, ldg(no), lsrc;
   std::vector<double> lF, lA, lPc, lW((size_t)no * b);
@@ -1474,7 +1487,7 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
     for (int q = 0; q < P; ++q)
       for (int32_t d : need0[q]) sendl[q][col0[d]].push_back(l0loc[d]);
     for (int32_t d : gh0) rcnt[own_cell[d]][col0[d]]++;
-    build_halo(h, h->l0_halo, g0, P, me, sendl, rcnt);
+    build_halo(h, h->l0_halo, g0, P, me, sendl, rcnt, no0);
   }
   {
     std::vector<int32_t> r0(no0 + 1, 0), c0v, rc0(no0);
@@ -1605,11 +1618,11 @@ void spmv_overlapped(msp_handle* h, int mode, double* x, int width, const double
 bool overlap_ok(const msp_handle* h) { return h->comm && h->b == 4 && h->s2 && h->overlap_halo; }
 
 // halo exchanges of the distributed mode (no-ops on a single GPU)
-void exch_cell(msp_handle* h, double* v, int width, int seg) {
-  if (h->comm) h->comm->halo(h->s, h->cell_halo, v, h->n, width, seg);
+void exch_cell(msp_handle* h, double* v, int width, int seg, bool packed = false) {
+  if (h->comm) h->comm->halo(h->s, h->cell_halo, v, h->n, width, seg, packed);
 }
-void exch_l0(msp_handle* h, double* x, int seg) {
-  if (h->comm) h->comm->halo(h->s, h->l0_halo, x, h->lv[0].n, 1, seg);
+void exch_l0(msp_handle* h, double* x, int seg, bool packed = false) {
+  if (h->comm) h->comm->halo(h->s, h->l0_halo, x, h->lv[0].n, 1, seg, packed);
 }
 
 // half: 0 both substitutions (the MSP apply), 1 forward only (v: r -> y), 2 backward only
@@ -1618,17 +1631,22 @@ template <int B, int MAXC, bool WF = false>
 void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, int half = 0) {
   constexpr int TM = MAXC * ((B <= 4) ? 4 : 8);
   const int g = h->bilu_ncolor;
+  const bool fused_pack = h->comm && h->cell_halo.d_slots && h->fuse_halo && !h->prm.bilu_local && !half;
   auto run = [&](int c, int kind) {
     const int b0 = h->color_blk[c], b1 = h->color_blk[c + 1];
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
+    // distributed: the kernel packs the halo of its color phase itself (v only: the BILU
+    // vector whose ghosts the next phases read)
+    const int2* sl = fused_pack ? (const int2*)h->cell_halo.d_slots : nullptr;
+    double* sb = fused_pack ? h->cell_halo.d_sendbuf : nullptr;
     if (kind == 0)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, false, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, sl, sb);
     else if (kind == 1)
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, false, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, sl, sb);
     else
-      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z);
+      klaunch(h->s, h->pdl, bilu_block_kernel<B, MAXC, true, true, WF>, grid, 128, b0, b1, h->blk_ptr, h->rp, h->ci, h->dg, h->bcnt, (const int4*)h->islot, h->Fval, v, wp, z, sl, sb);
   };
   if (half == 1) {
     for (int c = 0; c < g; ++c) run(c, 0);
@@ -1643,10 +1661,10 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
   // rank-local BILU: the factor blocks of couplings to other ranks are zero, ghost slots of v
   // are never read with a nonzero factor -> no exchange
   const bool ex = !h->prm.bilu_local;
-  for (int c = 0; c < g - 1; ++c) { run(c, 0); if (ex) exch_cell(h, v, B, c); }
+  for (int c = 0; c < g - 1; ++c) { run(c, 0); if (ex) exch_cell(h, v, B, c, fused_pack); }
   run(g - 1, 2);
-  if (g > 1 && ex) exch_cell(h, v, B, g - 1);
-  for (int c = g - 2; c >= 0; --c) { run(c, 1); if (c > 0 && ex) exch_cell(h, v, B, c); }
+  if (g > 1 && ex) exch_cell(h, v, B, g - 1, fused_pack);
+  for (int c = g - 2; c >= 0; --c) { run(c, 1); if (c > 0 && ex) exch_cell(h, v, B, c, fused_pack); }
 }
 
 template <int B>
@@ -1699,7 +1717,7 @@ void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfu
 }
 
 // a3 (+ the fused zero-guess first color of level 0 when it has a PGS-MC level)
-void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool fuse_init) {
+void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool fuse_init, HaloPack pk = HaloPack{}) {
   const unsigned grid = nblk(h->n, 256);
   double* x0 = nullptr;
   const double* d0 = nullptr;
@@ -1710,7 +1728,7 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool 
     c1 = h->lv[0].color_row[1];
   }
   switch (h->b) {
-#define CASE(BV) case BV: klaunch(h->s, h->pdl, restrict_pressure_kernel<BV>, grid, 256, h->n, h->W, g, h->cell_of_l0, rp0, x0, d0, c1); break;
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, restrict_pressure_kernel<BV>, grid, 256, h->n, h->W, g, h->cell_of_l0, rp0, x0, d0, c1, pk); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -1735,8 +1753,9 @@ void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
       s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
   ++h->nlaunch;
 }
+// returns true when the kernel also packed the halo (pk given, uniform level-0 layout)
 template <bool WR, bool RES>
-void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
+bool sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1, HaloPack pk = HaloPack{}) {
   if (L.lpr == 1 && L.uniform_w > 0 && s1 > s0) {
     int c = 0;                                     // the color holding slice s0
     while (c + 1 < L.ncolor && L.color_slice[c + 1] <= s0) ++c;
@@ -1744,9 +1763,9 @@ void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
       const int row_first = L.color_row[c] + (s0 - L.color_slice[c]) * kSell;
       klaunch(h->s, h->pdl, sell_row_uniform_kernel<WR, RES>, nblk((size_t)(s1 - s0) * kSell, 128), 128, s0, s1,
               row_first, L.color_row[c + 1], L.uniform_w, (const int*)L.col, (const double*)L.val,
-              (const double*)L.diag, (const double*)L.b, L.x, L.r);
+              (const double*)L.diag, (const double*)L.b, L.x, L.r, pk);
       ++h->nlaunch;
-      return;
+      return pk.slots != nullptr;
     }
   }
   switch (L.lpr) {
@@ -1755,6 +1774,7 @@ void sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1) {
     case 8: sell_rows<8, WR, RES>(h, L, s0, s1); break;
     default: sell_rows<1, WR, RES>(h, L, s0, s1); break;
   }
+  return false;
 }
 
 void sell_tail(msp_handle* h, DevLevel& L, int c0, int c1, bool asc, bool write_r) {
@@ -1865,7 +1885,7 @@ void vcycle(msp_handle* h, int l, bool init_done = false) {
                                                    fuse_next ? h->lv[l + 1].color_row[1] : 0);
   ++h->nlaunch;
   vcycle(h, l + 1, fuse_next);
-  klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, xn, L.x); ++h->nlaunch;
+  klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, xn, L.x, HaloPack{}); ++h->nlaunch;
   for (int s = 0; s < h->prm.post_sweeps; ++s) pgs_sweep(h, L, false, false);
 }
 
@@ -1883,12 +1903,16 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
   DevLevel& L0 = h->lv[0];
   const int L = (int)h->lv.size();
   CK(cudaMemsetAsync(L0.x + L0.n, 0, sizeof(double) * h->n0_ghost, h->s));    // zero guess of ghosts
-  launch_restrict_pressure(h, g, L0.b, true);                                // a3 + first color
-  exch_l0(h, L0.x, 0);
+  // producers pack the level-0 halo themselves (uniform level-0 layout)
+  const HaloPack pk0 = (h->fuse_halo && h->l0_halo.d_slots) ? HaloPack{h->l0_halo.d_slots, h->l0_halo.d_sendbuf}
+                                                            : HaloPack{nullptr, nullptr};
+  launch_restrict_pressure(h, g, L0.b, true, pk0);                           // a3 + first color
+  exch_l0(h, L0.x, 0, pk0.slots != nullptr);
   for (int c = 1; c < L0.ncolor; ++c) {
-    if (c == L0.ncolor - 1) sell_rows_any<true, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
-    else sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
-    exch_l0(h, L0.x, c);
+    bool packed;
+    if (c == L0.ncolor - 1) packed = sell_rows_any<true, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1], pk0);
+    else packed = sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1], pk0);
+    exch_l0(h, L0.x, c, packed);
   }
   if (L0.ncolor > 1) sell_rows_any<false, true>(h, L0, 0, L0.color_slice[L0.ncolor - 1]);
   else sell_rows_any<false, true>(h, L0, 0, L0.nslices);
@@ -1912,12 +1936,12 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
     vcycle(h, 1, init1);                                                     // levels >= 1 + coarsest
   }
   if (root_mode) h->comm->broadcast(h->s, x1, (L > 1) ? h->lv[1].n : h->nL, 0);   // level-1 correction
-  klaunch(h->s, h->pdl, prolong_kernel, nblk(L0.n, 256), 256, L0.n, (const int*)L0.agg, (const double*)x1, L0.x);
+  klaunch(h->s, h->pdl, prolong_kernel, nblk(L0.n, 256), 256, L0.n, (const int*)L0.agg, (const double*)x1, L0.x, pk0);
   ++h->nlaunch;
-  exch_l0(h, L0.x, -1);
+  exch_l0(h, L0.x, -1, pk0.slots != nullptr);
   for (int c = L0.ncolor - 1; c >= 0; --c) {
-    sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1]);
-    if (c > 0) exch_l0(h, L0.x, c);
+    const bool packed = sell_rows_any<false, false>(h, L0, L0.color_slice[c], L0.color_slice[c + 1], c > 0 ? pk0 : HaloPack{});
+    if (c > 0) exch_l0(h, L0.x, c, packed);
   }
   klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, (const int*)h->l0_of_cell, (const double*)L0.x, h->wp);
   ++h->nlaunch;
@@ -2810,7 +2834,7 @@ msp_status msp_prolong(msp_handle* h, int level, const double* e, double* x) {
     if (last) CK(cudaMemcpyAsync(xn, e, sizeof(double) * nn, cudaMemcpyDeviceToDevice, h->s));
     else { klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(nn, 256), 256, nn, h->lv[level + 1].perm, e, xn, 1); ++h->nlaunch; }
     klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, (const double*)x, L.x, 1); ++h->nlaunch;
-    klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, (const double*)xn, L.x); ++h->nlaunch;
+    klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, (const double*)xn, L.x, HaloPack{}); ++h->nlaunch;
     klaunch(h->s, h->pdl, scalar_perm_kernel, nblk(L.n, 256), 256, L.n, L.perm, (const double*)L.x, x, 0); ++h->nlaunch;
     CK(cudaStreamSynchronize(h->s));
     return MSP_OK;
@@ -3111,6 +3135,7 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     if (const char* e = std::getenv("MSP_DIST_OVERLAP")) h->overlap_halo = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSP_DIST_SETUP_ALL")) h->setup_rank0 = std::atoi(e) == 0;
+    if (const char* e = std::getenv("MSP_DIST_FUSE_PACK")) h->fuse_halo = std::atoi(e) != 0;
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     h->caller = (cudaStream_t)cuda_stream;

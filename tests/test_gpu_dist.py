@@ -213,3 +213,21 @@ def test_loopback_rank0_setup_error_propagates():
     p = gen.make_config("C2", nx=12, ny=10, nz=4)
     with pytest.raises(MspError):
         loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], 2, p["rhs"], coarsest_max_dof=1, max_levels=2)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_fused_halo_pack_bit_identical(nranks, monkeypatch):
+    """Halo packing inside the producer kernels (BILU color phases, level-0 PGS-MC colors,
+    a3's fused first color, the prolongation) instead of a separate pack kernel per
+    exchange: same send buffers, so bit-identical iterates."""
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C2", nx=24, ny=20, nz=9)
+    owner = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"], coarsest_max_dof=100).partition_owner(
+        p["nx"], p["ny"], p["nz"], nranks)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("MSP_DIST_FUSE_PACK", v)
+        out.append(loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=owner,
+                                  coarsest_max_dof=100))
+    assert out[0]["iters"] == out[1]["iters"]
+    assert np.array_equal(out[0]["x"], out[1]["x"])
