@@ -22,6 +22,7 @@
 #include "setup.h"
 #include "kernels.cuh"
 #include "setup_kernels.cuh"
+#include "bilu_meta.cuh"
 #include <nvtx3/nvToolsExt.h>
 
 using namespace mspk;
@@ -150,6 +151,9 @@ struct msp_handle {
   std::vector<int64_t> graph_kernels;
   double* flush = nullptr;           // 256 MB L2-flush scratch (msp_time_kernel)
   double* ftmp = nullptr;            // msp_bilu_set_factors scratch
+  // a9 per-slot metadata (bilu_meta.cuh; 4x4 blocks, single GPU)
+  int4 *bm_f = nullptr, *bm_b = nullptr, *bm_cf = nullptr, *bm_cb = nullptr, *bm_sl = nullptr;
+  int bilu_meta = 1;                 // MSP_BILU_META=0: bilu_block_kernel (the distributed path's kernel)
   bool setup_on_gpu = true;          // NEXT-2: S1 + Galerkin on the GPU (MSP_HOST_SETUP=1: host)
   cusolverDnHandle_t cs = nullptr;   // coarsest inverse (created once, reused by rebuilds)
   bool gpu_s1 = false;               // the last SETUP computed S1 on the GPU
@@ -1101,6 +1105,39 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     }
     h->bcnt = h->upload(cnt);
     h->islot = h->upload(make_islot(n, rp, ci, dg, S.blk_ptr));
+    h->bm_f = nullptr;
+    if (h->bilu_meta && b == 4 && h->max_blk <= 4) {
+      // per (block, cell slot) metadata of bilu_meta4_kernel
+      const int mx = h->max_blk <= 1 ? 1 : (h->max_blk <= 2 ? 2 : 4);
+      const size_t nbk = S.blk_ptr.size() - 1;
+      std::vector<int4> mf(nbk * mx, make_int4(-1, 0, 0, 0)), mb(nbk * mx, make_int4(-1, 0, 0, 0)),
+          cf(nbk * mx, make_int4(0, 0, 0, 0)), cb(nbk * mx, make_int4(0, 0, 0, 0)),
+          sl(nbk * mx, make_int4(-1, -1, -1, -1));
+      const std::vector<int4> isl = make_islot(n, rp, ci, dg, S.blk_ptr);
+      for (size_t k = 0; k < nbk; ++k) {
+        const int32_t c0 = S.blk_ptr[k], c1 = S.blk_ptr[k + 1];
+        for (int32_t i = c0; i < c1; ++i) {
+          const size_t sidx = k * mx + (i - c0);
+          int32_t next = 0, nint = 0;
+          for (int32_t e = rp[i]; e < dg[i]; ++e) if (ci[e] < c0) ++next;
+          for (int32_t e = dg[i] + 1; e < rp[i + 1]; ++e) if (ci[e] < c1) ++nint;
+          const int32_t ei = dg[i] + 1 + nint;
+          mf[sidx] = make_int4(i, rp[i], rp[i] + next, 0);
+          mb[sidx] = make_int4(i, dg[i], ei, rp[i + 1]);
+          int a[4] = {0, 0, 0, 0}, bq[4] = {0, 0, 0, 0};
+          for (int u = 0; u < 4 && u < next; ++u) a[u] = ci[rp[i] + u];
+          for (int u = 0; u < 4 && ei + u < rp[i + 1]; ++u) bq[u] = ci[ei + u];
+          cf[sidx] = make_int4(a[0], a[1], a[2], a[3]);
+          cb[sidx] = make_int4(bq[0], bq[1], bq[2], bq[3]);
+          sl[sidx] = isl[i];
+        }
+      }
+      h->bm_f = h->upload(mf);
+      h->bm_b = h->upload(mb);
+      h->bm_cf = h->upload(cf);
+      h->bm_cb = h->upload(cb);
+      h->bm_sl = h->upload(sl);
+    }
   }
     {
       std::vector<int32_t> l0(n);
@@ -1637,6 +1674,23 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
+    if constexpr (B == 4 && !WF) {
+      if (h->bm_f && !h->comm) {             // per-slot metadata: shorter dependent load chain
+        if (kind == 0)
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, false>, grid, 128, b0, b1, (const int4*)h->bm_f,
+                  (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
+                  (const int*)h->ci, (const double*)h->Fval, v, wp, z);
+        else if (kind == 1)
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, false, true>, grid, 128, b0, b1, (const int4*)h->bm_f,
+                  (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
+                  (const int*)h->ci, (const double*)h->Fval, v, wp, z);
+        else
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, true>, grid, 128, b0, b1, (const int4*)h->bm_f,
+                  (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
+                  (const int*)h->ci, (const double*)h->Fval, v, wp, z);
+        return;
+      }
+    }
     // distributed: the kernel packs the halo of its color phase itself (v only: the BILU
     // vector whose ghosts the next phases read)
     const int2* sl = fused_pack ? (const int2*)h->cell_halo.d_slots : nullptr;
@@ -2562,6 +2616,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   h->cfg = c;
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_HOST_SETUP")) h->setup_on_gpu = std::atoi(e) == 0;
+  if (const char* e = std::getenv("MSP_BILU_META")) h->bilu_meta = std::atoi(e);
   if (const char* e = std::getenv("MSP_CYCLE_GRAPH")) h->cycle_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
