@@ -448,3 +448,46 @@ def test_cycle_graph_matches_per_step_graphs(orth, monkeypatch):
     assert_hist_agree(out[0]["hist"], out[0]["iters"], out[1]["hist"], out[1]["iters"], 7, rtol=1e-7)
     x0, x1 = out[0]["x"].cpu().numpy(), out[1]["x"].cpu().numpy()
     assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x0)
+
+
+def test_caller_stream_ordering():
+    """the library orders its work after the caller's stream.  b is produced by
+    a kernel on a torch side stream that the solver was told about (set_stream), with no
+    host synchronisation in between; the solve must see the finished b."""
+    p = gen.make_config("C2", nx=20, ny=16, nz=6)
+    s = solver(p, coarsest_max_dof=80)
+    side = torch.cuda.Stream()
+    b0 = torch.from_numpy(p["rhs"]).cuda()
+    torch.cuda.synchronize()
+    s.set_stream(side.cuda_stream)
+    with torch.cuda.stream(side):
+        b = torch.empty_like(b0)
+        torch.cuda._sleep(50_000_000)                   # keep the side stream busy
+        b.copy_(b0)
+        x = torch.zeros_like(b)
+        r = s.solve(b, x, tol=1e-8)
+    assert r["final_rel"] <= 1e-8
+    ref = s.solve(b0.clone(), tol=1e-8)
+    assert r["iters"] == ref["iters"]
+
+
+def test_failed_rebuild_invalidates_handle():
+    """a rebuild that fails after the old device state was released (here: a
+    singular pivot / coarsest matrix) leaves the handle unusable (MSP_EINVAL) instead of
+    running kernels on freed memory; a good rebuild revives it.  (A failure in the host
+    steps before the release keeps the previous preconditioner.)"""
+    from paper_2208_08594_b200 import MspSolver
+    from paper_2208_08594_b200._binding import MspError
+    ptr, col = np.array([0, 1], np.int32), np.array([0], np.int32)
+    good = np.array([[[2.0, 1.0], [1.0, 2.0]]])
+    bad = np.array([[[1.0, 1.0], [1.0, 1.0]]])           # singular; C_NN fine, A_PP = 0
+    s = MspSolver(ptr, col, good, nc=1)
+    rhs = torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda")
+    assert s.solve(rhs, tol=1e-12)["final_rel"] <= 1e-12
+    with pytest.raises(MspError):
+        s.update(ptr, col, bad, iota=1, last_iterations=0, mu=0)
+    with pytest.raises(MspError) as ei:
+        s.solve(rhs)
+    assert ei.value.status == 1
+    assert s.update(ptr, col, good, iota=1, last_iterations=0, mu=0) is True
+    assert s.solve(rhs, tol=1e-12)["final_rel"] <= 1e-12

@@ -231,3 +231,17 @@ def test_loopback_fused_halo_pack_bit_identical(nranks, monkeypatch):
                                   coarsest_max_dof=100))
     assert out[0]["iters"] == out[1]["iters"]
     assert np.array_equal(out[0]["x"], out[1]["x"])
+
+
+def test_dist_update_reuses_with_global_sizes():
+    """msp_update on a distributed handle compares the GLOBAL size and pattern,
+    so an ASMSP step with last_iterations <= mu reuses the preconditioner."""
+    from paper_2208_08594_b200 import DistSolver, nccl_unique_id
+    p0 = gen.make_config("C2", nx=20, ny=16, nz=6)
+    p1 = gen.make_config("C2", nx=20, ny=16, nz=6, newton_step=1)
+    d = DistSolver(p0["row_ptr"], p0["col"], p0["val"], p0["nc"], 0, 1, nccl_unique_id(), coarsest_max_dof=80)
+    assert d.update(p1["row_ptr"], p1["col"], p1["val"], iota=2, last_iterations=5, mu=10) is False
+    assert d.stats()["reuse_calls"] == 1
+    r = d.solve(torch.from_numpy(p1["rhs"]).cuda())
+    assert r["final_rel"] <= 1e-6
+    assert d.update(p1["row_ptr"], p1["col"], p1["val"], iota=3, last_iterations=11, mu=10) is True
