@@ -174,4 +174,119 @@ __global__ void __launch_bounds__(128, MSP_BILU_META_MINB) bilu_meta4_kernel(
   }
 }
 
+// 5x5 .. 8x8 blocks: the same metadata scheme with 8-lane cell groups (lane q < B owns
+// row q; external couplings column-per-lane through col_accum8 and one reduce-scatter, as
+// bilu_block_kernel's B >= 5 path; the columns of the first four external entries come
+// from the metadata, so their gathers issue at once instead of one ci -> y chain each).
+template <int B, int MAXC, bool FWD, bool BWD>
+__global__ void __launch_bounds__(128, 8) bilu_meta8_kernel(
+    int b_first, int b_end, const int4* __restrict__ mf, const int4* __restrict__ cf, const int4* __restrict__ mb,
+    const int4* __restrict__ cb, const int4* __restrict__ slt, const int* __restrict__ ci,
+    const double* __restrict__ F, double* v, const double* __restrict__ wp, double* __restrict__ z) {
+  constexpr int TS = 8;
+  constexpr int TM = MAXC * TS;
+  constexpr int BB = B * B;
+  static_assert(B >= 5 && B <= 8 && TM <= 32, "8-lane groups");
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int blk = b_first + gtid / TM;
+  const int lane = threadIdx.x & 31;
+  const int tl = lane % TM;
+  const int cq = tl / TS, q = tl % TS;
+  const int tbase = lane - tl, cbase = lane - q;
+  const unsigned tmask = (TM == 32) ? 0xffffffffu : (((1u << TM) - 1u) << tbase);
+  const unsigned cmask = 0xffu << cbase;
+  if (blk >= b_end) return;
+  const size_t s = (size_t)blk * MAXC + cq;
+  const int4 m1 = FWD ? __ldg(mf + s) : __ldg(mb + s);
+  const int4 c1 = FWD ? __ldg(cf + s) : __ldg(cb + s);
+  int sl[4] = {-1, -1, -1, -1};
+  if (MAXC > 1) {
+    const int4 s4 = __ldg(slt + s);
+    sl[0] = s4.x; sl[1] = s4.y; sl[2] = s4.z; sl[3] = s4.w;
+  }
+  const int i = m1.x;
+  const bool valid = i >= 0;
+  const bool act = valid && q < B;
+  const int ir = valid ? i : 0;
+  if (MAXC > 1 && valid && q < B) {
+#pragma unroll
+    for (int sidx = 0; sidx < MAXC; ++sidx) {
+      const bool need = (FWD && sidx < cq) || (BWD && sidx >= cq);
+      if (need && sl[sidx] >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(F + (size_t)sl[sidx] * BB + q * B));
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  double t = 0.0;
+  auto ext = [&](int ea, int eb, const int4& cc) -> double {
+    double a8[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a8[r] = 0.0;
+    const int cs[4] = {cc.x, cc.y, cc.z, cc.w};
+    double yq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) yq[u] = (act && ea + u < eb) ? ldg(v + (size_t)cs[u] * B + q) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (valid && ea + u < eb) col_accum8<B>(F + (size_t)(ea + u) * BB, yq[u], q, a8);
+    if (valid) {
+      for (int e = ea + 4; e < eb; ++e) {
+        const double yv = (q < B) ? ldg(v + (size_t)ldg(ci + e) * B + q) : 0.0;
+        col_accum8<B>(F + (size_t)e * BB, yv, q, a8);
+      }
+    }
+    return reduce_scatter8(a8, q, cmask);
+  };
+  if (FWD) {
+    const double acc = ext(m1.y, m1.z, c1);
+    t = act ? (v[(size_t)ir * B + q] - acc) : 0.0;
+#pragma unroll
+    for (int sidx = 0; sidx < MAXC - 1; ++sidx) {
+      double contrib = 0.0;
+      const bool use = valid && cq > sidx && sl[sidx] >= 0;
+      const double* blkF = F + (size_t)(use ? sl[sidx] : 0) * BB;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double yu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
+        if (use && q < B) contrib = fma(ldg(blkF + u * B + q), yu, contrib);
+      }
+      if (use) t -= contrib;
+    }
+    if (act) v[(size_t)ir * B + q] = t;
+    __syncwarp(tmask);
+  }
+  if (BWD) {
+    const int4 mB = FWD ? __ldg(mb + s) : m1;
+    if (!FWD) t = act ? v[(size_t)ir * B + q] : 0.0;
+    const int4 cB = FWD ? __ldg(cb + s) : c1;
+    t -= ext(mB.z, mB.w, cB);
+    const double* Dg = F + (size_t)(valid ? mB.y : 0) * BB;
+    double x = 0.0;
+#pragma unroll
+    for (int sidx = MAXC - 1; sidx >= 0; --sidx) {
+      double xs = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double tu = __shfl_sync(tmask, t, tbase + sidx * TS + u);
+        if (cq == sidx && act) xs = fma(ldg(Dg + u * B + q), tu, xs);
+      }
+      if (cq == sidx) x = xs;
+      if (sidx == 0) break;
+      const bool use = valid && cq < sidx && sl[sidx] >= 0;
+      const double* blkF = F + (size_t)(use ? sl[sidx] : 0) * BB;
+      double contrib = 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const double xu = __shfl_sync(tmask, xs, tbase + sidx * TS + u);
+        if (use && q < B) contrib = fma(ldg(blkF + u * B + q), xu, contrib);
+      }
+      if (use) t -= contrib;
+    }
+    if (act) {
+      v[(size_t)ir * B + q] = x;
+      z[(size_t)ir * B + q] = x + ((q == 0) ? ldg(wp + ir) : 0.0);
+    }
+  }
+}
+
 }  // namespace mspk

@@ -1106,7 +1106,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->bcnt = h->upload(cnt);
     h->islot = h->upload(make_islot(n, rp, ci, dg, S.blk_ptr));
     h->bm_f = nullptr;
-    if (h->bilu_meta && b == 4 && h->max_blk <= 4) {
+    if (h->bilu_meta && b >= 4 && h->max_blk <= 4) {
       // per (block, cell slot) metadata of bilu_meta4_kernel
       const int mx = h->max_blk <= 1 ? 1 : (h->max_blk <= 2 ? 2 : 4);
       const size_t nbk = S.blk_ptr.size() - 1;
@@ -1674,6 +1674,15 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
     if (b1 <= b0) return;
     const unsigned grid = nblk((size_t)(b1 - b0) * TM, 128);
     ++h->nlaunch;
+    if constexpr (B >= 5 && !WF) {
+      if (h->bm_f && !h->comm) {             // per-slot metadata, 8-lane groups
+        auto kf = kind == 0 ? bilu_meta8_kernel<B, MAXC, true, false>
+                            : (kind == 1 ? bilu_meta8_kernel<B, MAXC, false, true> : bilu_meta8_kernel<B, MAXC, true, true>);
+        klaunch(h->s, h->pdl, kf, grid, 128, b0, b1, (const int4*)h->bm_f, (const int4*)h->bm_cf, (const int4*)h->bm_b,
+                (const int4*)h->bm_cb, (const int4*)h->bm_sl, (const int*)h->ci, (const double*)h->Fval, v, wp, z);
+        return;
+      }
+    }
     if constexpr (B == 4 && !WF) {
       if (h->bm_f && !h->comm) {             // per-slot metadata: shorter dependent load chain
         if (kind == 0)
