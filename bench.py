@@ -309,6 +309,17 @@ def main():
         kernels[kind] = {"ms": ms, "alg_bytes": by,
                          "GBps": (by / (ms * 1e-3) / 1e9) if by else None,
                          "frac": (by / (ms * 1e-3) / 1e9 / peak) if by else None}
+    # time spent AT each AMG level of the V-cycle (T(from l) - T(from l+1); the last entry
+    # is the coarsest dense solve): pre/post sweeps, restriction and prolongation of level l
+    vlev = None
+    levels = st0["level_n"]
+    if ws == 1 and len(levels) > 1:
+        try:
+            tl = [s.time_kernel(16 + l, reps=args.kernel_reps)[0] for l in range(len(levels))]
+            vlev = [{"level": l, "rows": levels[l], "ms": (tl[l] - tl[l + 1]) if l + 1 < len(tl) else tl[l]}
+                    for l in range(len(levels))]
+        except Exception as e:            # noqa: BLE001
+            vlev = [{"error": str(e)}]
     # estimated share of one solve of each HBM-bound kernel (launch counts per solve);
     # the V-cycle (many latency-bound launches) is reported in `kernels`, not as a roofline
     cyc = math.ceil(iters / RESTART)
@@ -353,7 +364,7 @@ def main():
                           "parallelism": (f"z-slab x{ws} (NCCL halo + allreduce, replicated coarse levels)"
                                           if ws > 1 else "single GPU"),
                           "wall_s_timed_region": wall},
-               "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
+               "roofline": roofline, "kernels": kernels, "vcycle_levels": vlev, "cpu_baseline": cpu,
                "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * N * 8,
                        "d2h_bytes_per_step": N * 8},
                "gpu_launches": launches, "clocks": clocks}

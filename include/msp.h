@@ -226,8 +226,11 @@ msp_status msp_set_stream(msp_handle* h, void* cuda_stream);
  * 3 a9 BILU(0) apply (all colors); 4 a10 CGS2 pass A (dot) over 16 basis vectors;
  * 5 a6 coarsest dense-inverse GEMV; 6 one whole MSP application; 7 one V-cycle B_P;
  * 8 BILU apply; 9 one whole Arnoldi step (j = 15); 10 the CGS2 of step 15 (55 vectors);
- * 11/12 Arnoldi step / CGS2 at j = 25 (bytes = 0 for kinds 6-9, 11, 12).  kind | 0x100: no L2 flush (warm caches).  Each piece is captured once
- * into a CUDA graph and replayed (as in the solve); the first replay is a warm-up.
+ * 11/12 Arnoldi step / CGS2 at j = 25; 13 a9 + SpMV; 14 MSP application + SpMV;
+ * 15 SpMV + orthogonalisation of step 15; 16 + l (0 <= l <= L, L = the number of
+ * smoothed AMG levels): the V-cycle from level l down (l = L: the coarsest solve alone), so
+ * the time spent AT level l is T(16 + l) - T(17 + l) (bytes = 0 for kinds 6-9, 11-15, >= 16).
+ * kind | 0x100: no L2 flush (warm caches).  Each piece is captured once into a CUDA graph and replayed (as in the solve); the first replay is a warm-up.
  * Scratch contents of the handle are overwritten. */
 msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,
                            double* bytes_per_launch);

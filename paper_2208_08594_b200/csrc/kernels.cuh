@@ -18,6 +18,9 @@ constexpr int kSell = 32;
 #define MSP_BILU_PREFETCH 1
 #endif
 constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
+#ifndef MSP_SELL_PFL
+#define MSP_SELL_PFL 8               // matrix entries per lane prefetched by the LPR > 1 (coarse) sweeps
+#endif
 #ifndef MSP_SELL_PF1
 #define MSP_SELL_PF1 6
 #endif
@@ -267,6 +270,70 @@ __global__ void __launch_bounds__(256) pcol_resid4_kernel(int n, const int* __re
   y[o] = g[o] - acc;
 }
 
+// a8, 4x4 blocks, ELL layout of the pressure columns: pe[(k*ld + row)*4 + j] = A[row, col k]
+// column 0 entry j, ce[k*ld + row] = that column, k < w (padding: zero block column, ce =
+// row).  One thread per row: the w column indices and 32-byte pressure columns are
+// immutable and loaded before the PDL wait (coalesced: a warp reads 1 KB of pe per k),
+// then w independent gathers of x_p, one 32-byte g load and one 32-byte y store.
+constexpr int kEllMax = 8;
+__global__ void __launch_bounds__(256) pcol_resid_ell4_kernel(int n, int ld, int w, const int* __restrict__ ce,
+                                                              const double* __restrict__ pe,
+                                                              const double* __restrict__ x,
+                                                              const double* __restrict__ g,
+                                                              double* __restrict__ y,
+                                                              const int* __restrict__ rows = nullptr) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < n;
+  const int row = live ? (rows ? ldg(rows + t) : t) : 0;
+  int c[kEllMax];
+  double2 lo[kEllMax], hi[kEllMax];
+#pragma unroll
+  for (int k = 0; k < kEllMax; ++k) {
+    if (live && k < w) {
+      const size_t o = (size_t)k * ld + row;
+      c[k] = ldg(ce + o);
+      const double2* q = reinterpret_cast<const double2*>(pe + o * 4);
+      lo[k] = ldstream2(q);
+      hi[k] = ldstream2(q + 1);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int k = 0; k < kEllMax; ++k) {
+    if (k < w) {
+      const double xc = ldg(x + c[k]);
+      a0 = fma(lo[k].x, xc, a0);
+      a1 = fma(lo[k].y, xc, a1);
+      a2 = fma(hi[k].x, xc, a2);
+      a3 = fma(hi[k].y, xc, a3);
+    }
+  }
+  const double2* gp = reinterpret_cast<const double2*>(g + (size_t)row * 4);
+  const double2 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+  double2* yp = reinterpret_cast<double2*>(y + (size_t)row * 4);
+  yp[0] = make_double2(g0.x - a0, g0.y - a1);
+  yp[1] = make_double2(g1.x - a2, g1.y - a3);
+}
+
+// ELL copy of the pressure columns (setup and msp_update): one thread per row.
+__global__ void pcol_ell_fill_kernel(int n, int w, const int* __restrict__ rp, const int* __restrict__ ci,
+                                     const double* __restrict__ pcol, int* __restrict__ ce, double* __restrict__ pe) {
+  PDL_ENTRY();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int e0 = rp[row], e1 = rp[row + 1];
+  for (int k = 0; k < w; ++k) {
+    const size_t o = (size_t)k * n + row;
+    const int e = e0 + k;
+    ce[o] = (e < e1) ? ci[e] : row;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pe[o * 4 + j] = (e < e1) ? pcol[(size_t)e * 4 + j] : 0.0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // a3: pressure restriction with decoupling weights (R4): rp_l0[dst[c]] = sum_k
 // W[c][k] * g[c*B+k]; dst maps internal cell positions to level-0 rows.
@@ -485,7 +552,7 @@ __global__ void __launch_bounds__(512) sell_row_kernel(int s_first, int s_end,
   const int o0 = ldg(slice_off + s), w = (ldg(slice_off + s + 1) - o0) / kSell;
   // prologue (overlaps the predecessor kernel): the first PF matrix entries of this
   // lane and the diagonal are immutable
-  constexpr int PF = (LPR == 1) ? MSP_SELL_PF1 : 4;
+  constexpr int PF = (LPR == 1) ? MSP_SELL_PF1 : MSP_SELL_PFL;
   int pc[PF];
   double pv[PF];
 #pragma unroll

@@ -86,6 +86,7 @@ struct DevLevel {
   double *b = nullptr, *x = nullptr, *r = nullptr;
   int64_t nnz_alloc = 0;
   int lpr = 1;                       // lanes per row (coarse levels)
+  int idx = 0;                       // AMG level index
   int uniform_w = 0;                 // > 0: every slice has this width (offsets arithmetic)
   int tail = 1 << 30;                // first color handled by the single-CTA tail kernel
   int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
@@ -153,6 +154,10 @@ struct msp_handle {
   double* ftmp = nullptr;            // msp_bilu_set_factors scratch
   // a9 per-slot metadata (bilu_meta.cuh; 4x4 blocks, single GPU)
   int4 *bm_f = nullptr, *bm_b = nullptr, *bm_cf = nullptr, *bm_cb = nullptr, *bm_sl = nullptr;
+  int a8_ell = 1;                    // MSP_A8_ELL=0: pcol_resid4_kernel on the BSR pressure columns
+  int32_t pell_w = 0;                // ELL width of the pressure columns (0: no ELL copy)
+  int32_t* pell_c = nullptr;
+  double* pell_v = nullptr;
   int bilu_meta = 1;                 // MSP_BILU_META=0: bilu_block_kernel (the distributed path's kernel)
   bool setup_on_gpu = true;          // NEXT-2: S1 + Galerkin on the GPU (MSP_HOST_SETUP=1: host)
   cusolverDnHandle_t cs = nullptr;   // coarsest inverse (created once, reused by rebuilds)
@@ -397,8 +402,17 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   L.nnz_alloc = slice_off[L.nslices];
   {
     const double avg = (double)rp[n] / std::max<int32_t>(n, 1);
-    L.lpr = (avg <= 8.0) ? 1 : (avg <= 20.0 ? 4 : 8);
+    // lanes per row: 1 for stencil-width rows; 2 when a color alone has enough rows to
+    // fill the GPU (C3 level 1: 35k rows per color, 88 -> 74 us per V-cycle vs 4 lanes);
+    // else 4 / 8 by the row width (latency-bound small levels)
+    const double rows_per_color = (double)n / std::max(ncolor, 1);
+    L.lpr = (avg <= 8.0) ? 1 : (rows_per_color >= 16384.0 ? 2 : (avg <= 20.0 ? 4 : 8));
     if (const char* e = std::getenv("MSP_LPR")) L.lpr = std::atoi(e);
+    {
+      char key[32];
+      std::snprintf(key, sizeof key, "MSP_LPR_L%d", L.idx);
+      if (const char* e = std::getenv(key)) L.lpr = std::atoi(e);
+    }
     int tail_rows = 0, t = ncolor;
     const int lim_env = std::getenv("MSP_TAIL_ROWS") ? std::atoi(std::getenv("MSP_TAIL_ROWS")) : 2048;
     const int lim_col = std::getenv("MSP_TAIL_COLOR") ? std::atoi(std::getenv("MSP_TAIL_COLOR")) : 1024;
@@ -818,6 +832,25 @@ std::unique_ptr<DBuf> gpu_bilu_global(msp_handle* h, const msp::BlockMat& A, con
   return F;
 }
 
+// a8, 4x4 blocks: ELL copy of the pressure columns (width = the longest row, <= kEllMax),
+// refreshed with the values (setup, msp_update)
+void fill_pell(msp_handle* h) {
+  if (!h->pell_w) return;
+  klaunch(h->s, false, pcol_ell_fill_kernel, nblk(h->n, 256), 256, (int)h->n, (int)h->pell_w, (const int*)h->rp,
+          (const int*)h->ci, (const double*)h->Pcol, h->pell_c, h->pell_v);
+}
+void setup_pell(msp_handle* h, const std::vector<int32_t>& rp) {
+  h->pell_w = 0;
+  if (h->b != 4 || !h->a8_ell || h->n == 0) return;
+  int w = 0;
+  for (size_t i = 0; i + 1 < rp.size(); ++i) w = std::max(w, rp[i + 1] - rp[i]);
+  if (w == 0 || w > kEllMax) return;
+  h->pell_w = w;
+  h->pell_c = h->dalloc<int32_t>((size_t)w * h->n);
+  h->pell_v = h->dalloc<double>((size_t)w * h->n * 4);
+  fill_pell(h);
+}
+
 void do_setup(msp_handle* h, const msp::BlockMat& A) {
   auto t0 = std::chrono::steady_clock::now();
   SetupTimer T;
@@ -931,6 +964,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->lv.resize(L);
   std::vector<std::vector<int32_t>> perms(L);
   for (int l = 0; l < L; ++l) {
+    h->lv[l].idx = l;
     if (l > 0 || !h->comm) upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
     else {
       // permutation of level 0 only (upload done by dist_localize)
@@ -1059,6 +1093,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
         throw std::pair<int, std::string>(MSP_ESINGULAR, "BILU: singular pivot block at cell " + std::to_string(S.order[bad]));
     }
   }
+  setup_pell(h, rp);
   T.mark("A/F/Pcol transpose+upload");
   if (h->prm.stages == 3) {
     const int nc = b - 1;
@@ -1464,6 +1499,7 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
     h->Aval = h->upload(lA);
     h->Pcol = h->upload(lPc);
   }
+  setup_pell(h, lrp);
   h->W = h->upload(lW);
   h->color_blk = lcolor_blk;
   h->blk_ptr = h->upload(lblk);
@@ -1617,6 +1653,11 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
 void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, double* y) {
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
+  if (mode == 2 && h->pell_w) {
+    klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(h->n, 256), 256, (int)h->n, (int)h->n, (int)h->pell_w,
+            (const int*)h->pell_c, (const double*)h->pell_v, x, g, y, (const int*)nullptr);
+    return;
+  }
   if (mode == 2 && h->b == 4) {
     klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)h->n * 4, 256), 256, h->n, h->rp, h->ci, val, x, g, y,
             (const int*)nullptr);
@@ -1641,7 +1682,10 @@ void spmv_overlapped(msp_handle* h, int mode, double* x, int width, const double
   auto part = [&](const int32_t* rows, int nr) {
     if (nr <= 0) return;
     ++h->nlaunch;
-    if (mode == 2)
+    if (mode == 2 && h->pell_w)
+      klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(nr, 256), 256, nr, (int)h->n, (int)h->pell_w,
+              (const int*)h->pell_c, (const double*)h->pell_v, (const double*)x, g, y, (const int*)rows);
+    else if (mode == 2)
       klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)nr * 4, 256), 256, nr, (const int*)h->rp,
               (const int*)h->ci, (const double*)h->Pcol, (const double*)x, g, y, (const int*)rows);
     else
@@ -2626,6 +2670,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_SELL_TPB")) h->sell_tpb = std::atoi(e);
   if (const char* e = std::getenv("MSP_HOST_SETUP")) h->setup_on_gpu = std::atoi(e) == 0;
   if (const char* e = std::getenv("MSP_BILU_META")) h->bilu_meta = std::atoi(e);
+  if (const char* e = std::getenv("MSP_A8_ELL")) h->a8_ell = std::atoi(e);
   if (const char* e = std::getenv("MSP_CYCLE_GRAPH")) h->cycle_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
@@ -2726,6 +2771,7 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
       CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     }
+    fill_pell(h);
     ++h->nlaunch;
     CK(cudaStreamSynchronize(h->s));
     h->st.reuse_calls++;
@@ -3123,6 +3169,12 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         bytes = 0.0;
         break;
       default:
+        if (kind >= 16 && kind <= 16 + (int)h->lv.size()) {   // V-cycle from level kind-16 down
+          const int l = kind - 16;
+          fn = [h, l]() { vcycle(h, l); };
+          bytes = 0.0;
+          break;
+        }
         throw std::pair<int, std::string>(MSP_EINVAL, "msp_time_kernel: unknown kind");
     }
     // replay the piece as a CUDA graph, exactly as inside the Arnoldi-step graphs

@@ -109,6 +109,26 @@ def test_a8_pcol_residual(name, gkw, kw):
     check(out.cpu().numpy(), ref, bound, normwise=False)
 
 
+@pytest.mark.parametrize("ell", ["1", "0"])
+def test_a8_both_layouts(monkeypatch, ell):
+    """a8 through the ELL copy of the pressure columns (default for 4x4 blocks, rows of
+    <= 8 blocks) and through the BSR layout (MSP_A8_ELL=0; the kernel rows wider than 8
+    blocks use): same componentwise bound against the oracle's Alg. 1 line 5."""
+    monkeypatch.setenv("MSP_A8_ELL", ell)
+    p = gen.make_config("C3", nx=21, ny=44, nz=9)
+    s = solver(p, coarsest_max_dof=100)
+    n, b = p["n"], p["b"]
+    g = gen.random_vector(n * b, 14)
+    xp = gen.random_vector(n, 15)
+    w = np.zeros(n * b)
+    w[0::b] = xp
+    ref = g - oracle.bsr_spmv(p["row_ptr"], p["col"], p["val"], w)
+    out = torch.zeros(n * b, dtype=torch.float64, device="cuda")
+    s.pcol_residual(dev(g), dev(xp), out)
+    bound = np.abs(g) + oracle.bsr_spmv(p["row_ptr"], p["col"], np.abs(p["val"]), np.abs(w))
+    check(out.cpu().numpy(), ref, bound, normwise=False)
+
+
 # ------------------------------------------------------------------ a9 halves
 @pytest.mark.parametrize("name,gkw,kw", CASES)
 def test_a9_bilu_forward_and_backward(name, gkw, kw):
