@@ -66,7 +66,10 @@ typedef struct {
   int32_t device;
 } msp_bsr;
 
-/* Device allocation callback (e.g. the PyTorch caching allocator).  NULL = cudaMalloc. */
+/* Device allocation callback (e.g. the PyTorch caching allocator).  NULL = cudaMalloc.
+ * `stream` is the caller's stream (msp_setup / msp_set_stream): the library's own stream
+ * waits on it before using the memory, and the library synchronises its stream before
+ * every free, so a stream-keyed caching allocator may reuse blocks across handles. */
 typedef void* (*msp_alloc_fn)(size_t bytes, void* stream, void* ctx);
 typedef void (*msp_free_fn)(void* ptr, void* ctx);
 

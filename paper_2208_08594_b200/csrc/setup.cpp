@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <numeric>
 #include <queue>
 #include <utility>
@@ -564,10 +565,22 @@ static SpMat graph_laplacian(const Graph& G) {
   return L;
 }
 
-static void make_ordering(HostSetup& S) {
+namespace {
+struct PhaseTimer {
+  bool on = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[msp setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
+static void make_ordering(HostSetup& S, PhaseTimer& T, const HostLevel* lv0, const Graph& G) {
   const BlockMat& A = *S.A;
   const int32_t n = A.n;
-  Graph G = block_graph(A, S.block_nz.empty() ? nullptr : &S.block_nz);
   std::vector<int32_t> blk(n), bcol;
   int32_t nb;
   if (S.prm.bilu_order == 0) {
@@ -576,7 +589,7 @@ static void make_ordering(HostSetup& S) {
     S.bilu_ncolor = color_groups(G, bcol);
   } else {
     if (off_diagonal_zero(S.App)) nb = aggregate_passes(graph_laplacian(G), S.prm.pair_passes, blk, nullptr);
-    else if (!S.lv.empty()) { blk = S.lv[0].agg; nb = S.lv[0].n_next; }
+    else if (lv0) { blk = lv0->agg; nb = lv0->n_next; }
     else nb = aggregate_passes(S.App, S.prm.pair_passes, blk, nullptr);
     std::vector<std::pair<int32_t, int32_t>> pr;
     for (int32_t c = 0; c < n; ++c)
@@ -585,7 +598,9 @@ static void make_ordering(HostSetup& S) {
         if (blk[c] != blk[d]) pr.push_back({blk[c], blk[d]});
       }
     Graph Q = graph_from_pairs(nb, pr);
+    T.mark("  ABMC: quotient graph");
     S.bilu_ncolor = color_groups(Q, bcol);
+    T.mark("  ABMC: block coloring");
   }
   S.level1_agg = blk;
   // counting sort by (color, block, cell): cells ascending within a block, blocks
@@ -615,18 +630,6 @@ static void make_ordering(HostSetup& S) {
   S.color_blk_ptr = ccount;
 }
 
-namespace {
-struct PhaseTimer {
-  bool on = std::getenv("MSP_SETUP_VERBOSE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[msp setup] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
-    t = n;
-  }
-};
-}  // namespace
 
 int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::string& err) {
   PhaseTimer T;
@@ -641,11 +644,31 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
     T.mark("A_PP");
   }
   S.lv.clear();
+  S.lv.reserve(prm.max_levels + 1);    // levels stay in place while their colorings run
   S.coarse_diag = false;
+  // The greedy steps are sequential by definition, but independent of one another once
+  // their input exists: the Alg. 2/3 coloring of level l needs only A_l, the ABMC order
+  // only level 0's aggregates and A's cell graph.  They run as host tasks concurrently
+  // with the NPAIR + Galerkin chain (same functions, same inputs: identical results).
+  std::vector<std::future<void>> jobs;
+  std::future<void> abmc;
+  // A's cell graph (the ABMC input besides level 0's aggregates) from the start
+  std::shared_future<Graph> cell_graph =
+      std::async(std::launch::async, [&S, &A]() { return block_graph(A, S.block_nz.empty() ? nullptr : &S.block_nz); })
+          .share();
+  // (level 0 is passed explicitly: the task never reads S.lv while the chain appends)
+  auto start_abmc = [&](const HostLevel* lv0) {
+    abmc = std::async(std::launch::async, [&S, lv0, cell_graph]() {
+      PhaseTimer Tq;
+      Tq.on = false;
+      make_ordering(S, Tq, lv0, cell_graph.get());
+    });
+  };
   SpMat cur = S.App;
+  int rc_loop = 0;
   for (int l = 0;; ++l) {
     if (cur.n <= prm.coarsest_max_dof) break;
-    if (l + 1 >= prm.max_levels) { err = "AMG: max_levels reached above coarsest_max_dof"; return 5; }
+    if (l + 1 >= prm.max_levels) { err = "AMG: max_levels reached above coarsest_max_dof"; rc_loop = 5; break; }
     HostLevel L;
     SpMat nxt;
     const int32_t nn = aggregate_passes(cur, prm.pair_passes, L.agg, &nxt, &prm.rap);
@@ -653,15 +676,23 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
     if ((double)nn > 0.9 * (double)cur.n) {
       if (off_diagonal_zero(cur)) { S.coarse_diag = true; break; }
       err = "AMG: coarsening stalled at level " + std::to_string(l);
-      return 5;
+      rc_loop = 5;
+      break;
     }
-    L.ncolor = color_groups(value_graph(cur), L.color);
-    T.mark("coloring level");
     L.n_next = nn;
     L.A = std::move(cur);
     S.lv.push_back(std::move(L));
+    HostLevel* Lp = &S.lv.back();
+    jobs.push_back(std::async(std::launch::async, [Lp]() { Lp->ncolor = color_groups(value_graph(Lp->A), Lp->color); }));
+    if (l == 0) start_abmc(Lp);
     cur = std::move(nxt);
   }
+  for (auto& j : jobs) j.get();
+  if (rc_loop) {
+    if (abmc.valid()) abmc.get();
+    return rc_loop;
+  }
+  T.mark("colorings (concurrent)");
   S.Ac = std::move(cur);
   for (int32_t i = 0; i < S.Ac.n; ++i) {
     bool has = false;
@@ -679,8 +710,9 @@ int run_host_setup(const BlockMat& A, const Params& prm, HostSetup& S, std::stri
     }
   }
   T.mark("checks");
-  make_ordering(S);
-  T.mark("ABMC ordering");
+  if (!abmc.valid()) start_abmc(S.lv.empty() ? nullptr : &S.lv[0]);
+  abmc.get();
+  T.mark("ABMC ordering (concurrent)");
   return 0;
 }
 

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <functional>
 #include <memory>
 #include <numeric>
@@ -195,7 +197,10 @@ struct msp_handle {
     size_t bytes_ = std::max<size_t>(count, 1) * sizeof(T);
     void* p = nullptr;
     if (cfg.alloc) {
-      p = cfg.alloc(bytes_, (void*)s, cfg.alloc_ctx);
+      // the caller's stream: the library's stream waits on it before touching the memory
+      // and is synchronised before every free, so a caching allocator may hand the
+      // blocks of a closed handle to the next one (keyed by the long-lived caller stream)
+      p = cfg.alloc(bytes_, (void*)caller, cfg.alloc_ctx);
       if (!p) throw CudaError{cudaErrorMemoryAllocation, "alloc callback"};
     } else {
       CK(cudaMalloc(&p, bytes_));
@@ -361,6 +366,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   std::vector<int32_t> sw(L.nslices, 0);
   int32_t wmax = 0;
   int64_t tot = 0;
+#pragma omp parallel for schedule(static) reduction(max : wmax) reduction(+ : tot)
   for (int32_t s = 0; s < L.nslices; ++s) {
     int32_t r1 = std::min(slice_row[s] + kSell, slice_row[s + 1]);
     int32_t w = 0;
@@ -379,6 +385,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   L.uniform_w = uniform ? wmax : 0;
   std::vector<int32_t> col(std::max<int32_t>(slice_off[L.nslices], 1));
   std::vector<double> val(col.size(), 0.0), diag(n, 0.0);
+#pragma omp parallel for schedule(static)
   for (int32_t s = 0; s < L.nslices; ++s) {
     const int32_t w = (slice_off[s + 1] - slice_off[s]) / kSell;
     for (int32_t l = 0; l < kSell; ++l) {
@@ -426,6 +433,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   }
   {
     std::vector<int32_t> rs(n), rw(n);
+#pragma omp parallel for schedule(static)
     for (int32_t s = 0; s < L.nslices; ++s)
       for (int32_t p = slice_row[s]; p < slice_row[s + 1]; ++p) {
         rs[p] = slice_off[s] + (p - slice_row[s]);
@@ -532,10 +540,43 @@ std::vector<int4> make_islot(int32_t n, const std::vector<int32_t>& rp, const st
 }
 
 // Device scratch for the GPU SETUP steps (freed on scope exit, stream-ordered).
+// SETUP temporaries come from a library-private stream-ordered pool that keeps its memory
+// across the synchronisations of one SETUP (release threshold = max; the default pool
+// returns freed memory at every sync, and re-mapping GBs per Galerkin product cost up to
+// 0.5 s); trimmed to zero when the SETUP ends (setup_pool_trim).
+cudaMemPool_t setup_pool() {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  CK(cudaMemPoolCreate(&pool, &props));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  pools[dev] = pool;
+  return pool;
+}
+void setup_pool_trim(cudaStream_t s) {
+  static const bool trim = !std::getenv("MSP_SETUP_POOL_TRIM") || std::atoi(std::getenv("MSP_SETUP_POOL_TRIM")) != 0;
+  if (!trim) return;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemPoolTrimTo(setup_pool(), 0));
+}
+
 struct DBuf {
   void* p = nullptr;
   cudaStream_t s;
-  DBuf(size_t bytes, cudaStream_t st) : s(st) { CK(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s)); }
+  DBuf(size_t bytes, cudaStream_t st) : s(st) {
+    CK(cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 16), setup_pool(), s));
+  }
   ~DBuf() { cudaFreeAsync(p, s); }
   template <class T> T* as() const { return static_cast<T*>(p); }
   DBuf(const DBuf&) = delete;
@@ -1055,6 +1096,10 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     h->Fval = h->dalloc<double>(nv);
     h->Aval = h->dalloc<double>(nv);
     h->Pcol = h->dalloc<double>(ci.size() * (size_t)b);
+    if (T.on) {
+      CK(cudaStreamSynchronize(h->s));
+      T.mark("  A/F buffers allocated");
+    }
     if (dAvals) CK(cudaMemcpyAsync(h->stage, dAvals->p, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
     else CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
     int* dbad = nullptr;
@@ -1086,6 +1131,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
 #undef CASE
     }
     CK(cudaStreamSynchronize(h->s));
+    T.mark("  values + BILU factors (GPU)");
     if (gpu_bilu) {
       int bad = -1;
       CK(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1231,6 +1277,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
     if (s2 != CUSOLVER_STATUS_SUCCESS) throw CudaError{cudaErrorUnknown, "cusolverDnDgetrs"};
   }
   T.mark("coarsest inverse");
+  setup_pool_trim(h->s);
+  T.mark("setup pool trim");
   // work vectors (cell-space vectors read through ghost columns carry ghost slots)
   const size_t Ng = (size_t)(h->n + h->n_ghost) * h->b;
   h->z = h->dalloc<double>(Ng);
