@@ -108,6 +108,14 @@ typedef struct {
                                 ranks removed before the factorization (block Jacobi across the
                                 slabs; no exchange in the substitutions; the preconditioner then
                                 depends on the partition).  Single-GPU handles: must be 0. */
+  int32_t dist_levels;       /* distributed handles (NEXT-3): AMG levels 1..dist_levels are
+                                partitioned like level 0 (a level-l row lives on the owner of
+                                its lowest-index member; general ghost lists per level, a halo
+                                per color in the sweeps, member / parent halos for the
+                                restriction / prolongation) and only the levels below run
+                                replicated (or on rank 0, coarse_mode 1).  0 (default): levels
+                                >= 1 replicated; clamped to the number of smoothed levels - 1.
+                                Bit-identical iterates for every value.  Single-GPU: ignored. */
 } msp_config;
 
 typedef struct msp_handle msp_handle;

@@ -36,7 +36,8 @@ class Config(ctypes.Structure):
                 ("use_coop", ctypes.c_int32), ("smoother", ctypes.c_int32),
                 ("gs_chunk", ctypes.c_int32),
                 ("alloc", ALLOC_FN), ("free_fn", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
-                ("coarse_mode", ctypes.c_int32), ("bilu_local", ctypes.c_int32)]
+                ("coarse_mode", ctypes.c_int32), ("bilu_local", ctypes.c_int32),
+                ("dist_levels", ctypes.c_int32)]
 
     @classmethod
     def make(cls, **kw):

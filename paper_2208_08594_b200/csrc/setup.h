@@ -36,7 +36,8 @@ using RapFn = std::function<int(const SpMat& A, const std::vector<int32_t>& agg,
 struct Params {
   int32_t coarsest_max_dof = 10000, max_levels = 20, pre_sweeps = 1, post_sweeps = 1,
           pair_passes = 2, decoupling = 2, bilu_order = 1, stages = 2, orth = 0, use_graphs = 1,
-          use_coop = 1, smoother = 0, gs_chunk = 32, coarse_mode = 0, bilu_local = 0;
+          use_coop = 1, smoother = 0, gs_chunk = 32, coarse_mode = 0, bilu_local = 0,
+          dist_levels = 0;
   RapFn rap;                           // optional: S3 Galerkin products of the hierarchy
   bool s1_given = false;               // S.W and S.App already computed (GPU S1)
 };

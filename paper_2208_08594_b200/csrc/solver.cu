@@ -92,6 +92,12 @@ struct DevLevel {
   int uniform_w = 0;                 // > 0: every slice has this width (offsets arithmetic)
   int tail = 1 << 30;                // first color handled by the single-CTA tail kernel
   int32_t *d_color_row = nullptr, *d_color_slice = nullptr, *row_start = nullptr, *row_width = nullptr;
+  // distributed level (dist_levels, NEXT-3): ghosts of x after the owned rows -- matrix
+  // ghosts (per-color halo xh) then parent ghosts (next-level rows the prolongation into
+  // the level above reads, halo ph); ghosts of r after the owned rows: members of owned
+  // next-level aggregates (halo mh, before the restriction)
+  int32_t ngx = 0, ngp = 0, ngm = 0;
+  msp::HaloPlan xh, ph, mh;
 };
 
 }  // namespace
@@ -181,7 +187,8 @@ struct msp_handle {
   int n_ghost = 0, n0_ghost = 0;     // cell-space / level-0 ghosts
   msp::HaloPlan cell_halo;           // segments = BILU block colors
   msp::HaloPlan l0_halo;             // segments = level-0 PGS-MC colors
-  int n_own_l1 = 0, l1_cmax = 0;     // owned level-1 rows (aggregates), max over ranks
+  int dist_D = 0;                    // levels 0..dist_D partitioned (msp_config.dist_levels, clamped)
+  int n_own_l1 = 0, l1_cmax = 0;     // owned rows of level dist_D+1 (replicated part), max over ranks
   int32_t *own_l1_pt = nullptr, *own_l1_idx = nullptr, *l1_scatter = nullptr;
   double *l1_send = nullptr, *l1_recv = nullptr, *lred = nullptr;
   std::vector<int32_t> owned_cells;  // natural ids of the owned cells, ascending
@@ -261,6 +268,7 @@ msp::Params params_of(const msp_config* c) {
   p.gs_chunk = c->gs_chunk;
   p.coarse_mode = c->coarse_mode;
   p.bilu_local = c->bilu_local;
+  p.dist_levels = c->dist_levels;
   return p;
 }
 
@@ -345,9 +353,19 @@ msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err
 // Build a SELL-32 device level from CSR rows that are already in their final (color-
 // major) order; color[i] non-decreasing.  Columns may reference ghost rows >= n (their
 // x values are received by halo exchanges); x is sized n_total = n + ghosts.
+// lanes per row: 1 for stencil-width rows; 2 when a color alone has enough rows to fill
+// the GPU (C3 level 1: 35k rows per color, 88 -> 74 us per V-cycle vs 4 lanes); else 4 / 8
+// by the row width (latency-bound small levels).  Distributed levels take the choice of
+// the whole level (same per-row summation grouping as one GPU).
+int choose_lpr(int64_t nnz, int32_t n, int32_t ncolor) {
+  const double avg = (double)nnz / std::max<int32_t>(n, 1);
+  const double rows_per_color = (double)n / std::max(ncolor, 1);
+  return (avg <= 8.0) ? 1 : (rows_per_color >= 16384.0 ? 2 : (avg <= 20.0 ? 4 : 8));
+}
+
 void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, const std::vector<int32_t>& rp,
                        const std::vector<int32_t>& ci, const std::vector<double>& v, int32_t ncolor,
-                       const std::vector<int32_t>& color) {
+                       const std::vector<int32_t>& color, int lpr_force = 0, int32_t n_r = -1) {
   L.n = n;
   L.ncolor = ncolor;
   std::vector<int32_t> cnt(ncolor + 1, 0);
@@ -408,12 +426,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   }
   L.nnz_alloc = slice_off[L.nslices];
   {
-    const double avg = (double)rp[n] / std::max<int32_t>(n, 1);
-    // lanes per row: 1 for stencil-width rows; 2 when a color alone has enough rows to
-    // fill the GPU (C3 level 1: 35k rows per color, 88 -> 74 us per V-cycle vs 4 lanes);
-    // else 4 / 8 by the row width (latency-bound small levels)
-    const double rows_per_color = (double)n / std::max(ncolor, 1);
-    L.lpr = (avg <= 8.0) ? 1 : (rows_per_color >= 16384.0 ? 2 : (avg <= 20.0 ? 4 : 8));
+    L.lpr = lpr_force > 0 ? lpr_force : choose_lpr(rp[n], n, ncolor);
     if (const char* e = std::getenv("MSP_LPR")) L.lpr = std::atoi(e);
     {
       char key[32];
@@ -453,7 +466,7 @@ void upload_level_rows(msp_handle* h, DevLevel& L, int32_t n, int32_t n_total, c
   L.diag = h->upload(diag);
   L.b = h->dalloc<double>(n);
   L.x = h->dalloc<double>(n_total);
-  L.r = h->dalloc<double>(n);
+  L.r = h->dalloc<double>(n_r >= 0 ? n_r : n);
 }
 
 // Build a SELL-32 device level from a natural-order CSR + coloring (rows permuted by
@@ -1004,17 +1017,19 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->level_colors.clear();
   h->lv.resize(L);
   std::vector<std::vector<int32_t>> perms(L);
+  h->dist_D = h->comm ? std::max(0, std::min(h->prm.dist_levels, L - 1)) : 0;
   for (int l = 0; l < L; ++l) {
     h->lv[l].idx = l;
-    if (l > 0 || !h->comm) upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
+    if (!h->comm || l > h->dist_D) upload_level(h, h->lv[l], S.lv[l].A, S.lv[l].ncolor, S.lv[l].color, perms[l]);
     else {
-      // permutation of level 0 only (upload done by dist_localize)
-      const auto& col = S.lv[0].color;
-      std::vector<int32_t> cnt(S.lv[0].ncolor + 1, 0);
+      // permutation only (the partitioned levels are uploaded by dist_localize)
+      const auto& col = S.lv[l].color;
+      const int32_t nl = S.lv[l].A.n;
+      std::vector<int32_t> cnt(S.lv[l].ncolor + 1, 0);
       for (int32_t c : col) cnt[c + 1]++;
-      for (int c = 0; c < S.lv[0].ncolor; ++c) cnt[c + 1] += cnt[c];
-      perms[0].resize(n);
-      for (int32_t i = 0; i < n; ++i) perms[0][i] = cnt[col[i]]++;
+      for (int c = 0; c < S.lv[l].ncolor; ++c) cnt[c + 1] += cnt[c];
+      perms[l].resize(nl);
+      for (int32_t i = 0; i < nl; ++i) perms[l][i] = cnt[col[i]]++;
     }
     h->level_n.push_back(S.lv[l].A.n);
     h->level_nnz.push_back(S.lv[l].A.nnz());
@@ -1025,7 +1040,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->level_n.push_back(S.Ac.n);
   h->level_nnz.push_back(S.Ac.nnz());
   h->level_colors.push_back(0);
-  for (int l = (h->comm ? 1 : 0); l < L; ++l) {
+  for (int l = (h->comm ? h->dist_D + 1 : 0); l < L; ++l) {   // replicated levels
     DevLevel& D = h->lv[l];
     const auto& agg = S.lv[l].agg;
     const int32_t nn = S.lv[l].n_next;
@@ -1623,44 +1638,198 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
     upload_level_rows(h, h->lv[0], no0, no0 + ng0, r0, c0v, v0, g0, rc0);
     h->n0_ghost = ng0;
   }
-  // level-0 -> level-1 (replicated) aggregate map and this rank's owned aggregates
+  // ---------------- levels 1..D partitioned (dist_levels, NEXT-3) and the hand-over to the
+  // replicated part (levels > D and the coarsest; ROOT: rank 0 only)
   {
-    const auto& agg0 = S.lv[0].agg;
-    auto l1row = [&](int32_t I) { return (L > 1) ? perms[1][I] : I; };
-    std::vector<int32_t> ap(no0);
-    for (int32_t k = 0; k < no0; ++k) ap[k] = l1row(agg0[rows0[k]]);
-    h->lv[0].agg = h->upload(ap);
-    const int32_t n1 = S.lv[0].n_next;
-    std::vector<int32_t> aown(n1, -1);
-    for (int32_t c = 0; c < n; ++c) aown[agg0[c]] = own_cell[c];     // whole aggregates per rank
-    std::vector<std::vector<int32_t>> ownl1(P);
-    for (int32_t I = 0; I < n1; ++I) ownl1[aown[I]].push_back(I);
-    for (int q = 0; q < P; ++q)
-      std::sort(ownl1[q].begin(), ownl1[q].end(), [&](int32_t x, int32_t y) { return l1row(x) < l1row(y); });
-    int cmax = 1;
-    for (int q = 0; q < P; ++q) cmax = std::max(cmax, (int)ownl1[q].size());
-    std::vector<int32_t> scat((size_t)P * cmax, -1);
-    for (int q = 0; q < P; ++q)
-      for (size_t k = 0; k < ownl1[q].size(); ++k) scat[(size_t)q * cmax + k] = l1row(ownl1[q][k]);
-    // member lists of my aggregates (local level-0 rows)
-    std::vector<int32_t> slot(n1, -1);
-    for (size_t k = 0; k < ownl1[me].size(); ++k) slot[ownl1[me][k]] = (int32_t)k;
-    const int32_t nm = (int32_t)ownl1[me].size();
-    std::vector<int32_t> pp(nm + 1, 0), pi(no0);
-    for (int32_t k = 0; k < no0; ++k) pp[slot[agg0[rows0[k]]] + 1]++;
-    for (int32_t k = 0; k < nm; ++k) pp[k + 1] += pp[k];
-    {
-      std::vector<int32_t> f(pp.begin(), pp.end() - 1);
-      for (int32_t k = 0; k < no0; ++k) pi[f[slot[agg0[rows0[k]]]]++] = k;
+    const int D = h->dist_D;
+    // owner of every row of levels 0..D+1: a level-(l+1) row (aggregate of level-l rows)
+    // lives on the owner of its lowest-index member (level 1: whole aggregates per rank)
+    std::vector<std::vector<int32_t>> own(D + 2);
+    own[0] = own_cell;
+    for (int l = 0; l <= D; ++l) {
+      const auto& agg = S.lv[l].agg;
+      own[l + 1].assign(S.lv[l].n_next, -1);
+      for (int32_t i = S.lv[l].A.n - 1; i >= 0; --i) own[l + 1][agg[i]] = own[l][i];
     }
-    h->n_own_l1 = nm;
-    h->l1_cmax = cmax;
-    h->own_l1_pt = h->upload(pp);
-    h->own_l1_idx = h->upload(pi);
-    h->l1_scatter = h->upload(scat);
-    h->l1_send = h->dalloc<double>(cmax);
-    h->l1_recv = h->dalloc<double>((size_t)P * cmax);
-    CK(cudaMemsetAsync(h->l1_send, 0, sizeof(double) * cmax, h->s));
+    // global row index of level l (the single-GPU color-major order; coarsest: natural)
+    auto rowidx = [&](int l, int32_t i) { return (l < L) ? perms[l][i] : i; };
+    struct LocLev {
+      std::vector<int32_t> rows;             // owned rows (natural), global row order
+      std::vector<int32_t> xloc, ploc, rloc; // natural -> local x (owned | matrix ghost),
+                                             // x (owned | parent ghost), r (owned | member ghost)
+      int32_t no = 0;
+    };
+    std::vector<LocLev> LL(D + 1);
+    LL[0].rows = rows0;
+    LL[0].no = no0;
+    LL[0].rloc.assign(n, -1);
+    for (int32_t k = 0; k < no0; ++k) LL[0].rloc[rows0[k]] = k;
+    for (int l = 1; l <= D; ++l) {
+      const msp::SpMat& Al = S.lv[l].A;
+      const auto& col = S.lv[l].color;
+      const int g = S.lv[l].ncolor;
+      const int32_t nl = Al.n;
+      const auto& ow = own[l];
+      const auto& pl = perms[l];
+      auto by_row = [&](int32_t x, int32_t y) { return pl[x] < pl[y]; };
+      auto by_owner_row = [&](int32_t x, int32_t y) { return ow[x] != ow[y] ? ow[x] < ow[y] : pl[x] < pl[y]; };
+      LocLev& Q = LL[l];
+      for (int32_t i = 0; i < nl; ++i) if (ow[i] == me) Q.rows.push_back(i);
+      std::sort(Q.rows.begin(), Q.rows.end(), by_row);
+      Q.no = (int32_t)Q.rows.size();
+      std::vector<int32_t> lo(nl, -1);
+      for (int32_t k = 0; k < Q.no; ++k) lo[Q.rows[k]] = k;
+      // matrix ghosts (read by the sweeps and the residual) and the x send lists
+      std::vector<std::vector<int32_t>> needx(P), needp(P), needm(P);
+      std::vector<int32_t> gx, gp, gm;
+      {
+        std::vector<uint8_t> mk(nl, 0);
+        for (int32_t i = 0; i < nl; ++i) {
+          const int t = ow[i];
+          for (int32_t e = Al.rp[i]; e < Al.rp[i + 1]; ++e) {
+            const int32_t d = Al.ci[e];
+            const int o = ow[d];
+            if (o == t) continue;
+            if (o == me) needx[t].push_back(d);
+            if (t == me && !mk[d]) { mk[d] = 1; gx.push_back(d); }
+          }
+        }
+      }
+      // parent ghosts: level-l rows my level-(l-1) rows prolongate from, owned elsewhere
+      {
+        const auto& aggp = S.lv[l - 1].agg;
+        const auto& owp = own[l - 1];
+        std::vector<uint8_t> mk(nl, 0);
+        for (int32_t i = 0; i < S.lv[l - 1].A.n; ++i) {
+          const int32_t I = aggp[i];
+          const int t = owp[i], o = ow[I];
+          if (o == t) continue;
+          if (o == me) needp[t].push_back(I);
+          if (t == me && !mk[I]) { mk[I] = 1; gp.push_back(I); }
+        }
+      }
+      // member ghosts: rows of aggregates (level l+1) I own, owned elsewhere
+      {
+        const auto& aggn = S.lv[l].agg;
+        const auto& own_n = own[l + 1];
+        for (int32_t i = 0; i < nl; ++i) {
+          const int t = own_n[aggn[i]], o = ow[i];
+          if (o == t) continue;
+          if (o == me) needm[t].push_back(i);
+          if (t == me) gm.push_back(i);
+        }
+      }
+      for (int q = 0; q < P; ++q)
+        for (auto* v : {&needx[q], &needp[q], &needm[q]}) {
+          std::sort(v->begin(), v->end(), by_row);
+          v->erase(std::unique(v->begin(), v->end()), v->end());
+        }
+      std::sort(gx.begin(), gx.end(), by_owner_row);      // peer-major, color-major inside a peer
+      std::sort(gp.begin(), gp.end(), by_owner_row);
+      std::sort(gm.begin(), gm.end(), by_owner_row);
+      const int32_t ngx = (int32_t)gx.size(), ngp = (int32_t)gp.size(), ngm = (int32_t)gm.size();
+      Q.xloc = lo;
+      Q.ploc = lo;
+      Q.rloc = lo;
+      for (int32_t k = 0; k < ngx; ++k) Q.xloc[gx[k]] = Q.no + k;
+      for (int32_t k = 0; k < ngp; ++k) Q.ploc[gp[k]] = Q.no + ngx + k;
+      for (int32_t k = 0; k < ngm; ++k) Q.rloc[gm[k]] = Q.no + k;
+      // local rows (entries in the row's natural column order, as upload_level)
+      std::vector<int32_t> r(Q.no + 1, 0), c, rc(Q.no);
+      std::vector<double> v;
+      for (int32_t k = 0; k < Q.no; ++k) {
+        const int32_t i = Q.rows[k];
+        for (int32_t e = Al.rp[i]; e < Al.rp[i + 1]; ++e) { c.push_back(Q.xloc[Al.ci[e]]); v.push_back(Al.v[e]); }
+        r[k + 1] = (int32_t)c.size();
+        rc[k] = col[i];
+      }
+      DevLevel& DL = h->lv[l];
+      upload_level_rows(h, DL, Q.no, Q.no + ngx + ngp, r, c, v, g, rc, choose_lpr(Al.nnz(), nl, g), Q.no + ngm);
+      DL.ngx = ngx;
+      DL.ngp = ngp;
+      DL.ngm = ngm;
+      {
+        std::vector<std::vector<std::vector<int32_t>>> sendl(P, std::vector<std::vector<int32_t>>(g));
+        std::vector<std::vector<int32_t>> rcnt(P, std::vector<int32_t>(g, 0));
+        for (int q = 0; q < P; ++q)
+          for (int32_t d : needx[q]) sendl[q][col[d]].push_back(lo[d]);
+        for (int32_t d : gx) rcnt[ow[d]][col[d]]++;
+        build_halo(h, DL.xh, g, P, me, sendl, rcnt);
+      }
+      auto one_seg = [&](msp::HaloPlan& plan, const std::vector<std::vector<int32_t>>& need,
+                         const std::vector<int32_t>& ghosts) {
+        std::vector<std::vector<std::vector<int32_t>>> sendl(P, std::vector<std::vector<int32_t>>(1));
+        std::vector<std::vector<int32_t>> rcnt(P, std::vector<int32_t>(1, 0));
+        for (int q = 0; q < P; ++q)
+          for (int32_t d : need[q]) sendl[q][0].push_back(lo[d]);
+        for (int32_t d : ghosts) rcnt[ow[d]][0]++;
+        build_halo(h, plan, 1, P, me, sendl, rcnt);
+      };
+      one_seg(DL.ph, needp, gp);
+      one_seg(DL.mh, needm, gm);
+    }
+    // restriction lists (level l -> l+1, members in the single-GPU summation order:
+    // ascending global level-l row) and prolongation maps of every partitioned level
+    for (int l = 0; l <= D; ++l) {
+      const auto& agg = S.lv[l].agg;
+      const int32_t nl = S.lv[l].A.n, nn = S.lv[l].n_next;
+      const bool next_dist = l + 1 <= D;
+      std::vector<std::vector<int32_t>> owned_next(P);   // every rank's owned level-(l+1) rows, target order
+      if (next_dist) owned_next[me] = LL[l + 1].rows;
+      else {
+        for (int32_t I = 0; I < nn; ++I) owned_next[own[l + 1][I]].push_back(I);
+        for (int q = 0; q < P; ++q)
+          std::sort(owned_next[q].begin(), owned_next[q].end(),
+                    [&](int32_t x, int32_t y) { return rowidx(l + 1, x) < rowidx(l + 1, y); });
+      }
+      const std::vector<int32_t>& tgt = owned_next[me];
+      const int32_t nt = (int32_t)tgt.size();
+      std::vector<int32_t> slot(nn, -1);
+      for (int32_t k = 0; k < nt; ++k) slot[tgt[k]] = k;
+      std::vector<int32_t> inv(nl);
+      for (int32_t i = 0; i < nl; ++i) inv[perms[l][i]] = i;
+      std::vector<int32_t> pp(nt + 1, 0), pi;
+      for (int32_t i = 0; i < nl; ++i) if (slot[agg[i]] >= 0) pp[slot[agg[i]] + 1]++;
+      for (int32_t k = 0; k < nt; ++k) pp[k + 1] += pp[k];
+      pi.assign(pp[nt], -1);
+      {
+        std::vector<int32_t> f(pp.begin(), pp.end() - 1);
+        for (int32_t p = 0; p < nl; ++p) {                 // ascending global level-l row
+          const int32_t i = inv[p];
+          const int32_t k = slot[agg[i]];
+          if (k < 0) continue;
+          const int32_t li = LL[l].rloc[i];
+          check_index(li >= 0, "restriction member without a local slot");
+          pi[f[k]++] = li;
+        }
+      }
+      // prolongation map of my level-l rows
+      std::vector<int32_t> ap(LL[l].no);
+      for (int32_t k = 0; k < LL[l].no; ++k) {
+        const int32_t I = agg[LL[l].rows[k]];
+        ap[k] = next_dist ? LL[l + 1].ploc[I] : rowidx(l + 1, I);
+        check_index(ap[k] >= 0, "prolongation source without a local slot");
+      }
+      h->lv[l].agg = h->upload(ap);
+      if (next_dist) {
+        h->lv[l].pt_ptr = h->upload(pp);
+        h->lv[l].pt_idx = h->upload(pi);
+      } else {                                             // hand-over to the replicated part
+        int cmax = 1;
+        for (int q = 0; q < P; ++q) cmax = std::max(cmax, (int)owned_next[q].size());
+        std::vector<int32_t> scat((size_t)P * cmax, -1);
+        for (int q = 0; q < P; ++q)
+          for (size_t k = 0; k < owned_next[q].size(); ++k) scat[(size_t)q * cmax + k] = rowidx(l + 1, owned_next[q][k]);
+        h->n_own_l1 = nt;
+        h->l1_cmax = cmax;
+        h->own_l1_pt = h->upload(pp);
+        h->own_l1_idx = h->upload(pi);
+        h->l1_scatter = h->upload(scat);
+        h->l1_send = h->dalloc<double>(cmax);
+        h->l1_recv = h->dalloc<double>((size_t)P * cmax);
+        CK(cudaMemsetAsync(h->l1_send, 0, sizeof(double) * cmax, h->s));
+      }
+    }
   }
   // cell <-> level-0 maps of the owned cells
   {
@@ -2054,9 +2223,88 @@ void msp_apply_npr(msp_handle* h, const double* g, double* z);
 // Distributed MSP (stages P, R): level 0 of the V-cycle is rank-local with halo
 // exchanges after every color; levels >= 1 and the coarsest are replicated (allgather
 // of the owned aggregates' right-hand side).
+// Hand-over from the last partitioned level l (= dist_D) to the replicated part: the
+// level-(l+1) right-hand side of every rank's owned aggregates (member ghosts of r
+// already exchanged), allgathered and scattered with the fused first color; levels > l
+// and the coarsest run on every rank (ROOT: rank 0, then a broadcast of the correction).
+// Returns x_{l+1} (replicated numbering).
+double* dist_handover(msp_handle* h, int l) {
+  DevLevel& Lv = h->lv[l];
+  const int L = (int)h->lv.size();
+  if (h->n_own_l1 > 0) {
+    klaunch(h->s, h->pdl, restrict_kernel, nblk(h->n_own_l1, 256), 256, h->n_own_l1, h->own_l1_pt, h->own_l1_idx,
+            (const double*)Lv.r, h->l1_send, (double*)nullptr, (const double*)nullptr, 0);
+    ++h->nlaunch;
+  }
+  h->comm->allgather(h->s, h->l1_send, h->l1_recv, h->l1_cmax);
+  const bool last = l + 1 == L;
+  const bool init = !last && h->prm.pre_sweeps > 0;
+  double* bn = last ? h->bL : h->lv[l + 1].b;
+  double* xn = last ? h->xL : h->lv[l + 1].x;
+  const bool root_mode = h->prm.coarse_mode == 1;
+  if (!root_mode || h->rank == 0) {
+    klaunch(h->s, h->pdl, scatter_l1_kernel, nblk((size_t)h->nranks * h->l1_cmax, 256), 256, h->nranks * h->l1_cmax,
+            (const int*)h->l1_scatter, (const double*)h->l1_recv, bn, init ? xn : (double*)nullptr,
+            init ? (const double*)h->lv[l + 1].diag : (const double*)nullptr, init ? h->lv[l + 1].color_row[1] : 0);
+    ++h->nlaunch;
+    vcycle(h, l + 1, init);
+  }
+  if (root_mode) h->comm->broadcast(h->s, xn, last ? h->nL : h->lv[l + 1].n, 0);
+  return xn;
+}
+
+// V-cycle on a partitioned level l (1 <= l <= dist_D): the level-0 pattern of
+// msp_apply_dist -- a halo of the color after every color of the sweeps, the residual's
+// member ghosts before the restriction, the next level's parent ghosts before the
+// prolongation, all ghosts after it.  Same per-row arithmetic as the replicated V-cycle
+// (bit-identical).  init_done: the first color was fused into the restriction.
+void vcycle_dist(msp_handle* h, int l, bool init_done) {
+  DevLevel& Lv = h->lv[l];
+  const int g = Lv.ncolor;
+  auto exch = [&](int c) { h->comm->halo(h->s, Lv.xh, Lv.x, Lv.n, 1, c); };
+  CK(cudaMemsetAsync(Lv.x + Lv.n, 0, sizeof(double) * (Lv.ngx + Lv.ngp), h->s));   // zero guess of ghosts
+  if (!init_done && Lv.n > 0) {
+    klaunch(h->s, h->pdl, pgs_init_kernel, nblk(Lv.n, 256), 256, Lv.n, Lv.color_row[1], (const double*)Lv.diag,
+            (const double*)Lv.b, Lv.x);
+    ++h->nlaunch;
+  }
+  exch(0);
+  for (int c = 1; c < g; ++c) {
+    if (c == g - 1) sell_rows_any<true, false>(h, Lv, Lv.color_slice[c], Lv.color_slice[c + 1]);
+    else sell_rows_any<false, false>(h, Lv, Lv.color_slice[c], Lv.color_slice[c + 1]);
+    exch(c);
+  }
+  if (g > 1) sell_rows_any<false, true>(h, Lv, 0, Lv.color_slice[g - 1]);
+  else sell_rows_any<false, true>(h, Lv, 0, Lv.nslices);
+  h->comm->halo(h->s, Lv.mh, Lv.r, Lv.n, 1, -1);                             // member ghosts of r
+  double* xn;
+  if (l + 1 <= h->dist_D) {
+    DevLevel& N = h->lv[l + 1];
+    if (N.n > 0) {                                 // (a rank may own no row of a small level)
+      klaunch(h->s, h->pdl, restrict_kernel, nblk(N.n, 256), 256, N.n, (const int*)Lv.pt_ptr, (const int*)Lv.pt_idx,
+              (const double*)Lv.r, N.b, N.x, (const double*)N.diag, N.color_row[1]);
+      ++h->nlaunch;
+    }
+    vcycle_dist(h, l + 1, true);
+    h->comm->halo(h->s, N.ph, N.x, N.n + N.ngx, 1, -1);                      // parent ghosts
+    xn = N.x;
+  } else {
+    xn = dist_handover(h, l);
+  }
+  if (Lv.n > 0) {
+    klaunch(h->s, h->pdl, prolong_kernel, nblk(Lv.n, 256), 256, Lv.n, (const int*)Lv.agg, (const double*)xn, Lv.x,
+            HaloPack{});
+    ++h->nlaunch;
+  }
+  h->comm->halo(h->s, Lv.xh, Lv.x, Lv.n, 1, -1);
+  for (int c = g - 1; c >= 0; --c) {
+    sell_rows_any<false, false>(h, Lv, Lv.color_slice[c], Lv.color_slice[c + 1]);
+    if (c > 0) exch(c);
+  }
+}
+
 void msp_apply_dist(msp_handle* h, const double* g, double* z) {
   DevLevel& L0 = h->lv[0];
-  const int L = (int)h->lv.size();
   CK(cudaMemsetAsync(L0.x + L0.n, 0, sizeof(double) * h->n0_ghost, h->s));    // zero guess of ghosts
   // producers pack the level-0 halo themselves (uniform level-0 layout)
   const HaloPack pk0 = (h->fuse_halo && h->l0_halo.d_slots) ? HaloPack{h->l0_halo.d_slots, h->l0_halo.d_sendbuf}
@@ -2071,26 +2319,20 @@ void msp_apply_dist(msp_handle* h, const double* g, double* z) {
   }
   if (L0.ncolor > 1) sell_rows_any<false, true>(h, L0, 0, L0.color_slice[L0.ncolor - 1]);
   else sell_rows_any<false, true>(h, L0, 0, L0.nslices);
-  if (h->n_own_l1 > 0) {
-    klaunch(h->s, h->pdl, restrict_kernel, nblk(h->n_own_l1, 256), 256, h->n_own_l1, h->own_l1_pt, h->own_l1_idx,
-            (const double*)L0.r, h->l1_send, (double*)nullptr, (const double*)nullptr, 0);
-    ++h->nlaunch;
+  double* x1;
+  if (h->dist_D >= 1) {                                                      // level 1 partitioned
+    DevLevel& L1 = h->lv[1];
+    if (L1.n > 0) {
+      klaunch(h->s, h->pdl, restrict_kernel, nblk(L1.n, 256), 256, L1.n, (const int*)L0.pt_ptr, (const int*)L0.pt_idx,
+              (const double*)L0.r, L1.b, L1.x, (const double*)L1.diag, L1.color_row[1]);
+      ++h->nlaunch;
+    }
+    vcycle_dist(h, 1, true);
+    h->comm->halo(h->s, L1.ph, L1.x, L1.n + L1.ngx, 1, -1);                 // parent ghosts
+    x1 = L1.x;
+  } else {
+    x1 = dist_handover(h, 0);
   }
-  // level-1 right-hand side: every rank's owned aggregates (replicated: all ranks; ROOT:
-  // only rank 0 goes on with it)
-  h->comm->allgather(h->s, h->l1_send, h->l1_recv, h->l1_cmax);
-  const bool init1 = L > 1 && h->prm.pre_sweeps > 0;
-  double* b1 = (L > 1) ? h->lv[1].b : h->bL;
-  double* x1 = (L > 1) ? h->lv[1].x : h->xL;
-  const bool root_mode = h->prm.coarse_mode == 1;
-  if (!root_mode || h->rank == 0) {
-    klaunch(h->s, h->pdl, scatter_l1_kernel, nblk((size_t)h->nranks * h->l1_cmax, 256), 256, h->nranks * h->l1_cmax,
-            (const int*)h->l1_scatter, (const double*)h->l1_recv, b1, init1 ? x1 : (double*)nullptr,
-            init1 ? (const double*)h->lv[1].diag : (const double*)nullptr, init1 ? h->lv[1].color_row[1] : 0);
-    ++h->nlaunch;
-    vcycle(h, 1, init1);                                                     // levels >= 1 + coarsest
-  }
-  if (root_mode) h->comm->broadcast(h->s, x1, (L > 1) ? h->lv[1].n : h->nL, 0);   // level-1 correction
   klaunch(h->s, h->pdl, prolong_kernel, nblk(L0.n, 256), 256, L0.n, (const int*)L0.agg, (const double*)x1, L0.x, pk0);
   ++h->nlaunch;
   exch_l0(h, L0.x, -1, pk0.slots != nullptr);
@@ -3267,7 +3509,8 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   msp_config_default(&c);
   if (cfg) c = *cfg;
   if (c.stages != 2 || c.pre_sweeps != 1 || c.post_sweeps != 1 || c.bilu_order != 1 || c.orth == 1 ||
-      c.smoother != 0 || c.coarse_mode < 0 || c.coarse_mode > 1 || c.bilu_local < 0 || c.bilu_local > 1)
+      c.smoother != 0 || c.coarse_mode < 0 || c.coarse_mode > 1 || c.bilu_local < 0 || c.bilu_local > 1 ||
+      c.dist_levels < 0)
     return fail(nullptr, MSP_EINVAL,
                 "msp_setup_dist: supports stages=2, 1 pre/post sweep, ABMC order, CGS2/DCGS2, PGS-MC, coarse_mode 0/1");
   // NCCL steps are replayed as CUDA graphs (halo send/recv groups and allreduces are

@@ -115,6 +115,43 @@ def test_loopback_full_size_c3_zslabs_vs_oracle_golden(nranks):
     assert info[:, 0].sum() == p["n"] and (info[:, 1] > 0).all()
 
 
+@pytest.mark.parametrize("nranks,owner", [(2, "zslab"), (3, "zslab"), (3, None)])
+@pytest.mark.parametrize("coarse_mode", [0, 1])
+def test_loopback_distributed_levels_bit_identical(nranks, owner, coarse_mode):
+    """dist_levels (NEXT-3): AMG levels 1..D partitioned (rows on the owner of their
+    lowest-index member, per-color halos in the sweeps, member / parent halos around the
+    transfers) instead of replicated.  Same per-row arithmetic and summation orders ->
+    iterates bit-identical to dist_levels=0 for every D (0 < D < levels, and clamped)."""
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C2", nx=24, ny=20, nz=9)
+    kw = dict(coarsest_max_dof=20)
+    H = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"], **kw)
+    assert H.info()["levels"] >= 4
+    own = H.partition_owner(p["nx"], p["ny"], p["nz"], nranks) if owner == "zslab" else None
+    ref = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=own,
+                         coarse_mode=coarse_mode, **kw)
+    for D in (1, 2, 99):
+        rd = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], nranks, p["rhs"], owner=own,
+                            coarse_mode=coarse_mode, dist_levels=D, **kw)
+        assert rd["iters"] == ref["iters"], (D, rd["iters"], ref["iters"])
+        assert np.array_equal(rd["x"], ref["x"]), D
+
+
+def test_loopback_distributed_levels_full_size_c3_vs_oracle_golden():
+    """C3 at full size over 2 z-slab ranks with EVERY smoothed level partitioned
+    (dist_levels clamped): the oracle's committed iteration count (+-1) and residual."""
+    import json
+    import os
+    from paper_2208_08594_b200 import loopback_solve, HostSetup
+    p = gen.make_config("C3")
+    owner = HostSetup(p["row_ptr"], p["col"], p["val"], p["nc"]).partition_owner(p["nx"], p["ny"], p["nz"], 2)
+    rd = loopback_solve(p["row_ptr"], p["col"], p["val"], p["nc"], 2, p["rhs"], owner=owner, dist_levels=99)
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_c3.json")))
+    assert abs(rd["iters"] - ref["iters"]) <= 1, (rd["iters"], ref["iters"])
+    A = sp.bsr_matrix((p["val"], p["col"], p["row_ptr"]), shape=(p["n"] * p["b"],) * 2)
+    assert np.linalg.norm(p["rhs"] - A @ rd["x"]) / np.linalg.norm(p["rhs"]) <= 1e-6
+
+
 def test_nccl_single_rank_coarse_root():
     from paper_2208_08594_b200 import DistSolver, MspSolver, nccl_unique_id
     p = gen.make_config("C2", nx=20, ny=16, nz=6)
