@@ -34,8 +34,9 @@ with open(dst_txt, "w") as f:
                 f"{byt[n] / t if t else 0:9.1f} {byt[n] / cnt[n] / 1e6:12.2f}  {n}\n")
 pieces = {
     "a2_bsr_spmv": lambda n: n.startswith("bsr_spmv4c_kernel<0>") or n.startswith("bsr_spmv_kernel<4, 0>"),
-    "a8_pcol_residual": lambda n: n.startswith("bsr_spmv_kernel<4, 2>") or "pcol_resid4_kernel" in n,
-    "a9_bilu_apply": lambda n: n.startswith("bilu_block_kernel"),
+    "a8_pcol_residual": lambda n: (n.startswith("bsr_spmv_kernel<4, 2>") or "pcol_resid4_kernel" in n
+                                   or "pcol_resid_ell4_kernel" in n),
+    "a9_bilu_apply": lambda n: n.startswith("bilu_block_kernel") or n.startswith("bilu_meta"),
 }
 out = {}
 for key, pred in pieces.items():
