@@ -313,6 +313,18 @@ msp_status msp_partition_owner(const msp_host_setup* s, int nx, int ny, int nz, 
 msp_status msp_dist_plan(const msp_host_setup* s, const int32_t* owner, int rank, int nranks, int32_t* n_own,
                          int32_t* owned_cells, int32_t* n_ghost, int32_t* ghost_cells, int32_t* send_ptr,
                          int32_t* send_cells, int32_t* recv_ptr);
+/* Host-only plan of a PARTITIONED AMG level (msp_config.dist_levels, SURVEY §8(e)
+ * "distribute levels 1..k"; no GPU): for `rank` of `nranks` (cell owners as msp_dist_plan),
+ * level 1 <= level < number of smoothed levels.  Serialised into buf (int32, capacity cap;
+ * *len = required length; buf NULL: length only), natural row ids of the level throughout:
+ *   n_own, n_gx, n_gp, n_gm, owned rows (global row order), matrix ghosts, parent ghosts,
+ *   member ghosts (each in receive order: peer-major, then global row order), then for every
+ *   peer q = 0..nranks-1: [count, rows sent to q for its matrix ghosts], [count, parent
+ *   ghosts sent], [count, member ghosts sent] (send order = the peer's receive order), then
+ *   the level's row count m, the owner of every row (m) and the global (color-major) row
+ *   index of every row (m). */
+msp_status msp_dist_level_plan(const msp_host_setup* s, const int32_t* owner, int rank, int nranks, int level,
+                               int32_t* buf, int64_t cap, int64_t* len);
 
 #ifdef __cplusplus
 }

@@ -483,6 +483,37 @@ class HostSetup:
         return dict(owned=owned[:no.value].copy(), ghosts=ghosts[:ng.value].copy(), send_ptr=sp_,
                     send_cells=sc[:sp_[-1]].copy(), recv_ptr=rp_)
 
+    def dist_level_plan(self, rank, nranks, level, owner=None):
+        """Host-only plan of a partitioned AMG level (msp_dist_level_plan), parsed."""
+        own = None if owner is None else _np(owner, np.int32)
+        op = _ptr(own) if own is not None else None
+        ln = ctypes.c_int64(0)
+        st = _lib.msp_dist_level_plan(self._h, op, rank, nranks, level, None, ctypes.c_int64(0), ctypes.byref(ln))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        buf = np.zeros(ln.value, np.int32)
+        st = _lib.msp_dist_level_plan(self._h, op, rank, nranks, level, _ptr(buf), ctypes.c_int64(ln.value),
+                                      ctypes.byref(ln))
+        if st:
+            raise MspError(st, _lib.msp_last_error(None).decode())
+        k = 4
+        cnt = buf[:4]
+        out = {}
+        for name, c in zip(("rows", "gx", "gp", "gm"), cnt):
+            out[name] = buf[k:k + c].copy()
+            k += c
+        for name in ("sendx", "sendp", "sendm"):
+            out[name] = []
+        for q in range(nranks):
+            for name in ("sendx", "sendp", "sendm"):
+                c = buf[k]
+                out[name].append(buf[k + 1:k + 1 + c].copy())
+                k += 1 + c
+        m = buf[k]
+        out["owner"] = buf[k + 1:k + 1 + m].copy()
+        out["row_index"] = buf[k + 1 + m:k + 1 + 2 * m].copy()
+        return out
+
     def partition_owner(self, nx, ny, nz, nranks):
         o = np.zeros(self.n, np.int32)
         st = _lib.msp_partition_owner(self._h, nx, ny, nz, nranks, _ptr(o))

@@ -526,6 +526,98 @@ std::vector<int32_t> block_counts(const msp::HostSetup& S, const std::vector<int
   return cnt;
 }
 
+// Partitioned AMG level l >= 1 of rank `me` (dist_levels, host-only integer work): owned
+// rows in the global row order, ghosts in receive order (peer-major, then global row
+// order, which is color-major) and, per peer, the rows sent to it in the same order --
+// matrix ghosts / x sends (the sweeps), parent ghosts / sends (the prolongation into
+// level l-1) and member ghosts / sends of r (the restriction into level l+1).
+struct LevelPlan {
+  std::vector<int32_t> rows, gx, gp, gm;
+  std::vector<std::vector<int32_t>> needx, needp, needm;
+};
+LevelPlan plan_level(const msp::HostSetup& S, const std::vector<std::vector<int32_t>>& perms,
+                     const std::vector<std::vector<int32_t>>& own, int l, int me, int P) {
+  const msp::SpMat& Al = S.lv[l].A;
+  const int32_t nl = Al.n;
+  const auto& ow = own[l];
+  const auto& pl = perms[l];
+  auto by_row = [&](int32_t x, int32_t y) { return pl[x] < pl[y]; };
+  auto by_owner_row = [&](int32_t x, int32_t y) { return ow[x] != ow[y] ? ow[x] < ow[y] : pl[x] < pl[y]; };
+  LevelPlan R;
+  for (int32_t i = 0; i < nl; ++i) if (ow[i] == me) R.rows.push_back(i);
+  std::sort(R.rows.begin(), R.rows.end(), by_row);
+  R.needx.assign(P, {});
+  R.needp.assign(P, {});
+  R.needm.assign(P, {});
+  {
+    std::vector<uint8_t> mk(nl, 0);
+    for (int32_t i = 0; i < nl; ++i) {
+      const int t = ow[i];
+      for (int32_t e = Al.rp[i]; e < Al.rp[i + 1]; ++e) {
+        const int32_t d = Al.ci[e];
+        const int o = ow[d];
+        if (o == t) continue;
+        if (o == me) R.needx[t].push_back(d);
+        if (t == me && !mk[d]) { mk[d] = 1; R.gx.push_back(d); }
+      }
+    }
+  }
+  {
+    const auto& aggp = S.lv[l - 1].agg;
+    const auto& owp = own[l - 1];
+    std::vector<uint8_t> mk(nl, 0);
+    for (int32_t i = 0; i < S.lv[l - 1].A.n; ++i) {
+      const int32_t I = aggp[i];
+      const int t = owp[i], o = ow[I];
+      if (o == t) continue;
+      if (o == me) R.needp[t].push_back(I);
+      if (t == me && !mk[I]) { mk[I] = 1; R.gp.push_back(I); }
+    }
+  }
+  {
+    const auto& aggn = S.lv[l].agg;
+    const auto& own_n = own[l + 1];
+    for (int32_t i = 0; i < nl; ++i) {
+      const int t = own_n[aggn[i]], o = ow[i];
+      if (o == t) continue;
+      if (o == me) R.needm[t].push_back(i);
+      if (t == me) R.gm.push_back(i);
+    }
+  }
+  for (int q = 0; q < P; ++q)
+    for (auto* v : {&R.needx[q], &R.needp[q], &R.needm[q]}) {
+      std::sort(v->begin(), v->end(), by_row);
+      v->erase(std::unique(v->begin(), v->end()), v->end());
+    }
+  std::sort(R.gx.begin(), R.gx.end(), by_owner_row);
+  std::sort(R.gp.begin(), R.gp.end(), by_owner_row);
+  std::sort(R.gm.begin(), R.gm.end(), by_owner_row);
+  return R;
+}
+
+// owners of the rows of levels 0..upto: a level-(l+1) row (aggregate of level-l rows)
+// lives on the owner of its lowest-index member
+std::vector<std::vector<int32_t>> level_owners(const msp::HostSetup& S, const std::vector<int32_t>& own_cell,
+                                               int upto) {
+  std::vector<std::vector<int32_t>> own(upto + 1);
+  own[0] = own_cell;
+  for (int l = 0; l + 1 <= upto; ++l) {
+    const auto& agg = S.lv[l].agg;
+    own[l + 1].assign(S.lv[l].n_next, -1);
+    for (int32_t i = S.lv[l].A.n - 1; i >= 0; --i) own[l + 1][agg[i]] = own[l][i];
+  }
+  return own;
+}
+
+// color-major permutation of a level (natural row -> global row), as upload_level
+std::vector<int32_t> level_perm(const msp::HostLevel& Lv) {
+  std::vector<int32_t> cnt(Lv.ncolor + 1, 0), perm(Lv.A.n);
+  for (int32_t c : Lv.color) cnt[c + 1]++;
+  for (int c = 0; c < Lv.ncolor; ++c) cnt[c + 1] += cnt[c];
+  for (int32_t i = 0; i < Lv.A.n; ++i) perm[i] = cnt[Lv.color[i]]++;
+  return perm;
+}
+
 void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& S, const std::vector<int32_t>& rp,
                    const std::vector<int32_t>& ci, const std::vector<int32_t>& dg, const std::vector<int32_t>& src,
                    const std::vector<double>& F, const std::vector<std::vector<int32_t>>& perms,
@@ -1670,63 +1762,14 @@ void dist_localize(msp_handle* h, const msp::BlockMat& A, const msp::HostSetup& 
       const int g = S.lv[l].ncolor;
       const int32_t nl = Al.n;
       const auto& ow = own[l];
-      const auto& pl = perms[l];
-      auto by_row = [&](int32_t x, int32_t y) { return pl[x] < pl[y]; };
-      auto by_owner_row = [&](int32_t x, int32_t y) { return ow[x] != ow[y] ? ow[x] < ow[y] : pl[x] < pl[y]; };
       LocLev& Q = LL[l];
-      for (int32_t i = 0; i < nl; ++i) if (ow[i] == me) Q.rows.push_back(i);
-      std::sort(Q.rows.begin(), Q.rows.end(), by_row);
+      LevelPlan LP = plan_level(S, perms, own, l, me, P);
+      Q.rows = LP.rows;
       Q.no = (int32_t)Q.rows.size();
       std::vector<int32_t> lo(nl, -1);
       for (int32_t k = 0; k < Q.no; ++k) lo[Q.rows[k]] = k;
-      // matrix ghosts (read by the sweeps and the residual) and the x send lists
-      std::vector<std::vector<int32_t>> needx(P), needp(P), needm(P);
-      std::vector<int32_t> gx, gp, gm;
-      {
-        std::vector<uint8_t> mk(nl, 0);
-        for (int32_t i = 0; i < nl; ++i) {
-          const int t = ow[i];
-          for (int32_t e = Al.rp[i]; e < Al.rp[i + 1]; ++e) {
-            const int32_t d = Al.ci[e];
-            const int o = ow[d];
-            if (o == t) continue;
-            if (o == me) needx[t].push_back(d);
-            if (t == me && !mk[d]) { mk[d] = 1; gx.push_back(d); }
-          }
-        }
-      }
-      // parent ghosts: level-l rows my level-(l-1) rows prolongate from, owned elsewhere
-      {
-        const auto& aggp = S.lv[l - 1].agg;
-        const auto& owp = own[l - 1];
-        std::vector<uint8_t> mk(nl, 0);
-        for (int32_t i = 0; i < S.lv[l - 1].A.n; ++i) {
-          const int32_t I = aggp[i];
-          const int t = owp[i], o = ow[I];
-          if (o == t) continue;
-          if (o == me) needp[t].push_back(I);
-          if (t == me && !mk[I]) { mk[I] = 1; gp.push_back(I); }
-        }
-      }
-      // member ghosts: rows of aggregates (level l+1) I own, owned elsewhere
-      {
-        const auto& aggn = S.lv[l].agg;
-        const auto& own_n = own[l + 1];
-        for (int32_t i = 0; i < nl; ++i) {
-          const int t = own_n[aggn[i]], o = ow[i];
-          if (o == t) continue;
-          if (o == me) needm[t].push_back(i);
-          if (t == me) gm.push_back(i);
-        }
-      }
-      for (int q = 0; q < P; ++q)
-        for (auto* v : {&needx[q], &needp[q], &needm[q]}) {
-          std::sort(v->begin(), v->end(), by_row);
-          v->erase(std::unique(v->begin(), v->end()), v->end());
-        }
-      std::sort(gx.begin(), gx.end(), by_owner_row);      // peer-major, color-major inside a peer
-      std::sort(gp.begin(), gp.end(), by_owner_row);
-      std::sort(gm.begin(), gm.end(), by_owner_row);
+      const auto &gx = LP.gx, &gp = LP.gp, &gm = LP.gm;
+      const auto &needx = LP.needx, &needp = LP.needp, &needm = LP.needm;
       const int32_t ngx = (int32_t)gx.size(), ngp = (int32_t)gp.size(), ngm = (int32_t)gm.size();
       Q.xloc = lo;
       Q.ploc = lo;
@@ -3788,6 +3831,48 @@ msp_status msp_dist_plan(const msp_host_setup* s, const int32_t* owner, int rank
     }
     send_ptr[q + 1] = ns;
     recv_ptr[q + 1] = recv_ptr[q] + nr;
+  }
+  return MSP_OK;
+}
+
+msp_status msp_dist_level_plan(const msp_host_setup* s, const int32_t* owner, int rank, int nranks, int level,
+                               int32_t* buf, int64_t cap, int64_t* len) {
+  if (!s || !len || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(nullptr, MSP_EINVAL, "msp_dist_level_plan: bad arguments");
+  const msp::HostSetup& S = s->S;
+  const int L = (int)S.lv.size();
+  if (level < 1 || level >= L) return fail(nullptr, MSP_EINVAL, "msp_dist_level_plan: level must be in [1, levels)");
+  const int32_t n = S.n;
+  std::vector<int32_t> own(n);
+  for (int32_t i = 0; i < n; ++i) {
+    own[i] = owner ? owner[i] : (int32_t)(((int64_t)i * nranks) / n);
+    if (own[i] < 0 || own[i] >= nranks) return fail(nullptr, MSP_EINVAL, "msp_dist_level_plan: owner out of range");
+  }
+  std::vector<int32_t> rp, ci, dg, src;
+  std::string err;
+  if (msp::permuted_pattern(S, s->M, rp, ci, dg, src, err)) return fail(nullptr, MSP_EINVAL, err);
+  // effective cell owners (ABMC blocks whole, as the distributed setup)
+  CellPlan C = compute_cell_plan(S, rp, ci, own, nranks, rank);
+  std::vector<int32_t> own_cell(n);
+  for (int32_t p = 0; p < n; ++p) own_cell[S.order[p]] = C.own_pos[p];
+  std::vector<std::vector<int32_t>> perms(L);
+  for (int l = 0; l < L; ++l) perms[l] = level_perm(S.lv[l]);
+  const auto owners = level_owners(S, own_cell, level + 1);
+  const LevelPlan R = plan_level(S, perms, owners, level, rank, nranks);
+  std::vector<int32_t> out = {(int32_t)R.rows.size(), (int32_t)R.gx.size(), (int32_t)R.gp.size(), (int32_t)R.gm.size()};
+  for (const auto* v : {&R.rows, &R.gx, &R.gp, &R.gm}) out.insert(out.end(), v->begin(), v->end());
+  for (int q = 0; q < nranks; ++q)
+    for (const auto* v : {&R.needx[q], &R.needp[q], &R.needm[q]}) {
+      out.push_back((int32_t)v->size());
+      out.insert(out.end(), v->begin(), v->end());
+    }
+  out.push_back((int32_t)owners[level].size());
+  out.insert(out.end(), owners[level].begin(), owners[level].end());
+  out.insert(out.end(), perms[level].begin(), perms[level].end());
+  *len = (int64_t)out.size();
+  if (buf) {
+    if (cap < *len) return fail(nullptr, MSP_EINVAL, "msp_dist_level_plan: buffer too small");
+    std::memcpy(buf, out.data(), sizeof(int32_t) * out.size());
   }
   return MSP_OK;
 }
