@@ -71,6 +71,8 @@ void klaunch(cudaStream_t s, bool pdl, void (*k)(KArgs...), dim3 grid, dim3 bloc
   CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
 }
 
+constexpr int kRecStride = 2 * kMaxV + 4;   // doubles per Arnoldi step record (host)
+
 struct DevLevel {
   int32_t n = 0, ncolor = 0, nslices = 0;
   std::vector<int32_t> color_row;    // host: row range per color (permuted)
@@ -144,6 +146,9 @@ struct msp_handle {
   double *V = nullptr;
   int V_m = -1;
   double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
+  double* hrec = nullptr;            // pinned: step j's Hessenberg record at hrec + j * kRecStride
+  cudaEvent_t ev_step[2] = {nullptr, nullptr};   // end of step j (parity j & 1)
+  int spec_steps = 1;                // MSP_SPEC_STEPS=0: no step enqueued ahead of the host's Givens update
   double *gv = nullptr, *hgv = nullptr;        // device Givens state / its pinned host copy
   cudaGraphExec_t cycle_exec = nullptr;        // one restart cycle as ONE graph (conditional steps)
   int cycle_m = -1;
@@ -241,6 +246,7 @@ struct msp_handle {
     cell_halo = msp::HaloPlan();
     l0_halo = msp::HaloPlan();
     if (hpin) { cudaFreeHost(hpin); hpin = nullptr; }
+    if (hrec) { cudaFreeHost(hrec); hrec = nullptr; }
     if (hgv) { cudaFreeHost(hgv); hgv = nullptr; }
     if (cycle_exec) { cudaGraphExecDestroy(cycle_exec); cycle_exec = nullptr; }
     cycle_m = -1;
@@ -1406,6 +1412,9 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   h->ticket = h->dalloc<unsigned>(4);
   CK(cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned), h->s));
   CK(cudaMallocHost(&h->hpin, sizeof(double) * kMaxV * 4));
+  CK(cudaMallocHost(&h->hrec, sizeof(double) * kMaxV * kRecStride));
+  for (auto& e : h->ev_step)
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaMallocHost(&h->hgv, sizeof(double) * kGvSize));
   h->gv = h->dalloc<double>(kGvSize);
   CK(cudaStreamSynchronize(h->s));
@@ -2666,7 +2675,8 @@ void arnoldi_step(msp_handle* h, int j, bool record_to_host = true) {
   const int nv = j + 1;
   if (h->prm.orth == 2) {
     dcgs2(h, j);
-    if (record_to_host) CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (2 * j + 4), cudaMemcpyDeviceToHost, h->s));
+    if (record_to_host)
+      CK(cudaMemcpyAsync(h->hrec + (size_t)j * kRecStride, h->hcol, sizeof(double) * (2 * j + 4), cudaMemcpyDeviceToHost, h->s));
     return;
   }
   if (h->prm.orth == 0) {
@@ -2680,7 +2690,8 @@ void arnoldi_step(msp_handle* h, int j, bool record_to_host = true) {
     klaunch(h->s, h->pdl, reduce_parts_kernel, 1, 1024, kRedBlocks, 1, h->part, h->hcol + nv, nullptr, 0); ++h->nlaunch;
     klaunch(h->s, h->pdl, scale_kernel, kRedBlocks, kRedThreads, N, w, h->hcol + nv, w); ++h->nlaunch;
   }
-  if (record_to_host) CK(cudaMemcpyAsync(h->hpin, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
+  if (record_to_host)
+    CK(cudaMemcpyAsync(h->hrec + (size_t)j * kRecStride, h->hcol, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, h->s));
 }
 
 // One restart cycle of GMRES(m) as ONE executable graph: a chain of m conditional (IF)
@@ -2768,6 +2779,8 @@ void run_step(msp_handle* h, int j, int m) {
 
 // GMRES(m), right preconditioned (R8); vectors internal order; xin holds x0 and
 // the solution; bin holds b.
+constexpr double kSpecMargin = 3.0;         // enqueue the next step while est > 3 tol
+
 msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double* final_rel,
                  double* hist, int cap, int* hlen) {
   const size_t N = h->N;
@@ -2829,13 +2842,27 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         for (int i = 0; i <= k; ++i) gam[i] = g[kGvGam + i];
         it += k;
       }
+      // Step j+1 is enqueued before the host reads step j's record (its own pinned slot)
+      // while the residual estimate is more than kSpecMargin x tol away: the GPU runs on
+      // through the host's Givens update.  A step enqueued past convergence is wasted work
+      // only (it writes V[j+2] and the DCGS2 state of step j+1; the cycle end reads V[0..j]
+      // and the host's y; step 0 of a cycle reads no lagged state): identical results.
+      int launched = -1;
+      double est_prev = rel;
+      auto launch = [&](int jj) {
+        run_step(h, jj, m);
+        CK(cudaEventRecord(h->ev_step[jj & 1], h->s));
+        launched = jj;
+      };
       for (int j = 0; j < m && !cyc; ++j) {
-        run_step(h, j, m);
-        CK(cudaStreamSynchronize(h->s));
+        if (launched < j) launch(j);
+        if (h->spec_steps && j + 1 < m && it + 1 < maxit && est_prev > kSpecMargin * tol) launch(j + 1);
+        CK(cudaEventSynchronize(h->ev_step[j & 1]));
+        const double* hr = h->hrec + (size_t)j * kRecStride;
         auto Hc = [&](int i) -> double& { return H[(size_t)i * m + j]; };
         if (h->prm.orth == 2) {
           // column j of the final basis: (nu [c + h2'; rho'] - sum_l h2_l Hraw[:, l]) / rho
-          const double* rec = h->hpin;
+          const double* rec = hr;
           for (int i = 0; i <= j + 1; ++i) {
             double v = nup * ((i <= j) ? rec[i] : rec[j + 1]);
             for (int l = 0; l < j; ++l) v -= h2p[l] * Hraw[(size_t)i * m + l];
@@ -2846,7 +2873,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
           nup = rec[j + 2];
           rhop = rec[j + 1];
         } else {
-          for (int i = 0; i <= j + 1; ++i) Hc(i) = h->hpin[i];
+          for (int i = 0; i <= j + 1; ++i) Hc(i) = hr[i];
         }
         const double hn = Hc(j + 1);
         ++it;
@@ -2863,6 +2890,7 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         gam[j + 1] = -sn[j] * gam[j];
         gam[j] = cs[j] * gam[j];
         const double est = std::fabs(gam[j + 1]) / bnorm;
+        est_prev = est;
         push(est);
         k = j + 1;
         broke = hn < 1e-14 * bnorm;
@@ -3005,6 +3033,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_BILU_META")) h->bilu_meta = std::atoi(e);
   if (const char* e = std::getenv("MSP_A8_ELL")) h->a8_ell = std::atoi(e);
   if (const char* e = std::getenv("MSP_CYCLE_GRAPH")) h->cycle_graphs = std::atoi(e) != 0;
+  if (const char* e = std::getenv("MSP_SPEC_STEPS")) h->spec_steps = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;
@@ -3391,6 +3420,7 @@ void msp_destroy(msp_handle* h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  for (auto e : h->ev_step) if (e) cudaEventDestroy(e);
   if (h->s2) cudaStreamDestroy(h->s2);
   if (h->cs) cusolverDnDestroy(h->cs);
   if (h->s) cudaStreamDestroy(h->s);

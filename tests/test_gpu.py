@@ -450,6 +450,23 @@ def test_cycle_graph_matches_per_step_graphs(orth, monkeypatch):
     assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x0)
 
 
+@pytest.mark.parametrize("orth", [0, 2])
+def test_speculative_steps_bit_identical(orth, monkeypatch):
+    """Step j+1 enqueued before the host's Givens update of step j (MSP_SPEC_STEPS, on by
+    default): bit-identical solution and history to the synchronous loop, over restarts,
+    at convergence (a step enqueued past it is discarded) and at maxit."""
+    p = gen.make_config("C2", nx=30, ny=30, nz=6)
+    for kw in (dict(restart=7, tol=1e-9), dict(restart=30, tol=1e-6), dict(restart=5, tol=1e-12, maxit=12)):
+        out = []
+        for v in ("0", "1"):
+            monkeypatch.setenv("MSP_SPEC_STEPS", v)
+            s = solver(p, coarsest_max_dof=100, orth=orth)
+            out.append(s.solve(torch.from_numpy(p["rhs"]).cuda(), **kw))
+        assert out[0]["iters"] == out[1]["iters"], kw
+        assert np.array_equal(out[0]["hist"], out[1]["hist"]), kw
+        assert torch.equal(out[0]["x"], out[1]["x"]), kw
+
+
 def test_caller_stream_ordering():
     """the library orders its work after the caller's stream.  b is produced by
     a kernel on a torch side stream that the solver was told about (set_stream), with no
