@@ -85,21 +85,40 @@ __global__ void __launch_bounds__(256) bsr_spmv_kernel(int n, const int* __restr
                                                        const double* __restrict__ x,
                                                        const double* __restrict__ g,
                                                        double* __restrict__ y) {
-  PDL_ENTRY();
   constexpr int TS = (B <= 4) ? 4 : 8;
   constexpr int BB = B * B;
+  constexpr int PF = 4;                        // MODE 2: entries prefetched before the PDL wait
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int row = gtid / TS;
   const int q = threadIdx.x % TS;
   const int lane = threadIdx.x & 31;
   const int base = lane - q;
-  if (row >= n) return;   // whole teams exit together (n*TS threads padded per team)
-  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  const bool live = row < n;                   // whole teams (n*TS threads padded per team)
+  const int e0 = live ? ldg(rp + row) : 0, e1 = live ? ldg(rp + row + 1) : 0;
+  int pc[PF];
+  double pv[PF];
+  if (MODE == 2) {                             // immutable columns and pressure columns
+#pragma unroll
+    for (int m = 0; m < PF; ++m) {
+      const int e = e0 + m;
+      pc[m] = (e < e1) ? ldg(ci + e) : 0;
+      pv[m] = (e < e1 && q < B) ? ldg(val + (size_t)e * B + q) : 0.0;
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
   double acc = 0.0;
   const unsigned mask = (TS == 32) ? 0xffffffffu : (((1u << TS) - 1u) << base);
   if (MODE == 2) {
+#pragma unroll
+    for (int m = 0; m < PF; ++m)
+      if (e0 + m < e1) {
+        const double xc = ldg(x + pc[m]);
+        if (q < B) acc = fma(pv[m], xc, acc);
+      }
 #pragma unroll 4
-    for (int e = e0; e < e1; ++e) {
+    for (int e = e0 + PF; e < e1; ++e) {
       const int c = ldg(ci + e);
       const double xc = ldg(x + c);
       if (q < B) acc = fma(ldg(val + (size_t)e * B + q), xc, acc);
@@ -172,7 +191,13 @@ __device__ __forceinline__ void col_accum8(const double* __restrict__ blk, doubl
   }
 }
 
-// a2 for 5x5..8x8 blocks, column-per-lane (8 lanes per block row, lane 7 idle for B = 7)
+// a2 for 5x5..8x8 blocks, column-per-lane (8 lanes per block row, lane 7 idle for B = 7).
+// The row's first MSP_SPMV8_PF entries (columns and block columns) are immutable and
+// loaded before the PDL wait; the rest stream with two entries in flight.  Entries are
+// accumulated in ascending order either way (same fma sequence as col_accum8).
+#ifndef MSP_SPMV8_PF
+#define MSP_SPMV8_PF 2
+#endif
 template <int B, int MODE>
 __global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
@@ -180,16 +205,37 @@ __global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __res
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ g,
                                                          double* __restrict__ y) {
-  PDL_ENTRY();
   constexpr int BB = B * B;
+  constexpr int PF = MSP_SPMV8_PF;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int row = gtid >> 3, q = threadIdx.x & 7;
-  if (row >= n) return;
-  const int e0 = ldg(rp + row), e1 = ldg(rp + row + 1);
+  const bool live = row < n;                   // whole 8-lane groups
+  const int e0 = live ? ldg(rp + row) : 0, e1 = live ? ldg(rp + row + 1) : 0;
+  int pc[PF];
+  double pv[PF][B];
+#pragma unroll
+  for (int m = 0; m < PF; ++m) {
+    const int e = e0 + m;
+    pc[m] = (e < e1) ? ldg(ci + e) : 0;
+#pragma unroll
+    for (int r = 0; r < B; ++r) pv[m][r] = (e < e1 && q < B) ? __ldcs(val + (size_t)e * BB + q * B + r) : 0.0;
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
   double a[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) a[r] = 0.0;
-  for (int e = e0; e < e1; ++e) {
+#pragma unroll
+  for (int m = 0; m < PF; ++m) {
+    if (e0 + m < e1 && q < B) {
+      const double xq = ldg(x + (size_t)pc[m] * B + q);
+#pragma unroll
+      for (int r = 0; r < B; ++r) a[r] = fma(pv[m][r], xq, a[r]);
+    }
+  }
+#pragma unroll 2
+  for (int e = e0 + PF; e < e1; ++e) {
     const int c = ldg(ci + e);
     const double xq = (q < B) ? ldg(x + (size_t)c * B + q) : 0.0;
     col_accum8<B>(val + (size_t)e * BB, xq, q, a);
@@ -276,7 +322,10 @@ __global__ void __launch_bounds__(256) pcol_resid4_kernel(int n, const int* __re
 // immutable and loaded before the PDL wait (coalesced: a warp reads 1 KB of pe per k),
 // then w independent gathers of x_p, one 32-byte g load and one 32-byte y store.
 constexpr int kEllMax = 8;
-__global__ void __launch_bounds__(256) pcol_resid_ell4_kernel(int n, int ld, int w, const int* __restrict__ ce,
+#ifndef MSP_A8_MINB
+#define MSP_A8_MINB 1
+#endif
+__global__ void __launch_bounds__(256, MSP_A8_MINB) pcol_resid_ell4_kernel(int n, int ld, int w, const int* __restrict__ ce,
                                                               const double* __restrict__ pe,
                                                               const double* __restrict__ x,
                                                               const double* __restrict__ g,
