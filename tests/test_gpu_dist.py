@@ -78,6 +78,24 @@ def test_nccl_backend_single_rank_matches_single_gpu(nograph, monkeypatch):
     assert np.linalg.norm(rd["x"].cpu().numpy() - x1) <= 1e-8 * np.linalg.norm(x1)
 
 
+@pytest.mark.parametrize("nograph", ["0", "1"])
+def test_nccl_single_rank_partitioned_levels(nograph, monkeypatch):
+    """The NCCL path (graph-captured and direct) with every AMG level partitioned
+    (dist_levels clamped; one rank: no ghosts, the hand-over goes straight to the
+    coarsest) is bit-identical to the same handle with replicated levels."""
+    from paper_2208_08594_b200 import DistSolver, nccl_unique_id
+    monkeypatch.setenv("MSP_DIST_NOGRAPH", nograph)
+    p = gen.make_config("C2", nx=20, ny=16, nz=6)
+    out = []
+    for D in (0, 99):
+        d = DistSolver(p["row_ptr"], p["col"], p["val"], p["nc"], 0, 1, nccl_unique_id(), coarsest_max_dof=40,
+                       dist_levels=D)
+        out.append(d.solve(torch.from_numpy(p["rhs"]).cuda()))
+        d.close()
+    assert out[0]["iters"] == out[1]["iters"]
+    assert torch.equal(out[0]["x"], out[1]["x"])
+
+
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_loopback_coarse_root_bit_identical(nranks):
     """coarse_mode=1 (ROOT, north_star's "coarse levels agglomerated onto one GPU"): rank 0
