@@ -297,7 +297,7 @@ def main():
     peak, peak_src = measured_peak()
     kernels = {}
     kinds = ("a2_bsr_spmv", "a4_pgs_sweep_l0", "a8_pcol_residual", "a9_bilu_apply",
-             "a10_multidot16", "orth_step15", "a6_coarse_gemv", "vcycle", "msp_apply")
+             "a10_multidot16", "orth_step15", "orth_step25", "a6_coarse_gemv", "vcycle", "msp_apply")
     if ws > 1:                                     # rank-local kernels only
         kinds = ("a2_bsr_spmv", "a8_pcol_residual", "a10_multidot16")
     for kind in kinds:

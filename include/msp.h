@@ -240,7 +240,7 @@ msp_status msp_set_stream(msp_handle* h, void* cuda_stream);
  * 11/12 Arnoldi step / CGS2 at j = 25; 13 a9 + SpMV; 14 MSP application + SpMV;
  * 15 SpMV + orthogonalisation of step 15; 16 + l (0 <= l <= L, L = the number of
  * smoothed AMG levels): the V-cycle from level l down (l = L: the coarsest solve alone), so
- * the time spent AT level l is T(16 + l) - T(17 + l) (bytes = 0 for kinds 6-9, 11-15, >= 16).
+ * the time spent AT level l is T(16 + l) - T(17 + l) (bytes = 0 for kinds 6-9, 11, 13-15, >= 16; kind 12 counts DCGS2 only).
  * kind | 0x100: no L2 flush (warm caches).  Each piece is captured once into a CUDA graph and replayed (as in the solve); the first replay is a warm-up.
  * Scratch contents of the handle are overwritten. */
 msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_launch,

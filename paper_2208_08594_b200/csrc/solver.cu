@@ -3512,9 +3512,13 @@ msp_status msp_time_kernel(msp_handle* h, int kind, int reps, double* ms_per_lau
         bytes = 0.0;
         break;
       case 12:
-        if (h->prm.orth == 2) fn = [&]() { dcgs2(h, 25); };
-        else fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
-        bytes = 0.0;
+        if (h->prm.orth == 2) {
+          fn = [&]() { dcgs2(h, 25); };
+          bytes = 56.0 * 8 * (double)N;        // pass 1 (25+2 vectors) + pass 2 (25 + 2 read, 2 written)
+        } else {
+          fn = [&]() { cgs2(h, 26, h->V + (size_t)26 * N); };
+          bytes = 0.0;
+        }
         break;
       case 13:                                   // a9 followed by the Arnoldi SpMV
         fn = [&]() { launch_bilu(h, h->r, h->wp, h->z); launch_spmv(h, 0, h->z, nullptr, h->u); };
