@@ -18,10 +18,43 @@ struct SpMat {                       // scalar CSR, ascending columns
   int64_t nnz() const { return (int64_t)ci.size(); }
 };
 
+// Block values: owned, or a read-only view of the caller's host buffer for the duration of
+// one SETUP call (no multi-GB copy of A before the setup reads or uploads it).
+struct Values {
+  std::vector<double> own;
+  const double* p = nullptr;
+  size_t n = 0;
+  Values() = default;
+  Values(const Values& o) { *this = o; }
+  Values& operator=(const Values& o) {
+    if (this == &o) return *this;
+    own = o.own;
+    n = o.n;
+    p = own.empty() ? o.p : own.data();
+    return *this;
+  }
+  const double& operator[](size_t i) const { return p[i]; }
+  const double* data() const { return p; }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  double* owned(size_t count) {               // (re)allocate an owned buffer of count values
+    own.resize(count);
+    p = own.data();
+    n = count;
+    return own.data();
+  }
+  void view(const double* q, size_t count) {
+    own.clear();
+    own.shrink_to_fit();
+    p = q;
+    n = count;
+  }
+};
+
 struct BlockMat {                    // BSR, row-major b x b blocks (ABI layout)
   int32_t n = 0, b = 0;
   std::vector<int32_t> rp, ci;
-  std::vector<double> v;
+  Values v;
 };
 
 struct Graph {                       // symmetric adjacency, ascending neighbours

@@ -309,7 +309,8 @@ void check_perm(const std::vector<int32_t>& v, const char* what) {
 }
 
 // Copy the ABI's BSR into a host BlockMat (validating it).
-msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err) {
+// view: host values are read in place during the call (SETUP entry points), not copied.
+msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err, bool view = false) {
   if (!A || A->n_cells <= 0 || A->n_cells > INT32_MAX || A->block != nc + 1 || nc < 0 || nc > 7 ||
       !A->row_ptr || !A->col_idx || !A->values) {
     err = "msp_bsr: invalid shape/pointers (block must equal nc+1, nc <= 7)";
@@ -331,16 +332,17 @@ msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err
   const int64_t nnzb = M.rp[n];
   if (M.rp[0] != 0 || nnzb <= 0) { err = "msp_bsr: bad row_ptr"; return MSP_EINVAL; }
   M.ci.resize(nnzb);
-  M.v.resize((size_t)nnzb * b * b);
+  const size_t nv = (size_t)nnzb * b * b;
   if (A->device >= 0) {
     if (cudaMemcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(M.v.data(), A->values, sizeof(double) * M.v.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaMemcpy(M.v.owned(nv), A->values, sizeof(double) * nv, cudaMemcpyDeviceToHost) != cudaSuccess) {
       err = "msp_bsr: device copy failed";
       return MSP_ECUDA;
     }
   } else {
     std::memcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb);
-    std::memcpy(M.v.data(), A->values, sizeof(double) * M.v.size());
+    if (view) M.v.view(A->values, nv);
+    else std::memcpy(M.v.owned(nv), A->values, sizeof(double) * nv);
   }
   for (int32_t i = 0; i < n; ++i) {
     if (M.rp[i + 1] < M.rp[i]) { err = "msp_bsr: row_ptr decreasing at row " + std::to_string(i); return MSP_EINVAL; }
@@ -3038,7 +3040,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
-  msp_status st = read_bsr(A, nc, M, err);
+  msp_status st = read_bsr(A, nc, M, err, true);
   if (st) return fail(nullptr, st, err);
   st = guarded(h.get(), [&]() -> msp_status {
     CK(cudaGetDevice(&h->device));
@@ -3108,7 +3110,7 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
   if (rebuild) {
     msp::BlockMat M;
     std::string err;
-    msp_status st = read_bsr(A_new, h->nc, M, err);
+    msp_status st = read_bsr(A_new, h->nc, M, err, true);
     if (st) return fail(h, st, err);
     return guarded(h, [&]() -> msp_status {
       do_setup(h, M);
@@ -3600,7 +3602,7 @@ static msp_status setup_dist_common(const msp_bsr* A, int nc, const msp_config* 
   h->prm = params_of(&c);
   msp::BlockMat M;
   std::string err;
-  msp_status st = read_bsr(A, nc, M, err);
+  msp_status st = read_bsr(A, nc, M, err, true);
   if (st) return fail(nullptr, st, err);
   h->owner_in.resize(M.n);
   for (int32_t i = 0; i < M.n; ++i) {
