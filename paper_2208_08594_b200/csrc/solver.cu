@@ -653,6 +653,50 @@ std::vector<int4> make_islot(int32_t n, const std::vector<int32_t>& rp, const st
 }
 
 // Device scratch for the GPU SETUP steps (freed on scope exit, stream-ordered).
+// Large host -> device uploads of PAGEABLE caller buffers (the block values at SETUP and at
+// msp_update): staged through a pinned ring in 32 MB chunks, the host copies of a chunk
+// split over OpenMP threads while the previous chunks' DMAs run, instead of the driver's
+// single-threaded pageable staging (~11 GB/s measured).  Pinned / small buffers: direct.
+void h2d_large(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = (size_t)32 << 20;
+  constexpr int kSlots = 4;
+  cudaPointerAttributes a;
+  const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type != cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  if (bytes < 2 * kChunk || pinned) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  static std::mutex mu;
+  static char* ring = nullptr;
+  static cudaEvent_t ev[kSlots];
+  static bool used[kSlots];
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ring) {
+    CK(cudaMallocHost(&ring, kChunk * kSlots));
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  size_t i = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, ++i) {
+    const int k = (int)(i % kSlots);
+    const size_t len = std::min(kChunk, bytes - off);
+    if (used[k]) CK(cudaEventSynchronize(ev[k]));
+    char* slot = ring + (size_t)k * kChunk;
+    constexpr size_t kPiece = (size_t)1 << 20;
+    const int64_t np = (int64_t)((len + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) num_threads(8)
+    for (int64_t q = 0; q < np; ++q) {
+      const size_t o = (size_t)q * kPiece;
+      std::memcpy(slot + o, sp + off + o, std::min(kPiece, len - o));
+    }
+    CK(cudaMemcpyAsync(dp + off, slot, len, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ev[k], s));
+    used[k] = true;
+  }
+}
+
 // SETUP temporaries come from a library-private stream-ordered pool that keeps its memory
 // across the synchronisations of one SETUP (release threshold = max; the default pool
 // returns freed memory at every sync, and re-mapping GBs per Galerkin product cost up to
@@ -719,7 +763,7 @@ std::unique_ptr<DBuf> gpu_setup_s1(cudaStream_t s, int decoupling, const msp::Bl
   DBuf& dP = *dPp;
   DBuf dnz((size_t)nnzb, s);
   DBuf drp((size_t)(n + 1) * 4, s), dbad(4, s);
-  CK(cudaMemcpyAsync(dA.p, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, s));
+  h2d_large(s, dA.p, A.v.data(), sizeof(double) * A.v.size());
   h2d(s, drp.as<int32_t>(), A.rp);
   CK(cudaMemsetAsync(dbad.p, 0xff, 4, s));
   std::unique_ptr<DBuf> dcp, dce;
@@ -1023,7 +1067,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   const bool run_here = !rank0_setup || h->rank == 0;
   if (rank0_setup && h->rank != 0 && h->setup_on_gpu) {
     dAvals.reset(new DBuf(A.v.size() * sizeof(double), h->s));
-    CK(cudaMemcpyAsync(dAvals->p, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+    h2d_large(h->s, dAvals->p, A.v.data(), sizeof(double) * A.v.size());
   }
   if (h->setup_on_gpu && run_here) {     // NEXT-2: S1 and the Galerkin products on the GPU
     DBuf* dApp = nullptr;
@@ -1216,7 +1260,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
       T.mark("  A/F buffers allocated");
     }
     if (dAvals) CK(cudaMemcpyAsync(h->stage, dAvals->p, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
-    else CK(cudaMemcpyAsync(h->stage, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice, h->s));
+    else h2d_large(h->s, h->stage, A.v.data(), sizeof(double) * A.v.size());
     int* dbad = nullptr;
     if (gpu_bilu) {
       dbad = h->dalloc<int>(1);
@@ -3126,7 +3170,7 @@ msp_status msp_update(msp_handle* h, const msp_bsr* A_new, int iota, int last_it
     const double* nat = A_new->values;
     if (A_new->device < 0) {
       if (!h->stage) h->stage = h->dalloc<double>(nglob);
-      CK(cudaMemcpyAsync(h->stage, A_new->values, sizeof(double) * nglob, cudaMemcpyHostToDevice, h->s));
+      h2d_large(h->s, h->stage, A_new->values, sizeof(double) * nglob);
       nat = h->stage;
     }
     switch (h->b) {
