@@ -114,6 +114,25 @@ def _np(a, dt):
     return np.ascontiguousarray(a, dtype=dt)
 
 
+def _bsr_any(row_ptr, col, val):
+    """msp_bsr from numpy arrays (host) or CUDA torch tensors (device pointers, no copy):
+    all three on the same side; device arrays must already be int32 / int32 / float64."""
+    if _is_cuda(val):
+        if not (_is_cuda(row_ptr) and _is_cuda(col)):
+            raise ValueError("row_ptr, col and val must all be CUDA tensors (or all host arrays)")
+        import torch
+        if row_ptr.dtype != torch.int32 or col.dtype != torch.int32 or val.dtype != torch.float64:
+            raise ValueError("device BSR arrays must be int32, int32, float64")
+        rp, ci, v = row_ptr.contiguous(), col.contiguous(), val.contiguous()
+        dev = v.device.index if v.device.index is not None else 0
+        return _bsr(rp, ci, v, device=dev)
+    return _bsr(_np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64))
+
+
+def _is_cuda(a):
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
 class _TorchAllocator:
     """Routes the library's device allocations through PyTorch's caching allocator."""
 
@@ -173,8 +192,7 @@ class MspSolver:
             except ImportError:
                 pass
         self.cfg = c
-        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
-        A, keep = _bsr(rp, ci, v)
+        A, keep = _bsr_any(row_ptr, col, val)
         h = ctypes.c_void_p()
         st = _lib.msp_setup(ctypes.byref(A), nc, ctypes.byref(c), ctypes.c_void_p(_caller_stream(stream)),
                             ctypes.byref(h))
@@ -200,8 +218,7 @@ class MspSolver:
 
     def update(self, row_ptr, col, val, iota, last_iterations, mu):
         """ASMSP: returns True when SETUP was executed."""
-        rp, ci, v = _np(row_ptr, np.int32), _np(col, np.int32), _np(val, np.float64)
-        A, keep = _bsr(rp, ci, v)
+        A, keep = _bsr_any(row_ptr, col, val)
         did = ctypes.c_int(0)
         self._check(_lib.msp_update(self._h, ctypes.byref(A), iota, last_iterations, mu,
                                     ctypes.byref(did)))
