@@ -18,11 +18,15 @@ struct SpMat {                       // scalar CSR, ascending columns
   int64_t nnz() const { return (int64_t)ci.size(); }
 };
 
-// Block values: owned, or a read-only view of the caller's host buffer for the duration of
-// one SETUP call (no multi-GB copy of A before the setup reads or uploads it).
+// Block values: owned, a read-only view of the caller's host buffer, or (dptr) the caller's
+// DEVICE buffer, for the duration of one SETUP call -- no multi-GB copy of A before the
+// setup uploads it; a host copy of device values is fetched (d2h) only if a host step
+// reads them.
 struct Values {
-  std::vector<double> own;
-  const double* p = nullptr;
+  mutable std::vector<double> own;
+  mutable const double* p = nullptr;
+  const double* dptr = nullptr;
+  void (*d2h)(double* dst, const double* src, size_t count) = nullptr;
   size_t n = 0;
   Values() = default;
   Values(const Values& o) { *this = o; }
@@ -30,16 +34,34 @@ struct Values {
     if (this == &o) return *this;
     own = o.own;
     n = o.n;
+    dptr = o.dptr;
+    d2h = o.d2h;
     p = own.empty() ? o.p : own.data();
     return *this;
   }
-  const double& operator[](size_t i) const { return p[i]; }
-  const double* data() const { return p; }
+  const double* host() const {
+    if (!p && dptr) {
+      own.resize(n);
+      d2h(own.data(), dptr, n);
+      p = own.data();
+    }
+    return p;
+  }
+  const double& operator[](size_t i) const { return p ? p[i] : host()[i]; }
+  const double* data() const { return host(); }
   size_t size() const { return n; }
   bool empty() const { return n == 0; }
+  void device_view(const double* d, size_t count, void (*fetch)(double*, const double*, size_t)) {
+    own.clear();
+    p = nullptr;
+    dptr = d;
+    d2h = fetch;
+    n = count;
+  }
   double* owned(size_t count) {               // (re)allocate an owned buffer of count values
     own.resize(count);
     p = own.data();
+    dptr = nullptr;
     n = count;
     return own.data();
   }
@@ -47,6 +69,7 @@ struct Values {
     own.clear();
     own.shrink_to_fit();
     p = q;
+    dptr = nullptr;
     n = count;
   }
 };

@@ -115,7 +115,8 @@ std::unique_ptr<DBuf> gpu_setup_s1(cudaStream_t s, int decoupling, const msp::Bl
   DBuf& dP = *dPp;
   DBuf dnz((size_t)nnzb, s);
   DBuf drp((size_t)(n + 1) * 4, s), dbad(4, s);
-  h2d_large(s, dA.p, A.v.data(), sizeof(double) * A.v.size());
+  if (A.v.dptr) CK(cudaMemcpyAsync(dA.p, A.v.dptr, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, s));
+  else h2d_large(s, dA.p, A.v.data(), sizeof(double) * A.v.size());
   h2d(s, drp.as<int32_t>(), A.rp);
   CK(cudaMemsetAsync(dbad.p, 0xff, 4, s));
   std::unique_ptr<DBuf> dcp, dce;
@@ -419,7 +420,8 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
   const bool run_here = !rank0_setup || h->rank == 0;
   if (rank0_setup && h->rank != 0 && h->setup_on_gpu) {
     dAvals.reset(new DBuf(A.v.size() * sizeof(double), h->s));
-    h2d_large(h->s, dAvals->p, A.v.data(), sizeof(double) * A.v.size());
+    if (A.v.dptr) CK(cudaMemcpyAsync(dAvals->p, A.v.dptr, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
+    else h2d_large(h->s, dAvals->p, A.v.data(), sizeof(double) * A.v.size());
   }
   if (h->setup_on_gpu && run_here) {     // NEXT-2: S1 and the Galerkin products on the GPU
     DBuf* dApp = nullptr;
@@ -612,6 +614,7 @@ void do_setup(msp_handle* h, const msp::BlockMat& A) {
       T.mark("  A/F buffers allocated");
     }
     if (dAvals) CK(cudaMemcpyAsync(h->stage, dAvals->p, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
+    else if (A.v.dptr) CK(cudaMemcpyAsync(h->stage, A.v.dptr, sizeof(double) * A.v.size(), cudaMemcpyDeviceToDevice, h->s));
     else h2d_large(h->s, h->stage, A.v.data(), sizeof(double) * A.v.size());
     int* dbad = nullptr;
     if (gpu_bilu) {

@@ -83,8 +83,15 @@ msp_status read_bsr(const msp_bsr* A, int nc, msp::BlockMat& M, std::string& err
   M.ci.resize(nnzb);
   const size_t nv = (size_t)nnzb * b * b;
   if (A->device >= 0) {
-    if (cudaMemcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(M.v.owned(nv), A->values, sizeof(double) * nv, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    if (cudaMemcpy(M.ci.data(), A->col_idx, sizeof(int32_t) * nnzb, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      err = "msp_bsr: device copy failed";
+      return MSP_ECUDA;
+    }
+    if (view) {                                  // values stay on the device (fetched if a host step needs them)
+      M.v.device_view(A->values, nv, [](double* dst, const double* src, size_t count) {
+        CK(cudaMemcpy(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost));
+      });
+    } else if (cudaMemcpy(M.v.owned(nv), A->values, sizeof(double) * nv, cudaMemcpyDeviceToHost) != cudaSuccess) {
       err = "msp_bsr: device copy failed";
       return MSP_ECUDA;
     }
