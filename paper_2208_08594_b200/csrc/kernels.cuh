@@ -1812,7 +1812,7 @@ __global__ void __launch_bounds__(kRedThreads, MSP_DCGS_MINB) dcgs_update_kernel
 // shared memory instead of L2.  Each thread reads only the slots it filled: no block
 // barriers in the stream.  Same per-element arithmetic as dcgs_update_kernel; also
 // covers k > 16 in ONE pass (the register kernel needs a separate dot pass there).
-constexpr int kDcgsStThreads = 256;        // NV = 16 (k <= 16); NV = 32 runs 128 threads
+constexpr int kDcgsStThreads = 256;        // default CTA size (the launches choose per NV)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
 }
