@@ -108,16 +108,17 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
     }
     if constexpr (B == 4 && !WF) {
       if (h->bm_f && !h->comm) {             // per-slot metadata: shorter dependent load chain
+        const unsigned grid4 = nblk((size_t)(b1 - b0) * TM, MSP_BILU_META_TPB);
         if (kind == 0)
-          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, false>, grid, 128, b0, b1, (const int4*)h->bm_f,
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, false>, grid4, MSP_BILU_META_TPB, b0, b1, (const int4*)h->bm_f,
                   (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
                   (const int*)h->ci, (const double*)h->Fval, v, wp, z);
         else if (kind == 1)
-          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, false, true>, grid, 128, b0, b1, (const int4*)h->bm_f,
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, false, true>, grid4, MSP_BILU_META_TPB, b0, b1, (const int4*)h->bm_f,
                   (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
                   (const int*)h->ci, (const double*)h->Fval, v, wp, z);
         else
-          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, true>, grid, 128, b0, b1, (const int4*)h->bm_f,
+          klaunch(h->s, h->pdl, bilu_meta4_kernel<MAXC, true, true>, grid4, MSP_BILU_META_TPB, b0, b1, (const int4*)h->bm_f,
                   (const int4*)h->bm_cf, (const int4*)h->bm_b, (const int4*)h->bm_cb, (const int4*)h->bm_sl,
                   (const int*)h->ci, (const double*)h->Fval, v, wp, z);
         return;
