@@ -18,6 +18,15 @@ constexpr int kSell = 32;
 #define MSP_BILU_PREFETCH 1
 #endif
 constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
+#ifndef MSP_UNI_TPB
+#define MSP_UNI_TPB 128              // CTA size of the level-0 (uniform SELL) sweep kernel
+#endif
+#ifndef MSP_A8_TPB
+#define MSP_A8_TPB 64                // CTA size of the ELL a8 kernel (C3: 65.6 -> 63.2 us vs 256)
+#endif
+#ifndef MSP_SPMV_TPB
+#define MSP_SPMV_TPB 256             // CTA size of the 4x4 SpMV
+#endif
 #ifndef MSP_SELL_PFL
 #define MSP_SELL_PFL 8               // matrix entries per lane prefetched by the LPR > 1 (coarse) sweeps
 #endif
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __res
 template <int MODE>
 // rows != null: process only the n rows listed (distributed mode: the slab-interior rows
 // while the z halo is in flight, then the boundary rows)
-__global__ void __launch_bounds__(256) bsr_spmv4c_kernel(int n, const int* __restrict__ rp,
+__global__ void __launch_bounds__(MSP_SPMV_TPB) bsr_spmv4c_kernel(int n, const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x,
@@ -325,7 +334,7 @@ constexpr int kEllMax = 8;
 #ifndef MSP_A8_MINB
 #define MSP_A8_MINB 1
 #endif
-__global__ void __launch_bounds__(256, MSP_A8_MINB) pcol_resid_ell4_kernel(int n, int ld, int w, const int* __restrict__ ce,
+__global__ void __launch_bounds__(MSP_A8_TPB, MSP_A8_MINB) pcol_resid_ell4_kernel(int n, int ld, int w, const int* __restrict__ ce,
                                                               const double* __restrict__ pe,
                                                               const double* __restrict__ x,
                                                               const double* __restrict__ g,
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(512) sell_row_kernel(int s_first, int s_end,
 // arithmetic, so the PDL prologue loads all of the row's matrix entries and its diagonal
 // with no slice-metadata round trip.  Same per-row arithmetic and summation order.
 template <bool WRITE_R, bool MODE_RES>
-__global__ void __launch_bounds__(128) sell_row_uniform_kernel(int s_first, int s_end, int row_first, int row_end,
+__global__ void __launch_bounds__(MSP_UNI_TPB) sell_row_uniform_kernel(int s_first, int s_end, int row_first, int row_end,
                                                                int W, const int* __restrict__ col,
                                                                const double* __restrict__ val,
                                                                const double* __restrict__ diag,

@@ -13,8 +13,9 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
   const unsigned grid = nblk((size_t)n * TS, 256);
   if (B == 4 && mode != 2) {
     const int* none = nullptr;
-    if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, grid, 256, n, rp, ci, val, x, g, y, none);
-    else klaunch(s, pdl, bsr_spmv4c_kernel<1>, grid, 256, n, rp, ci, val, x, g, y, none);
+    const unsigned g4 = nblk((size_t)n * 4, MSP_SPMV_TPB);
+    if (mode == 0) klaunch(s, pdl, bsr_spmv4c_kernel<0>, g4, MSP_SPMV_TPB, n, rp, ci, val, x, g, y, none);
+    else klaunch(s, pdl, bsr_spmv4c_kernel<1>, g4, MSP_SPMV_TPB, n, rp, ci, val, x, g, y, none);
     return;
   }
   if constexpr (B >= 5) {
@@ -33,7 +34,7 @@ void launch_spmv(msp_handle* h, int mode, const double* x, const double* g, doub
   ++h->nlaunch;
   const double* val = (mode == 2) ? h->Pcol : h->Aval;
   if (mode == 2 && h->pell_w) {
-    klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(h->n, 256), 256, (int)h->n, (int)h->n, (int)h->pell_w,
+    klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(h->n, MSP_A8_TPB), MSP_A8_TPB, (int)h->n, (int)h->n, (int)h->pell_w,
             (const int*)h->pell_c, (const double*)h->pell_v, x, g, y, (const int*)nullptr);
     return;
   }
@@ -62,13 +63,13 @@ void spmv_overlapped(msp_handle* h, int mode, double* x, int width, const double
     if (nr <= 0) return;
     ++h->nlaunch;
     if (mode == 2 && h->pell_w)
-      klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(nr, 256), 256, nr, (int)h->n, (int)h->pell_w,
+      klaunch(h->s, h->pdl, pcol_resid_ell4_kernel, nblk(nr, MSP_A8_TPB), MSP_A8_TPB, nr, (int)h->n, (int)h->pell_w,
               (const int*)h->pell_c, (const double*)h->pell_v, (const double*)x, g, y, (const int*)rows);
     else if (mode == 2)
       klaunch(h->s, h->pdl, pcol_resid4_kernel, nblk((size_t)nr * 4, 256), 256, nr, (const int*)h->rp,
               (const int*)h->ci, (const double*)h->Pcol, (const double*)x, g, y, (const int*)rows);
     else
-      klaunch(h->s, h->pdl, bsr_spmv4c_kernel<0>, nblk((size_t)nr * 4, 256), 256, nr, (const int*)h->rp,
+      klaunch(h->s, h->pdl, bsr_spmv4c_kernel<0>, nblk((size_t)nr * 4, MSP_SPMV_TPB), MSP_SPMV_TPB, nr, (const int*)h->rp,
               (const int*)h->ci, (const double*)h->Aval, (const double*)x, g, y, (const int*)rows);
   };
   part(h->rows_in, h->n_rows_in);
@@ -235,7 +236,8 @@ void coarsest_solve(msp_handle* h) {
 template <int LPR, bool WR, bool RES>
 void sell_rows(msp_handle* h, DevLevel& L, int s0, int s1) {
   if (s1 <= s0) return;
-  const int tpb = (LPR == 1) ? h->sell_tpb : 128;
+  static const int tpb_coarse = std::getenv("MSP_SELL_TPB_COARSE") ? std::atoi(std::getenv("MSP_SELL_TPB_COARSE")) : 64;   // C3 V-cycle 277.4 -> 275.2 us vs 128
+  const int tpb = (LPR == 1) ? h->sell_tpb : tpb_coarse;
   klaunch(h->s, h->pdl, sell_row_kernel<LPR, WR, RES>, nblk((size_t)(s1 - s0) * kSell * LPR, tpb), tpb, 
       s0, s1, L.slice_row, L.slice_off, L.col, L.val, L.diag, L.b, L.x, L.r);
   ++h->nlaunch;
@@ -248,7 +250,7 @@ bool sell_rows_any(msp_handle* h, DevLevel& L, int s0, int s1, HaloPack pk = Hal
     while (c + 1 < L.ncolor && L.color_slice[c + 1] <= s0) ++c;
     if (s1 <= L.color_slice[c + 1]) {              // range inside one color: uniform kernel
       const int row_first = L.color_row[c] + (s0 - L.color_slice[c]) * kSell;
-      klaunch(h->s, h->pdl, sell_row_uniform_kernel<WR, RES>, nblk((size_t)(s1 - s0) * kSell, 128), 128, s0, s1,
+      klaunch(h->s, h->pdl, sell_row_uniform_kernel<WR, RES>, nblk((size_t)(s1 - s0) * kSell, MSP_UNI_TPB), MSP_UNI_TPB, s0, s1,
               row_first, L.color_row[c + 1], L.uniform_w, (const int*)L.col, (const double*)L.val,
               (const double*)L.diag, (const double*)L.b, L.x, L.r, pk);
       ++h->nlaunch;
