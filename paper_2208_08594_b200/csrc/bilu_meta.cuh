@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(MSP_BILU_META_TPB, MSP_BILU_META_MINB) bilu_me
 // bilu_block_kernel's B >= 5 path; the columns of the first four external entries come
 // from the metadata, so their gathers issue at once instead of one ci -> y chain each).
 template <int B, int MAXC, bool FWD, bool BWD>
-__global__ void __launch_bounds__(128, 8) bilu_meta8_kernel(
+#ifndef MSP_BILU_META8_TPB
+#define MSP_BILU_META8_TPB 64                // C4 apply 878 -> 857 us vs 128
+#endif
+__global__ void __launch_bounds__(MSP_BILU_META8_TPB, 1024 / MSP_BILU_META8_TPB) bilu_meta8_kernel(
     int b_first, int b_end, const int4* __restrict__ mf, const int4* __restrict__ cf, const int4* __restrict__ mb,
     const int4* __restrict__ cb, const int4* __restrict__ slt, const int* __restrict__ ci,
     const double* __restrict__ F, double* v, const double* __restrict__ wp, double* __restrict__ z) {

@@ -27,6 +27,9 @@ constexpr bool kBiluPrefetch = MSP_BILU_PREFETCH != 0;
 #ifndef MSP_SPMV_TPB
 #define MSP_SPMV_TPB 256             // CTA size of the 4x4 SpMV
 #endif
+#ifndef MSP_XFER_TPB
+#define MSP_XFER_TPB 256             // CTA size of a3, restriction, prolongation, gather
+#endif
 #ifndef MSP_SELL_PFL
 #define MSP_SELL_PFL 8               // matrix entries per lane prefetched by the LPR > 1 (coarse) sweeps
 #endif
@@ -208,7 +211,10 @@ __device__ __forceinline__ void col_accum8(const double* __restrict__ blk, doubl
 #define MSP_SPMV8_PF 2
 #endif
 template <int B, int MODE>
-__global__ void __launch_bounds__(256) bsr_spmv8c_kernel(int n, const int* __restrict__ rp,
+#ifndef MSP_SPMV8_TPB
+#define MSP_SPMV8_TPB 256
+#endif
+__global__ void __launch_bounds__(MSP_SPMV8_TPB) bsr_spmv8c_kernel(int n, const int* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x,

@@ -20,8 +20,9 @@ void launch_spmv_t(cudaStream_t s, bool pdl, int mode, int n, const int* rp, con
   }
   if constexpr (B >= 5) {
     if (mode != 2) {
-      if (mode == 0) klaunch(s, pdl, bsr_spmv8c_kernel<B, 0>, grid, 256, n, rp, ci, val, x, g, y);
-      else klaunch(s, pdl, bsr_spmv8c_kernel<B, 1>, grid, 256, n, rp, ci, val, x, g, y);
+      const unsigned g8 = nblk((size_t)n * 8, MSP_SPMV8_TPB);
+      if (mode == 0) klaunch(s, pdl, bsr_spmv8c_kernel<B, 0>, g8, MSP_SPMV8_TPB, n, rp, ci, val, x, g, y);
+      else klaunch(s, pdl, bsr_spmv8c_kernel<B, 1>, g8, MSP_SPMV8_TPB, n, rp, ci, val, x, g, y);
       return;
     }
   }
@@ -102,7 +103,8 @@ void launch_bilu_block(msp_handle* h, double* v, const double* wp, double* z, in
       if (h->bm_f && !h->comm) {             // per-slot metadata, 8-lane groups
         auto kf = kind == 0 ? bilu_meta8_kernel<B, MAXC, true, false>
                             : (kind == 1 ? bilu_meta8_kernel<B, MAXC, false, true> : bilu_meta8_kernel<B, MAXC, true, true>);
-        klaunch(h->s, h->pdl, kf, grid, 128, b0, b1, (const int4*)h->bm_f, (const int4*)h->bm_cf, (const int4*)h->bm_b,
+        klaunch(h->s, h->pdl, kf, nblk((size_t)(b1 - b0) * TM, MSP_BILU_META8_TPB), MSP_BILU_META8_TPB, b0, b1,
+                (const int4*)h->bm_f, (const int4*)h->bm_cf, (const int4*)h->bm_b,
                 (const int4*)h->bm_cb, (const int4*)h->bm_sl, (const int*)h->ci, (const double*)h->Fval, v, wp, z);
         return;
       }
@@ -206,7 +208,7 @@ void launch_bilu(msp_handle* h, double* v, const double* wp, double* z, bool wfu
 
 // a3 (+ the fused zero-guess first color of level 0 when it has a PGS-MC level)
 void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool fuse_init, HaloPack pk = HaloPack{}) {
-  const unsigned grid = nblk(h->n, 256);
+  const unsigned grid = nblk(h->n, MSP_XFER_TPB);
   double* x0 = nullptr;
   const double* d0 = nullptr;
   int c1 = 0;
@@ -216,7 +218,7 @@ void launch_restrict_pressure(msp_handle* h, const double* g, double* rp0, bool 
     c1 = h->lv[0].color_row[1];
   }
   switch (h->b) {
-#define CASE(BV) case BV: klaunch(h->s, h->pdl, restrict_pressure_kernel<BV>, grid, 256, h->n, h->W, g, h->cell_of_l0, rp0, x0, d0, c1, pk); break;
+#define CASE(BV) case BV: klaunch(h->s, h->pdl, restrict_pressure_kernel<BV>, grid, MSP_XFER_TPB, h->n, h->W, g, h->cell_of_l0, rp0, x0, d0, c1, pk); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
   }
@@ -368,13 +370,13 @@ void vcycle(msp_handle* h, int l, bool init_done = false) {
     sell_rows_any<false, true>(h, L, 0, L.nslices);
   }
   const bool fuse_next = !last && h->prm.pre_sweeps > 0 && h->prm.smoother == 0;
-  klaunch(h->s, h->pdl, restrict_kernel, nblk(nn, 256), 256, nn, L.pt_ptr, L.pt_idx, L.r, bn,
+  klaunch(h->s, h->pdl, restrict_kernel, nblk(nn, MSP_XFER_TPB), MSP_XFER_TPB, nn, L.pt_ptr, L.pt_idx, L.r, bn,
                                                    fuse_next ? h->lv[l + 1].x : nullptr,
                                                    fuse_next ? h->lv[l + 1].diag : nullptr,
                                                    fuse_next ? h->lv[l + 1].color_row[1] : 0);
   ++h->nlaunch;
   vcycle(h, l + 1, fuse_next);
-  klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, 256), 256, L.n, L.agg, xn, L.x, HaloPack{}); ++h->nlaunch;
+  klaunch(h->s, h->pdl, prolong_kernel, nblk(L.n, MSP_XFER_TPB), MSP_XFER_TPB, L.n, L.agg, xn, L.x, HaloPack{}); ++h->nlaunch;
   for (int s = 0; s < h->prm.post_sweeps; ++s) pgs_sweep(h, L, false, false);
 }
 
@@ -536,7 +538,7 @@ void msp_apply_dev(msp_handle* h, const double* g, double* z) {
     Nvtx nv("a4-a7 V-cycle (PGS-MC, transfers, coarsest)");
     vcycle_any(h, fuse);                                               // a4-a7: B_P
   }
-  klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, 256), 256, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
+  klaunch(h->s, h->pdl, gather_kernel, nblk(h->n, MSP_XFER_TPB), MSP_XFER_TPB, h->n, h->l0_of_cell, level0_x(h), h->wp); ++h->nlaunch;
   {
     Nvtx nv("a8 pressure-column residual");
     launch_spmv(h, 2, h->wp, g, h->r);                                 // a8: r = g - A Pi_P x_p
