@@ -1434,8 +1434,14 @@ __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ 
 // a10 (K8): GMRES vector kernels with deterministic two-stage reductions.
 // multidot: part[blk][i] = sum over this block's elements of V_i . w, i = 0..nv-1.
 // ---------------------------------------------------------------------------
-constexpr int kRedBlocks = 592;     // 4 x 148 SMs
-constexpr int kRedThreads = 256;
+#ifndef MSP_RED_BLOCKS
+#define MSP_RED_BLOCKS 592
+#endif
+#ifndef MSP_RED_THREADS
+#define MSP_RED_THREADS 256
+#endif
+constexpr int kRedBlocks = MSP_RED_BLOCKS;     // 4 x 148 SMs
+constexpr int kRedThreads = MSP_RED_THREADS;
 constexpr int kMaxV = 32;
 
 template <int NV>
