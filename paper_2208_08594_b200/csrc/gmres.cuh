@@ -35,10 +35,13 @@ constexpr bool kCgsWide32 = false;         // NV=32 basis kernels use 8-byte loa
 // N apart, so an odd N also breaks 16-byte alignment of V[1], V[3], ...)
 bool ew2_ok(const msp_handle* h) { return (h->N % 2) == 0; }
 
+#ifndef MSP_DOT_MINB
+#define MSP_DOT_MINB 2
+#endif
 template <int NV>
 void cgs_dot_t(msp_handle* h, int nv, const double* V, const double* w, double* out, const double* addend,
                double* raw, int sq) {
-  constexpr int MINB = 2;
+  constexpr int MINB = MSP_DOT_MINB;
   if ((NV <= 16 || kCgsWide32) && ew2_ok(h))
     klaunch(h->s, h->pdl, cgs_dot_kernel<NV, 2, MINB>, kRedBlocks, kRedThreads, h->N / 2, nv, V, h->N, w, h->part, out,
             addend, raw, sq, h->ticket);
@@ -56,10 +59,10 @@ void cgs_dot(msp_handle* h, int nv, const double* V, const double* w, double* ou
     // 16 vectors per CTA row (gridDim.y = 2), 16-byte loads: full occupancy instead of
     // 32 accumulators per thread
     if (ew2_ok(h))
-      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 2, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N / 2, nv, V,
+      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 2, MSP_DOT_MINB>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N / 2, nv, V,
               h->N, w, h->part, out, addend, raw, sq, h->ticket);
     else
-      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 1, 2>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N, nv, V,
+      klaunch(h->s, h->pdl, cgs_dot_kernel<16, 1, MSP_DOT_MINB>, dim3(kRedBlocks, (nv + 15) / 16), kRedThreads, h->N, nv, V,
               h->N, w, h->part, out, addend, raw, sq, h->ticket);
     ++h->nlaunch;
   }
