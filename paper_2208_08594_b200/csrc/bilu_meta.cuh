@@ -15,6 +15,9 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef MSP_BILU_META_PRE
+#define MSP_BILU_META_PRE 2                  // external factor columns loaded before the PDL wait (<= 4)
+#endif
 #ifndef MSP_BILU_META_TPB
 #define MSP_BILU_META_TPB 64                 // 64-thread CTAs (24 per SM): C3 apply 311.2 -> 308.2 us vs 128
 #endif
@@ -58,9 +61,9 @@ __global__ void __launch_bounds__(MSP_BILU_META_TPB, MSP_BILU_META_MINB) bilu_me
   // (and an L1 prefetch of the intra-block factor blocks used by the triangle)
   const int xa = FWD ? m1.y : m1.z;                 // external range of the first phase
   const int xb = FWD ? m1.z : m1.w;
-  double2 plo[2], phi[2];
+  double2 plo[MSP_BILU_META_PRE], phi[MSP_BILU_META_PRE];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < MSP_BILU_META_PRE; ++u) {
     const int e = xa + u;
     if (valid && e < xb) {
       const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(MSP_BILU_META_TPB, MSP_BILU_META_MINB) bilu_me
     double2 lo[4], hi[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (pre && u < 2) { lo[u] = plo[u]; hi[u] = phi[u]; continue; }
+      if (pre && u < MSP_BILU_META_PRE) { lo[u] = plo[u]; hi[u] = phi[u]; continue; }
       const int e = ea + u;
       if (valid && e < eb) {
         const double2* cp = reinterpret_cast<const double2*>(F + (size_t)e * 16 + q * 4);
