@@ -1,4 +1,4 @@
-"""Print ms/step and per-kernel ms of the bench lines written by tools/gpu_ab_env.sh."""
+"""Print ms/step, per-kernel and per-level times of bench lines (tools/gpu_ab_*.sh output)."""
 import glob
 import json
 import sys
