@@ -150,15 +150,15 @@ void dcgs_staged_launch(msp_handle* h, int k, double* vk, double* w, const doubl
 template <int NV>
 void dcgs_update_t(msp_handle* h, int k, double* vk, double* w, const double* st_in) {
   constexpr bool DOT = NV <= 16;
-  // staged (cp.async) pass 2, one CTA per SM: k <= 8 at 1024 threads, 9 <= k <= 16 at 512
-  // and k > 16 at 384 threads (209 KB of slots; 256 threads: DCGS2 at j = 25 454 -> 388 us
-  // with 384), single-buffered (C3: orthogonalisation at k = 15 0.295 ->
+  // staged (cp.async) pass 2, one CTA per SM: k <= 8 at 1024 threads, 9 <= k <= 16 and
+  // k > 16 at 384 threads (k > 16: 209 KB of slots; DCGS2 at j = 25 454 -> 388 us vs 256
+  // threads, at j = 15 251 -> 245 us vs 512), single-buffered (C3: orthogonalisation at k = 15 0.295 ->
   // 0.255 ms, at k = 25 0.503 -> 0.457 ms; double-buffered forms measured slower, removed)
   if constexpr (NV == 8) {
     if (ew2_ok(h)) { dcgs_staged_launch<8, 1024, 1>(h, k, vk, w, st_in); return; }
   }
   if constexpr (NV == 16) {
-    if (ew2_ok(h)) { dcgs_staged_launch<16, 512, 1>(h, k, vk, w, st_in); return; }
+    if (ew2_ok(h)) { dcgs_staged_launch<16, 384, 1>(h, k, vk, w, st_in); return; }
   }
   if constexpr (NV == 32) {                       // fused staged pass 2 for k > 16
     if (ew2_ok(h)) { dcgs_staged_launch<32, 384, 1>(h, k, vk, w, st_in); return; }
