@@ -492,6 +492,23 @@ def test_device_bsr_input_matches_host():
     assert r0["iters"] == r1["iters"] and torch.equal(r0["x"], r1["x"])
 
 
+def test_time_kernel_per_level_vcycle():
+    """msp_time_kernel kinds 16 + l (the V-cycle from level l down; 16 + L = the coarsest
+    solve alone, the same piece as kind 5): positive, monotone in l (each level adds its
+    sweeps and transfers), and the last one matches the coarsest-GEMV kind."""
+    p = gen.make_config("C2", nx=30, ny=30, nz=8)
+    s = solver(p, coarsest_max_dof=60)
+    L = s.stats()["levels"]
+    assert L >= 2
+    t = [s.time_kernel(16 + l, reps=5)[0] for l in range(L + 1)]
+    assert all(x > 0 for x in t)
+    assert all(t[l] > t[l + 1] for l in range(L)), t
+    c = s.time_kernel("a6_coarse_gemv", reps=5)[0]
+    assert 0.5 * c < t[L] < 2.0 * c, (t[L], c)
+    with pytest.raises(Exception):
+        s.time_kernel(17 + L, reps=1)
+
+
 def test_caller_stream_ordering():
     """the library orders its work after the caller's stream.  b is produced by
     a kernel on a torch side stream that the solver was told about (set_stream), with no
