@@ -45,6 +45,7 @@ msp_status msp_setup(const msp_bsr* A, int nc, const msp_config* cfg, void* cuda
   if (const char* e = std::getenv("MSP_A8_ELL")) h->a8_ell = std::atoi(e);
   if (const char* e = std::getenv("MSP_CYCLE_GRAPH")) h->cycle_graphs = std::atoi(e) != 0;
   if (const char* e = std::getenv("MSP_SPEC_STEPS")) h->spec_steps = std::atoi(e);
+  if (const char* e = std::getenv("MSP_ZBASIS")) h->zbasis = std::atoi(e);
   if (const char* e = std::getenv("MSP_PDL")) h->pdl = std::atoi(e) != 0;
   h->prm = params_of(&c);
   msp::BlockMat M;

@@ -190,20 +190,26 @@ void dcgs2(msp_handle* h, int k) {
   ++h->nlaunch;
 }
 
+// zbasis mode: each Arnoldi step keeps z_j = B v_j (it computes it anyway), so the cycle end
+// forms x += Z y' (one pass over k vectors) instead of applying B to V y (a whole MSP
+// application per cycle end).  Single GPU, per-step graphs or direct launches.
+bool zmode(const msp_handle* h) { return h->zbasis && !h->comm && !h->cycle_graphs; }
+
 // One Arnoldi step j: z = B v_j; w = A z (into V[j+1]); orthogonalise (CGS2 or MGS);
 // hcol[0..j+1] = H(:, j); V[j+1] normalised; hcol copied to pinned host memory.
 void arnoldi_step(msp_handle* h, int j, bool record_to_host = true) {
   const size_t N = h->N;
   double* vj = h->V + (size_t)j * N;
   double* w = h->V + (size_t)(j + 1) * N;
-  msp_apply_dev(h, vj, h->z);
+  double* zj = (h->Z && zmode(h)) ? h->Z + (size_t)j * N : h->z;
+  msp_apply_dev(h, vj, zj);
   {
     Nvtx nvt("a2 BSR SpMV");
     if (overlap_ok(h)) {
-      spmv_overlapped(h, 0, h->z, h->b, nullptr, w);
+      spmv_overlapped(h, 0, zj, h->b, nullptr, w);
     } else {
-      exch_cell(h, h->z, h->b, -1);
-      launch_spmv(h, 0, h->z, nullptr, w);
+      exch_cell(h, zj, h->b, -1);
+      launch_spmv(h, 0, zj, nullptr, w);
     }
   }
   Nvtx nvt("a10 orthogonalisation");
@@ -275,6 +281,7 @@ void build_cycle_graph(msp_handle* h, int m) {
 void ensure_basis(msp_handle* h, int m) {
   if (h->V_m >= m) return;
   h->V = h->dalloc<double>((size_t)(m + 1) * h->N);
+  h->Z = zmode(h) ? h->dalloc<double>((size_t)(m + 1) * h->N) : nullptr;
   h->V_m = m;
   for (auto g : h->graphs) if (g) cudaGraphExecDestroy(g);
   h->graphs.clear();
@@ -384,6 +391,8 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       // and the host's y; step 0 of a cycle reads no lagged state): identical results.
       int launched = -1;
       double est_prev = rel;
+      std::vector<double> nu_used(m, 1.0), rho_used(m, 1.0);
+      std::vector<std::vector<double>> h2_used(m);
       auto launch = [&](int jj) {
         run_step(h, jj, m);
         CK(cudaEventRecord(h->ev_step[jj & 1], h->s));
@@ -396,6 +405,9 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
         const double* hr = h->hrec + (size_t)j * kRecStride;
         auto Hc = [&](int i) -> double& { return H[(size_t)i * m + j]; };
         if (h->prm.orth == 2) {
+          nu_used[j] = nup;                  // v_j's finalisation in step j (zbasis cycle end)
+          rho_used[j] = rhop;
+          h2_used[j] = h2p;
           // column j of the final basis: (nu [c + h2'; rho'] - sum_l h2_l Hraw[:, l]) / rho
           const double* rec = hr;
           for (int i = 0; i <= j + 1; ++i) {
@@ -440,12 +452,40 @@ msp_status gmres(msp_handle* h, double tol, int m, int maxit, int* iters, double
       // u = V_k y ; x += B u ; r = b - A x
       // u = V y through the CGS axpy pass on a zeroed u with coefficients -y (the same
       // fma(y_i, V_i, .) sequence as a plain V y, with the multi-vector pass's loads)
+      const bool zb = h->Z && zmode(h) && !cyc;
+      if (zb && h->prm.orth == 2) {
+        // DCGS2: step j applied B to the provisional v_j; the final basis vector is
+        // v_j = (nu_j v_j' - sum_{l<j} h2_j[l] v_l) / rho_j, so B v_j = sum_{i<=j} T[i][j] z_i
+        // with T upper triangular, and B V y = Z (T y)
+        std::vector<double> T((size_t)k * k, 0.0), yt(k, 0.0);
+        for (int j = 0; j < k; ++j) {
+          T[(size_t)j * k + j] = nu_used[j] / rho_used[j];
+          for (int i = 0; i < j; ++i) {
+            double acc = 0.0;
+            for (int l = i; l < j; ++l) acc += h2_used[j][l] * T[(size_t)i * k + l];
+            T[(size_t)i * k + j] = -acc / rho_used[j];
+          }
+        }
+        for (int i = 0; i < k; ++i) {
+          double acc = 0.0;
+          for (int j = i; j < k; ++j) acc += T[(size_t)i * k + j] * y[j];
+          yt[i] = acc;
+        }
+        y.assign(yt.begin(), yt.end());
+        y.resize(m);
+      }
       for (int i = 0; i < k; ++i) y[i] = -y[i];
       CK(cudaMemcpyAsync(h->dh1, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, h->s));
       CK(cudaMemsetAsync(h->u, 0, sizeof(double) * N, h->s));
-      cgs_axpy<false>(h, k, h->V, h->dh1, h->u, h->lred, nullptr, nullptr, -1);
-      msp_apply_dev(h, h->u, h->z);
-      klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->z, h->xin); ++h->nlaunch;
+      if (zb) {
+        // x += Z y (z_j = B v_j kept by the steps): no MSP application at the cycle end
+        cgs_axpy<false>(h, k, h->Z, h->dh1, h->u, h->lred, nullptr, nullptr, -1);
+        klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->u, h->xin); ++h->nlaunch;
+      } else {
+        cgs_axpy<false>(h, k, h->V, h->dh1, h->u, h->lred, nullptr, nullptr, -1);
+        msp_apply_dev(h, h->u, h->z);
+        klaunch(h->s, h->pdl, axpy_kernel, kRedBlocks, kRedThreads, N, 1.0, h->z, h->xin); ++h->nlaunch;
+      }
       exch_cell(h, h->xin, h->b, -1);
       launch_spmv(h, 1, h->xin, h->bin, h->r);
       norm_dev(h, h->r, h->hcol);

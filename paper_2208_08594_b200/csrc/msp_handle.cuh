@@ -149,6 +149,8 @@ struct msp_handle {
   double *z = nullptr, *r = nullptr, *wp = nullptr, *xin = nullptr, *bin = nullptr, *u = nullptr;
   double *V = nullptr;
   int V_m = -1;
+  double* Z = nullptr;               // z_j = B v_j of every step of a cycle (zbasis mode), m x N
+  int zbasis = 1;                    // MSP_ZBASIS=0: the cycle end applies B to V y instead of Z y'
   double *part = nullptr, *dh1 = nullptr, *dh2 = nullptr, *hcol = nullptr, *hpin = nullptr;
   double* hrec = nullptr;            // pinned: step j's Hessenberg record at hrec + j * kRecStride
   cudaEvent_t ev_step[2] = {nullptr, nullptr};   // end of step j (parity j & 1)
@@ -247,6 +249,7 @@ struct msp_handle {
     lv.clear();
     V = nullptr;
     V_m = -1;
+    Z = nullptr;
     cell_halo = msp::HaloPlan();
     l0_halo = msp::HaloPlan();
     if (hpin) { cudaFreeHost(hpin); hpin = nullptr; }

@@ -492,6 +492,24 @@ def test_device_bsr_input_matches_host():
     assert r0["iters"] == r1["iters"] and torch.equal(r0["x"], r1["x"])
 
 
+@pytest.mark.parametrize("orth", [0, 1, 2])
+def test_zbasis_cycle_end_matches_b_of_v_y(orth, monkeypatch):
+    """zbasis mode (default): the cycle end forms x += Z y' from the z_j = B v_j the steps
+    computed (DCGS2: y' = T y maps the provisional vectors the steps saw to the final
+    basis) instead of applying B to V y.  Same iterations, histories within the parity
+    rule, solutions equal to rounding, over several restarts."""
+    p = gen.make_config("C2", nx=30, ny=30, nz=6)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("MSP_ZBASIS", v)
+        s = solver(p, coarsest_max_dof=100, orth=orth)
+        out.append(s.solve(torch.from_numpy(p["rhs"]).cuda(), restart=7, tol=1e-9))
+    assert out[0]["iters"] == out[1]["iters"] and out[0]["iters"] > 14
+    assert_hist_agree(out[0]["hist"], out[0]["iters"], out[1]["hist"], out[1]["iters"], 7, rtol=1e-7)
+    x0, x1 = out[0]["x"].cpu().numpy(), out[1]["x"].cpu().numpy()
+    assert np.linalg.norm(x0 - x1) <= 1e-9 * np.linalg.norm(x0)
+
+
 def test_time_kernel_per_level_vcycle():
     """msp_time_kernel kinds 16 + l (the V-cycle from level l down; 16 + L = the coarsest
     solve alone, the same piece as kind 5): positive, monotone in l (each level adds its
